@@ -1,0 +1,365 @@
+"""Benchmark: FP64 blocked Cholesky GFLOP/s at n=32768 on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1]): FP64 Cholesky, n=32768, two-level
+blocking.  One step = one in-place factorization of a fresh SPD matrix
+A = M M^T + n I (M ~ U(-1,1), the reference generator cli.py:55-64, formed on
+the device with this package's own SYRK).  Work per step is the reference's
+flop count n^3/3 (cli.py:78-79).
+
+* value      device time of K factorizations, inputs resident in HBM (8.6 GB,
+             far larger than the 126 MB L2), CUDA events on the launch stream;
+             the pristine input is restored between steps outside the events.
+* e2e        the same metric through the public API from HOST memory: pinned
+             host matrix -> device (from_numpy-style upload), cholesky(),
+             factor -> pinned host, all inside the timed region.
+* roofline   the dominant kernel (the DMMA GEMMT/SYRK of the trailing update),
+             timed alone with CUDA events over every top-level trailing update
+             of the factorization: algorithmic flops n_k(n_k+1)*bs per launch.
+* cpu_baseline  the oracle port of the reference (oracle/, C++ restatement,
+             bit-identical to the reference) on this host's cores on a bounded
+             sample (a smaller n of the same algorithm).
+--impl reference   times that CPU port alone (the reference's own code is
+             Python + numba and is not installed on the GPU box).
+N > 1 ranks currently run independent replicas (multi-GPU).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_DEFAULT = 32768
+GPU_TREE = {
+    "op": "cholesky", "variant": 3, "bs": 1024, "kernel": {"kc": 1024},
+    "child": {"op": "cholesky", "variant": 3, "bs": 128, "kernel": {"kc": 128},
+              "child": {"op": "cholesky", "variant": "unblocked3"}},
+}
+# FP64 roofline denominator.  MEASURED_PEAKS.json carries no FP64 entry and
+# B200_PROFILING.md no FP64 fallback, so this is our own measurement on this
+# pool (tools/fp64_peak.cu, profiles/r01_fp64_peak.txt): register-resident DMMA
+# m8n8k4, 148 SMs, best and sustained 37.1 TFLOP/s at 1965 MHz.
+FP64_PEAK_TFLOPS = 37.1
+FP64_PEAK_SOURCE = "measured: tools/fp64_peak.cu DMMA register-resident, 37.1 TF/s (profiles/r01_fp64_peak.txt)"
+
+
+def chol_flops(n: int) -> float:
+    return n ** 3 / 3.0
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples: list[tuple] = []
+        self._proc = None
+        self._thread = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._thread = threading.Thread(target=self._read, daemon=True)
+            self._thread.start()
+        except OSError:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        smax = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[4 + i].lower() == "active"})
+        power = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "power_w_max": max(power) if power else None, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------- CPU oracle --
+def cpu_baseline(n_target: int, budget_s: float = 15.0) -> dict:
+    """The oracle port of the reference (bit-identical to it) on this host,
+    all cores, on a bounded sample: the largest n (multiple of 1024) whose
+    factorization fits the time budget, same tree shape as the reference C1
+    (v3, bs=128, unblocked3 leaf; kc=256 default)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+
+    O.build()
+    threads = O.host_threads()
+    levels = O.levels_from_tree({"op": "cholesky", "variant": 3, "bs": 128,
+                                 "child": {"op": "cholesky", "variant": "unblocked3"}}, 0, "f64")
+
+    def run(n):
+        rng = np.random.default_rng(42)
+        m = rng.integers(-4, 5, (n, n)).astype(np.float64)
+        a = (m @ m.T + n * np.eye(n)).reshape(-1).copy()
+        t0 = time.perf_counter()
+        bad = O.cholesky(a, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1}, levels, nthreads=threads)
+        dt = time.perf_counter() - t0
+        assert bad == -1
+        return dt
+
+    n = 2048
+    dt = run(n)
+    rate = chol_flops(n) / dt
+    n_s = int((budget_s * rate * 3) ** (1 / 3) // 1024 * 1024)
+    n_s = max(2048, min(n_s, n_target, 16384))
+    if n_s != n:
+        dt = run(n_s)
+        n = n_s
+    return {"value": chol_flops(n) / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"oracle C++ port of the reference (bit-identical), n={n} v3/bs128/unblocked3 kc=256, "
+                      f"{threads} threads, one factorization ({dt:.2f} s)"}
+
+
+# ----------------------------------------------------------------- GPU arm --
+def make_spd(bf, torch, n: int, device, seed: int = 42):
+    """A = M M^T + n I (lower triangle) with this package's own SYRK."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    m = torch.rand(n, n, dtype=torch.float64, device=device, generator=g) * 2 - 1
+    a = torch.zeros(n, n, dtype=torch.float64, device=device)
+    va = bf.from_torch(a)
+    vm = bf.from_torch(m)
+    bf.syrk_lower(1.0, vm, 0.0, va, cfg=bf.KernelConfig(8, 6, 64, 4096, 2048, bf.DType.F64, bf.DType.F64))
+    a.diagonal().add_(float(n))
+    del m
+    return a
+
+
+def roofline_syrk(bf, torch, a0, n: int, bs: int, kc: int) -> dict:
+    """Time the dominant kernel alone: the trailing GEMMT of every top-level
+    step (n_k = n - (k+1)*bs, K = bs), on the launch stream."""
+    work = a0.clone()
+    v = bf.from_torch(work)
+    cfg = bf.KernelConfig(8, 6, 64, kc, 2048, bf.DType.F64, bf.DType.F64)
+    stream = torch.cuda.current_stream()
+    flops, ms = 0.0, 0.0
+    launches = 0
+    for k in range(n // bs - 1):
+        r2 = (k + 1) * bs
+        nk = n - r2
+        a21 = v.subview(bf.Range(r2, nk), bf.Range(k * bs, bs))
+        a22 = v.subview(bf.Range(r2, nk), bf.Range(r2, nk))
+        bf.syrk_lower(-1.0, a21, 1.0, a22, cfg=cfg)  # warm
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        bf.syrk_lower(-1.0, a21, 1.0, a22, cfg=cfg)
+        e1.record(stream)
+        e1.synchronize()
+        ms += e0.elapsed_time(e1)
+        flops += float(nk) * (nk + 1) * bs
+        launches += 1
+    del work
+    achieved = flops / (ms / 1e3) / 1e12
+    return {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+            "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": None,
+            "kernel": "gemm_dmma_kernel<128x128x16, k-major/k-major> (GEMMT lower, trailing SYRK)",
+            "per_launch_flops": "n_k*(n_k+1)*bs, n_k = n-(k+1)*bs", "launches_timed": launches,
+            "syrk_ms_total": round(ms, 3), "peak_source": FP64_PEAK_SOURCE}
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--tree", type=str, default=json.dumps(GPU_TREE))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-roofline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = args.n
+    workload = f"FP64 blocked Cholesky n={n}, two-level blocking (BASELINE configs[1])"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        steps = []
+        base = None
+        for i in range(args.warmup + args.steps):
+            base = cpu_baseline(n, budget_s=8.0)
+            if i >= args.warmup:
+                steps.append(base["value"])
+        value = statistics.median(steps)
+        line = {"metric": "Cholesky GFLOP/s (n=32768 FP64)", "value": round(value, 3), "unit": "GFLOP/s",
+                "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic SPD (integer M, exact M M^T + n I), seed 42",
+                "config": {"workload": workload, "tree": "v3/bs128/unblocked3 (reference default, kc=256)"},
+                "cpu_baseline": dict(base, value=round(value, 3)),
+                "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_07311_b200 as bf
+    from paper_2604_07311_b200.control import parse_tree
+    from paper_2604_07311_b200.engine import _lib
+
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    tree = parse_tree(args.tree)
+
+    a0 = make_spd(bf, torch, n, dev)
+    work = torch.empty_like(a0)
+    torch.cuda.synchronize()
+
+    def one_step(timed: list | None):
+        work.copy_(a0)
+        v = bf.from_torch(work)
+        stream = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        info = bf.cholesky_async(v, "lower", tree)
+        e1.record(stream)
+        if timed is not None:
+            timed.append((e0, e1, info))
+        return info
+
+    for _ in range(args.warmup):
+        info = one_step(None)
+    torch.cuda.synchronize()
+    assert int(info.item()) == -1, "warm-up factorization failed"
+
+    lib = _lib.lib()
+    timed: list = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.bf_launch_count()
+    with ClockSampler(local) as clocks:
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            one_step(timed)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    launches = (lib.bf_launch_count() - launches0) // max(1, args.steps)
+    if world > 1:
+        dist.barrier()
+    for _, _, info in timed:
+        assert int(info.item()) == -1
+    step_ms = [e0.elapsed_time(e1) for e0, e1, _ in timed]
+    ms = sum(step_ms) / len(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = chol_flops(n) * world / (ms / 1e3) / 1e9
+
+    # ---- end to end through the public API from host memory -------------
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(n, n, dtype=torch.float64, pin_memory=True)
+        host.copy_(a0)
+        out = torch.empty_like(host, pin_memory=True)
+        dev_buf = work
+        e2e_ms = []
+        for i in range(1 + args.e2e_steps):
+            torch.cuda.synchronize()
+            stream = torch.cuda.current_stream()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dev_buf.copy_(host, non_blocking=True)
+            bf.cholesky(bf.from_torch(dev_buf), "lower", tree)  # syncs to read the pivot flag
+            out.copy_(dev_buf, non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            if i > 0:
+                e2e_ms.append(e0.elapsed_time(e1))
+        ems = sum(e2e_ms) / len(e2e_ms)
+        nbytes = n * n * 8
+        e2e = {"value": round(chol_flops(n) * world / (ems / 1e3) / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(ems, 3),
+               "path": "pinned host -> HBM copy, paper_2604_07311_b200.cholesky(), HBM -> pinned host"}
+        del host, out
+
+    roof = None
+    if not args.no_roofline and rank == 0:
+        bs = tree.bs or 128
+        kc = (tree.kernel or {}).get("kc", 256)
+        roof = roofline_syrk(bf, torch, a0, n, bs, kc)
+        roof["share_of_step"] = round(roof["syrk_ms_total"] / ms, 4)
+
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        cpu = cpu_baseline(n)
+
+    if rank == 0:
+        clk = clocks.summary()
+        line = {
+            "metric": "Cholesky GFLOP/s (n=32768 FP64)",
+            "value": round(value, 3),
+            "unit": "GFLOP/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms, 3),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic: A = M M^T + n I, M ~ U(-1,1) seed 42 (reference generator cli.py:55-64), formed on device",
+            "config": {"workload": workload, "n": n, "tree": json.loads(args.tree),
+                       "l2": "input 8.6 GB >> 126 MB L2 (no flush needed); pristine copy restored outside the events",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+            "pct_of_fp64_peak": round(100 * value / world / 1e3 / FP64_PEAK_TFLOPS, 2),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "wall_s_timed": round(wall, 3),
+            "step_ms": [round(x, 3) for x in step_ms],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,125 @@
+/* blockfam-b200: C ABI of the B200-native level-3 hot path.
+ *
+ * This is the drop-in boundary for the reference package `blockfam`
+ * (/root/reference/pkg/src/blockfam).  The reference's algorithm layer calls
+ * its engine by name (factor/cholesky.py:24: gemm, syrk_lower, trsm) and its
+ * leaves through `_UNBLOCKED[variant](storage, offset, rs, cs, n) -> int`
+ * (factor/cholesky.py:92-96,123); the contraction calls
+ * `gemm_scatter(alpha, ScatterMatrix a, b, beta, c, cfg, ways)`
+ * (tensor/contract.py:177-185).  Each of those maps to one function below.
+ *
+ * Conventions
+ *   - A matrix operand is a strided view: element (i, j) lives at
+ *     ((T*)base)[off + i*rs + j*cs]  (views.py:131-146 MatrixView).  base is a
+ *     DEVICE pointer; the library never allocates, frees or copies caller
+ *     memory, and never touches host memory.
+ *   - A block-scatter operand (tensor/scatter.py:22-39) is element
+ *     (i, j) at ((T*)base)[rscat[i] + cscat[j]] with rscat/cscat DEVICE int64
+ *     vectors.
+ *   - Suffix d = FP64, s = FP32 (FP32 accumulation), sd = FP32 storage with
+ *     FP64 accumulation (engine/config.py:14-48 acc_dtype).
+ *   - `kc` is the reference's kc cache block, which is the only blocking
+ *     parameter that changes arithmetic: the k range is folded into C every
+ *     kc elements (engine/gemm.py:124-126).  Passing the reference's kc makes
+ *     results bit-identical to the reference.
+ *   - All functions are asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and thread-safe for distinct streams.  Device-side
+ *     failure indices are reported through caller-owned device ints that the
+ *     caller initialises to -1 and reads after synchronising.
+ *   - Return codes: BF_OK, or a negative BF_ERR_* (no fallback path exists:
+ *     an unsupported request fails loudly).
+ */
+#ifndef BLOCKFAM_B200_H
+#define BLOCKFAM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BF_OK 0
+#define BF_ERR_SHAPE (-1)       /* dims mismatch (reference ShapeError) */
+#define BF_ERR_ALIAS (-2)       /* reserved: aliasing is checked by the host layer */
+#define BF_ERR_UNSUPPORTED (-3) /* layout / size this build does not handle */
+#define BF_ERR_VALUE (-4)       /* bad argument (variant, kc < 1, ...) */
+#define BF_ERR_CUDA (-11)       /* a CUDA launch or attribute call failed */
+
+typedef struct bf_view {
+  void* base;
+  int64_t off, m, n, rs, cs;
+} bf_view;
+
+typedef struct bf_scatter_view {
+  void* base;
+  int64_t m, n;
+  const int64_t* rscat; /* device, length m */
+  const int64_t* cscat; /* device, length n */
+} bf_scatter_view;
+
+/* One level of a Cholesky control tree (control.py:47-71 ControlNode):
+ * variant 1/2/3 = blocked (bs required), 11/12/13 = unblocked1/2/3 leaf;
+ * kc = the level's effective kernel kc (control.py:67-68 effective_config). */
+typedef struct bf_chol_level {
+  int32_t variant;
+  int32_t pad_;
+  int64_t bs;
+  int64_t kc;
+} bf_chol_level;
+
+int bf_abi_version(void);
+/* Number of kernels this library has launched in this process (all devices). */
+int64_t bf_launch_count(void);
+const char* bf_last_error(void);
+int bf_device_sm_count(void);
+
+/* C := beta*C + alpha*A*B (lower_only: only i >= j of C is read or written).
+ * Replaces engine/gemm.py:179-242 gemm / gemmt_lower / syrk_lower (syrk =
+ * gemm(a, a^T view, lower_only=1)).  Edge semantics of engine/gemm.py:97-108:
+ * alpha==0 && beta==1 -> no-op; k==0 || alpha==0 -> C := beta*C only.
+ * d_abort: optional device int; the kernels do nothing if *d_abort >= 0. */
+int bf_gemm_d(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c, int lower_only,
+              int64_t kc, const int* d_abort, void* stream);
+int bf_gemm_s(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c, int lower_only,
+              int64_t kc, const int* d_abort, void* stream);
+int bf_gemm_sd(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c, int lower_only,
+               int64_t kc, const int* d_abort, void* stream);
+
+/* C := beta*C over all of C or its lower triangle (engine/kernels.py:125-139). */
+int bf_scale_d(double beta, const bf_view* c, int lower_only, void* stream);
+int bf_scale_s(double beta, const bf_view* c, int lower_only, void* stream);
+int bf_scale_sd(double beta, const bf_view* c, int lower_only, void* stream);
+
+/* Unblocked Cholesky leaf on a square view, variant 1/2/3 (factor/cholesky.py:31-96).
+ * On a non-positive pivot k writes base_index + k to *d_info (if *d_info < 0). */
+int bf_potrf_leaf_d(const bf_view* a, int variant, int64_t base_index, int* d_info, void* stream);
+int bf_potrf_leaf_s(const bf_view* a, int variant, int64_t base_index, int* d_info, void* stream);
+
+/* B := alpha * B * tril(T)^-T, recursive halving to a 32 base exactly as
+ * engine/trsm.py:29-68,96-111 (off-diagonal blocks through bf_gemm with kc).
+ * A zero diagonal writes the base-local column index to *d_singular and stops. */
+int bf_trsm_rltn_d(double alpha, const bf_view* tri, const bf_view* b, int64_t kc, int* d_singular, void* stream);
+int bf_trsm_rltn_s(double alpha, const bf_view* tri, const bf_view* b, int64_t kc, int* d_singular, void* stream);
+
+/* In-place lower Cholesky of a square view driven by a flattened control tree
+ * (levels[0] = root; a blocked level without a successor recurses on
+ * unblocked3, factor/cholesky.py:154-158).  Same operation sequence as
+ * factor/cholesky.py:118-151.  First failing global pivot -> *d_info. */
+int bf_cholesky_d(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream);
+int bf_cholesky_s(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream);
+
+/* Block-scatter GEMM for tensor contraction (engine/gemm.py:74-160 on
+ * tensor/contract.py facades): C := beta*C + alpha*A*B with every operand
+ * addressed through its scatter vectors. */
+int bf_gemm_scatter_d(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
+                      const bf_scatter_view* c, int64_t kc, void* stream);
+int bf_gemm_scatter_s(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
+                      const bf_scatter_view* c, int64_t kc, void* stream);
+int bf_gemm_scatter_sd(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
+                       const bf_scatter_view* c, int64_t kc, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BLOCKFAM_B200_H */

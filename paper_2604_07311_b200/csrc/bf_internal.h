@@ -1,0 +1,73 @@
+// Internal (C++) parameter blocks shared by the kernels and the C-ABI layer.
+// Nothing here crosses the library boundary; include/blockfam_b200.h is the ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bf {
+
+// How an operand tile is fetched from global memory.
+enum GlobalLayout : int {
+  GL_KMAJOR = 0,   // unit stride along k   (row-major A, "NT" B)  -> k-major smem
+  GL_MNMAJOR = 1,  // unit stride along m/n (col-major A, row-major B) -> mn-major smem
+  GL_GENERIC = 2,  // arbitrary strides or block-scatter vectors     -> k-major smem, 1 element per copy
+};
+
+// One GEMM operand viewed as an (mn x k) matrix: A is (m x k), B^T is (n x k).
+// Element (i, p) lives at base[off + i*s_mn + p*s_k], or at
+// base[mn_scat[i] + k_scat[p]] when the scatter vectors are given
+// (tensor/scatter.py:69-98 block-scatter facades).
+struct OperandMK {
+  const void* base;
+  int64_t off;
+  int64_t s_mn;
+  int64_t s_k;
+  const int64_t* mn_scat;
+  const int64_t* k_scat;
+  int layout;  // GlobalLayout
+  int vec;     // elements per vector copy along the unit-stride dim (1, or 16B/elem)
+};
+
+// C := beta*C + alpha*A*B with the reference's accumulation structure:
+// the k range is cut into segments of kc (engine/gemm.py:124-126); each
+// segment is summed from +0 as an ascending fma chain and folded into C as
+// C = beta_eff*C + alpha*t with beta_eff = beta on the first segment, 1 after
+// (engine/kernels.py:228-253).  lower_only writes only i >= j.
+struct GemmParams {
+  int64_t m, n, k;
+  int64_t kc;
+  OperandMK a;
+  OperandMK b;
+  void* c;
+  int64_t c_off, c_rs, c_cs;
+  const int64_t* c_rscat;  // scatter C (contraction), else nullptr
+  const int64_t* c_cscat;
+  double alpha, beta;
+  int lower_only;
+  int tiles_m, tiles_n;
+  int group;              // raster group height in tiles
+  int64_t num_tiles;
+  const int* abort_flag;  // skip all work when non-null and *abort_flag >= 0
+};
+
+// Every kernel launch of this library bumps a process-wide counter
+// (bf_launch_count in the ABI) so benchmarks can report how many of OUR
+// kernels ran in a timed region.
+void note_launch(int64_t n = 1);
+
+// Kernel-family entry points (implemented in the .cu files).
+int launch_gemm_dmma(const GemmParams& p, cudaStream_t s);            // f64 storage, f64 acc
+int launch_gemm_simt_f32(const GemmParams& p, cudaStream_t s);        // f32 storage, f32 acc
+int launch_gemm_simt_f32acc64(const GemmParams& p, cudaStream_t s);   // f32 storage, f64 acc
+int launch_scale(int is_f64, double beta, void* c, int64_t off, int64_t m, int64_t n, int64_t rs,
+                 int64_t cs, const int64_t* rscat, const int64_t* cscat, int lower_only,
+                 cudaStream_t s);
+int launch_potrf_leaf(int is_f64, int variant, void* a, int64_t off, int64_t n, int64_t rs,
+                      int64_t cs, int64_t base_index, int* d_info, cudaStream_t s);
+int launch_trsm_base_right(int is_f64, double alpha, const void* t, int64_t toff, int64_t trs,
+                           int64_t tcs, void* b, int64_t boff, int64_t brs, int64_t bcs, int64_t m,
+                           int64_t n, int* d_singular, int64_t index_base, const int* abort_flag,
+                           cudaStream_t s);
+
+}  // namespace bf

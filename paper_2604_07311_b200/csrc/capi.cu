@@ -1,0 +1,341 @@
+// extern "C" boundary (include/blockfam_b200.h) and the native host drivers
+// that sit directly above the kernels: operand classification, the
+// reference's GEMM edge semantics, the recursive TRSM and the control-tree
+// Cholesky loop.  The drivers issue exactly the reference's sequence of
+// level-3 calls, so results are bit-identical to the reference when the same
+// tree (and hence the same kc) is used.
+#include "bf_internal.h"
+#include "blockfam_b200.h"
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+namespace bf {
+static std::atomic<int64_t> g_launches{0};
+void note_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace bf
+
+namespace {
+
+using bf::GemmParams;
+using bf::OperandMK;
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* msg) {
+  g_last_error = msg;
+  return code;
+}
+
+enum Mode { MODE_D = 0, MODE_S = 1, MODE_SD = 2 };
+
+inline bool storage_is_f64(Mode m) { return m == MODE_D; }
+inline int64_t elem_bytes(Mode m) { return storage_is_f64(m) ? 8 : 4; }
+
+// --- view helpers (views.py:172-199 subview / transposed) ------------------
+inline bf_view subview(const bf_view& v, int64_t r0, int64_t nr, int64_t c0, int64_t nc) {
+  bf_view s = v;
+  s.off = v.off + r0 * v.rs + c0 * v.cs;
+  s.m = nr;
+  s.n = nc;
+  return s;
+}
+inline bf_view transposed(const bf_view& v) {
+  bf_view t = v;
+  t.m = v.n;
+  t.n = v.m;
+  t.rs = v.cs;
+  t.cs = v.rs;
+  return t;
+}
+
+// Classify an operand seen as (MN x K) with strides (s_mn, s_k).
+OperandMK classify(const void* base, int64_t off, int64_t s_mn, int64_t s_k, int64_t MN, int64_t K, int64_t kc,
+                   Mode mode) {
+  OperandMK o{};
+  o.base = base;
+  o.off = off;
+  o.s_mn = s_mn;
+  o.s_k = s_k;
+  o.mn_scat = nullptr;
+  o.k_scat = nullptr;
+  o.vec = 1;
+  const bool base16 = (reinterpret_cast<uintptr_t>(base) % 16) == 0;
+  const int64_t per16 = 16 / elem_bytes(mode);
+  if (s_k == 1 || K <= 1) {
+    o.layout = bf::GL_KMAJOR;
+    o.s_k = 1;
+    const bool kc_ok = (kc % per16 == 0) || kc >= K;
+    if (storage_is_f64(mode) && base16 && off % per16 == 0 && (s_mn % per16 == 0 || MN <= 1) && kc_ok) o.vec = 2;
+  } else if (s_mn == 1 || MN <= 1) {
+    o.layout = bf::GL_MNMAJOR;
+    o.s_mn = 1;
+    if (storage_is_f64(mode) && base16 && off % per16 == 0 && s_k % per16 == 0) o.vec = 2;
+  } else {
+    o.layout = bf::GL_GENERIC;
+  }
+  return o;
+}
+
+int launch_family(Mode mode, const GemmParams& p, cudaStream_t s) {
+  switch (mode) {
+    case MODE_D: return bf::launch_gemm_dmma(p, s);
+    case MODE_S: return bf::launch_gemm_simt_f32(p, s);
+    case MODE_SD: return bf::launch_gemm_simt_f32acc64(p, s);
+  }
+  return BF_ERR_VALUE;
+}
+
+int scale_impl(Mode mode, double beta, const bf_view& c, int lower_only, cudaStream_t s) {
+  int kind = mode == MODE_D ? 1 : (mode == MODE_SD ? 2 : 0);
+  int rc = bf::launch_scale(kind, beta, c.base, c.off, c.m, c.n, c.rs, c.cs, nullptr, nullptr, lower_only, s);
+  return rc ? fail(BF_ERR_CUDA, "scale launch failed") : BF_OK;
+}
+
+// engine/gemm.py:74-160 gemm_scatter edge semantics + launch
+int gemm_impl(Mode mode, double alpha, const bf_view& a, const bf_view& b, double beta, const bf_view& c,
+              int lower_only, int64_t kc, const int* d_abort, cudaStream_t s) {
+  if (a.n != b.m || c.m != a.m || c.n != b.n) return fail(BF_ERR_SHAPE, "gemm dims mismatch");
+  if (lower_only && c.m != c.n) return fail(BF_ERR_SHAPE, "gemmt needs square c");
+  if (kc < 1) return fail(BF_ERR_VALUE, "kc must be >= 1");
+  if (a.rs < 0 || a.cs < 0 || b.rs < 0 || b.cs < 0 || c.rs < 0 || c.cs < 0)
+    return fail(BF_ERR_SHAPE, "engine packing requires non-negative strides (use transposed views)");
+  const int64_t m = c.m, n = c.n, k = a.n;
+  if (m == 0 || n == 0) return BF_OK;
+  double al = alpha, be = beta;
+  if (mode == MODE_S) {  // alpha/beta in the accumulation dtype (engine/gemm.py:99-102)
+    al = double(float(alpha));
+    be = double(float(beta));
+  }
+  if (al == 0.0 && be == 1.0) return BF_OK;
+  if (k == 0 || al == 0.0) {
+    if (be != 1.0) return scale_impl(mode, be, c, lower_only, s);
+    return BF_OK;
+  }
+  GemmParams p{};
+  p.m = m;
+  p.n = n;
+  p.k = k;
+  p.kc = kc;
+  p.a = classify(a.base, a.off, a.rs, a.cs, m, k, kc, mode);
+  p.b = classify(b.base, b.off, b.cs, b.rs, n, k, kc, mode);  // B^T as (n x k)
+  p.c = c.base;
+  p.c_off = c.off;
+  p.c_rs = c.rs;
+  p.c_cs = c.cs;
+  p.alpha = al;
+  p.beta = be;
+  p.lower_only = lower_only;
+  p.group = 8;
+  p.abort_flag = d_abort;
+  int rc = launch_family(mode, p, s);
+  if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "gemm: unsupported size/layout");
+  return rc ? fail(BF_ERR_CUDA, "gemm launch failed") : BF_OK;
+}
+
+// engine/trsm.py:51-68 (_solve_right) with the 32-wide base (engine/trsm.py:96-111)
+int trsm_rec(Mode mode, double alpha, const bf_view& tri, const bf_view& b, int64_t kc, int* d_sing,
+             const int* d_abort, cudaStream_t s) {
+  const int64_t n = tri.n;
+  if (b.m == 0 || n == 0) return BF_OK;
+  if (n <= 32) {
+    int rc = bf::launch_trsm_base_right(storage_is_f64(mode), alpha, tri.base, tri.off, tri.rs, tri.cs, b.base,
+                                        b.off, b.rs, b.cs, b.m, n, d_sing, 0, d_abort, s);
+    return rc ? fail(BF_ERR_CUDA, "trsm base launch failed") : BF_OK;
+  }
+  const int64_t n1 = n / 2, n2 = n - n1;
+  bf_view l11 = subview(tri, 0, n1, 0, n1);
+  bf_view l21 = subview(tri, n1, n2, 0, n1);
+  bf_view l22 = subview(tri, n1, n2, n1, n2);
+  bf_view b1 = subview(b, 0, b.m, 0, n1);
+  bf_view b2 = subview(b, 0, b.m, n1, n2);
+  int rc = trsm_rec(mode, alpha, l11, b1, kc, d_sing, d_abort, s);
+  if (rc) return rc;
+  rc = gemm_impl(mode, -1.0, b1, transposed(l21), alpha, b2, 0, kc, d_abort, s);
+  if (rc) return rc;
+  return trsm_rec(mode, 1.0, l22, b2, kc, d_sing, d_abort, s);
+}
+
+int trsm_impl(Mode mode, double alpha, const bf_view* tri, const bf_view* b, int64_t kc, int* d_sing,
+              cudaStream_t s) {
+  if (!tri || !b) return fail(BF_ERR_VALUE, "null view");
+  if (tri->m != tri->n) return fail(BF_ERR_SHAPE, "triangular operand must be square");
+  if (b->n != tri->n) return fail(BF_ERR_SHAPE, "right solve dims mismatch");
+  return trsm_rec(mode, alpha, *tri, *b, kc, d_sing, d_sing, s);
+}
+
+int leaf_impl(Mode mode, const bf_view& a, int variant, int64_t base, int* d_info, cudaStream_t s) {
+  if (a.m != a.n) return fail(BF_ERR_SHAPE, "square matrix required");
+  if (variant < 1 || variant > 3) return fail(BF_ERR_VALUE, "leaf variant must be 1, 2 or 3");
+  int rc = bf::launch_potrf_leaf(storage_is_f64(mode), variant, a.base, a.off, a.n, a.rs, a.cs, base, d_info, s);
+  if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "leaf too large");
+  return rc ? fail(BF_ERR_CUDA, "leaf launch failed") : BF_OK;
+}
+
+// factor/cholesky.py:118-158 (_run / _recurse) on a flattened control tree.
+int chol_run(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int idx, int64_t base, int* d_info,
+             cudaStream_t s) {
+  const int64_t n = a.n;
+  if (n == 0) return BF_OK;
+  bf_chol_level node;
+  if (idx < nl) {
+    node = lv[idx];
+  } else {
+    node.variant = 13;  // missing child -> unblocked3 (factor/cholesky.py:156-157)
+    node.bs = 0;
+    node.kc = idx > 0 ? lv[idx - 1].kc : 256;
+  }
+  if (node.variant >= 11 && node.variant <= 13) return leaf_impl(mode, a, node.variant - 10, base, d_info, s);
+  if (node.variant < 1 || node.variant > 3) return fail(BF_ERR_VALUE, "unknown blocked variant");
+  if (node.bs < 1) return fail(BF_ERR_VALUE, "blocked node requires bs >= 1");
+  const int64_t bs = node.bs, kc = node.kc;
+  int rc = BF_OK;
+  for (int64_t done = 0; done < n && rc == BF_OK; done += (bs < n - done ? bs : n - done)) {
+    const int64_t b = bs < n - done ? bs : n - done;
+    const int64_t r2s = done + b, r2n = n - r2s;
+    bf_view a00 = subview(a, 0, done, 0, done);
+    bf_view a10 = subview(a, done, b, 0, done);
+    bf_view a11 = subview(a, done, b, done, b);
+    bf_view a20 = subview(a, r2s, r2n, 0, done);
+    bf_view a21 = subview(a, r2s, r2n, done, b);
+    bf_view a22 = subview(a, r2s, r2n, r2s, r2n);
+    switch (node.variant) {
+      case 1:
+        rc = trsm_rec(mode, 1.0, a00, a10, kc, nullptr, d_info, s);
+        if (!rc) rc = gemm_impl(mode, -1.0, a10, transposed(a10), 1.0, a11, 1, kc, d_info, s);
+        if (!rc) rc = chol_run(mode, a11, lv, nl, idx + 1, base + done, d_info, s);
+        break;
+      case 2:
+        rc = gemm_impl(mode, -1.0, a10, transposed(a10), 1.0, a11, 1, kc, d_info, s);
+        if (!rc) rc = chol_run(mode, a11, lv, nl, idx + 1, base + done, d_info, s);
+        if (!rc) rc = gemm_impl(mode, -1.0, a20, transposed(a10), 1.0, a21, 0, kc, d_info, s);
+        if (!rc) rc = trsm_rec(mode, 1.0, a11, a21, kc, nullptr, d_info, s);
+        break;
+      case 3:
+        rc = chol_run(mode, a11, lv, nl, idx + 1, base + done, d_info, s);
+        if (!rc) rc = trsm_rec(mode, 1.0, a11, a21, kc, nullptr, d_info, s);
+        if (!rc) rc = gemm_impl(mode, -1.0, a21, transposed(a21), 1.0, a22, 1, kc, d_info, s);
+        break;
+    }
+  }
+  return rc;
+}
+
+int chol_impl(Mode mode, const bf_view* a, const bf_chol_level* lv, int nl, int* d_info, cudaStream_t s) {
+  if (!a || (nl > 0 && !lv)) return fail(BF_ERR_VALUE, "null argument");
+  if (a->m != a->n) return fail(BF_ERR_SHAPE, "square matrix required");
+  if (nl < 1) return fail(BF_ERR_VALUE, "empty control tree");
+  return chol_run(mode, *a, lv, nl, 0, 0, d_info, s);
+}
+
+int scatter_impl(Mode mode, double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
+                 const bf_scatter_view* c, int64_t kc, cudaStream_t s) {
+  if (!a || !b || !c) return fail(BF_ERR_VALUE, "null view");
+  if (b->m != a->n || c->m != a->m || c->n != b->n) return fail(BF_ERR_SHAPE, "gemm dims mismatch");
+  if (kc < 1) return fail(BF_ERR_VALUE, "kc must be >= 1");
+  const int64_t m = c->m, n = c->n, k = a->n;
+  if (m == 0 || n == 0) return BF_OK;
+  double al = alpha, be = beta;
+  if (mode == MODE_S) {
+    al = double(float(alpha));
+    be = double(float(beta));
+  }
+  if (al == 0.0 && be == 1.0) return BF_OK;
+  if (k == 0 || al == 0.0) {
+    if (be == 1.0) return BF_OK;
+    int kind = mode == MODE_D ? 1 : (mode == MODE_SD ? 2 : 0);
+    int rc = bf::launch_scale(kind, be, c->base, 0, m, n, 0, 0, c->rscat, c->cscat, 0, s);
+    return rc ? fail(BF_ERR_CUDA, "scale launch failed") : BF_OK;
+  }
+  GemmParams p{};
+  p.m = m;
+  p.n = n;
+  p.k = k;
+  p.kc = kc;
+  p.a = OperandMK{a->base, 0, 0, 0, a->rscat, a->cscat, bf::GL_GENERIC, 1};
+  p.b = OperandMK{b->base, 0, 0, 0, b->cscat, b->rscat, bf::GL_GENERIC, 1};
+  p.c = c->base;
+  p.c_rscat = c->rscat;
+  p.c_cscat = c->cscat;
+  p.alpha = al;
+  p.beta = be;
+  p.lower_only = 0;
+  p.group = 8;
+  int rc = launch_family(mode, p, s);
+  return rc ? fail(BF_ERR_CUDA, "scatter gemm launch failed") : BF_OK;
+}
+
+inline cudaStream_t S(void* p) { return static_cast<cudaStream_t>(p); }
+
+}  // namespace
+
+extern "C" {
+
+int bf_abi_version(void) { return 1; }
+int64_t bf_launch_count(void) { return bf::g_launches.load(std::memory_order_relaxed); }
+const char* bf_last_error(void) { return g_last_error.c_str(); }
+int bf_device_sm_count(void) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return sms;
+}
+
+#define BF_GEMM_ENTRY(NAME, MODE)                                                                            \
+  int NAME(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c, int lower_only, \
+           int64_t kc, const int* d_abort, void* stream) {                                                  \
+    if (!a || !b || !c) return fail(BF_ERR_VALUE, "null view");                                             \
+    return gemm_impl(MODE, alpha, *a, *b, beta, *c, lower_only, kc, d_abort, S(stream));                   \
+  }
+BF_GEMM_ENTRY(bf_gemm_d, MODE_D)
+BF_GEMM_ENTRY(bf_gemm_s, MODE_S)
+BF_GEMM_ENTRY(bf_gemm_sd, MODE_SD)
+#undef BF_GEMM_ENTRY
+
+int bf_scale_d(double beta, const bf_view* c, int lower_only, void* stream) {
+  return c ? scale_impl(MODE_D, beta, *c, lower_only, S(stream)) : fail(BF_ERR_VALUE, "null view");
+}
+int bf_scale_s(double beta, const bf_view* c, int lower_only, void* stream) {
+  return c ? scale_impl(MODE_S, double(float(beta)), *c, lower_only, S(stream)) : fail(BF_ERR_VALUE, "null view");
+}
+int bf_scale_sd(double beta, const bf_view* c, int lower_only, void* stream) {
+  return c ? scale_impl(MODE_SD, beta, *c, lower_only, S(stream)) : fail(BF_ERR_VALUE, "null view");
+}
+
+int bf_potrf_leaf_d(const bf_view* a, int variant, int64_t base_index, int* d_info, void* stream) {
+  return a ? leaf_impl(MODE_D, *a, variant, base_index, d_info, S(stream)) : fail(BF_ERR_VALUE, "null view");
+}
+int bf_potrf_leaf_s(const bf_view* a, int variant, int64_t base_index, int* d_info, void* stream) {
+  return a ? leaf_impl(MODE_S, *a, variant, base_index, d_info, S(stream)) : fail(BF_ERR_VALUE, "null view");
+}
+
+int bf_trsm_rltn_d(double alpha, const bf_view* tri, const bf_view* b, int64_t kc, int* d_singular, void* stream) {
+  return trsm_impl(MODE_D, alpha, tri, b, kc, d_singular, S(stream));
+}
+int bf_trsm_rltn_s(double alpha, const bf_view* tri, const bf_view* b, int64_t kc, int* d_singular, void* stream) {
+  return trsm_impl(MODE_S, alpha, tri, b, kc, d_singular, S(stream));
+}
+
+int bf_cholesky_d(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream) {
+  return chol_impl(MODE_D, a, levels, nlevels, d_info, S(stream));
+}
+int bf_cholesky_s(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream) {
+  return chol_impl(MODE_S, a, levels, nlevels, d_info, S(stream));
+}
+
+int bf_gemm_scatter_d(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
+                      const bf_scatter_view* c, int64_t kc, void* stream) {
+  return scatter_impl(MODE_D, alpha, a, b, beta, c, kc, S(stream));
+}
+int bf_gemm_scatter_s(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
+                      const bf_scatter_view* c, int64_t kc, void* stream) {
+  return scatter_impl(MODE_S, alpha, a, b, beta, c, kc, S(stream));
+}
+int bf_gemm_scatter_sd(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
+                       const bf_scatter_view* c, int64_t kc, void* stream) {
+  return scatter_impl(MODE_SD, alpha, a, b, beta, c, kc, S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,168 @@
+"""ctypes binding of the sm_100a C-ABI library (include/blockfam_b200.h).
+
+The library is built in-tree by paper_2604_07311_b200/build.py.  There is no
+fallback: if it is missing, or a compute call is given non-CUDA storage, the
+call raises DeviceError.  `declared_symbols()` parses the header so tests can
+check that every declared entry point is exported.
+"""
+from __future__ import annotations
+
+import ctypes
+import re
+import threading
+from pathlib import Path
+from typing import Optional
+
+import torch
+
+from ..errors import DeviceError, ShapeError
+from ..views import DType, MatrixView
+
+__all__ = [
+    "lib",
+    "lib_path",
+    "header_path",
+    "declared_symbols",
+    "BfView",
+    "BfScatterView",
+    "BfCholLevel",
+    "as_bfview",
+    "stream_ptr",
+    "check",
+    "require_cuda",
+]
+
+_PKG = Path(__file__).resolve().parents[1]
+_LIB_PATH = _PKG / "_lib" / "libblockfam_b200.so"
+_HEADER = _PKG.parent / "include" / "blockfam_b200.h"
+
+BF_OK = 0
+BF_ERR_SHAPE = -1
+
+
+class BfView(ctypes.Structure):
+    _fields_ = [
+        ("base", ctypes.c_void_p),
+        ("off", ctypes.c_int64),
+        ("m", ctypes.c_int64),
+        ("n", ctypes.c_int64),
+        ("rs", ctypes.c_int64),
+        ("cs", ctypes.c_int64),
+    ]
+
+
+class BfScatterView(ctypes.Structure):
+    _fields_ = [
+        ("base", ctypes.c_void_p),
+        ("m", ctypes.c_int64),
+        ("n", ctypes.c_int64),
+        ("rscat", ctypes.c_void_p),
+        ("cscat", ctypes.c_void_p),
+    ]
+
+
+class BfCholLevel(ctypes.Structure):
+    _fields_ = [("variant", ctypes.c_int32), ("pad_", ctypes.c_int32), ("bs", ctypes.c_int64), ("kc", ctypes.c_int64)]
+
+
+_lock = threading.Lock()
+_lib: Optional[ctypes.CDLL] = None
+
+_P = ctypes.POINTER
+_V = _P(BfView)
+_SV = _P(BfScatterView)
+_I = ctypes.c_int
+_D = ctypes.c_double
+_L = ctypes.c_int64
+_VP = ctypes.c_void_p
+
+_SIGNATURES = {
+    "bf_abi_version": ([], _I),
+    "bf_launch_count": ([], _L),
+    "bf_last_error": ([], ctypes.c_char_p),
+    "bf_device_sm_count": ([], _I),
+    "bf_gemm_d": ([_D, _V, _V, _D, _V, _I, _L, _VP, _VP], _I),
+    "bf_gemm_s": ([_D, _V, _V, _D, _V, _I, _L, _VP, _VP], _I),
+    "bf_gemm_sd": ([_D, _V, _V, _D, _V, _I, _L, _VP, _VP], _I),
+    "bf_scale_d": ([_D, _V, _I, _VP], _I),
+    "bf_scale_s": ([_D, _V, _I, _VP], _I),
+    "bf_scale_sd": ([_D, _V, _I, _VP], _I),
+    "bf_potrf_leaf_d": ([_V, _I, _L, _VP, _VP], _I),
+    "bf_potrf_leaf_s": ([_V, _I, _L, _VP, _VP], _I),
+    "bf_trsm_rltn_d": ([_D, _V, _V, _L, _VP, _VP], _I),
+    "bf_trsm_rltn_s": ([_D, _V, _V, _L, _VP, _VP], _I),
+    "bf_cholesky_d": ([_V, _P(BfCholLevel), _I, _VP, _VP], _I),
+    "bf_cholesky_s": ([_V, _P(BfCholLevel), _I, _VP, _VP], _I),
+    "bf_gemm_scatter_d": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
+    "bf_gemm_scatter_s": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
+    "bf_gemm_scatter_sd": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
+}
+
+
+def lib_path() -> Path:
+    return _LIB_PATH
+
+
+def header_path() -> Path:
+    return _HEADER
+
+
+def declared_symbols() -> list[str]:
+    """Function names declared in include/blockfam_b200.h."""
+    text = _HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(bf_\w+)\s*\(", text, flags=re.M)))
+
+
+def lib() -> ctypes.CDLL:
+    """Load (once) the sm_100a library; raise loudly if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not _LIB_PATH.exists():
+                raise DeviceError(
+                    f"{_LIB_PATH} is missing: build it with `python -m paper_2604_07311_b200.build` "
+                    "(there is no CPU fallback)"
+                )
+            handle = ctypes.CDLL(str(_LIB_PATH))
+            for name, (args, res) in _SIGNATURES.items():
+                fn = getattr(handle, name)
+                fn.argtypes = args
+                fn.restype = res
+            _lib = handle
+    return _lib
+
+
+def require_cuda(*objs) -> None:
+    """Every operand (a view or a raw tensor) must live in GPU memory."""
+    for o in objs:
+        st = o if isinstance(o, torch.Tensor) else o.storage
+        if not st.is_cuda:
+            raise DeviceError(
+                "blockfam-b200 computes on the GPU only; operand storage is on "
+                f"{st.device} (create views with make_view(..., device='cuda'))"
+            )
+
+
+def as_bfview(v: MatrixView) -> BfView:
+    return BfView(v.storage.data_ptr(), v.offset, v.m, v.n, v.rs, v.cs)
+
+
+def stream_ptr(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def check(rc: int, what: str) -> None:
+    if rc == BF_OK:
+        return
+    msg = (lib().bf_last_error() or b"").decode(errors="replace")
+    if rc == BF_ERR_SHAPE:
+        raise ShapeError(f"{what}: {msg}")
+    raise DeviceError(f"{what} failed (code {rc}): {msg}")
+
+
+def suffix(dtype: DType, acc: DType) -> str:
+    if dtype is DType.F64:
+        return "d"
+    return "sd" if acc is DType.F64 else "s"

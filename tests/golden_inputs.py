@@ -1,0 +1,66 @@
+"""Seeded, platform-independent input generators for the golden fixtures.
+
+Shared by tools/gen_golden.py (which feeds them to the reference) and the
+tests (which feed them to the oracle and the CUDA path), so the fixture file
+only needs output digests.  numpy's PCG64 streams are platform independent;
+SPD matrices are built from small integers so M @ M.T is exact whatever BLAS
+kernel forms it.
+"""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+
+NP = {"f64": np.float64, "f32": np.float32}
+
+
+def digest(arr: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(arr).tobytes()).hexdigest()
+
+
+def strided_operand(rng: np.random.Generator, m: int, n: int, dt: str, kind: str):
+    """(storage, meta) of an m x n operand laid out as kind."""
+    vals = rng.uniform(-1, 1, (m, n)).astype(NP[dt])
+    if kind == "contiguous":
+        return vals.reshape(-1).copy(), {"off": 0, "m": m, "n": n, "rs": n, "cs": 1}
+    if kind == "transposed":
+        return np.ascontiguousarray(vals.T).reshape(-1), {"off": 0, "m": m, "n": n, "rs": 1, "cs": m}
+    parent = rng.uniform(-1, 1, (m + 3, n + 5)).astype(NP[dt])
+    parent[2 : 2 + m, 3 : 3 + n] = vals
+    return parent.reshape(-1).copy(), {"off": 2 * (n + 5) + 3, "m": m, "n": n, "rs": n + 5, "cs": 1}
+
+
+def gemm_inputs(seed: int, op: str, dt: str, m: int, n: int, k: int, kinds: tuple[str, str, str]):
+    rng = np.random.default_rng(seed)
+    n_eff = m if op in ("syrk", "gemmt") else n
+    a = strided_operand(rng, m, k, dt, kinds[0])
+    b = strided_operand(rng, k, n_eff, dt, kinds[1]) if op != "syrk" else None
+    c = strided_operand(rng, m, n_eff, dt, kinds[2])
+    return a, b, c
+
+
+def spd_int(seed: int, n: int, dt: str = "f64") -> np.ndarray:
+    """A = M M^T + n I with small-integer M: exact in any summation order."""
+    rng = np.random.default_rng(seed)
+    m = rng.integers(-4, 5, (n, n)).astype(np.float64)
+    return (m @ m.T + n * np.eye(n)).astype(NP[dt])
+
+
+def spd_float(seed: int, n: int) -> np.ndarray:
+    """The reference's own generator (tests/util.py:7-10); BLAS-dependent bits."""
+    rng = np.random.default_rng(seed)
+    m = rng.uniform(-1, 1, (n, n))
+    return m @ m.T + n * np.eye(n)
+
+
+def trsm_inputs(seed: int, dt: str, n: int, m: int):
+    rng = np.random.default_rng(seed)
+    tri = (np.tril(rng.uniform(-1, 1, (n, n))) + n * np.eye(n)).astype(NP[dt])
+    b = rng.uniform(-1, 1, (m, n)).astype(NP[dt])
+    return tri, b
+
+
+def tensor_inputs(seed: int, a_dims, b_dims, c_dims):
+    rng = np.random.default_rng(seed)
+    return (rng.uniform(-1, 1, a_dims), rng.uniform(-1, 1, b_dims), rng.uniform(-1, 1, c_dims))

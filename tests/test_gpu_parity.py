@@ -1,0 +1,153 @@
+"""GPU parity beyond the golden fixtures: larger sizes against the (golden-
+pinned) oracle on identical bytes, the reference's bitwise contracts, its
+edge semantics, and size-independent properties at bench sizes."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2604_07311_b200 as bf
+from golden_inputs import digest, spd_int
+from paper_2604_07311_b200.control import parse_tree
+from paper_2604_07311_b200.engine import KernelConfig
+from paper_2604_07311_b200.views import DType, Range, make_view
+
+pytestmark = pytest.mark.gpu
+
+F64 = DType.F64
+
+
+def chol_gpu(a0: np.ndarray, tree_doc, uplo="lower"):
+    n = a0.shape[0]
+    v = make_view(n, n, fill=a0)
+    bf.cholesky(v, uplo, parse_tree(tree_doc) if tree_doc else None)
+    return v.storage.cpu().numpy()
+
+
+def chol_oracle(a0: np.ndarray, tree_doc, uplo="lower"):
+    import json
+
+    n = a0.shape[0]
+    st = a0.reshape(-1).copy()
+    bad = O.cholesky(st, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1},
+                     O.levels_from_tree(json.loads(tree_doc) if tree_doc else None, n, "f64"), uplo=uplo,
+                     nthreads=O.host_threads())
+    assert bad == -1
+    return st
+
+
+TREES = [
+    '{"op":"cholesky","variant":3,"bs":128,"child":{"op":"cholesky","variant":"unblocked3"}}',
+    '{"op":"cholesky","variant":3,"bs":512,"kernel":{"kc":512},"child":{"op":"cholesky","variant":3,"bs":64,'
+    '"child":{"op":"cholesky","variant":"unblocked3"}}}',
+    '{"op":"cholesky","variant":2,"bs":256,"child":{"op":"cholesky","variant":"unblocked2"}}',
+    '{"op":"cholesky","variant":1,"bs":192,"kernel":{"kc":96},"child":{"op":"cholesky","variant":"unblocked1"}}',
+]
+
+
+@pytest.mark.parametrize("tree", TREES)
+def test_cholesky_2000_bitwise_vs_oracle(cuda, tree):
+    a0 = spd_int(777, 2000)
+    assert digest(chol_gpu(a0, tree)) == digest(chol_oracle(a0, tree))
+
+
+def test_upper_is_bitwise_transpose_of_lower(cuda):
+    a0 = spd_int(5, 700)
+    t = TREES[1]
+    lo = chol_gpu(a0, t, "lower").reshape(700, 700)
+    up = chol_gpu(a0, t, "upper").reshape(700, 700)
+    assert np.tril(lo).tobytes() == np.tril(up.T).tobytes()
+    assert np.triu(lo, 1).tobytes() == np.triu(a0, 1).tobytes()  # other triangle untouched
+
+
+def test_npd_reports_global_index_and_stops(cuda):
+    a0 = spd_int(9, 300)
+    a0[211, 211] = -1e6
+    v = make_view(300, 300, fill=a0)
+    with pytest.raises(bf.errors.NotPositiveDefiniteError) as e:
+        bf.cholesky(v, tree=parse_tree(TREES[1]))
+    assert e.value.index == 211
+    st = a0.reshape(-1).copy()
+    import json
+
+    bad = O.cholesky(st, {"off": 0, "m": 300, "n": 300, "rs": 300, "cs": 1},
+                     O.levels_from_tree(json.loads(TREES[1]), 300, "f64"))
+    assert bad == 211
+    assert digest(v.storage.cpu().numpy()) == digest(st)  # same partial state as the reference stops in
+
+
+def test_gemmt_lower_equals_gemm_lower_bitwise(cuda):
+    rng = np.random.default_rng(13)
+    n, k = 777, 513
+    a = make_view(n, k, fill=rng.uniform(-1, 1, (n, k)))
+    b = make_view(k, n, fill=rng.uniform(-1, 1, (k, n)))
+    c0 = rng.uniform(-1, 1, (n, n))
+    ct, cf = make_view(n, n, fill=c0), make_view(n, n, fill=c0)
+    bf.gemmt_lower(-1.0, a, b, 1.0, ct)
+    bf.gemm(-1.0, a, b, 1.0, cf)
+    assert np.tril(ct.to_numpy()).tobytes() == np.tril(cf.to_numpy()).tobytes()
+    assert np.triu(ct.to_numpy(), 1).tobytes() == np.triu(c0, 1).tobytes()
+
+
+@pytest.mark.parametrize("kind", ["contiguous", "transposed", "padded"])
+def test_gemm_layouts_bitwise_vs_oracle(cuda, kind):
+    from golden_inputs import gemm_inputs
+
+    for seed, (m, n, k), kc in [(1, (300, 200, 700), 256), (2, (129, 1000, 64), 33), (3, (1000, 40, 500), 500)]:
+        a, b, c = gemm_inputs(seed, "gemm", "f64", m, n, k, (kind, kind, kind))
+        cst = c[0].copy()
+        O.gemm(0.75, a, b, -1.5, (cst, c[1]), kc=kc)
+        cfg = KernelConfig(8, 6, 64, kc, 2048, F64, F64)
+        dv = lambda s, meta: bf.MatrixView(torch.as_tensor(s).cuda(), meta["off"], meta["m"], meta["n"],
+                                           meta["rs"], meta["cs"], F64)
+        vc = dv(*c)
+        bf.gemm(0.75, dv(*a), dv(*b), -1.5, vc, cfg=cfg)
+        assert digest(vc.storage.cpu().numpy()) == digest(cst)
+
+
+def test_edge_semantics(cuda):
+    nan = float("nan")
+    c = make_view(3, 3, fill=np.full((3, 3), nan))
+    bf.gemm(1.0, make_view(3, 2, fill=np.ones((3, 2))), make_view(2, 3, fill=np.ones((2, 3))), 0.0, c)
+    assert np.array_equal(c.to_numpy(), np.full((3, 3), 2.0))  # beta=0 never reads C
+    c0 = np.array([[0.25, -0.0], [np.pi, 7.0]])
+    c = make_view(2, 2, fill=c0)
+    bf.gemm(0.0, make_view(2, 2, fill=np.full((2, 2), nan)), make_view(2, 2), 1.0, c)
+    assert c.to_numpy().tobytes() == c0.tobytes()  # alpha=0, beta=1: exact no-op
+    c = make_view(2, 2, fill=[[1, 2], [3, 4]])
+    bf.gemm(1.0, make_view(2, 0), make_view(0, 2), 0.0, c)
+    assert c.to_numpy().tolist() == [[0, 0], [0, 0]]
+    c = make_view(3, 3, fill=np.arange(9.0).reshape(3, 3))
+    bf.gemmt_lower(1.0, make_view(3, 2), make_view(2, 3), 0.5, c)
+    cn = c.to_numpy()
+    assert np.array_equal(np.tril(cn), 0.5 * np.tril(np.arange(9.0).reshape(3, 3)))
+    assert np.array_equal(np.triu(cn, 1), np.triu(np.arange(9.0).reshape(3, 3), 1))
+
+
+def test_trsm_singular_and_hand(cuda):
+    tri = make_view(2, 2, fill=[[2, 0], [1, 2]])
+    b = make_view(1, 2, fill=[[2, 5]])
+    bf.trsm(bf.engine.RIGHT_LOWER_TRANS_NONUNIT, 1.0, tri, b)
+    assert b.to_numpy().tolist() == [[1, 2]]
+    with pytest.raises(bf.errors.SingularMatrixError):
+        bf.trsm(bf.engine.RIGHT_LOWER_TRANS_NONUNIT, 1.0, make_view(2, 2, fill=[[1, 0], [1, 0]]),
+                make_view(1, 2, fill=[[1, 1]]))
+
+
+def test_cholesky_bench_size_residual(cuda):
+    """n=8192 with the bench tree: randomized backward error on device."""
+    n = 8192
+    torch.manual_seed(0)
+    m = torch.rand(n, n, dtype=torch.float64, device="cuda") * 2 - 1
+    a0 = m @ m.T + n * torch.eye(n, dtype=torch.float64, device="cuda")
+    a = bf.from_torch(a0.clone())
+    tree = parse_tree('{"op":"cholesky","variant":3,"bs":1024,"kernel":{"kc":1024},"child":{"op":"cholesky",'
+                      '"variant":3,"bs":128,"kernel":{"kc":128},"child":{"op":"cholesky","variant":"unblocked3"}}}')
+    bf.cholesky(a, tree=tree)
+    L = torch.tril(a.to_torch())
+    x = torch.randn(n, 4, dtype=torch.float64, device="cuda")
+    r = a0 @ x - L @ (L.T @ x)
+    rel = (r.norm() / (a0.norm() * x.norm())).item()
+    assert rel <= 10 * n * np.finfo(np.float64).eps / n  # far inside 10*n*eps

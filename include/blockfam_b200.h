@@ -71,6 +71,9 @@ int bf_abi_version(void);
 /* Number of kernels this library has launched in this process (all devices). */
 int64_t bf_launch_count(void);
 const char* bf_last_error(void);
+/* Process-wide switches: "lookahead" (default 1) overlaps the next panel's
+ * POTRF+TRSM with the trailing update in bf_cholesky_* (same arithmetic). */
+int bf_set_option(const char* name, int64_t value);
 int bf_device_sm_count(void);
 
 /* C := beta*C + alpha*A*B (lower_only: only i >= j of C is read or written).

@@ -48,8 +48,16 @@ struct GemmParams {
   int tiles_m, tiles_n;
   int group;              // raster group height in tiles
   int64_t num_tiles;
-  const int* abort_flag;  // skip all work when non-null and *abort_flag >= 0
+  const int* abort_flag;  // skip all work when non-null and 0 <= *abort_flag < abort_limit
+  int64_t abort_limit;    // a failure at a pivot >= abort_limit happened "later" in the
+                          // reference's order and must not cancel this launch
 };
+
+__device__ __forceinline__ bool aborted(const GemmParams& p) {
+  if (p.abort_flag == nullptr) return false;
+  const int f = *p.abort_flag;
+  return f >= 0 && f < p.abort_limit;
+}
 
 // Every kernel launch of this library bumps a process-wide counter
 // (bf_launch_count in the ABI) so benchmarks can report how many of OUR
@@ -58,6 +66,9 @@ void note_launch(int64_t n = 1);
 
 // Kernel-family entry points (implemented in the .cu files).
 int launch_gemm_dmma(const GemmParams& p, cudaStream_t s);            // f64 storage, f64 acc
+bool gemm_dmma_tma_eligible(const GemmParams& p);                     // TMA/mbarrier fast path?
+int launch_gemm_dmma_tma(const GemmParams& p, cudaStream_t s);
+extern int g_use_tma;                                                 // bf_set_option("tma", 0|1)
 int launch_gemm_simt_f32(const GemmParams& p, cudaStream_t s);        // f32 storage, f32 acc
 int launch_gemm_simt_f32acc64(const GemmParams& p, cudaStream_t s);   // f32 storage, f64 acc
 int launch_scale(int is_f64, double beta, void* c, int64_t off, int64_t m, int64_t n, int64_t rs,

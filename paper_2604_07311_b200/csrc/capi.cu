@@ -8,6 +8,7 @@
 #include "blockfam_b200.h"
 
 #include <atomic>
+#include <climits>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -23,6 +24,7 @@ using bf::GemmParams;
 using bf::OperandMK;
 
 thread_local std::string g_last_error;
+int g_lookahead = 1;  // bf_set_option("lookahead", 0) restores the plain reference schedule
 
 int fail(int code, const char* msg) {
   g_last_error = msg;
@@ -96,7 +98,8 @@ int scale_impl(Mode mode, double beta, const bf_view& c, int lower_only, cudaStr
 
 // engine/gemm.py:74-160 gemm_scatter edge semantics + launch
 int gemm_impl(Mode mode, double alpha, const bf_view& a, const bf_view& b, double beta, const bf_view& c,
-              int lower_only, int64_t kc, const int* d_abort, cudaStream_t s) {
+              int lower_only, int64_t kc, const int* d_abort, cudaStream_t s,
+              int64_t abort_limit = INT64_MAX) {
   if (a.n != b.m || c.m != a.m || c.n != b.n) return fail(BF_ERR_SHAPE, "gemm dims mismatch");
   if (lower_only && c.m != c.n) return fail(BF_ERR_SHAPE, "gemmt needs square c");
   if (kc < 1) return fail(BF_ERR_VALUE, "kc must be >= 1");
@@ -130,6 +133,7 @@ int gemm_impl(Mode mode, double alpha, const bf_view& a, const bf_view& b, doubl
   p.lower_only = lower_only;
   p.group = 8;
   p.abort_flag = d_abort;
+  p.abort_limit = abort_limit;
   int rc = launch_family(mode, p, s);
   if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "gemm: unsupported size/layout");
   return rc ? fail(BF_ERR_CUDA, "gemm launch failed") : BF_OK;
@@ -223,10 +227,85 @@ int chol_run(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int i
   return rc;
 }
 
+// High-priority side stream per device for the panel chain of the lookahead
+// schedule (its CTAs are preferred whenever trailing-update CTAs retire).
+cudaStream_t panel_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, hi);
+  }
+  return streams[dev];
+}
+
+// Right-looking (variant 3) top level with depth-1 lookahead.  Same operation
+// set as factor/cholesky.py:146-149 — every element of A22 still receives the
+// step's whole K=bs update as one kc-segmented chain and one fold per
+// segment — only the launch split and the stream order change:
+//   main  : [A(k+1 col block) -= L21 L21_top^T]  ...  [rest of A22 -= L21 L21^T]
+//   panel :                       chol(A11') ; A21' := A21' tril(A11')^-T
+// so the next panel's POTRF+TRSM overlaps the bulk of this step's SYRK.
+int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int64_t base, int* d_info,
+                      cudaStream_t s) {
+  const int64_t n = a.n, bs = lv[0].bs, kc = lv[0].kc;
+  cudaStream_t ps = panel_stream();
+  if (!ps) return fail(BF_ERR_CUDA, "cannot create the panel stream");
+  cudaEvent_t ev_main, ev_panel;
+  cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming);
+  auto panel = [&](int64_t done, int64_t b, cudaStream_t st) {
+    bf_view a11 = subview(a, done, b, done, b);
+    bf_view a21 = subview(a, done + b, n - done - b, done, b);
+    int rc = chol_run(mode, a11, lv, nl, 1, base + done, d_info, st);
+    if (!rc) rc = trsm_rec(mode, 1.0, a11, a21, kc, nullptr, d_info, st);
+    return rc;
+  };
+  int rc = panel(0, bs < n ? bs : n, s);
+  for (int64_t done = 0; done < n && rc == BF_OK;) {
+    const int64_t b = bs < n - done ? bs : n - done;
+    const int64_t r2 = done + b, nr2 = n - r2;
+    if (nr2 == 0) break;
+    const int64_t b2 = bs < nr2 ? bs : nr2;  // next panel width
+    bf_view l21 = subview(a, r2, nr2, done, b);
+    bf_view l21_top = subview(l21, 0, b2, 0, b);
+    bf_view l21_rest = subview(l21, b2, nr2 - b2, 0, b);
+    // (1) next block column, on the main stream
+    rc = gemm_impl(mode, -1.0, l21_top, transposed(l21_top), 1.0, subview(a, r2, b2, r2, b2), 1, kc, d_info, s);
+    if (!rc && nr2 > b2)
+      rc = gemm_impl(mode, -1.0, l21_rest, transposed(l21_top), 1.0, subview(a, r2 + b2, nr2 - b2, r2, b2), 0, kc,
+                     d_info, s);
+    if (rc) break;
+    // (2) next panel on the side stream once (1) has landed
+    cudaEventRecord(ev_main, s);
+    cudaStreamWaitEvent(ps, ev_main, 0);
+    rc = panel(r2, b2, ps);
+    if (rc) break;
+    cudaEventRecord(ev_panel, ps);
+    // (3) the rest of the trailing update, concurrently with (2).  It belongs
+    // to step k, so a pivot failure inside panel k+1 (index >= base+r2) must
+    // not cancel it: the reference finishes step k before it meets that pivot.
+    if (nr2 > b2)
+      rc = gemm_impl(mode, -1.0, l21_rest, transposed(l21_rest), 1.0, subview(a, r2 + b2, nr2 - b2, r2 + b2, nr2 - b2),
+                     1, kc, d_info, s, base + r2);
+    cudaStreamWaitEvent(s, ev_panel, 0);  // step k+1 needs panel k+1
+    done = r2;
+  }
+  cudaEventDestroy(ev_main);
+  cudaEventDestroy(ev_panel);
+  return rc;
+}
+
 int chol_impl(Mode mode, const bf_view* a, const bf_chol_level* lv, int nl, int* d_info, cudaStream_t s) {
   if (!a || (nl > 0 && !lv)) return fail(BF_ERR_VALUE, "null argument");
   if (a->m != a->n) return fail(BF_ERR_SHAPE, "square matrix required");
   if (nl < 1) return fail(BF_ERR_VALUE, "empty control tree");
+  if (a->n == 0) return BF_OK;
+  if (lv[0].variant == 3 && lv[0].bs >= 1 && a->n > 2 * lv[0].bs && g_lookahead)
+    return chol_v3_lookahead(mode, *a, lv, nl, 0, d_info, s);
   return chol_run(mode, *a, lv, nl, 0, 0, d_info, s);
 }
 
@@ -276,6 +355,18 @@ extern "C" {
 int bf_abi_version(void) { return 1; }
 int64_t bf_launch_count(void) { return bf::g_launches.load(std::memory_order_relaxed); }
 const char* bf_last_error(void) { return g_last_error.c_str(); }
+int bf_set_option(const char* name, int64_t value) {
+  if (name && std::strcmp(name, "lookahead") == 0) {
+    g_lookahead = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "tma") == 0) {
+    bf::g_use_tma = value != 0;
+    return BF_OK;
+  }
+  return fail(BF_ERR_VALUE, "unknown option");
+}
+
 int bf_device_sm_count(void) {
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;

@@ -169,7 +169,7 @@ __device__ __forceinline__ void tile_coords(const GemmParams& p, int64_t bid, bo
 
 template <class Cfg>
 __global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_dmma_kernel(const GemmParams p) {
-  if (p.abort_flag != nullptr && *p.abort_flag >= 0) return;
+  if (aborted(p)) return;
   extern __shared__ __align__(16) double smem[];
   constexpr int BM = Cfg::BM, BN = Cfg::BN, BK = Cfg::BK, STAGES = Cfg::STAGES;
   constexpr int MI = Cfg::MI, NJ = Cfg::NJ;
@@ -309,7 +309,10 @@ static int run_layouts(const GemmParams& p, cudaStream_t s) {
   return run_cfg<DmmaCfg<128, 128, 16, 2, 4, 4, LA, LB>>(p, s);
 }
 
+int g_use_tma = 1;
+
 int launch_gemm_dmma(const GemmParams& p, cudaStream_t s) {
+  if (g_use_tma && gemm_dmma_tma_eligible(p)) return launch_gemm_dmma_tma(p, s);
   const int la = p.a.layout, lb = p.b.layout;
 #define BF_CASE(A, B) \
   if (la == A && lb == B) return run_layouts<A, B>(p, s);

@@ -27,7 +27,7 @@ __device__ __forceinline__ T ld_elem(const OperandMK& op, int64_t mn, int64_t k)
 
 template <typename T, typename Acc>
 __global__ void __launch_bounds__(SB_THREADS) gemm_simt_kernel(const GemmParams p) {
-  if (p.abort_flag != nullptr && *p.abort_flag >= 0) return;
+  if (aborted(p)) return;
   __shared__ Acc sA[2][SB_K][SB_M + 1];
   __shared__ Acc sB[2][SB_K][SB_N + 1];
 

@@ -189,50 +189,155 @@ __global__ void __launch_bounds__(LEAF_THREADS) potrf_leaf_kernel(T* g, int64_t 
   if (tid == 0 && bad >= 0 && d_info != nullptr) *d_info = int(base_index + bad);
 }
 
-// --------------------------------------------------------- TRSM base case --
-// X * tril(T)^T = alpha * B, B is m x n (n <= 32), T n x n; one thread per row.
+// Variant 3 for n <= 128 with every element of the lower triangle owned by
+// one thread in registers for the whole factorization (32 x 16 threads, each
+// holding rows ty+16a and columns tx+32b).  Per pivot k: the owner of (k,k)
+// takes the sqrt, the owners of column k scale it and publish it in shared
+// memory, everyone applies a(i,j) -= a(i,k)*a(j,k).  Each element sees the
+// reference's operations in the reference's order (factor/cholesky.py:74-89).
 template <typename T>
-__global__ void trsm_base_right_kernel(double alpha, const T* t, int64_t toff, int64_t trs, int64_t tcs, T* b,
-                                       int64_t boff, int64_t brs, int64_t bcs, int64_t m, int n,
-                                       int* d_singular, int64_t index_base, const int* abort_flag) {
-  if (abort_flag != nullptr && *abort_flag >= 0) return;
-  __shared__ T st[32][33];
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    int j = e / n, p = e % n;
-    st[j][p] = (p <= j) ? t[toff + j * trs + p * tcs] : T(0);
-  }
+__global__ void __launch_bounds__(512) potrf_leaf_v3_reg_kernel(T* g, int64_t off, int n, int64_t rs, int64_t cs,
+                                                                int64_t base_index, int* d_info) {
+  if (d_info != nullptr && *d_info >= 0) return;
+  __shared__ T colk[128];
+  __shared__ T s_d;
+  __shared__ int s_flag;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  T v[8][4];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, j = tx + 32 * b;
+      v[a][b] = (i < n && j <= i) ? g[off + i * rs + j * cs] : T(0);
+    }
+  if (threadIdx.x == 0) s_flag = -1;
   __syncthreads();
-  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
-  if (i >= m) return;
-  T x[32];
-  T* row = b + boff + i * brs;
-#pragma unroll
-  for (int j = 0; j < 32; ++j)
-    if (j < n) x[j] = row[j * bcs];
-  if (alpha != 1.0) {  // bbuf *= alpha: the product is formed in f64 (alpha is a Python float)
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < n) x[j] = T(Ops<double>::mul(double(x[j]), alpha));
-  }
   int bad = -1;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    if (j < n && bad < 0) {
-      const T d = st[j][j];
-      if (d == T(0)) {
-        bad = j;
-      } else {
-        T acc = x[j];
+  for (int k = 0; k < 128; ++k) {
+    if (k < n) {
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int ka = k >> 4, kb = k >> 5;
+      if (tx == (k & 31) && ty == (k & 15)) {
+        T d = v[ka][kb];
+        if (!(d > T(0))) {
+          s_flag = k;
+        } else {
+          d = Ops<T>::sqrt_(d);
+          v[ka][kb] = d;
+          s_d = d;
+        }
+      }
+      __syncthreads();
+      if (s_flag >= 0) {
+        bad = s_flag;
+        break;
+      }
+      const T d = s_d;
+      if (tx == (k & 31)) {
 #pragma unroll
-        for (int p = 0; p < 32; ++p)
-          if (p < j) acc = Ops<T>::sub(acc, Ops<T>::mul(x[p], st[j][p]));
-        x[j] = Ops<T>::div(acc, d);
+        for (int a = 0; a < 8; ++a) {
+          const int i = ty + 16 * a;
+          if (16 * a + 15 > k && i > k && i < n) {
+            const T x = Ops<T>::div(v[a][kb], d);
+            v[a][kb] = x;
+            colk[i] = x;
+          }
+        }
+      }
+      __syncthreads();
+      T cj[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) cj[b] = (32 * b + 31 > k) ? colk[(tx + 32 * b) & 127] : T(0);
+#pragma unroll
+      for (int a = 0; a < 8; ++a) {
+        if (16 * a + 15 > k) {
+          const int i = ty + 16 * a;
+          const T ci = colk[i & 127];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int j = tx + 32 * b;
+            if (32 * b + 31 > k && 32 * b <= 16 * a + 15 && j > k && i >= j && i < n)
+              v[a][b] = Ops<T>::sub(v[a][b], Ops<T>::mul(ci, cj[b]));
+          }
+        }
       }
     }
   }
 #pragma unroll
-  for (int j = 0; j < 32; ++j)
-    if (j < n) row[j * bcs] = x[j];
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = ty + 16 * a, j = tx + 32 * b;
+      if (i < n && j <= i) g[off + i * rs + j * cs] = v[a][b];
+    }
+  if (threadIdx.x == 0 && bad >= 0 && d_info != nullptr) *d_info = int(base_index + bad);
+}
+
+// --------------------------------------------------------- TRSM base case --
+// X * tril(T)^T = alpha * B, B is m x n (n <= 32), T n x n; one thread per
+// row, the CTA's 128 x n block of B staged through shared memory so global
+// loads and stores are coalesced whatever B's strides are.
+template <typename T>
+__global__ void __launch_bounds__(128) trsm_base_right_kernel(double alpha, const T* t, int64_t toff, int64_t trs,
+                                                              int64_t tcs, T* b, int64_t boff, int64_t brs,
+                                                              int64_t bcs, int64_t m, int n, int* d_singular,
+                                                              int64_t index_base, const int* abort_flag) {
+  if (abort_flag != nullptr && *abort_flag >= 0) return;
+  __shared__ T st[32][33];
+  __shared__ T sb[128][33];
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    int j = e / n, p = e % n;
+    st[j][p] = (p <= j) ? t[toff + j * trs + p * tcs] : T(0);
+  }
+  const int64_t r0 = int64_t(blockIdx.x) * 128;
+  const int rows = int(m - r0 < 128 ? m - r0 : 128);
+  const bool col_fast = (bcs == 1);
+  for (int e = threadIdx.x; e < rows * n; e += blockDim.x) {
+    int r, c;
+    if (col_fast) { r = e / n; c = e % n; } else { c = e / rows; r = e % rows; }
+    sb[r][c] = b[boff + (r0 + r) * brs + c * bcs];
+  }
+  __syncthreads();
+  const int me = threadIdx.x;
+  int bad = -1;
+  if (me < rows) {
+    T x[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < n) x[j] = sb[me][j];
+    if (alpha != 1.0) {  // bbuf *= alpha: the product is formed in f64 (alpha is a Python float)
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < n) x[j] = T(Ops<double>::mul(double(x[j]), alpha));
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j < n && bad < 0) {
+        const T d = st[j][j];
+        if (d == T(0)) {
+          bad = j;
+        } else {
+          T acc = x[j];
+#pragma unroll
+          for (int p = 0; p < 32; ++p)
+            if (p < j) acc = Ops<T>::sub(acc, Ops<T>::mul(x[p], st[j][p]));
+          x[j] = Ops<T>::div(acc, d);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < n) sb[me][j] = x[j];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < rows * n; e += blockDim.x) {
+    int r, c;
+    if (col_fast) { r = e / n; c = e % n; } else { c = e / rows; r = e % rows; }
+    b[boff + (r0 + r) * brs + c * bcs] = sb[r][c];
+  }
   // every row meets the same zero pivot, so the racing stores write one value
   if (bad >= 0 && d_singular != nullptr) *d_singular = int(index_base + bad);
 }
@@ -259,6 +364,11 @@ static constexpr int LEAF_SMEM_LIMIT = 220 * 1024;
 template <typename T>
 static int leaf_launch(T* a, int64_t off, int64_t n, int64_t rs, int64_t cs, int variant, int64_t base_index,
                        int* d_info, cudaStream_t s) {
+  if (variant == 3 && n <= 128) {
+    note_launch();
+    potrf_leaf_v3_reg_kernel<T><<<1, 512, 0, s>>>(a, off, int(n), rs, cs, base_index, d_info);
+    return cudaGetLastError() == cudaSuccess ? 0 : -11;
+  }
   size_t smem = size_t(n) * (n + 1) * sizeof(T) + size_t(n) * sizeof(double);
   if (smem <= size_t(LEAF_SMEM_LIMIT)) {
     static bool attr = false;
@@ -296,7 +406,7 @@ int launch_trsm_base_right(int is_f64, double alpha, const void* t, int64_t toff
                            int64_t index_base, const int* abort_flag, cudaStream_t s) {
   if (m <= 0 || n <= 0) return 0;
   if (n > 32) return -3;
-  const int threads = 128;
+  const int threads = 128;  // == rows per CTA (the kernel's staging tile)
   const int64_t blocks = (m + threads - 1) / threads;
   note_launch();
   if (is_f64)

@@ -24,7 +24,8 @@ using bf::GemmParams;
 using bf::OperandMK;
 
 thread_local std::string g_last_error;
-int g_lookahead = 1;  // bf_set_option("lookahead", 0) restores the plain reference schedule
+int g_lookahead = 1;
+int g_group = 8;  // bf_set_option("group", g): raster group height in tiles  // bf_set_option("lookahead", 0) restores the plain reference schedule
 
 int fail(int code, const char* msg) {
   g_last_error = msg;
@@ -131,7 +132,7 @@ int gemm_impl(Mode mode, double alpha, const bf_view& a, const bf_view& b, doubl
   p.alpha = al;
   p.beta = be;
   p.lower_only = lower_only;
-  p.group = 8;
+  p.group = g_group;
   p.abort_flag = d_abort;
   p.abort_limit = abort_limit;
   int rc = launch_family(mode, p, s);
@@ -362,6 +363,14 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "tma") == 0) {
     bf::g_use_tma = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "group") == 0 && value >= 1) {
+    g_group = int(value);
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "tma_variant") == 0) {
+    bf::g_tma_variant = int(value & 3);
     return BF_OK;
   }
   return fail(BF_ERR_VALUE, "unknown option");

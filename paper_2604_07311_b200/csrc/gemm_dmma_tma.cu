@@ -8,14 +8,13 @@
 //
 //   16 warps, a 4x4 grid of 32x32 DMMA (m8n8k4) tiles over the 128x128 CTA
 //   tile.  Operands arrive by TMA (cp.async.bulk.tensor) in a ring of STAGES
-//   128B-swizzled stages: `full[s]` completes through complete_tx, `empty[s]`
-//   when all 16 warps have read stage s.  Lane 0 of warp 0 is also the
-//   producer: it refills a stage as soon as `empty` says it is free, polling
-//   without blocking and only waiting when the tile it needs next was never
-//   issued.  (A dedicated producer warp would make the CTA 17 warps, which the
-//   register allocator rounds to 20 and caps every thread at 96 registers.)
-//   The warps never meet at a CTA barrier in the main loop, so their drift
-//   hides each other's waits.
+//   128B-swizzled stages; `full[s]` completes through mbarrier complete_tx.
+//   There is no producer warp (a 17th warp would make the register allocator
+//   cap every thread at 96 registers): each warp, when done with stage s,
+//   bumps a shared counter, and the warp that releases it last issues the TMA
+//   refill of s for k tile kt+STAGES right away.  No warp ever waits for a
+//   slower one except through data it actually needs, and the warps never
+//   meet at a CTA barrier in the main loop.
 //
 // Bank conflicts: with SWIZZLE_128B a 128-byte tile row r holds its 16-byte
 // chunk c at c ^ (r & 7).  A fragment load has lanes (g, t) read (row g, k t);
@@ -32,12 +31,9 @@ namespace bf {
 namespace {
 
 constexpr int TM_BM = 128, TM_BN = 128, TM_BK = 16;
-constexpr int TM_STAGES = 6;
 constexpr int TM_CONSUMER_WARPS = 16;
 constexpr int TM_THREADS = TM_CONSUMER_WARPS * 32;
 constexpr int TM_TILE_BYTES = TM_BM * TM_BK * 8;  // 16 KB per operand per stage
-constexpr int TM_STAGE_BYTES = 2 * TM_TILE_BYTES;
-constexpr size_t TM_SMEM = size_t(TM_STAGES) * TM_STAGE_BYTES + 1024 /*align*/ + 2 * TM_STAGES * 8;
 
 __device__ __forceinline__ int perm8(int g) { return g < 4 ? 2 * g : 2 * (g - 4) + 1; }
 
@@ -124,162 +120,227 @@ __device__ __forceinline__ void tile_coords_tma(const GemmParams& p, int64_t bid
   }
 }
 
+__device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+// Persistent CTA: tiles blockIdx.x, +gridDim.x, ... share one ring of stages,
+// so the TMA for the next tile's first k tiles is in flight while this
+// tile's fold is written back.  MMAK = 4 (m8n8k4) or 8 (m16n8k8); KBOX =
+// 16-wide k boxes per stage.
+template <int MMAK, int KBOX, int STAGES>
 __global__ void __launch_bounds__(TM_THREADS, 1)
     gemm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                          const GemmParams p) {
   if (aborted(p)) return;
+  constexpr int BKS = 16 * KBOX;                    // k per stage
+  constexpr int OP_BYTES = KBOX * TM_TILE_BYTES;    // one operand, one stage
+  constexpr int STAGE_BYTES = 2 * OP_BYTES;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t tiles = (raw + 1023u) & ~1023u;  // SWIZZLE_128B wants 1 KB alignment
-  const uint32_t bars = tiles + TM_STAGES * TM_STAGE_BYTES;
+  const uint32_t bars = tiles + STAGES * STAGE_BYTES;
   auto full = [&](int s) { return bars + 8u * s; };
-  auto empty = [&](int s) { return bars + 8u * (TM_STAGES + s); };
-
-  const bool tri = p.lower_only != 0;
-  int64_t ti, tj;
-  tile_coords_tma(p, blockIdx.x, tri, ti, tj);
-  const int64_t m0 = ti * TM_BM, n0 = tj * TM_BN;
-  if (p.lower_only) {
-    int64_t row_hi = (m0 + TM_BM < p.m ? m0 + TM_BM : p.m) - 1;
-    if (row_hi < n0) return;
-  }
+  __shared__ int released[STAGES];
+  // (ti, tj) of every tile this CTA owns, packed ti<<16 | tj, so a refill
+  // (issued by whichever warp releases a stage last) costs one LDS
+  uint32_t* tile_tab = reinterpret_cast<uint32_t*>(smem_raw + (bars + 8u * STAGES - raw));
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  const bool tri = p.lower_only != 0;
+  const int64_t ntile_all = p.num_tiles;
+  const int64_t G = gridDim.x;
+  const int W = int((ntile_all - blockIdx.x + G - 1) / G);  // tiles of this CTA
+  for (int w = tid; w < W; w += TM_THREADS) {
+    int64_t ti, tj;
+    tile_coords_tma(p, blockIdx.x + int64_t(w) * G, tri, ti, tj);
+    tile_tab[w] = (uint32_t(ti) << 16) | uint32_t(tj);
+  }
   if (tid == 0) {
-    for (int s = 0; s < TM_STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(full(s), 1);
-      mbar_init(empty(s), TM_CONSUMER_WARPS);
+      released[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  // k segmentation in 32-bit (eligibility guarantees K < 2^31)
+  // k segmentation in 32-bit (eligibility guarantees K < 2^31, kc % BKS == 0 or kc >= K)
   const int K = int(p.k);
   const int kc = p.kc < p.k ? int(p.kc) : K;
   const int nseg = (K + kc - 1) / kc;
-  const int tps = (kc + TM_BK - 1) / TM_BK;
+  const int tps = (kc + BKS - 1) / BKS;
   const int last_len = K - (nseg - 1) * kc;
-  const int tps_last = (last_len + TM_BK - 1) / TM_BK;
-  const int ntiles = (nseg - 1) * tps + tps_last;
+  const int tps_last = (last_len + BKS - 1) / BKS;
+  const int ntiles = (nseg - 1) * tps + tps_last;  // k tiles per output tile
+  const int F = W * ntiles;                         // stage fills of this CTA
 
-  // ---------------- producer (warp 0, lane 0) ----------------
-  const bool producer = (tid == 0);
-  int next_fill = 0;
   auto issue = [&](int f) {
-    const int st = f % TM_STAGES;
-    const int seg = f / tps, sub = f - seg * tps;
-    const int k_lo = seg * kc + sub * TM_BK;
-    const uint32_t sa = tiles + st * TM_STAGE_BYTES;
-    mbar_expect_tx(full(st), TM_STAGE_BYTES);
-    tma_load_2d(sa, &tma_a, k_lo, int(m0), full(st));
-    tma_load_2d(sa + TM_TILE_BYTES, &tma_b, k_lo, int(n0), full(st));
-  };
-  // Refill stages whose previous tile every warp has released; block only if
-  // tile `need` itself has not been issued yet.
-  auto refill = [&](int need) {
-    while (next_fill < ntiles) {
-      const int st = next_fill % TM_STAGES;
-      const int round = next_fill / TM_STAGES;
-      if (round > 0) {
-        const uint32_t par = uint32_t((round - 1) & 1);
-        if (next_fill <= need)
-          mbar_wait(empty(st), par);
-        else if (!mbar_test(empty(st), par))
-          break;
-      }
-      issue(next_fill);
-      ++next_fill;
+    const int w = f / ntiles, kt = f - w * ntiles;
+    const uint32_t tt = tile_tab[w];
+    const int ti = int(tt >> 16), tj = int(tt & 0xffffu);
+    const int st = f % STAGES;
+    const int seg = kt / tps, sub = kt - seg * tps;
+    const int k_lo = seg * kc + sub * BKS;
+    const uint32_t sa = tiles + st * STAGE_BYTES;
+    mbar_expect_tx(full(st), STAGE_BYTES);
+#pragma unroll
+    for (int b = 0; b < KBOX; ++b) {
+      tma_load_2d(sa + b * TM_TILE_BYTES, &tma_a, k_lo + 16 * b, int(ti * TM_BM), full(st));
+      tma_load_2d(sa + OP_BYTES + b * TM_TILE_BYTES, &tma_b, k_lo + 16 * b, int(tj * TM_BN), full(st));
     }
   };
-  if (producer) {
+  if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
-    for (; next_fill < ntiles && next_fill < TM_STAGES; ++next_fill) issue(next_fill);
+    for (int f = 0; f < F && f < STAGES; ++f) issue(f);
   }
 
-  // ---------------- consumers ----------------
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;
   const int pg = perm8(g);
-  // byte offsets inside a stage tile
   const uint32_t a_row = uint32_t((wm * 32 + pg) * 128);
   const uint32_t b_row = uint32_t((wn * 32 + pg) * 128);
-  uint32_t koff[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) koff[q] = uint32_t(((((q * 4 + t) >> 1) ^ pg) << 4) | ((t & 1) << 3));
+  // swizzled byte offset of k (0..15) inside a 128-byte row of this thread's rows
+  auto koff = [&](int k) -> uint32_t { return uint32_t((((k >> 1) ^ pg) << 4) | ((k & 1) << 3)); };
+  const int pj[2] = {perm8(2 * t), perm8(2 * t + 1)};
+  double* C = static_cast<double*>(p.c);
 
-  double acc[4][4][2];
+  constexpr int MI = MMAK == 4 ? 4 : 2;  // row fragments per warp (8 or 16 rows each)
+  double acc[4][4][2];                    // 32 accumulators in either shape
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  double* C = static_cast<double*>(p.c);
-  const int pj[2] = {perm8(2 * t), perm8(2 * t + 1)};  // epilogue column permutation
-
-  int s = 0, round = 0, seg = 0, sub = 0;
-  for (int kt = 0; kt < ntiles; ++kt) {
-    if (producer && next_fill <= kt) refill(kt);
-    mbar_wait(full(s), uint32_t(round & 1));
-    const uint32_t sa = tiles + s * TM_STAGE_BYTES;
-    const uint32_t sb = sa + TM_TILE_BYTES;
-    // fragments double-buffered by hand to bound register pressure
-    double af[2][4], bfr[2][4];
+  int s = 0, round = 0, f = 0;
+  for (int w = 0; w < W; ++w) {
+    const uint32_t tt = tile_tab[w];
+    const int64_t m0 = int64_t(tt >> 16) * TM_BM, n0 = int64_t(tt & 0xffffu) * TM_BN;
+    int seg = 0, sub = 0;
+    for (int kt = 0; kt < ntiles; ++kt, ++f) {
+      mbar_wait(full(s), uint32_t(round & 1));
+      const uint32_t sa = tiles + s * STAGE_BYTES;
+      const uint32_t sb = sa + OP_BYTES;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) af[0][i] = lds64(sa + a_row + i * 1024 + koff[0]);
+      for (int bx = 0; bx < KBOX; ++bx) {
+        const uint32_t ab = sa + bx * TM_TILE_BYTES + a_row;
+        const uint32_t bb = sb + bx * TM_TILE_BYTES + b_row;
+        if constexpr (MMAK == 4) {
+          double af[2][4], bfr[2][4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) bfr[0][j] = lds64(sb + b_row + j * 1024 + koff[0]);
+          for (int i = 0; i < 4; ++i) af[0][i] = lds64(ab + i * 1024 + koff(t));
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int cur = q & 1;
-      if (q < 3) {
+          for (int j = 0; j < 4; ++j) bfr[0][j] = lds64(bb + j * 1024 + koff(t));
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[cur ^ 1][i] = lds64(sa + a_row + i * 1024 + koff[q + 1]);
+          for (int q = 0; q < 4; ++q) {
+            const int cur = q & 1;
+            if (q < 3) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bfr[cur ^ 1][j] = lds64(sb + b_row + j * 1024 + koff[q + 1]);
-      }
+              for (int i = 0; i < 4; ++i) af[cur ^ 1][i] = lds64(ab + i * 1024 + koff(4 * (q + 1) + t));
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cur][i], bfr[cur][j]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty(s));
-    if (producer) refill(-1);
-
-    const bool seg_done = (seg < nseg - 1) ? (sub == tps - 1) : (sub == tps_last - 1);
-    if (seg_done) {
-      const double beta_eff = seg == 0 ? p.beta : 1.0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int64_t gi = m0 + wm * 32 + i * 8 + pg;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
-            if (gi < p.m && gj < p.n && (!p.lower_only || gi >= gj)) {
-              const int64_t addr = p.c_off + gi * p.c_rs + gj * p.c_cs;
-              double v = __dmul_rn(p.alpha, acc[i][j][h]);
-              if (beta_eff != 0.0) v = __dadd_rn(__dmul_rn(beta_eff, C[addr]), v);
-              C[addr] = v;
+              for (int j = 0; j < 4; ++j) bfr[cur ^ 1][j] = lds64(bb + j * 1024 + koff(4 * (q + 1) + t));
             }
-            acc[i][j][h] = 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[cur][i], bfr[cur][j]);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {  // two k8 steps per 16-wide box
+            double af[2][4], bfr[4][2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              af[i][0] = lds64(ab + i * 2048 + koff(8 * q + t));
+              af[i][1] = lds64(ab + i * 2048 + 1024 + koff(8 * q + t));
+              af[i][2] = lds64(ab + i * 2048 + koff(8 * q + t + 4));
+              af[i][3] = lds64(ab + i * 2048 + 1024 + koff(8 * q + t + 4));
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              bfr[j][0] = lds64(bb + j * 1024 + koff(8 * q + t));
+              bfr[j][1] = lds64(bb + j * 1024 + koff(8 * q + t + 4));
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                double (&c)[4] = *reinterpret_cast<double (*)[4]>(&acc[2 * i][j][0]);
+                // acc[2i][j] holds rows pg (c0,c1); acc[2i+1][j] rows 8+pg (c2,c3)
+                double cc[4] = {acc[2 * i][j][0], acc[2 * i][j][1], acc[2 * i + 1][j][0], acc[2 * i + 1][j][1]};
+                (void)c;
+                dmma_16x8x8(cc, af[i], bfr[j]);
+                acc[2 * i][j][0] = cc[0];
+                acc[2 * i][j][1] = cc[1];
+                acc[2 * i + 1][j][0] = cc[2];
+                acc[2 * i + 1][j][1] = cc[3];
+              }
           }
         }
       }
-    }
-    if (++s == TM_STAGES) {
-      s = 0;
-      ++round;
-    }
-    if (++sub == (seg < nseg - 1 ? tps : tps_last)) {
-      sub = 0;
-      ++seg;
+      __syncwarp();
+      if (lane == 0) {
+        // release stage s; the last warp out refills it (generic reads ordered
+        // before the async-proxy TMA write by the fences)
+        __threadfence_block();
+        const int c = atomicAdd(&released[s], 1);
+        if (c == TM_CONSUMER_WARPS - 1) {
+          released[s] = 0;
+          if (f + STAGES < F) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            issue(f + STAGES);
+          }
+        }
+      }
+      if (++s == STAGES) {
+        s = 0;
+        ++round;
+      }
+      if (kt == ntiles - 4 || (ntiles < 4 && kt == 0)) {
+        // warm L2 with this warp's 32x32 block of C before the fold reads it
+        const int64_t r = m0 + wm * 32 + lane, c0 = n0 + wn * 32;
+        if (r < p.m && c0 < p.n) {
+          const double* rowp = C + p.c_off + r * p.c_rs + c0 * p.c_cs;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp));
+          if (p.c_cs == 1 && c0 + 16 < p.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + 16));
+        }
+      }
+      const bool seg_done = (seg < nseg - 1) ? (sub == tps - 1) : (sub == tps_last - 1);
+      if (seg_done) {
+        const double beta_eff = seg == 0 ? p.beta : 1.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          // m8n8k4: fragment i covers rows 8i..8i+7; m16n8k8: acc[2i'] / acc[2i'+1]
+          // are rows 16i'+pg and 16i'+8+pg, i.e. again 8i+pg.
+          const int64_t gi = m0 + wm * 32 + i * 8 + pg;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
+              if (gi < p.m && gj < p.n && (!p.lower_only || gi >= gj)) {
+                const int64_t addr = p.c_off + gi * p.c_rs + gj * p.c_cs;
+                double v = __dmul_rn(p.alpha, acc[i][j][h]);
+                if (beta_eff != 0.0) v = __dadd_rn(__dmul_rn(beta_eff, C[addr]), v);
+                C[addr] = v;
+              }
+              acc[i][j][h] = 0.0;
+            }
+          }
+        }
+      }
+      if (++sub == (seg < nseg - 1 ? tps : tps_last)) {
+        sub = 0;
+        ++seg;
+      }
     }
   }
+  (void)MI;
 }
 
 // ---- host side -------------------------------------------------------------
@@ -332,14 +393,40 @@ bool gemm_dmma_tma_eligible(const GemmParams& p) {
   return encoder() != nullptr;
 }
 
-int launch_gemm_dmma_tma(const GemmParams& p_in, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(gemm_dmma_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TM_SMEM)) !=
-        cudaSuccess)
-      return -10;
-    attr = true;
+int g_tma_variant = 0;  // 0: m8n8k4/1 box/6 stages, 1: m16n8k8/1/6, 2: m8n8k4/2 boxes/3, 3: m16n8k8/2/3
+
+template <int MMAK, int KBOX, int STAGES>
+static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t s) {
+  static size_t attr_smem = 0;
+  constexpr size_t base_smem = size_t(STAGES) * 2 * KBOX * TM_TILE_BYTES + 1024 + 8 * STAGES;
+  constexpr size_t max_smem = 200 * 1024;  // leaves room for the static __shared__ words
+  auto kern = gemm_dmma_tma_kernel<MMAK, KBOX, STAGES>;
+  GemmParams p = p_in;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
+  int64_t grid = p.num_tiles < sms ? p.num_tiles : sms;
+  // tile table: one u32 per tile of the busiest CTA; widen the grid if the
+  // table would not fit (only for astronomically many tiles)
+  while ((p.num_tiles + grid - 1) / grid * 4 + base_smem > max_smem) grid *= 2;
+  if (p.m >= (1 << 16) * int64_t(TM_BM) || p.n >= (1 << 16) * int64_t(TM_BN)) return -3;
+  const size_t smem = base_smem + size_t((p.num_tiles + grid - 1) / grid) * 4;
+  if (smem > attr_smem) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
+      cudaGetLastError();
+      return -10;
+    }
+    attr_smem = smem;
+  }
+  note_launch();
+  kern<<<unsigned(grid), TM_THREADS, smem, s>>>(ma, mb, p);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+int launch_gemm_dmma_tma(const GemmParams& p_in, cudaStream_t s) {
   GemmParams p = p_in;
   CUtensorMap ma, mb;
   if (!make_map(&ma, p.a, p.m, p.k) || !make_map(&mb, p.b, p.n, p.k)) return -3;
@@ -349,9 +436,13 @@ int launch_gemm_dmma_tma(const GemmParams& p_in, cudaStream_t s) {
   p.num_tiles = p.lower_only ? int64_t(p.tiles_m) * (p.tiles_m + 1) / 2 : int64_t(p.tiles_m) * p.tiles_n;
   if (p.num_tiles <= 0) return 0;
   if (p.num_tiles > 0x7fffffffLL) return -3;
-  note_launch();
-  gemm_dmma_tma_kernel<<<unsigned(p.num_tiles), TM_THREADS, TM_SMEM, s>>>(ma, mb, p);
-  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+  const bool two_box_ok = (p.kc % 32 == 0) || p.kc >= p.k;
+  switch (two_box_ok ? g_tma_variant : (g_tma_variant & 1)) {
+    case 1: return run_tma<8, 1, 6>(p, ma, mb, s);
+    case 2: return run_tma<4, 2, 3>(p, ma, mb, s);
+    case 3: return run_tma<8, 2, 3>(p, ma, mb, s);
+    default: return run_tma<4, 1, 6>(p, ma, mb, s);
+  }
 }
 
 }  // namespace bf

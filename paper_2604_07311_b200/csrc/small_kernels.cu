@@ -189,97 +189,129 @@ __global__ void __launch_bounds__(LEAF_THREADS) potrf_leaf_kernel(T* g, int64_t 
   if (tid == 0 && bad >= 0 && d_info != nullptr) *d_info = int(base_index + bad);
 }
 
-// Variant 3 for n <= 128 with every element of the lower triangle owned by
-// one thread in registers for the whole factorization (32 x 16 threads, each
-// holding rows ty+16a and columns tx+32b).  Per pivot k: the owner of (k,k)
-// takes the sqrt, the owners of column k scale it and publish it in shared
-// memory, everyone applies a(i,j) -= a(i,k)*a(j,k).  Each element sees the
-// reference's operations in the reference's order (factor/cholesky.py:74-89).
+// Variant 3 (right-looking) for n <= 128, blocked in 32-column panels while
+// keeping unblocked3's exact per-element operation sequence: element (i,j)
+// still receives a(i,j) -= a(i,k)*a(j,k) for k = 0..j-1 in ascending order,
+// each product and difference rounded separately, then a(i,j) /= d_j
+// (factor/cholesky.py:74-89).  Only the schedule differs:
+//   (A) panel: 128 threads, thread r owns row p0+r of the 32-column panel in
+//       registers; per pivot: sqrt by the diagonal owner, scale, publish the
+//       top-32 column values, rank-1 update inside the panel (named barrier);
+//   (B) trailing: all 16 warps apply the panel's 32 pivots to the trailing
+//       triangle, each element updated sequentially k = p0..p0+31 from
+//       registers, operands broadcast from shared memory.
+// The whole leaf lives in shared memory (n x (n+1) doubles).
 template <typename T>
-__global__ void __launch_bounds__(512) potrf_leaf_v3_reg_kernel(T* g, int64_t off, int n, int64_t rs, int64_t cs,
+__global__ void __launch_bounds__(512) potrf_leaf_v3_blk_kernel(T* g, int64_t off, int n, int64_t rs, int64_t cs,
                                                                 int64_t base_index, int* d_info) {
   if (d_info != nullptr && *d_info >= 0) return;
-  __shared__ T colk[128];
+  extern __shared__ __align__(16) unsigned char leaf_blk_smem[];
+  T* A = reinterpret_cast<T*>(leaf_blk_smem);  // A[i * LD + j]
+  constexpr int LD = 129;
+  __shared__ T s_col[32];
   __shared__ T s_d;
   __shared__ int s_flag;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  T v[8][4];
-#pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int i = ty + 16 * a, j = tx + 32 * b;
-      v[a][b] = (i < n && j <= i) ? g[off + i * rs + j * cs] : T(0);
-    }
-  if (threadIdx.x == 0) s_flag = -1;
-  __syncthreads();
-  int bad = -1;
-#pragma unroll
-  for (int k = 0; k < 128; ++k) {
-    if (k < n) {
-      constexpr int dummy = 0;
-      (void)dummy;
-      const int ka = k >> 4, kb = k >> 5;
-      if (tx == (k & 31) && ty == (k & 15)) {
-        T d = v[ka][kb];
-        if (!(d > T(0))) {
-          s_flag = k;
-        } else {
-          d = Ops<T>::sqrt_(d);
-          v[ka][kb] = d;
-          s_d = d;
-        }
-      }
-      __syncthreads();
-      if (s_flag >= 0) {
-        bad = s_flag;
-        break;
-      }
-      const T d = s_d;
-      if (tx == (k & 31)) {
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-          const int i = ty + 16 * a;
-          if (16 * a + 15 > k && i > k && i < n) {
-            const T x = Ops<T>::div(v[a][kb], d);
-            v[a][kb] = x;
-            colk[i] = x;
-          }
-        }
-      }
-      __syncthreads();
-      T cj[4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) cj[b] = (32 * b + 31 > k) ? colk[(tx + 32 * b) & 127] : T(0);
-#pragma unroll
-      for (int a = 0; a < 8; ++a) {
-        if (16 * a + 15 > k) {
-          const int i = ty + 16 * a;
-          const T ci = colk[i & 127];
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const int j = tx + 32 * b;
-            if (32 * b + 31 > k && 32 * b <= 16 * a + 15 && j > k && i >= j && i < n)
-              v[a][b] = Ops<T>::sub(v[a][b], Ops<T>::mul(ci, cj[b]));
-          }
-        }
-      }
-    }
+  const int tid = threadIdx.x;
+  for (int e = tid; e < n * n; e += 512) {
+    const int i = e / n, j = e % n;
+    if (j <= i) A[i * LD + j] = g[off + i * rs + j * cs];
   }
+  if (tid == 0) s_flag = -1;
+  __syncthreads();
+
+  for (int p0 = 0; p0 < n; p0 += 32) {
+    const int pw = n - p0 < 32 ? n - p0 : 32;
+    // ---- (A) panel columns [p0, p0+pw), rows [p0, n) ----
+    if (tid < 128) {
+      const int i = p0 + tid;
+      const bool own = i < n;
+      T r[32];
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+      for (int c = 0; c < 32; ++c) r[c] = (own && c < pw && p0 + c <= i) ? A[i * LD + p0 + c] : T(0);
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int i = ty + 16 * a, j = tx + 32 * b;
-      if (i < n && j <= i) g[off + i * rs + j * cs] = v[a][b];
+      for (int kk = 0; kk < 32; ++kk) {
+        if (kk < pw) {
+          const int k = p0 + kk;
+          if (tid == kk) {
+            T d = r[kk];
+            if (!(d > T(0))) {
+              s_flag = k;
+            } else {
+              d = Ops<T>::sqrt_(d);
+              r[kk] = d;
+              s_d = d;
+            }
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (s_flag >= 0) break;
+          const T d = s_d;
+          if (own && i > k) {
+            r[kk] = Ops<T>::div(r[kk], d);
+            if (tid < pw) s_col[tid] = r[kk];
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (own && i > k) {
+            const T x = r[kk];
+#pragma unroll
+            for (int c = kk + 1; c < 32; ++c)
+              if (c < pw && p0 + c <= i) r[c] = Ops<T>::sub(r[c], Ops<T>::mul(x, s_col[c]));
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (own && c < pw && p0 + c <= i) A[i * LD + p0 + c] = r[c];
     }
-  if (threadIdx.x == 0 && bad >= 0 && d_info != nullptr) *d_info = int(base_index + bad);
+    __syncthreads();
+    if (s_flag >= 0) break;
+    // ---- (B) trailing triangle: columns/rows >= q0 ----
+    const int q0 = p0 + pw, m = n - q0;
+    if (m > 0) {
+      const int tx = tid & 31, ty = tid >> 5;  // element (q0+ty+16a, q0+tx+32b)
+      T v[6][3];
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          const int i = ty + 16 * a, j = tx + 32 * b;
+          v[a][b] = (i < m && j <= i) ? A[(q0 + i) * LD + q0 + j] : T(0);
+        }
+#pragma unroll 4
+      for (int kk = 0; kk < pw; ++kk) {
+        const int k = p0 + kk;
+        T xi[6], xj[3];
+#pragma unroll
+        for (int a = 0; a < 6; ++a) xi[a] = A[((q0 + ty + 16 * a) & 127) * LD + k];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) xj[b] = A[((q0 + tx + 32 * b) & 127) * LD + k];
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            const int i = ty + 16 * a, j = tx + 32 * b;
+            if (16 * a + 15 >= 32 * b && i < m && j <= i) v[a][b] = Ops<T>::sub(v[a][b], Ops<T>::mul(xi[a], xj[b]));
+          }
+      }
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          const int i = ty + 16 * a, j = tx + 32 * b;
+          if (i < m && j <= i) A[(q0 + i) * LD + q0 + j] = v[a][b];
+        }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < n * n; e += 512) {
+    const int i = e / n, j = e % n;
+    if (j <= i) g[off + i * rs + j * cs] = A[i * LD + j];
+  }
+  if (tid == 0 && s_flag >= 0 && d_info != nullptr) *d_info = int(base_index + s_flag);
 }
 
 // --------------------------------------------------------- TRSM base case --
 // X * tril(T)^T = alpha * B, B is m x n (n <= 32), T n x n; one thread per
-// row, the CTA's 128 x n block of B staged through shared memory so global
-// loads and stores are coalesced whatever B's strides are.
+// right-hand-side row held in registers, the triangle in shared memory.
 template <typename T>
 __global__ void __launch_bounds__(128) trsm_base_right_kernel(double alpha, const T* t, int64_t toff, int64_t trs,
                                                               int64_t tcs, T* b, int64_t boff, int64_t brs,
@@ -287,57 +319,39 @@ __global__ void __launch_bounds__(128) trsm_base_right_kernel(double alpha, cons
                                                               int64_t index_base, const int* abort_flag) {
   if (abort_flag != nullptr && *abort_flag >= 0) return;
   __shared__ T st[32][33];
-  __shared__ T sb[128][33];
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
     int j = e / n, p = e % n;
     st[j][p] = (p <= j) ? t[toff + j * trs + p * tcs] : T(0);
   }
-  const int64_t r0 = int64_t(blockIdx.x) * 128;
-  const int rows = int(m - r0 < 128 ? m - r0 : 128);
-  const bool col_fast = (bcs == 1);
-  for (int e = threadIdx.x; e < rows * n; e += blockDim.x) {
-    int r, c;
-    if (col_fast) { r = e / n; c = e % n; } else { c = e / rows; r = e % rows; }
-    sb[r][c] = b[boff + (r0 + r) * brs + c * bcs];
-  }
   __syncthreads();
-  const int me = threadIdx.x;
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= m) return;
+  T x[32];
+  T* row = b + boff + i * brs;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) x[j] = (j < n) ? row[j * bcs] : T(0);
+  if (alpha != 1.0) {  // bbuf *= alpha: the product is formed in f64 (alpha is a Python float)
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = T(Ops<double>::mul(double(x[j]), alpha));
+  }
   int bad = -1;
-  if (me < rows) {
-    T x[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < n) x[j] = sb[me][j];
-    if (alpha != 1.0) {  // bbuf *= alpha: the product is formed in f64 (alpha is a Python float)
+  for (int j = 0; j < 32; ++j) {
+    if (j < n && bad < 0) {
+      const T d = st[j][j];
+      if (d == T(0)) {
+        bad = j;
+      } else {
+        T acc = x[j];
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < n) x[j] = T(Ops<double>::mul(double(x[j]), alpha));
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (j < n && bad < 0) {
-        const T d = st[j][j];
-        if (d == T(0)) {
-          bad = j;
-        } else {
-          T acc = x[j];
-#pragma unroll
-          for (int p = 0; p < 32; ++p)
-            if (p < j) acc = Ops<T>::sub(acc, Ops<T>::mul(x[p], st[j][p]));
-          x[j] = Ops<T>::div(acc, d);
-        }
+        for (int p = 0; p < j; ++p) acc = Ops<T>::sub(acc, Ops<T>::mul(x[p], st[j][p]));
+        x[j] = Ops<T>::div(acc, d);
       }
     }
+  }
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < n) sb[me][j] = x[j];
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < rows * n; e += blockDim.x) {
-    int r, c;
-    if (col_fast) { r = e / n; c = e % n; } else { c = e / rows; r = e % rows; }
-    b[boff + (r0 + r) * brs + c * bcs] = sb[r][c];
-  }
+  for (int j = 0; j < 32; ++j)
+    if (j < n) row[j * bcs] = x[j];
   // every row meets the same zero pivot, so the racing stores write one value
   if (bad >= 0 && d_singular != nullptr) *d_singular = int(index_base + bad);
 }
@@ -365,8 +379,16 @@ template <typename T>
 static int leaf_launch(T* a, int64_t off, int64_t n, int64_t rs, int64_t cs, int variant, int64_t base_index,
                        int* d_info, cudaStream_t s) {
   if (variant == 3 && n <= 128) {
+    static bool blk_attr = false;
+    const size_t smem = size_t(128) * 129 * sizeof(T);  // full tile: the trailing loop reads rows < 128 unguarded
+    if (!blk_attr) {
+      if (cudaFuncSetAttribute(potrf_leaf_v3_blk_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(128 * 129 * sizeof(T))) != cudaSuccess)
+        return -10;
+      blk_attr = true;
+    }
     note_launch();
-    potrf_leaf_v3_reg_kernel<T><<<1, 512, 0, s>>>(a, off, int(n), rs, cs, base_index, d_info);
+    potrf_leaf_v3_blk_kernel<T><<<1, 512, smem, s>>>(a, off, int(n), rs, cs, base_index, d_info);
     return cudaGetLastError() == cudaSuccess ? 0 : -11;
   }
   size_t smem = size_t(n) * (n + 1) * sizeof(T) + size_t(n) * sizeof(double);

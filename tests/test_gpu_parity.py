@@ -151,3 +151,31 @@ def test_cholesky_bench_size_residual(cuda):
     r = a0 @ x - L @ (L.T @ x)
     rel = (r.norm() / (a0.norm() * x.norm())).item()
     assert rel <= 10 * n * np.finfo(np.float64).eps / n  # far inside 10*n*eps
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+def test_tma_kernel_variants_bitwise(cuda, variant):
+    """Every TMA mainloop variant (m8n8k4 / m16n8k8, 1 or 2 k boxes per stage)
+    must give the oracle's bits on SYRK and on a full factorization."""
+    from paper_2604_07311_b200.engine import _lib
+
+    lib = _lib.lib()
+    lib.bf_set_option(b"tma_variant", variant)
+    try:
+        a0 = spd_int(4242 + variant, 1500)
+        tree = ('{"op":"cholesky","variant":3,"bs":384,"kernel":{"kc":128},"child":{"op":"cholesky",'
+                '"variant":3,"bs":64,"child":{"op":"cholesky","variant":"unblocked3"}}}')
+        assert digest(chol_gpu(a0, tree)) == digest(chol_oracle(a0, tree))
+        rng = np.random.default_rng(variant)
+        n, k = 1000, 512
+        a = rng.uniform(-1, 1, (n, k))
+        c0 = rng.uniform(-1, 1, (n, n))
+        va, vc = make_view(n, k, fill=a), make_view(n, n, fill=c0)
+        cfg = KernelConfig(8, 6, 64, 256, 2048, F64, F64)
+        bf.syrk_lower(-0.5, va, 2.0, vc, cfg=cfg)
+        cst = c0.reshape(-1).copy()
+        O.syrk(-0.5, (a.reshape(-1).copy(), {"off": 0, "m": n, "n": k, "rs": k, "cs": 1}), 2.0,
+               (cst, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1}), kc=256)
+        assert digest(vc.storage.cpu().numpy()) == digest(cst)
+    finally:
+        lib.bf_set_option(b"tma_variant", 0)

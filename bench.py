@@ -203,6 +203,7 @@ def main() -> int:
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--tiles-per-cta", type=int, default=None, help="library option (tuning)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -238,6 +239,8 @@ def main() -> int:
     from paper_2604_07311_b200.control import parse_tree
     from paper_2604_07311_b200.engine import _lib
 
+    if args.tiles_per_cta is not None:
+        _lib.lib().bf_set_option(b"tiles_per_cta", args.tiles_per_cta)
     if world > 1:
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)

@@ -47,6 +47,7 @@ struct GemmParams {
   int lower_only;
   int tiles_m, tiles_n;
   int group;              // raster group height in tiles
+  int tiles_per_cta;      // TMA kernel: contiguous raster tiles per CTA
   int64_t num_tiles;
   const int* abort_flag;  // skip all work when non-null and 0 <= *abort_flag < abort_limit
   int64_t abort_limit;    // a failure at a pivot >= abort_limit happened "later" in the
@@ -69,7 +70,8 @@ int launch_gemm_dmma(const GemmParams& p, cudaStream_t s);            // f64 sto
 bool gemm_dmma_tma_eligible(const GemmParams& p);                     // TMA/mbarrier fast path?
 int launch_gemm_dmma_tma(const GemmParams& p, cudaStream_t s);
 extern int g_use_tma;                                                 // bf_set_option("tma", 0|1)
-extern int g_tma_variant;                                             // bf_set_option("tma_variant", 0..3)
+extern int g_tma_variant;
+extern int g_tiles_per_cta;                                           // bf_set_option("tiles_per_cta", t)                                             // bf_set_option("tma_variant", 0..3)
 int launch_gemm_simt_f32(const GemmParams& p, cudaStream_t s);        // f32 storage, f32 acc
 int launch_gemm_simt_f32acc64(const GemmParams& p, cudaStream_t s);   // f32 storage, f64 acc
 int launch_scale(int is_f64, double beta, void* c, int64_t off, int64_t m, int64_t n, int64_t rs,

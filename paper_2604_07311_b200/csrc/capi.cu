@@ -365,6 +365,10 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_use_tma = value != 0;
     return BF_OK;
   }
+  if (name && std::strcmp(name, "tiles_per_cta") == 0 && value >= 0) {
+    bf::g_tiles_per_cta = int(value);
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "group") == 0 && value >= 1) {
     g_group = int(value);
     return BF_OK;

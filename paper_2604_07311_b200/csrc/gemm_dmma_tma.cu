@@ -152,12 +152,15 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const bool tri = p.lower_only != 0;
-  const int64_t ntile_all = p.num_tiles;
-  const int64_t G = gridDim.x;
-  const int W = int((ntile_all - blockIdx.x + G - 1) / G);  // tiles of this CTA
+  // Each CTA owns a contiguous run of `tiles_per_cta` raster positions: long
+  // enough to overlap a tile's fold with the next tile's first loads, short
+  // enough that CTAs retire every few hundred microseconds and the
+  // high-priority panel stream of the Cholesky lookahead gets SMs promptly.
+  const int64_t first_tile = int64_t(blockIdx.x) * p.tiles_per_cta;
+  const int W = int(p.num_tiles - first_tile < p.tiles_per_cta ? p.num_tiles - first_tile : p.tiles_per_cta);
   for (int w = tid; w < W; w += TM_THREADS) {
     int64_t ti, tj;
-    tile_coords_tma(p, blockIdx.x + int64_t(w) * G, tri, ti, tj);
+    tile_coords_tma(p, first_tile + w, tri, ti, tj);
     tile_tab[w] = (uint32_t(ti) << 16) | uint32_t(tj);
   }
   if (tid == 0) {
@@ -393,7 +396,8 @@ bool gemm_dmma_tma_eligible(const GemmParams& p) {
   return encoder() != nullptr;
 }
 
-int g_tma_variant = 0;  // 0: m8n8k4/1 box/6 stages, 1: m16n8k8/1/6, 2: m8n8k4/2 boxes/3, 3: m16n8k8/2/3
+int g_tiles_per_cta = 1;
+int g_tma_variant = 2;  // 0: m8n8k4/1 box/6 stages, 1: m16n8k8/1/6, 2: m8n8k4/2 boxes/3, 3: m16n8k8/2/3
 
 template <int MMAK, int KBOX, int STAGES>
 static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t s) {
@@ -408,12 +412,15 @@ static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensor
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  int64_t grid = p.num_tiles < sms ? p.num_tiles : sms;
-  // tile table: one u32 per tile of the busiest CTA; widen the grid if the
-  // table would not fit (only for astronomically many tiles)
-  while ((p.num_tiles + grid - 1) / grid * 4 + base_smem > max_smem) grid *= 2;
+  // tiles per CTA: g_tiles_per_cta (0 = fully persistent, one CTA per SM)
+  int64_t tpc = g_tiles_per_cta > 0 ? g_tiles_per_cta : (p.num_tiles + sms - 1) / sms;
+  while (tpc * 4 + base_smem > max_smem) tpc /= 2;  // the tile table must fit
+  if (tpc < 1) tpc = 1;
+  p.tiles_per_cta = int(tpc);
+  const int64_t grid = (p.num_tiles + tpc - 1) / tpc;
+  if (grid > 0x7fffffffLL) return -3;
   if (p.m >= (1 << 16) * int64_t(TM_BM) || p.n >= (1 << 16) * int64_t(TM_BN)) return -3;
-  const size_t smem = base_smem + size_t((p.num_tiles + grid - 1) / grid) * 4;
+  const size_t smem = base_smem + size_t(tpc) * 4;
   if (smem > attr_smem) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
       cudaGetLastError();

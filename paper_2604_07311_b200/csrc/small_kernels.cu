@@ -263,10 +263,12 @@ __global__ void __launch_bounds__(512) potrf_leaf_v3_blk_kernel(T* g, int64_t of
         if (own && c < pw && p0 + c <= i) A[i * LD + p0 + c] = r[c];
     }
     __syncthreads();
-    if (s_flag >= 0) break;
+    // A failed pivot k stops the reference after steps < k have updated the
+    // whole trailing triangle, so the trailing pass still applies p0..k-1.
+    const int kend = s_flag >= 0 ? s_flag - p0 : pw;
     // ---- (B) trailing triangle: columns/rows >= q0 ----
     const int q0 = p0 + pw, m = n - q0;
-    if (m > 0) {
+    if (m > 0 && kend > 0) {
       const int tx = tid & 31, ty = tid >> 5;  // element (q0+ty+16a, q0+tx+32b)
       T v[6][3];
 #pragma unroll
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(512) potrf_leaf_v3_blk_kernel(T* g, int64_t of
           v[a][b] = (i < m && j <= i) ? A[(q0 + i) * LD + q0 + j] : T(0);
         }
 #pragma unroll 4
-      for (int kk = 0; kk < pw; ++kk) {
+      for (int kk = 0; kk < kend; ++kk) {
         const int k = p0 + kk;
         T xi[6], xj[3];
 #pragma unroll
@@ -301,6 +303,7 @@ __global__ void __launch_bounds__(512) potrf_leaf_v3_blk_kernel(T* g, int64_t of
         }
     }
     __syncthreads();
+    if (s_flag >= 0) break;
   }
   for (int e = tid; e < n * n; e += 512) {
     const int i = e / n, j = e % n;

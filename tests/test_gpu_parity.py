@@ -178,4 +178,4 @@ def test_tma_kernel_variants_bitwise(cuda, variant):
                (cst, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1}), kc=256)
         assert digest(vc.storage.cpu().numpy()) == digest(cst)
     finally:
-        lib.bf_set_option(b"tma_variant", 0)
+        lib.bf_set_option(b"tma_variant", 2)

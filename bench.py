@@ -43,7 +43,7 @@ sys.path.insert(0, str(ROOT))
 
 N_DEFAULT = 32768
 GPU_TREE = {
-    "op": "cholesky", "variant": 3, "bs": 1024, "kernel": {"kc": 1024},
+    "op": "cholesky", "variant": 3, "bs": 2048, "kernel": {"kc": 2048},
     "child": {"op": "cholesky", "variant": 3, "bs": 128, "kernel": {"kc": 128},
               "child": {"op": "cholesky", "variant": "unblocked3"}},
 }

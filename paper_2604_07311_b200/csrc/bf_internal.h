@@ -84,4 +84,8 @@ int launch_trsm_base_right(int is_f64, double alpha, const void* t, int64_t toff
                            int64_t n, int* d_singular, int64_t index_base, const int* abort_flag,
                            cudaStream_t s);
 
+int launch_trsm_small_right(int is_f64, double alpha, const void* t, int64_t toff, int64_t trs, int64_t tcs, void* b,
+                            int64_t boff, int64_t brs, int64_t bcs, int64_t m, int64_t n, int64_t kc,
+                            const int* abort_flag, cudaStream_t s);
+
 }  // namespace bf

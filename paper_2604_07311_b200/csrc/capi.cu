@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 namespace bf {
 static std::atomic<int64_t> g_launches{0};
@@ -25,7 +26,8 @@ using bf::OperandMK;
 
 thread_local std::string g_last_error;
 int g_lookahead = 1;
-int g_group = 8;  // bf_set_option("group", g): raster group height in tiles  // bf_set_option("lookahead", 0) restores the plain reference schedule
+int g_group = 8;
+int g_fused_trsm = 1;  // bf_set_option("fused_trsm", 0) keeps every recursion level a separate launch  // bf_set_option("group", g): raster group height in tiles  // bf_set_option("lookahead", 0) restores the plain reference schedule
 
 int fail(int code, const char* msg) {
   g_last_error = msg;
@@ -145,6 +147,18 @@ int trsm_rec(Mode mode, double alpha, const bf_view& tri, const bf_view& b, int6
              const int* d_abort, cudaStream_t s) {
   const int64_t n = tri.n;
   if (b.m == 0 || n == 0) return BF_OK;
+  // Whole subtrees of order <= 128 run fused (same tree, same operations),
+  // unless a zero pivot must be reported (the standalone trsm entry point).
+  if (n <= 128 && n > 32 && d_sing == nullptr && g_fused_trsm && (mode == MODE_D || mode == MODE_S)) {
+    int rc = bf::launch_trsm_small_right(mode == MODE_D, alpha, tri.base, tri.off, tri.rs,
+                                         tri.cs, b.base, b.off, b.rs, b.cs, b.m, n, kc, d_abort, s);
+    if (rc) {
+      static thread_local std::string msg;
+      msg = std::string("fused trsm launch failed: ") + cudaGetErrorString(cudaPeekAtLastError());
+      return fail(BF_ERR_CUDA, msg.c_str());
+    }
+    return BF_OK;
+  }
   if (n <= 32) {
     int rc = bf::launch_trsm_base_right(storage_is_f64(mode), alpha, tri.base, tri.off, tri.rs, tri.cs, b.base,
                                         b.off, b.rs, b.cs, b.m, n, d_sing, 0, d_abort, s);
@@ -250,6 +264,16 @@ cudaStream_t panel_stream() {
 //   main  : [A(k+1 col block) -= L21 L21_top^T]  ...  [rest of A22 -= L21 L21^T]
 //   panel :                       chol(A11') ; A21' := A21' tril(A11')^-T
 // so the next panel's POTRF+TRSM overlaps the bulk of this step's SYRK.
+// Optional timeline of the lookahead schedule (bf_set_option("timeline", 1)):
+// per step, events after the next-column update, after the rest of the
+// trailing update, and around the panel on the side stream.
+struct TimelineStep {
+  cudaEvent_t main_col, main_rest, panel_begin, panel_end;
+};
+int g_timeline = 0;
+std::vector<TimelineStep> g_tl;
+cudaEvent_t g_tl_origin = nullptr;
+
 int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int64_t base, int* d_info,
                       cudaStream_t s) {
   const int64_t n = a.n, bs = lv[0].bs, kc = lv[0].kc;
@@ -265,6 +289,23 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     if (!rc) rc = trsm_rec(mode, 1.0, a11, a21, kc, nullptr, d_info, st);
     return rc;
   };
+  for (auto& st : g_tl) {
+    cudaEventDestroy(st.main_col);
+    cudaEventDestroy(st.main_rest);
+    cudaEventDestroy(st.panel_begin);
+    cudaEventDestroy(st.panel_end);
+  }
+  g_tl.clear();
+  auto mark = [&](cudaStream_t st) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    return e;
+  };
+  if (g_timeline) {
+    if (g_tl_origin) cudaEventDestroy(g_tl_origin);
+    g_tl_origin = mark(s);
+  }
   int rc = panel(0, bs < n ? bs : n, s);
   for (int64_t done = 0; done < n && rc == BF_OK;) {
     const int64_t b = bs < n - done ? bs : n - done;
@@ -280,11 +321,15 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
       rc = gemm_impl(mode, -1.0, l21_rest, transposed(l21_top), 1.0, subview(a, r2 + b2, nr2 - b2, r2, b2), 0, kc,
                      d_info, s);
     if (rc) break;
+    TimelineStep ts{};
+    if (g_timeline) ts.main_col = mark(s);
     // (2) next panel on the side stream once (1) has landed
     cudaEventRecord(ev_main, s);
     cudaStreamWaitEvent(ps, ev_main, 0);
+    if (g_timeline) ts.panel_begin = mark(ps);
     rc = panel(r2, b2, ps);
     if (rc) break;
+    if (g_timeline) ts.panel_end = mark(ps);
     cudaEventRecord(ev_panel, ps);
     // (3) the rest of the trailing update, concurrently with (2).  It belongs
     // to step k, so a pivot failure inside panel k+1 (index >= base+r2) must
@@ -292,6 +337,10 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     if (nr2 > b2)
       rc = gemm_impl(mode, -1.0, l21_rest, transposed(l21_rest), 1.0, subview(a, r2 + b2, nr2 - b2, r2 + b2, nr2 - b2),
                      1, kc, d_info, s, base + r2);
+    if (g_timeline) {
+      ts.main_rest = mark(s);
+      g_tl.push_back(ts);
+    }
     cudaStreamWaitEvent(s, ev_panel, 0);  // step k+1 needs panel k+1
     done = r2;
   }
@@ -369,6 +418,14 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_tiles_per_cta = int(value);
     return BF_OK;
   }
+  if (name && std::strcmp(name, "timeline") == 0) {
+    g_timeline = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "fused_trsm") == 0) {
+    g_fused_trsm = value != 0;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "group") == 0 && value >= 1) {
     g_group = int(value);
     return BF_OK;
@@ -378,6 +435,23 @@ int bf_set_option(const char* name, int64_t value) {
     return BF_OK;
   }
   return fail(BF_ERR_VALUE, "unknown option");
+}
+
+int bf_timeline(float* out, int max_steps) {
+  // out[4*i + 0..3] = ms from the start to: next-column update done, rest of
+  // the trailing update done, panel start, panel end (step i of the last
+  // lookahead factorization).  Synchronises on the recorded events.
+  int nsteps = int(g_tl.size());
+  if (!out || !g_tl_origin) return nsteps;
+  for (int i = 0; i < nsteps && i < max_steps; ++i) {
+    cudaEvent_t ev[4] = {g_tl[i].main_col, g_tl[i].main_rest, g_tl[i].panel_begin, g_tl[i].panel_end};
+    for (int q = 0; q < 4; ++q) {
+      float ms = -1.f;
+      if (ev[q] && cudaEventSynchronize(ev[q]) == cudaSuccess) cudaEventElapsedTime(&ms, g_tl_origin, ev[q]);
+      out[4 * i + q] = ms;
+    }
+  }
+  return nsteps;
 }
 
 int bf_device_sm_count(void) {

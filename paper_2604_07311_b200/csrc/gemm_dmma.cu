@@ -248,25 +248,33 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_dmma_kernel(const GemmPa
     const int64_t seg = kt / tps, sub = kt - seg * tps;
     const bool seg_done = (seg < nseg - 1) ? (sub == tps - 1) : (sub == tps_last - 1);
     if (seg_done) {
-      // fold the segment into C: C = beta_eff*C + alpha*t  (engine/kernels.py:585-610)
+      // fold the segment into C: C = beta_eff*C + alpha*t  (engine/kernels.py:585-610);
+      // one row fragment at a time, its reads issued before its writes
       const double beta_eff = seg == 0 ? p.beta : 1.0;
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
         const int64_t gi = m0 + wm0 + i * 8 + g;
+        int64_t addr[NJ][2];
+        bool ok[NJ][2];
+        double cold[NJ][2];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) {
+        for (int j = 0; j < NJ; ++j)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int64_t gj = n0 + wn0 + j * 8 + 2 * t + h;
-            if (gi < p.m && gj < p.n && (!p.lower_only || gi >= gj)) {
-              int64_t addr = p.c_rscat ? p.c_rscat[gi] + p.c_cscat[gj] : p.c_off + gi * p.c_rs + gj * p.c_cs;
-              double v = __dmul_rn(p.alpha, acc[i][j][h]);
-              if (beta_eff != 0.0) v = __dadd_rn(__dmul_rn(beta_eff, C[addr]), v);
-              C[addr] = v;
-            }
+            ok[j][h] = gi < p.m && gj < p.n && (!p.lower_only || gi >= gj);
+            addr[j][h] = ok[j][h] ? (p.c_rscat ? p.c_rscat[gi] + p.c_cscat[gj] : p.c_off + gi * p.c_rs + gj * p.c_cs) : 0;
+            cold[j][h] = (ok[j][h] && beta_eff != 0.0) ? __ldcg(C + addr[j][h]) : 0.0;
+          }
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double v = __dmul_rn(p.alpha, acc[i][j][h]);
+            if (beta_eff != 0.0) v = __dadd_rn(__dmul_rn(beta_eff, cold[j][h]), v);
+            if (ok[j][h]) C[addr[j][h]] = v;
             acc[i][j][h] = 0.0;
           }
-        }
       }
     }
   }

@@ -315,25 +315,41 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
       }
       const bool seg_done = (seg < nseg - 1) ? (sub == tps - 1) : (sub == tps_last - 1);
       if (seg_done) {
+        // Fold: C is not __restrict__, so a load-use-store loop would
+        // serialise one L2 round trip per element; instead each half of the
+        // thread's 32 elements has all its reads in flight before its writes.
         const double beta_eff = seg == 0 ? p.beta : 1.0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          // m8n8k4: fragment i covers rows 8i..8i+7; m16n8k8: acc[2i'] / acc[2i'+1]
-          // are rows 16i'+pg and 16i'+8+pg, i.e. again 8i+pg.
-          const int64_t gi = m0 + wm * 32 + i * 8 + pg;
+        for (int half = 0; half < 2; ++half) {
+          double cold[2][4][2];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int ii = 0; ii < 2; ++ii) {
+            // m8n8k4: fragment i covers rows 8i..8i+7; m16n8k8: acc[2i'] / acc[2i'+1]
+            // are rows 16i'+pg and 16i'+8+pg, i.e. again 8i+pg.
+            const int64_t gi = m0 + wm * 32 + (2 * half + ii) * 8 + pg;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
-              if (gi < p.m && gj < p.n && (!p.lower_only || gi >= gj)) {
-                const int64_t addr = p.c_off + gi * p.c_rs + gj * p.c_cs;
-                double v = __dmul_rn(p.alpha, acc[i][j][h]);
-                if (beta_eff != 0.0) v = __dadd_rn(__dmul_rn(beta_eff, C[addr]), v);
-                C[addr] = v;
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
+                const bool ok = gi < p.m && gj < p.n && (!p.lower_only || gi >= gj);
+                cold[ii][j][h] = (ok && beta_eff != 0.0) ? __ldcg(C + p.c_off + gi * p.c_rs + gj * p.c_cs) : 0.0;
               }
-              acc[i][j][h] = 0.0;
-            }
+          }
+#pragma unroll
+          for (int ii = 0; ii < 2; ++ii) {
+            const int i = 2 * half + ii;
+            const int64_t gi = m0 + wm * 32 + i * 8 + pg;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
+                double v = __dmul_rn(p.alpha, acc[i][j][h]);
+                if (beta_eff != 0.0) v = __dadd_rn(__dmul_rn(beta_eff, cold[ii][j][h]), v);
+                if (gi < p.m && gj < p.n && (!p.lower_only || gi >= gj)) C[p.c_off + gi * p.c_rs + gj * p.c_cs] = v;
+                acc[i][j][h] = 0.0;
+              }
           }
         }
       }

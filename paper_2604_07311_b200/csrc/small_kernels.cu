@@ -189,127 +189,120 @@ __global__ void __launch_bounds__(LEAF_THREADS) potrf_leaf_kernel(T* g, int64_t 
   if (tid == 0 && bad >= 0 && d_info != nullptr) *d_info = int(base_index + bad);
 }
 
-// Variant 3 (right-looking) for n <= 128, blocked in 32-column panels while
-// keeping unblocked3's exact per-element operation sequence: element (i,j)
-// still receives a(i,j) -= a(i,k)*a(j,k) for k = 0..j-1 in ascending order,
-// each product and difference rounded separately, then a(i,j) /= d_j
-// (factor/cholesky.py:74-89).  Only the schedule differs:
-//   (A) panel: 128 threads, thread r owns row p0+r of the 32-column panel in
-//       registers; per pivot: sqrt by the diagonal owner, scale, publish the
-//       top-32 column values, rank-1 update inside the panel (named barrier);
-//   (B) trailing: all 16 warps apply the panel's 32 pivots to the trailing
-//       triangle, each element updated sequentially k = p0..p0+31 from
-//       registers, operands broadcast from shared memory.
-// The whole leaf lives in shared memory (n x (n+1) doubles).
+// Variant 3 (right-looking, factor/cholesky.py:74-89) for n <= 128: the
+// block lives in shared memory; 8 warps, warp w updating columns j = w mod 8
+// (lanes over rows).  The pivot is on the critical path, so at step k the
+// warp owning column k+1 updates that column first, then takes the sqrt and
+// scales it in place before turning to its other columns; one barrier per
+// step.  (Register-resident variants with 16 warps lost to issue contention:
+// the arbiter favours high warp ids, so a low-id pivot warp was starved by
+// its neighbours' updates.)  Every element receives the reference's
+// operations in the reference's order; a failing pivot leaves the
+// reference's partial state.
 template <typename T>
-__global__ void __launch_bounds__(512) potrf_leaf_v3_blk_kernel(T* g, int64_t off, int n, int64_t rs, int64_t cs,
-                                                                int64_t base_index, int* d_info) {
+__global__ void __launch_bounds__(256) potrf_leaf_v3_smem_kernel(T* g, int64_t off, int n, int64_t rs, int64_t cs,
+                                                                 int64_t base_index, int* d_info) {
   if (d_info != nullptr && *d_info >= 0) return;
-  extern __shared__ __align__(16) unsigned char leaf_blk_smem[];
-  T* A = reinterpret_cast<T*>(leaf_blk_smem);  // A[i * LD + j]
+  extern __shared__ __align__(16) unsigned char leaf_v3_smem[];
+  T* A = reinterpret_cast<T*>(leaf_v3_smem);
   constexpr int LD = 129;
-  __shared__ T s_col[32];
-  __shared__ T s_d;
   __shared__ int s_flag;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < n * n; e += 512) {
-    const int i = e / n, j = e % n;
-    if (j <= i) A[i * LD + j] = g[off + i * rs + j * cs];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int e = tid; e < n * n; e += 256) {
+    int i, j;
+    if (cs == 1) { i = e / n; j = e % n; } else { j = e / n; i = e % n; }
+    if (j <= i) {
+      if constexpr (sizeof(T) == 8)
+        cp_async_8(&A[i * LD + j], &g[off + i * rs + j * cs], 8);
+      else
+        cp_async_4(&A[i * LD + j], &g[off + i * rs + j * cs], 4);
+    }
   }
+  cp_async_commit();
   if (tid == 0) s_flag = -1;
+  cp_async_wait<0>();
   __syncthreads();
-
-  for (int p0 = 0; p0 < n; p0 += 32) {
-    const int pw = n - p0 < 32 ? n - p0 : 32;
-    // ---- (A) panel columns [p0, p0+pw), rows [p0, n) ----
-    if (tid < 128) {
-      const int i = p0 + tid;
-      const bool own = i < n;
-      T r[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) r[c] = (own && c < pw && p0 + c <= i) ? A[i * LD + p0 + c] : T(0);
-#pragma unroll
-      for (int kk = 0; kk < 32; ++kk) {
-        if (kk < pw) {
-          const int k = p0 + kk;
-          if (tid == kk) {
-            T d = r[kk];
-            if (!(d > T(0))) {
-              s_flag = k;
-            } else {
-              d = Ops<T>::sqrt_(d);
-              r[kk] = d;
-              s_d = d;
-            }
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (s_flag >= 0) break;
-          const T d = s_d;
-          if (own && i > k) {
-            r[kk] = Ops<T>::div(r[kk], d);
-            if (tid < pw) s_col[tid] = r[kk];
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (own && i > k) {
-            const T x = r[kk];
-#pragma unroll
-            for (int c = kk + 1; c < 32; ++c)
-              if (c < pw && p0 + c <= i) r[c] = Ops<T>::sub(r[c], Ops<T>::mul(x, s_col[c]));
-          }
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        if (own && c < pw && p0 + c <= i) A[i * LD + p0 + c] = r[c];
+  // Step k in two barrier-separated halves so every division runs in
+  // parallel (one per thread) and the only serial work per pivot is one
+  // multiply-subtract, a sqrt and a division:
+  //   half 1: the last thread updates (k+1,k+1) and takes its sqrt; thread t
+  //           updates (k+2+t, k+1); all warps update columns j > k+1;
+  //   half 2: thread t scales its element of column k+1.
+  __shared__ T s_d;
+  constexpr int PIV = 255;  // highest warp id: favoured by the issue arbiter
+  if (tid == PIV) {
+    const T diag = A[0];
+    if (!(diag > T(0))) {
+      s_flag = 0;
+    } else {
+      s_d = Ops<T>::sqrt_(diag);
+      A[0] = s_d;
     }
-    __syncthreads();
-    // A failed pivot k stops the reference after steps < k have updated the
-    // whole trailing triangle, so the trailing pass still applies p0..k-1.
-    const int kend = s_flag >= 0 ? s_flag - p0 : pw;
-    // ---- (B) trailing triangle: columns/rows >= q0 ----
-    const int q0 = p0 + pw, m = n - q0;
-    if (m > 0 && kend > 0) {
-      const int tx = tid & 31, ty = tid >> 5;  // element (q0+ty+16a, q0+tx+32b)
-      T v[6][3];
-#pragma unroll
-      for (int a = 0; a < 6; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          const int i = ty + 16 * a, j = tx + 32 * b;
-          v[a][b] = (i < m && j <= i) ? A[(q0 + i) * LD + q0 + j] : T(0);
-        }
-#pragma unroll 4
-      for (int kk = 0; kk < kend; ++kk) {
-        const int k = p0 + kk;
-        T xi[6], xj[3];
-#pragma unroll
-        for (int a = 0; a < 6; ++a) xi[a] = A[((q0 + ty + 16 * a) & 127) * LD + k];
-#pragma unroll
-        for (int b = 0; b < 3; ++b) xj[b] = A[((q0 + tx + 32 * b) & 127) * LD + k];
-#pragma unroll
-        for (int a = 0; a < 6; ++a)
-#pragma unroll
-          for (int b = 0; b < 3; ++b) {
-            const int i = ty + 16 * a, j = tx + 32 * b;
-            if (16 * a + 15 >= 32 * b && i < m && j <= i) v[a][b] = Ops<T>::sub(v[a][b], Ops<T>::mul(xi[a], xj[b]));
-          }
-      }
-#pragma unroll
-      for (int a = 0; a < 6; ++a)
-#pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          const int i = ty + 16 * a, j = tx + 32 * b;
-          if (i < m && j <= i) A[(q0 + i) * LD + q0 + j] = v[a][b];
-        }
-    }
-    __syncthreads();
-    if (s_flag >= 0) break;
   }
-  for (int e = tid; e < n * n; e += 512) {
-    const int i = e / n, j = e % n;
+  __syncthreads();
+  if (s_flag < 0 && tid + 1 < n) A[(tid + 1) * LD] = Ops<T>::div(A[(tid + 1) * LD], s_d);
+  int bad = -1;
+#pragma unroll 1
+  for (int k = 0; k < n; ++k) {
+    __syncthreads();  // column k final (or its pivot failed)
+    if (s_flag >= 0) {
+      bad = s_flag;
+      break;
+    }
+    const int kn = k + 1;
+    if (kn >= n) break;
+    const T akn = A[kn * LD + k];
+    if (tid == PIV) {
+      const T diag = Ops<T>::sub(A[kn * LD + kn], Ops<T>::mul(akn, akn));
+      if (!(diag > T(0))) {
+        A[kn * LD + kn] = diag;
+        s_flag = kn;
+      } else {
+        s_d = Ops<T>::sqrt_(diag);
+        A[kn * LD + kn] = s_d;
+      }
+    }
+    T x = T(0);
+    const int ir = kn + 1 + tid;
+    if (ir < n) x = Ops<T>::sub(A[ir * LD + kn], Ops<T>::mul(A[ir * LD + k], akn));
+    // Columns j = w + 8c > kn, rows i = lane + 32q >= j; rows >= n hold
+    // garbage that is never stored back.  Loads, arithmetic and stores are
+    // separate phases (a fused load-use-store loop serialises on the
+    // may-alias shared-memory dependences).
+    T aik[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) aik[q] = A[(lane + 32 * q) * LD + k];
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) {
+      if (w + 8 * (4 * cb + 3) <= kn) continue;  // whole batch finished (uniform)
+      T val[4][4], ajk[4];
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int j = w + 8 * (4 * cb + cc);
+        ajk[cc] = A[(j & 127) * LD + k];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) val[cc][q] = A[(lane + 32 * q) * LD + (j & 127)];
+      }
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int j = w + 8 * (4 * cb + cc);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int i = lane + 32 * q;
+          if (j > kn && j < n && i >= j) A[i * LD + j] = Ops<T>::sub(val[cc][q], Ops<T>::mul(aik[q], ajk[cc]));
+        }
+      }
+    }
+    __syncthreads();  // s_d / s_flag ready
+    if (ir < n) A[ir * LD + kn] = s_flag >= 0 ? x : Ops<T>::div(x, s_d);
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += 256) {
+    int i, j;
+    if (cs == 1) { i = e / n; j = e % n; } else { j = e / n; i = e % n; }
     if (j <= i) g[off + i * rs + j * cs] = A[i * LD + j];
   }
-  if (tid == 0 && s_flag >= 0 && d_info != nullptr) *d_info = int(base_index + s_flag);
+  if (tid == 0 && bad >= 0 && d_info != nullptr) *d_info = int(base_index + bad);
 }
 
 // --------------------------------------------------------- TRSM base case --
@@ -359,6 +352,187 @@ __global__ void __launch_bounds__(128) trsm_base_right_kernel(double alpha, cons
   if (bad >= 0 && d_singular != nullptr) *d_singular = int(index_base + bad);
 }
 
+// ------------------------------------------------- fused TRSM subtree (n<=128) --
+// The whole recursion of engine/trsm.py:51-68 below a triangle of order
+// n <= 128 in one launch: each CTA owns 64 rows of B (staged in shared memory
+// with the triangle) and walks the same tree — split n//2 until <= 32, solve
+// the left half, fold the right half with gemm(-1, b1, l21^T, alpha, b2) in
+// kc segments (ascending fma chain from +0 per segment, unfused fold with
+// beta = alpha on the first segment, 1 after), recurse on the right half with
+// alpha = 1 — so every element sees the reference's operations in order.
+constexpr int TS_ROWS = 64, TS_THREADS = 256, TS_LD = 129;
+
+template <typename T>
+struct TrsmSmall {
+  T* sb;        // [TS_ROWS][TS_LD]  B rows of this CTA
+  const T* sl;  // [128][TS_LD]      triangle
+  int rows;
+  int64_t kc;
+
+  __device__ void base(int lo, int hi, double alpha) const {
+    const int r = threadIdx.x;
+    if (r >= rows) return;
+    const int n = hi - lo;
+    T x[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = j < n ? sb[r * TS_LD + lo + j] : T(0);
+    if (alpha != 1.0) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] = T(Ops<double>::mul(double(x[j]), alpha));
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (j < n) {
+        T acc = x[j];
+#pragma unroll
+        for (int p = 0; p < j; ++p) acc = Ops<T>::sub(acc, Ops<T>::mul(x[p], sl[(lo + j) * TS_LD + lo + p]));
+        x[j] = Ops<T>::div(acc, sl[(lo + j) * TS_LD + lo + j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < n) sb[r * TS_LD + lo + j] = x[j];
+  }
+
+  // b[:, mid:hi] = beta*b[:, mid:hi] - b[:, lo:mid] * l[mid:hi, lo:mid]^T,
+  // one kc-segmented fma chain per element (gemm_scatter's arithmetic).
+  // 16 x 16 threads, each a 4 x 4 register block: rows tr+16a, cols tc+16b.
+  __device__ void fold(int lo, int mid, int hi, double beta) const {
+    const int K = mid - lo;
+    const int tr = threadIdx.x >> 4, tc = threadIdx.x & 15;
+    bool rok[4], cok[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) rok[a] = tr + 16 * a < rows;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) cok[b] = mid + tc + 16 * b < hi;
+    T c[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        c[a][b] = (rok[a] && cok[b]) ? sb[(tr + 16 * a) * TS_LD + mid + tc + 16 * b] : T(0);
+    for (int k0 = 0, seg = 0; k0 < K; k0 += int(kc), ++seg) {
+      const int k1 = (K - k0) < kc ? K : k0 + int(kc);
+      double t[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) t[a][b] = 0.0;
+      for (int p = lo + k0; p < lo + k1; ++p) {
+        T bv[4], lv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) bv[a] = sb[((tr + 16 * a) & (TS_ROWS - 1)) * TS_LD + p];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) lv[b] = sl[((mid + tc + 16 * b) & 127) * TS_LD + p];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            if constexpr (sizeof(T) == 8)
+              t[a][b] = __fma_rn(bv[a], lv[b], t[a][b]);
+            else  // f32 storage, f32 acc: f32 products summed in f64 (engine/kernels.py:507-522)
+              t[a][b] = __dadd_rn(t[a][b], double(__fmul_rn(bv[a], lv[b])));
+          }
+      }
+      const double be = seg == 0 ? beta : 1.0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if constexpr (sizeof(T) == 8) {
+            double v = __dmul_rn(-1.0, t[a][b]);
+            if (be != 0.0) v = __dadd_rn(__dmul_rn(be, c[a][b]), v);
+            c[a][b] = v;
+          } else {
+            float v = __fmul_rn(-1.0f, float(t[a][b]));
+            if (be != 0.0) v = __fadd_rn(__fmul_rn(float(be), c[a][b]), v);
+            c[a][b] = v;
+          }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (rok[a] && cok[b]) sb[(tr + 16 * a) * TS_LD + mid + tc + 16 * b] = c[a][b];
+  }
+
+  // n <= 64: split once into two <= 32 bases
+  __device__ void solve64(int lo, int hi, double alpha) const {
+    const int n = hi - lo;
+    if (n <= 32) {
+      base(lo, hi, alpha);
+      __syncthreads();
+      return;
+    }
+    const int mid = lo + n / 2;
+    base(lo, mid, alpha);
+    __syncthreads();
+    fold(lo, mid, hi, alpha);
+    __syncthreads();
+    base(mid, hi, 1.0);
+    __syncthreads();
+  }
+  // n <= 128: the reference recursion (engine/trsm.py:51-68) unrolled by hand
+  // (no device-side recursion, so no dynamic stack)
+  __device__ void solve(int lo, int hi, double alpha) const {
+    const int n = hi - lo;
+    if (n <= 64) {
+      solve64(lo, hi, alpha);
+      return;
+    }
+    const int mid = lo + n / 2;
+    solve64(lo, mid, alpha);
+    fold(lo, mid, hi, alpha);
+    __syncthreads();
+    solve64(mid, hi, 1.0);
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(TS_THREADS) trsm_small_right_kernel(double alpha, const T* t, int64_t toff,
+                                                                      int64_t trs, int64_t tcs, T* b, int64_t boff,
+                                                                      int64_t brs, int64_t bcs, int64_t m, int n,
+                                                                      int64_t kc, const int* abort_flag) {
+  if (abort_flag != nullptr && *abort_flag >= 0) return;
+  extern __shared__ __align__(16) unsigned char ts_smem[];
+  T* sl = reinterpret_cast<T*>(ts_smem);
+  T* sb = sl + 128 * TS_LD;
+  const int64_t r0 = int64_t(blockIdx.x) * TS_ROWS;
+  const int rows = int(m - r0 < TS_ROWS ? m - r0 : TS_ROWS);
+  // Stage the triangle and this CTA's rows with asynchronous element copies
+  // (hundreds in flight per thread instead of one dependent load at a time).
+  // The strict upper part of the triangle is copied too but never read.
+  const bool t_col_fast = tcs == 1;
+  for (int e = threadIdx.x; e < n * n; e += TS_THREADS) {
+    int j, p;
+    if (t_col_fast) { j = e / n; p = e % n; } else { p = e / n; j = e % n; }
+    if constexpr (sizeof(T) == 8)
+      cp_async_8(&sl[j * TS_LD + p], &t[toff + j * trs + p * tcs], 8);
+    else
+      cp_async_4(&sl[j * TS_LD + p], &t[toff + j * trs + p * tcs], 4);
+  }
+  const bool col_fast = bcs == 1;
+  for (int e = threadIdx.x; e < rows * n; e += TS_THREADS) {
+    int r, c;
+    if (col_fast) { r = e / n; c = e % n; } else { c = e / rows; r = e % rows; }
+    if constexpr (sizeof(T) == 8)
+      cp_async_8(&sb[r * TS_LD + c], &b[boff + (r0 + r) * brs + c * bcs], 8);
+    else
+      cp_async_4(&sb[r * TS_LD + c], &b[boff + (r0 + r) * brs + c * bcs], 4);
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  TrsmSmall<T> ts{sb, sl, rows, kc};
+  ts.solve(0, n, alpha);
+  for (int e = threadIdx.x; e < rows * n; e += TS_THREADS) {
+    int r, c;
+    if (col_fast) { r = e / n; c = e % n; } else { c = e / rows; r = e % rows; }
+    b[boff + (r0 + r) * brs + c * bcs] = sb[r * TS_LD + c];
+  }
+}
+
 }  // namespace
 
 int launch_scale(int is_f64, double beta, void* c, int64_t off, int64_t m, int64_t n, int64_t rs, int64_t cs,
@@ -382,16 +556,16 @@ template <typename T>
 static int leaf_launch(T* a, int64_t off, int64_t n, int64_t rs, int64_t cs, int variant, int64_t base_index,
                        int* d_info, cudaStream_t s) {
   if (variant == 3 && n <= 128) {
-    static bool blk_attr = false;
-    const size_t smem = size_t(128) * 129 * sizeof(T);  // full tile: the trailing loop reads rows < 128 unguarded
-    if (!blk_attr) {
-      if (cudaFuncSetAttribute(potrf_leaf_v3_blk_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static bool v3_attr = false;
+    const size_t smem = size_t(128) * 129 * sizeof(T);  // full tile: the update reads rows < 128 unguarded
+    if (!v3_attr) {
+      if (cudaFuncSetAttribute(potrf_leaf_v3_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(128 * 129 * sizeof(T))) != cudaSuccess)
         return -10;
-      blk_attr = true;
+      v3_attr = true;
     }
     note_launch();
-    potrf_leaf_v3_blk_kernel<T><<<1, 512, smem, s>>>(a, off, int(n), rs, cs, base_index, d_info);
+    potrf_leaf_v3_smem_kernel<T><<<1, 256, smem, s>>>(a, off, int(n), rs, cs, base_index, d_info);
     return cudaGetLastError() == cudaSuccess ? 0 : -11;
   }
   size_t smem = size_t(n) * (n + 1) * sizeof(T) + size_t(n) * sizeof(double);
@@ -445,4 +619,40 @@ int launch_trsm_base_right(int is_f64, double alpha, const void* t, int64_t toff
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
+}  // namespace bf
+
+namespace bf {
+int launch_trsm_small_right(int is_f64, double alpha, const void* t, int64_t toff, int64_t trs, int64_t tcs, void* b,
+                            int64_t boff, int64_t brs, int64_t bcs, int64_t m, int64_t n, int64_t kc,
+                            const int* abort_flag, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return 0;
+  if (n > 128) return -3;
+  const int64_t blocks = (m + TS_ROWS - 1) / TS_ROWS;
+  if (blocks > 0x7fffffffLL) return -3;
+  note_launch();
+  if (is_f64) {
+    const size_t smem = size_t(128 + TS_ROWS) * TS_LD * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(trsm_small_right_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)) != cudaSuccess)
+        return -10;
+      attr = true;
+    }
+    trsm_small_right_kernel<double><<<unsigned(blocks), TS_THREADS, smem, s>>>(
+        alpha, (const double*)t, toff, trs, tcs, (double*)b, boff, brs, bcs, m, int(n), kc, abort_flag);
+  } else {
+    const size_t smem = size_t(128 + TS_ROWS) * TS_LD * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(trsm_small_right_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem)) != cudaSuccess)
+        return -10;
+      attr = true;
+    }
+    trsm_small_right_kernel<float><<<unsigned(blocks), TS_THREADS, smem, s>>>(
+        alpha, (const float*)t, toff, trs, tcs, (float*)b, boff, brs, bcs, m, int(n), kc, abort_flag);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
 }  // namespace bf

@@ -82,6 +82,7 @@ _SIGNATURES = {
     "bf_last_error": ([], ctypes.c_char_p),
     "bf_device_sm_count": ([], _I),
     "bf_set_option": ([ctypes.c_char_p, _L], _I),
+    "bf_timeline": ([ctypes.POINTER(ctypes.c_float), _I], _I),
     "bf_gemm_d": ([_D, _V, _V, _D, _V, _I, _L, _VP, _VP], _I),
     "bf_gemm_s": ([_D, _V, _V, _D, _V, _I, _L, _VP, _VP], _I),
     "bf_gemm_sd": ([_D, _V, _V, _D, _V, _I, _L, _VP, _VP], _I),

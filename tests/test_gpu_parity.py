@@ -179,3 +179,31 @@ def test_tma_kernel_variants_bitwise(cuda, variant):
         assert digest(vc.storage.cpu().numpy()) == digest(cst)
     finally:
         lib.bf_set_option(b"tma_variant", 2)
+
+
+@pytest.mark.parametrize("dt,kc,bs", [("f64", 40, 128), ("f64", 1024, 96), ("f32", 20, 96), ("f32", 512, 100)])
+def test_fused_trsm_subtree_bitwise(cuda, dt, kc, bs):
+    """Panels of width <= 128 take the fused TRSM kernel; multi-segment kc and
+    f32 must still give the oracle's bits (and the unfused launches' bits)."""
+    import json
+
+    from paper_2604_07311_b200.engine import _lib
+
+    n = 700
+    doc = json.dumps({"op": "cholesky", "variant": 3, "bs": bs, "kernel": {"kc": kc},
+                      "child": {"op": "cholesky", "variant": "unblocked3"}})
+    a0 = spd_int(99, n, dt)
+    st = a0.reshape(-1).copy()
+    bad = O.cholesky(st, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1}, O.levels_from_tree(json.loads(doc), n, dt))
+    assert bad == -1
+    outs = []
+    lib = _lib.lib()
+    for fused in (1, 0):
+        lib.bf_set_option(b"fused_trsm", fused)
+        try:
+            v = make_view(n, n, DType.parse(dt), fill=a0)
+            bf.cholesky(v, "lower", parse_tree(doc))
+            outs.append(digest(v.storage.cpu().numpy()))
+        finally:
+            lib.bf_set_option(b"fused_trsm", 1)
+    assert outs[0] == outs[1] == digest(st)

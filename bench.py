@@ -22,7 +22,9 @@ flop count n^3/3 (cli.py:78-79).
              sample (a smaller n of the same algorithm).
 --impl reference   times that CPU port alone (the reference's own code is
              Python + numba and is not installed on the GPU box).
-N > 1 ranks currently run independent replicas (multi-GPU).
+N > 1 ranks factor ONE n=32768 matrix together (strong scaling): 2D
+block-cyclic tiles over a grid_for(N) process grid, NCCL panel broadcasts,
+bit-identical to the single-GPU factor (paper_2604_07311_b200/dist).
 """
 from __future__ import annotations
 
@@ -191,6 +193,105 @@ def roofline_syrk(bf, torch, a0, n: int, bs: int, kc: int) -> dict:
             "syrk_ms_total": round(ms, 3), "peak_source": FP64_PEAK_SOURCE}
 
 
+DIST_TREE = {
+    "op": "cholesky", "variant": 3, "bs": 1024, "kernel": {"kc": 1024},
+    "child": {"op": "cholesky", "variant": 3, "bs": 128, "kernel": {"kc": 128},
+              "child": {"op": "cholesky", "variant": "unblocked3"}},
+}
+
+
+def run_distributed(args, bf, torch, dist, dev, world: int, rank: int, n: int) -> int:
+    """All ranks factor one n x n matrix: 2D block-cyclic, NCCL broadcasts."""
+    from paper_2604_07311_b200.control import parse_tree
+    from paper_2604_07311_b200.dist import BlockCyclic2D, TorchComm, cholesky_distributed, grid_for
+    from paper_2604_07311_b200.engine import _lib
+
+    tree_doc = DIST_TREE if args.tree == json.dumps(GPU_TREE) else json.loads(args.tree)
+    tree = parse_tree(json.dumps(tree_doc))
+    pr, pc = grid_for(world)
+    layout = BlockCyclic2D(n, tree.bs, pr, pc)
+    prow, pcol = layout.coords(rank)
+    a0 = make_spd(bf, torch, n, dev)
+    rows = torch.cat([torch.arange(t * layout.nb, t * layout.nb + layout.tile_len(t), device=dev)
+                      for t in layout.row_tiles(prow)])
+    cols = torch.cat([torch.arange(t * layout.nb, t * layout.nb + layout.tile_len(t), device=dev)
+                      for t in layout.col_tiles(pcol)])
+    local0 = a0.index_select(0, rows).index_select(1, cols).contiguous()
+    del a0, rows, cols
+    torch.cuda.empty_cache()
+    work = torch.empty_like(local0)
+    comm = TorchComm()
+    stream = torch.cuda.current_stream()
+
+    def one(timed):
+        work.copy_(local0)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        bad = cholesky_distributed(work, layout, tree, comm)
+        e1.record(stream)
+        e1.synchronize()
+        assert bad == -1
+        if timed is not None:
+            timed.append(e0.elapsed_time(e1))
+
+    for _ in range(args.warmup):
+        one(None)
+    lib = _lib.lib()
+    timed: list = []
+    l0 = lib.bf_launch_count()
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) as clocks:
+        for _ in range(args.steps):
+            one(timed)
+    launches = (lib.bf_launch_count() - l0) // max(1, args.steps)
+    t = torch.tensor([sum(timed) / len(timed)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = chol_flops(n) / (ms / 1e3) / 1e9
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty_like(local0, device="cpu").pin_memory()
+        host.copy_(local0)
+        out = torch.empty_like(host).pin_memory()
+        e2e_ms = []
+        for i in range(1 + args.e2e_steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            work.copy_(host, non_blocking=True)
+            cholesky_distributed(work, layout, tree, comm)
+            out.copy_(work, non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            if i:
+                e2e_ms.append(e0.elapsed_time(e1))
+        t2 = torch.tensor([sum(e2e_ms) / len(e2e_ms)], device=dev)
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        nbytes = local0.numel() * 8
+        e2e = {"value": round(chol_flops(n) / (float(t2.item()) / 1e3) / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(float(t2.item()), 3),
+               "path": "per rank: pinned host local block -> HBM, cholesky_distributed(), HBM -> pinned host"}
+    if rank == 0:
+        line = {
+            "metric": "Cholesky GFLOP/s (n=32768 FP64)", "value": round(value, 3), "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: A = M M^T + n I, M ~ U(-1,1) seed 42, formed on device",
+            "config": {"workload": f"FP64 blocked Cholesky n={n}, 2D block-cyclic over {pr}x{pc} GPUs (BASELINE configs[1]/[2])",
+                       "n": n, "tree": tree_doc, "parallelism": f"2D block-cyclic {pr}x{pc}, NCCL panel broadcasts",
+                       "l2": "matrix >> L2"},
+            "pct_of_fp64_peak": round(100 * value / world / 1e3 / FP64_PEAK_TFLOPS, 2),
+            "roofline": None, "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -204,6 +305,7 @@ def main() -> int:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--tiles-per-cta", type=int, default=None, help="library option (tuning)")
+    ap.add_argument("--dist", action="store_true", help="use the distributed driver even at one rank")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -241,11 +343,17 @@ def main() -> int:
 
     if args.tiles_per_cta is not None:
         _lib.lib().bf_set_option(b"tiles_per_cta", args.tiles_per_cta)
-    if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
+    if world > 1 or args.dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", init_method="env://", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     tree = parse_tree(args.tree)
+
+    if world > 1 or args.dist:
+        return run_distributed(args, bf, torch, dist, dev, world, rank, n)
 
     a0 = make_spd(bf, torch, n, dev)
     work = torch.empty_like(a0)

@@ -115,6 +115,15 @@ int bf_trsm_rltn_s(double alpha, const bf_view* tri, const bf_view* b, int64_t k
 int bf_cholesky_d(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream);
 int bf_cholesky_s(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream);
 
+/* Building blocks of the distributed driver (paper_2604_07311_b200/dist):
+ * the tree walk without the root lookahead, reporting pivots offset by
+ * base_index; and the TRSM with separate (nullable) singular-report and abort
+ * flags (d_singular == NULL selects the fused subtree kernels). */
+int bf_cholesky_ex_d(const bf_view* a, const bf_chol_level* levels, int nlevels, int64_t base_index, int* d_info,
+                     void* stream);
+int bf_trsm_rltn_ex_d(double alpha, const bf_view* tri, const bf_view* b, int64_t kc, int* d_singular,
+                      const int* d_abort, void* stream);
+
 /* Block-scatter GEMM for tensor contraction (engine/gemm.py:74-160 on
  * tensor/contract.py facades): C := beta*C + alpha*A*B with every operand
  * addressed through its scatter vectors. */

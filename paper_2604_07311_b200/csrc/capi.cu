@@ -496,6 +496,20 @@ int bf_trsm_rltn_s(double alpha, const bf_view* tri, const bf_view* b, int64_t k
   return trsm_impl(MODE_S, alpha, tri, b, kc, d_singular, S(stream));
 }
 
+int bf_cholesky_ex_d(const bf_view* a, const bf_chol_level* levels, int nlevels, int64_t base_index, int* d_info,
+                     void* stream) {
+  if (!a || !levels || nlevels < 1) return fail(BF_ERR_VALUE, "null argument");
+  if (a->m != a->n) return fail(BF_ERR_SHAPE, "square matrix required");
+  return chol_run(MODE_D, *a, levels, nlevels, 0, base_index, d_info, S(stream));
+}
+int bf_trsm_rltn_ex_d(double alpha, const bf_view* tri, const bf_view* b, int64_t kc, int* d_singular,
+                      const int* d_abort, void* stream) {
+  if (!tri || !b) return fail(BF_ERR_VALUE, "null view");
+  if (tri->m != tri->n) return fail(BF_ERR_SHAPE, "triangular operand must be square");
+  if (b->n != tri->n) return fail(BF_ERR_SHAPE, "right solve dims mismatch");
+  return trsm_rec(MODE_D, alpha, *tri, *b, kc, d_singular, d_abort, S(stream));
+}
+
 int bf_cholesky_d(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream) {
   return chol_impl(MODE_D, a, levels, nlevels, d_info, S(stream));
 }

@@ -95,6 +95,8 @@ _SIGNATURES = {
     "bf_trsm_rltn_s": ([_D, _V, _V, _L, _VP, _VP], _I),
     "bf_cholesky_d": ([_V, _P(BfCholLevel), _I, _VP, _VP], _I),
     "bf_cholesky_s": ([_V, _P(BfCholLevel), _I, _VP, _VP], _I),
+    "bf_cholesky_ex_d": ([_V, _P(BfCholLevel), _I, _L, _VP, _VP], _I),
+    "bf_trsm_rltn_ex_d": ([_D, _V, _V, _L, _VP, _VP, _VP], _I),
     "bf_gemm_scatter_d": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
     "bf_gemm_scatter_s": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
     "bf_gemm_scatter_sd": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),

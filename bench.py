@@ -186,9 +186,16 @@ def roofline_syrk(bf, torch, a0, n: int, bs: int, kc: int) -> dict:
         launches += 1
     del work
     achieved = flops / (ms / 1e3) / 1e12
+    traffic, traffic_note = None, None
+    tpath = ROOT / "profiles" / "r01_syrk_traffic.json"
+    if tpath.exists():
+        t = json.loads(tpath.read_text())
+        traffic = t["traffic_bytes"]
+        traffic_note = (f"dram read+write of one launch ({t['launch']}) from {t['source']}; algorithmic "
+                        f"{t['algorithmic_bytes'] / 1e9:.2f} GB for that launch")
     return {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-            "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": None,
-            "kernel": "gemm_dmma_kernel<128x128x16, k-major/k-major> (GEMMT lower, trailing SYRK)",
+            "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic, "traffic_note": traffic_note,
+            "kernel": "gemm_dmma_tma_kernel<m8n8k4, 2x16-k TMA boxes, 3 stages> (GEMMT lower, trailing SYRK)",
             "per_launch_flops": "n_k*(n_k+1)*bs, n_k = n-(k+1)*bs", "launches_timed": launches,
             "syrk_ms_total": round(ms, 3), "peak_source": FP64_PEAK_SOURCE}
 

@@ -134,6 +134,20 @@ int bf_gemm_scatter_s(double alpha, const bf_scatter_view* a, const bf_scatter_v
 int bf_gemm_scatter_sd(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
                        const bf_scatter_view* c, int64_t kc, void* stream);
 
+/* Mixed precision (BASELINE configs[3]; no reference counterpart).
+ * bf_gemm_bf16: C(fp32 view) := beta*C + alpha * A * B^T on tcgen05/TMEM, with
+ * A (c->m x k) and B (c->n x k) row-major bf16 (ld in elements, 16-byte aligned).
+ * bf_convert_*: precision conversions between views / dense buffers.
+ * bf_residual_d: r := b - A x for a dense row-major fp64 A (n x n).
+ * bf_potrs_f32_d: x := (L L^T)^-1 x for the fp32 lower factor L (row-major ld),
+ * fp64 right-hand side and arithmetic. */
+int bf_gemm_bf16(double alpha, const void* a, int64_t lda, const void* b, int64_t ldb, double beta, const bf_view* c,
+                 int64_t k, int lower_only, void* stream);
+int bf_convert_f32_bf16(const bf_view* src, void* dst, int64_t ld, int transpose, void* stream);
+int bf_convert_f64_f32(const bf_view* src, const bf_view* dst, int lower_only, void* stream);
+int bf_residual_d(const double* a, int64_t lda, const double* x, const double* b, double* r, int64_t n, void* stream);
+int bf_potrs_f32_d(const float* l, int64_t ld, double* x, int64_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -88,4 +88,15 @@ int launch_trsm_small_right(int is_f64, double alpha, const void* t, int64_t tof
                             int64_t boff, int64_t brs, int64_t bcs, int64_t m, int64_t n, int64_t kc,
                             const int* abort_flag, cudaStream_t s);
 
+int launch_gemm_bf16_tc(double alpha, const void* a, int64_t lda, const void* b, int64_t ldb, double beta, float* c,
+                        int64_t c_off, int64_t c_rs, int64_t c_cs, int64_t m, int64_t n, int64_t k, int lower_only,
+                        cudaStream_t s);
+int launch_to_bf16(const float* src, int64_t soff, int64_t srs, int64_t scs, void* dst, int64_t ld, int64_t m,
+                   int64_t n, int transpose, cudaStream_t s);
+int launch_f64_to_f32(const double* src, int64_t soff, int64_t srs, int64_t scs, float* dst, int64_t doff, int64_t drs,
+                      int64_t dcs, int64_t m, int64_t n, int lower_only, cudaStream_t s);
+int launch_residual(const double* A, int64_t lda, const double* x, const double* b, double* r, int64_t n,
+                    cudaStream_t s);
+int launch_potrs_f32_f64(const float* L, int64_t ld, double* x, int64_t n, cudaStream_t s);
+
 }  // namespace bf

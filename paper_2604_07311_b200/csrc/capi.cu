@@ -517,6 +517,39 @@ int bf_cholesky_s(const bf_view* a, const bf_chol_level* levels, int nlevels, in
   return chol_impl(MODE_S, a, levels, nlevels, d_info, S(stream));
 }
 
+int bf_gemm_bf16(double alpha, const void* a, int64_t lda, const void* b, int64_t ldb, double beta, const bf_view* c,
+                 int64_t k, int lower_only, void* stream) {
+  if (!c) return fail(BF_ERR_VALUE, "null view");
+  if (lower_only && c->m != c->n) return fail(BF_ERR_SHAPE, "gemmt needs square c");
+  int rc = bf::launch_gemm_bf16_tc(alpha, a, lda, b, ldb, beta, static_cast<float*>(c->base), c->off, c->rs, c->cs,
+                                   c->m, c->n, k, lower_only, S(stream));
+  if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "bf16 gemm: operands must be 16-byte aligned k-contiguous bf16");
+  return rc ? fail(BF_ERR_CUDA, "bf16 gemm launch failed") : BF_OK;
+}
+int bf_convert_f32_bf16(const bf_view* src, void* dst, int64_t ld, int transpose, void* stream) {
+  if (!src) return fail(BF_ERR_VALUE, "null view");
+  int rc = bf::launch_to_bf16(static_cast<const float*>(src->base), src->off, src->rs, src->cs, dst, ld, src->m,
+                              src->n, transpose, S(stream));
+  return rc ? fail(BF_ERR_CUDA, "conversion launch failed") : BF_OK;
+}
+int bf_convert_f64_f32(const bf_view* src, const bf_view* dst, int lower_only, void* stream) {
+  if (!src || !dst) return fail(BF_ERR_VALUE, "null view");
+  if (src->m != dst->m || src->n != dst->n) return fail(BF_ERR_SHAPE, "conversion dims mismatch");
+  int rc = bf::launch_f64_to_f32(static_cast<const double*>(src->base), src->off, src->rs, src->cs,
+                                 static_cast<float*>(dst->base), dst->off, dst->rs, dst->cs, src->m, src->n, lower_only,
+                                 S(stream));
+  return rc ? fail(BF_ERR_CUDA, "conversion launch failed") : BF_OK;
+}
+int bf_residual_d(const double* a, int64_t lda, const double* x, const double* b, double* r, int64_t n, void* stream) {
+  int rc = bf::launch_residual(a, lda, x, b, r, n, S(stream));
+  if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "residual needs a 16-byte aligned A with even lda");
+  return rc ? fail(BF_ERR_CUDA, "residual launch failed") : BF_OK;
+}
+int bf_potrs_f32_d(const float* l, int64_t ld, double* x, int64_t n, void* stream) {
+  int rc = bf::launch_potrs_f32_f64(l, ld, x, n, S(stream));
+  return rc ? fail(BF_ERR_CUDA, "potrs launch failed") : BF_OK;
+}
+
 int bf_gemm_scatter_d(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
                       const bf_scatter_view* c, int64_t kc, void* stream) {
   return scatter_impl(MODE_D, alpha, a, b, beta, c, kc, S(stream));

@@ -1,0 +1,308 @@
+// bf16 x bf16 -> fp32 GEMM / GEMMT on the 5th-generation tensor cores
+// (tcgen05.mma kind::f16, accumulator in TMEM), operands staged by TMA.
+//
+// The trailing update of the mixed-precision Cholesky (BASELINE configs[3]):
+// C(fp32) := beta*C + alpha * A * B^T with A (M x K) and B (N x K) bf16,
+// both k-contiguous; lower_only restricts C to i >= j.  This path has no
+// reference counterpart (the reference's only mixed mode is f32-storage /
+// f64-accumulation GEMM); its parity is the FP64 solution after iterative
+// refinement.
+//
+// One 128x128 output tile per CTA, 6 warps:
+//   warp 0      TMA producer (one elected lane): A/B boxes {64 k, 128 rows},
+//               128B swizzle, into a 6-stage ring (full/empty mbarriers)
+//   warp 1      TMEM allocator + MMA issuer (one lane): 4 x UMMA 128x128x16
+//               per stage from smem descriptors, tcgen05.commit frees the
+//               stage, the last commit signals the accumulator
+//   warps 2..5  epilogue: tcgen05.ld 32x32b (each warp its TMEM lane
+//               quadrant) -> registers -> fp32 C read-modify-write
+#include "bf_common.cuh"
+#include "bf_internal.h"
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+namespace bf {
+
+namespace {
+
+constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 64;  // 64 bf16 = one 128-byte swizzle row
+constexpr int TC_STAGES = 6;
+constexpr int TC_THREADS = 192;
+constexpr int TC_A_BYTES = TC_BM * TC_BK * 2, TC_B_BYTES = TC_BN * TC_BK * 2;
+constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
+constexpr size_t TC_SMEM = size_t(TC_STAGES) * TC_STAGE_BYTES + 1024 + 256;
+
+__device__ __forceinline__ void mbar_init_tc(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx_tc(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_tc(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_tc(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+// tcgen05 shared-memory matrix descriptor: K-major, 128B swizzle, 8-row atoms
+// of 1024 bytes (SBO), fixed version bits 46-48 = 0b001.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr & 0x3FFFF) >> 4);
+  d |= uint64_t(1) << 16;             // LBO (unused for swizzled K-major)
+  d |= uint64_t(1024 >> 4) << 32;     // SBO: next 8-row group
+  d |= uint64_t(1) << 46;             // version
+  d |= uint64_t(2) << 61;             // SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M=128, N=128
+__host__ __device__ constexpr uint32_t idesc_bf16_f32(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                        const GemmParams p) {
+  extern __shared__ __align__(16) unsigned char tc_smem[];
+  const uint32_t raw = smem_u32(tc_smem);
+  const uint32_t tiles = (raw + 1023u) & ~1023u;
+  const uint32_t bars = tiles + TC_STAGES * TC_STAGE_BYTES;
+  auto full = [&](int s) { return bars + 8u * s; };
+  auto empty = [&](int s) { return bars + 8u * (TC_STAGES + s); };
+  const uint32_t accum_bar = bars + 8u * (2 * TC_STAGES);
+  const uint32_t tmem_slot = accum_bar + 8u;  // u32 written by tcgen05.alloc
+
+  // tile (lower-triangle enumeration row by row for GEMMT, else row-major)
+  int64_t ti, tj;
+  if (p.lower_only) {
+    const int64_t b = blockIdx.x;
+    int64_t r = int64_t((sqrt(8.0 * double(b) + 1.0) - 1.0) * 0.5);
+    while (r * (r + 1) / 2 > b) --r;
+    while ((r + 1) * (r + 2) / 2 <= b) ++r;
+    ti = r;
+    tj = b - r * (r + 1) / 2;
+  } else {
+    ti = blockIdx.x % p.tiles_m;
+    tj = blockIdx.x / p.tiles_m;
+  }
+  const int64_t m0 = ti * TC_BM, n0 = tj * TC_BN;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_STAGES; ++s) {
+      mbar_init_tc(full(s), 1);
+      mbar_init_tc(empty(s), 1);
+    }
+    mbar_init_tc(accum_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tmem_slot), "n"(128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  uint32_t tmem_base;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(tmem_base) : "r"(tmem_slot));
+
+  const int ktiles = int((p.k + TC_BK - 1) / TC_BK);
+  if (warp == 0 && lane == 0) {
+    // ---- TMA producer ----
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const int s = kt % TC_STAGES;
+      const uint32_t round = uint32_t(kt / TC_STAGES);
+      mbar_wait_tc(empty(s), (round & 1u) ^ 1u);
+      const uint32_t sa = tiles + s * TC_STAGE_BYTES;
+      mbar_expect_tx_tc(full(s), TC_STAGE_BYTES);
+      tma_load_2d_tc(sa, &tma_a, kt * TC_BK, int(m0), full(s));
+      tma_load_2d_tc(sa + TC_A_BYTES, &tma_b, kt * TC_BK, int(n0), full(s));
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---- MMA issuer ----
+    constexpr uint32_t idesc = idesc_bf16_f32(TC_BM, TC_BN);
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const int s = kt % TC_STAGES;
+      const uint32_t round = uint32_t(kt / TC_STAGES);
+      mbar_wait_tc(full(s), round & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t sa = tiles + s * TC_STAGE_BYTES;
+      const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + TC_A_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < TC_BK / 16; ++kk)  // K=16 per MMA: advance 32 bytes inside the swizzle row
+        umma_bf16(tmem_base, da + uint64_t(2 * kk), db + uint64_t(2 * kk), idesc, (kt | kk) != 0);
+      umma_commit(empty(s));
+    }
+    umma_commit(accum_bar);
+  } else if (warp >= 2) {
+    // ---- epilogue: TMEM lane quadrant (warp % 4) -> rows ----
+    mbar_wait_tc(accum_bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const int quad = warp & 3;
+    const int64_t gi = m0 + quad * 32 + lane;
+    float* C = static_cast<float*>(p.c);
+    const float alpha = float(p.alpha), beta = float(p.beta);
+#pragma unroll 1
+    for (int cb = 0; cb < TC_BN / 32; ++cb) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem_base + (uint32_t(quad * 32) << 16) + uint32_t(cb * 32);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      if (gi < p.m) {
+        float old[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int64_t gj = n0 + cb * 32 + j;
+          const bool ok = gj < p.n && (!p.lower_only || gi >= gj);
+          old[j] = (ok && beta != 0.f) ? C[p.c_off + gi * p.c_rs + gj * p.c_cs] : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int64_t gj = n0 + cb * 32 + j;
+          if (gj < p.n && (!p.lower_only || gi >= gj)) {
+            float v = alpha * __uint_as_float(r[j]);
+            if (beta != 0.f) v = fmaf(beta, old[j], v);
+            C[p.c_off + gi * p.c_rs + gj * p.c_cs] = v;
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(128));
+  }
+}
+
+typedef CUresult (*EncodeTiledFnTc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFnTc encoder_tc() {
+  static EncodeTiledFnTc fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult res;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &res) == cudaSuccess &&
+        res == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFnTc>(q);
+  }
+  return fn;
+}
+
+bool make_map_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t k, int64_t ld) {
+  EncodeTiledFnTc enc = encoder_tc();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cuuint64_t(k), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
+  cuuint32_t box[2] = {TC_BK, 128};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// fp32 (strided) -> bf16 (row-major, ld) conversion; transposes when asked
+__global__ void to_bf16_kernel(const float* src, int64_t soff, int64_t srs, int64_t scs, __nv_bfloat16* dst,
+                               int64_t ld, int64_t m, int64_t n, int transpose) {
+  const int64_t total = m * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    const float v = src[soff + i * srs + j * scs];
+    if (transpose)
+      dst[j * ld + i] = __float2bfloat16_rn(v);
+    else
+      dst[i * ld + j] = __float2bfloat16_rn(v);
+  }
+}
+
+}  // namespace
+
+// C(fp32 view) = beta*C + alpha * A(bf16 m x k, row stride lda) * B(bf16 n x k, ldb)^T
+int launch_gemm_bf16_tc(double alpha, const void* a, int64_t lda, const void* b, int64_t ldb, double beta, float* c,
+                        int64_t c_off, int64_t c_rs, int64_t c_cs, int64_t m, int64_t n, int64_t k, int lower_only,
+                        cudaStream_t s) {
+  if (m <= 0 || n <= 0) return 0;
+  if ((reinterpret_cast<uintptr_t>(a) % 16) || (reinterpret_cast<uintptr_t>(b) % 16) || (lda * 2) % 16 ||
+      (ldb * 2) % 16 || k < 1)
+    return -3;
+  CUtensorMap ma, mb;
+  if (!make_map_bf16(&ma, a, m, k, lda) || !make_map_bf16(&mb, b, n, k, ldb)) return -3;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(gemm_bf16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TC_SMEM)) !=
+        cudaSuccess)
+      return -10;
+    attr = true;
+  }
+  GemmParams p{};
+  p.m = m;
+  p.n = n;
+  p.k = k;
+  p.c = c;
+  p.c_off = c_off;
+  p.c_rs = c_rs;
+  p.c_cs = c_cs;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.lower_only = lower_only;
+  p.tiles_m = int((m + TC_BM - 1) / TC_BM);
+  p.tiles_n = int((n + TC_BN - 1) / TC_BN);
+  if (lower_only && (m != n)) return -1;
+  const int64_t grid = lower_only ? int64_t(p.tiles_m) * (p.tiles_m + 1) / 2 : int64_t(p.tiles_m) * p.tiles_n;
+  if (grid > 0x7fffffffLL) return -3;
+  note_launch();
+  gemm_bf16_tc_kernel<<<unsigned(grid), TC_THREADS, TC_SMEM, s>>>(ma, mb, p);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+int launch_to_bf16(const float* src, int64_t soff, int64_t srs, int64_t scs, void* dst, int64_t ld, int64_t m,
+                   int64_t n, int transpose, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return 0;
+  const int64_t total = m * n;
+  const int blocks = int((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+  note_launch();
+  to_bf16_kernel<<<blocks, 256, 0, s>>>(src, soff, srs, scs, static_cast<__nv_bfloat16*>(dst), ld, m, n, transpose);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+}  // namespace bf

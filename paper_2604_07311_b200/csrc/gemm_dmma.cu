@@ -107,6 +107,24 @@ __device__ __forceinline__ void load_tile(double* s, const OperandMK& op, int64_
   }
   // k-major unaligned, generic strided, or block-scatter: element copies, k fastest.
   constexpr int ELEMS = BMN * BK;
+  if constexpr (THREADS % BK == 0 && ELEMS % THREADS == 0) {
+    // every thread keeps one k for all its elements: one k-offset lookup per
+    // tile and one (L1-resident) row-offset lookup per element
+    const int k = tid % BK;
+    const int64_t gk = k_lo + k;
+    const bool kok = gk < k_hi;
+    const int64_t koff = kok ? (op.k_scat ? __ldg(op.k_scat + gk) : gk * op.s_k) : 0;
+#pragma unroll
+    for (int it = 0; it < ELEMS / THREADS; ++it) {
+      const int mn = tid / BK + it * (THREADS / BK);
+      const int64_t gm = mn0 + mn;
+      const bool ok = kok && gm < MN;
+      const double* src = g;
+      if (ok) src = g + (op.mn_scat ? __ldg(op.mn_scat + gm) : op.off + gm * op.s_mn) + koff;
+      cp_async_8(s + sidx<false, BMN, BK>(mn, k), src, ok ? 8 : 0);
+    }
+    return;
+  }
 #pragma unroll
   for (int it = 0; it < (ELEMS + THREADS - 1) / THREADS; ++it) {
     int q = tid + it * THREADS;

@@ -97,6 +97,11 @@ _SIGNATURES = {
     "bf_cholesky_s": ([_V, _P(BfCholLevel), _I, _VP, _VP], _I),
     "bf_cholesky_ex_d": ([_V, _P(BfCholLevel), _I, _L, _VP, _VP], _I),
     "bf_trsm_rltn_ex_d": ([_D, _V, _V, _L, _VP, _VP, _VP], _I),
+    "bf_gemm_bf16": ([_D, _VP, _L, _VP, _L, _D, _V, _L, _I, _VP], _I),
+    "bf_convert_f32_bf16": ([_V, _VP, _L, _I, _VP], _I),
+    "bf_convert_f64_f32": ([_V, _V, _I, _VP], _I),
+    "bf_residual_d": ([_VP, _L, _VP, _VP, _VP, _L, _VP], _I),
+    "bf_potrs_f32_d": ([_VP, _L, _VP, _L, _VP], _I),
     "bf_gemm_scatter_d": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
     "bf_gemm_scatter_s": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
     "bf_gemm_scatter_sd": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),

@@ -71,8 +71,12 @@ int bf_abi_version(void);
 /* Number of kernels this library has launched in this process (all devices). */
 int64_t bf_launch_count(void);
 const char* bf_last_error(void);
-/* Process-wide switches: "lookahead" (default 1) overlaps the next panel's
- * POTRF+TRSM with the trailing update in bf_cholesky_* (same arithmetic). */
+/* Process-wide switches (none changes arithmetic): "lookahead" (default 1)
+ * overlaps the next panel's POTRF+TRSM with the trailing update in
+ * bf_cholesky_*; "tma" / "tma_variant" / "tiles_per_cta" / "group" select the
+ * FP64 GEMM kernel and its tile schedule; "fused_trsm" the single-kernel TRSM
+ * subtree; "timeline" records per-step events; "bf16_tma_c" the TMA C-tile
+ * epilogue of the bf16 GEMM. */
 int bf_set_option(const char* name, int64_t value);
 int bf_device_sm_count(void);
 /* With bf_set_option("timeline", 1): per top-level step of the last lookahead
@@ -140,13 +144,18 @@ int bf_gemm_scatter_sd(double alpha, const bf_scatter_view* a, const bf_scatter_
  * bf_convert_*: precision conversions between views / dense buffers.
  * bf_residual_d: r := b - A x for a dense row-major fp64 A (n x n).
  * bf_potrs_f32_d: x := (L L^T)^-1 x for the fp32 lower factor L (row-major ld),
- * fp64 right-hand side and arithmetic. */
+ * fp64 right-hand side and arithmetic (one CTA per diagonal block: reference-grade, slow).
+ * bf_potrs_blocked_f32_d: the same solve as matrix-vector products against the
+ * explicit diagonal-block inverses xinv[k] = L_kk^-T (nblk x bs x bs fp32, kept by
+ * the mixed factorization); work holds 129*bs doubles. */
 int bf_gemm_bf16(double alpha, const void* a, int64_t lda, const void* b, int64_t ldb, double beta, const bf_view* c,
                  int64_t k, int lower_only, void* stream);
 int bf_convert_f32_bf16(const bf_view* src, void* dst, int64_t ld, int transpose, void* stream);
 int bf_convert_f64_f32(const bf_view* src, const bf_view* dst, int lower_only, void* stream);
 int bf_residual_d(const double* a, int64_t lda, const double* x, const double* b, double* r, int64_t n, void* stream);
 int bf_potrs_f32_d(const float* l, int64_t ld, double* x, int64_t n, void* stream);
+int bf_potrs_blocked_f32_d(const float* l, int64_t ld, const float* xinv, int64_t bs, double* x, int64_t n,
+                           double* work, void* stream);
 
 #ifdef __cplusplus
 }

@@ -71,6 +71,7 @@ bool gemm_dmma_tma_eligible(const GemmParams& p);                     // TMA/mba
 int launch_gemm_dmma_tma(const GemmParams& p, cudaStream_t s);
 extern int g_use_tma;                                                 // bf_set_option("tma", 0|1)
 extern int g_tma_variant;
+extern int g_bf16_tma_c;  // bf16 GEMM: TMA C-tile epilogue (1) or per-element fallback (0)
 extern int g_tiles_per_cta;                                           // bf_set_option("tiles_per_cta", t)                                             // bf_set_option("tma_variant", 0..3)
 int launch_gemm_simt_f32(const GemmParams& p, cudaStream_t s);        // f32 storage, f32 acc
 int launch_gemm_simt_f32acc64(const GemmParams& p, cudaStream_t s);   // f32 storage, f64 acc
@@ -98,5 +99,7 @@ int launch_f64_to_f32(const double* src, int64_t soff, int64_t srs, int64_t scs,
 int launch_residual(const double* A, int64_t lda, const double* x, const double* b, double* r, int64_t n,
                     cudaStream_t s);
 int launch_potrs_f32_f64(const float* L, int64_t ld, double* x, int64_t n, cudaStream_t s);
+int launch_potrs_blocked(const float* L, int64_t ld, const float* xinv, int64_t bs, double* x, int64_t n,
+                         double* work, cudaStream_t s);
 
 }  // namespace bf

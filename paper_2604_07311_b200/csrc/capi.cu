@@ -434,6 +434,10 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_tma_variant = int(value & 3);
     return BF_OK;
   }
+  if (name && std::strcmp(name, "bf16_tma_c") == 0) {
+    bf::g_bf16_tma_c = value != 0;
+    return BF_OK;
+  }
   return fail(BF_ERR_VALUE, "unknown option");
 }
 
@@ -544,6 +548,12 @@ int bf_residual_d(const double* a, int64_t lda, const double* x, const double* b
   int rc = bf::launch_residual(a, lda, x, b, r, n, S(stream));
   if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "residual needs a 16-byte aligned A with even lda");
   return rc ? fail(BF_ERR_CUDA, "residual launch failed") : BF_OK;
+}
+int bf_potrs_blocked_f32_d(const float* l, int64_t ld, const float* xinv, int64_t bs, double* x, int64_t n,
+                           double* work, void* stream) {
+  if (bs <= 0) return fail(BF_ERR_VALUE, "bs must be positive");
+  int rc = bf::launch_potrs_blocked(l, ld, xinv, bs, x, n, work, S(stream));
+  return rc ? fail(BF_ERR_CUDA, "potrs launch failed") : BF_OK;
 }
 int bf_potrs_f32_d(const float* l, int64_t ld, double* x, int64_t n, void* stream) {
   int rc = bf::launch_potrs_f32_f64(l, ld, x, n, S(stream));

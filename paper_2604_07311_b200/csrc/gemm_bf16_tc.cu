@@ -8,14 +8,23 @@
 // f64-accumulation GEMM); its parity is the FP64 solution after iterative
 // refinement.
 //
-// One 128x128 output tile per CTA, 6 warps:
+// Persistent: one CTA per SM walks the 128x128 output tiles (lower-triangle
+// tiles only for GEMMT) with a static stride; 6 warps:
 //   warp 0      TMA producer (one elected lane): A/B boxes {64 k, 128 rows},
-//               128B swizzle, into a 6-stage ring (full/empty mbarriers)
+//               128B swizzle, into a 6-stage ring (full/empty mbarriers) that
+//               runs on across tile boundaries
 //   warp 1      TMEM allocator + MMA issuer (one lane): 4 x UMMA 128x128x16
-//               per stage from smem descriptors, tcgen05.commit frees the
-//               stage, the last commit signals the accumulator
-//   warps 2..5  epilogue: tcgen05.ld 32x32b (each warp its TMEM lane
-//               quadrant) -> registers -> fp32 C read-modify-write
+//               per stage from smem descriptors into one of TWO 128-column
+//               TMEM accumulators, so tile t+1 accumulates while the
+//               epilogue drains tile t; tcgen05.commit frees smem stages and
+//               signals the accumulator
+//   warps 2..5  epilogue: tcgen05.ld 32x32b (each warp its TMEM lane quadrant,
+//               all 128 columns, then the accumulator is released); the fp32
+//               C tile comes in by TMA while the tile's mainloop runs (four
+//               {32 col, 128 row} boxes, 128B swizzle, read conflict-free as
+//               float4 per row), is combined in smem and leaves by TMA store.
+//               Unaligned C views fall back to a warp-private smem transpose
+//               and coalesced per-element read-modify-write.
 #include "bf_common.cuh"
 #include "bf_internal.h"
 
@@ -24,14 +33,18 @@
 
 namespace bf {
 
+int g_bf16_tma_c = 1;
+
 namespace {
 
 constexpr int TC_BM = 128, TC_BN = 128, TC_BK = 64;  // 64 bf16 = one 128-byte swizzle row
-constexpr int TC_STAGES = 6;
+constexpr int TC_STAGES = 5;
 constexpr int TC_THREADS = 192;
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2, TC_B_BYTES = TC_BN * TC_BK * 2;
 constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
-constexpr size_t TC_SMEM = size_t(TC_STAGES) * TC_STAGE_BYTES + 1024 + 256;
+constexpr int TC_CBOX_BYTES = 128 * 32 * 4;         // one {32 col, 128 row} fp32 box
+constexpr int TC_CTILE_BYTES = 4 * TC_CBOX_BYTES;    // C tile staging (TMA path) / transposes (fallback)
+constexpr size_t TC_SMEM = size_t(TC_STAGES) * TC_STAGE_BYTES + TC_CTILE_BYTES + 1024 + 256;
 
 __device__ __forceinline__ void mbar_init_tc(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
@@ -88,32 +101,46 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar) : "memory");
 }
 
+__device__ __forceinline__ void tile_of(const GemmParams& p, int64_t t, int64_t& ti, int64_t& tj) {
+  if (p.lower_only) {  // lower-triangle enumeration, row by row
+    int64_t r = int64_t((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
+    while (r * (r + 1) / 2 > t) --r;
+    while ((r + 1) * (r + 2) / 2 <= t) ++r;
+    ti = r;
+    tj = t - r * (r + 1) / 2;
+  } else {
+    ti = t % p.tiles_m;
+    tj = t / p.tiles_m;
+  }
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+
+template <bool TMAC>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                        const GemmParams p) {
+                        const __grid_constant__ CUtensorMap tma_c, const GemmParams p) {
   extern __shared__ __align__(16) unsigned char tc_smem[];
   const uint32_t raw = smem_u32(tc_smem);
   const uint32_t tiles = (raw + 1023u) & ~1023u;
-  const uint32_t bars = tiles + TC_STAGES * TC_STAGE_BYTES;
+  const uint32_t cbuf = tiles + TC_STAGES * TC_STAGE_BYTES;
+  float* xpose = reinterpret_cast<float*>(tc_smem + (cbuf - raw));
+  const uint32_t bars = cbuf + TC_CTILE_BYTES;
   auto full = [&](int s) { return bars + 8u * s; };
   auto empty = [&](int s) { return bars + 8u * (TC_STAGES + s); };
-  const uint32_t accum_bar = bars + 8u * (2 * TC_STAGES);
-  const uint32_t tmem_slot = accum_bar + 8u;  // u32 written by tcgen05.alloc
-
-  // tile (lower-triangle enumeration row by row for GEMMT, else row-major)
-  int64_t ti, tj;
-  if (p.lower_only) {
-    const int64_t b = blockIdx.x;
-    int64_t r = int64_t((sqrt(8.0 * double(b) + 1.0) - 1.0) * 0.5);
-    while (r * (r + 1) / 2 > b) --r;
-    while ((r + 1) * (r + 2) / 2 <= b) ++r;
-    ti = r;
-    tj = b - r * (r + 1) / 2;
-  } else {
-    ti = blockIdx.x % p.tiles_m;
-    tj = blockIdx.x / p.tiles_m;
-  }
-  const int64_t m0 = ti * TC_BM, n0 = tj * TC_BN;
+  auto acc_full = [&](int b) { return bars + 8u * (2 * TC_STAGES + b); };
+  auto acc_empty = [&](int b) { return bars + 8u * (2 * TC_STAGES + 2 + b); };
+  const uint32_t cload = bars + 8u * (2 * TC_STAGES + 4);
+  const uint32_t tmem_slot = cload + 8u;  // u32 written by tcgen05.alloc
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -121,11 +148,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init_tc(full(s), 1);
       mbar_init_tc(empty(s), 1);
     }
-    mbar_init_tc(accum_bar, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init_tc(acc_full(b), 1);
+      mbar_init_tc(acc_empty(b), 4);  // one arrival per epilogue warp
+    }
+    mbar_init_tc(cload, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tmem_slot), "n"(128));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tmem_slot), "n"(256));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -135,71 +166,160 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(tmem_base) : "r"(tmem_slot));
 
   const int ktiles = int((p.k + TC_BK - 1) / TC_BK);
+  const int64_t ntiles = p.num_tiles;
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
-    for (int kt = 0; kt < ktiles; ++kt) {
-      const int s = kt % TC_STAGES;
-      const uint32_t round = uint32_t(kt / TC_STAGES);
-      mbar_wait_tc(empty(s), (round & 1u) ^ 1u);
-      const uint32_t sa = tiles + s * TC_STAGE_BYTES;
-      mbar_expect_tx_tc(full(s), TC_STAGE_BYTES);
-      tma_load_2d_tc(sa, &tma_a, kt * TC_BK, int(m0), full(s));
-      tma_load_2d_tc(sa + TC_A_BYTES, &tma_b, kt * TC_BK, int(n0), full(s));
+    uint32_t it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int64_t ti, tj;
+      tile_of(p, t, ti, tj);
+      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+        const int s = int(it % TC_STAGES);
+        mbar_wait_tc(empty(s), ((it / TC_STAGES) & 1u) ^ 1u);
+        const uint32_t sa = tiles + s * TC_STAGE_BYTES;
+        mbar_expect_tx_tc(full(s), TC_STAGE_BYTES);
+        tma_load_2d_tc(sa, &tma_a, kt * TC_BK, int(ti * TC_BM), full(s));
+        tma_load_2d_tc(sa + TC_A_BYTES, &tma_b, kt * TC_BK, int(tj * TC_BN), full(s));
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer ----
     constexpr uint32_t idesc = idesc_bf16_f32(TC_BM, TC_BN);
-    for (int kt = 0; kt < ktiles; ++kt) {
-      const int s = kt % TC_STAGES;
-      const uint32_t round = uint32_t(kt / TC_STAGES);
-      mbar_wait_tc(full(s), round & 1u);
+    uint32_t it = 0, lt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      const uint32_t buf = lt & 1u;
+      mbar_wait_tc(acc_empty(buf), ((lt >> 1) & 1u) ^ 1u);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const uint32_t sa = tiles + s * TC_STAGE_BYTES;
-      const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + TC_A_BYTES);
+      const uint32_t dst = tmem_base + buf * TC_BN;
+      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+        const int s = int(it % TC_STAGES);
+        mbar_wait_tc(full(s), (it / TC_STAGES) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t sa = tiles + s * TC_STAGE_BYTES;
+        const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + TC_A_BYTES);
 #pragma unroll
-      for (int kk = 0; kk < TC_BK / 16; ++kk)  // K=16 per MMA: advance 32 bytes inside the swizzle row
-        umma_bf16(tmem_base, da + uint64_t(2 * kk), db + uint64_t(2 * kk), idesc, (kt | kk) != 0);
-      umma_commit(empty(s));
+        for (int kk = 0; kk < TC_BK / 16; ++kk)  // K=16 per MMA: advance 32 bytes inside the swizzle row
+          umma_bf16(dst, da + uint64_t(2 * kk), db + uint64_t(2 * kk), idesc, (kt | kk) != 0);
+        umma_commit(empty(s));
+      }
+      umma_commit(acc_full(buf));
     }
-    umma_commit(accum_bar);
-  } else if (warp >= 2) {
-    // ---- epilogue: TMEM lane quadrant (warp % 4) -> rows ----
-    mbar_wait_tc(accum_bar, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  } else if (warp >= 2 && TMAC) {
+    // ---- epilogue, TMA C tile: TMEM lane quadrant (warp % 4) -> rows ----
     const int quad = warp & 3;
-    const int64_t gi = m0 + quad * 32 + lane;
+    const int r = quad * 32 + lane;  // tile row of this thread
+    const bool leader = warp == 2 && lane == 0;
+    const float alpha = float(p.alpha), beta = float(p.beta);
+    uint32_t lt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      int64_t ti, tj;
+      tile_of(p, t, ti, tj);
+      if (leader) {  // C tile load overlaps this tile's mainloop
+        mbar_expect_tx_tc(cload, TC_CTILE_BYTES);
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb)
+          tma_load_2d_tc(cbuf + cb * TC_CBOX_BYTES, &tma_c, int(tj * TC_BN + cb * 32), int(ti * TC_BM), cload);
+      }
+      const uint32_t buf = lt & 1u;
+      mbar_wait_tc(acc_full(buf), (lt >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      uint32_t acc[4][32];
+      const uint32_t taddr = tmem_base + (uint32_t(quad * 32) << 16) + buf * TC_BN;
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) tmem_ld32(taddr + uint32_t(cb * 32), acc[cb]);
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(acc_empty(buf)) : "memory");
+      mbar_wait_tc(cload, lt & 1u);
+      const int64_t gi = ti * TC_BM + r;
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t addr = cbuf + cb * TC_CBOX_BYTES + r * 128 + ((c ^ (r & 7)) << 4);
+          float o[4];
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+                       : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3])
+                       : "r"(addr));
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int64_t gj = tj * TC_BN + cb * 32 + c * 4 + e;
+            if (!p.lower_only || gj <= gi) {
+              const float v = alpha * __uint_as_float(acc[cb][c * 4 + e]);
+              o[e] = beta != 0.f ? fmaf(beta, o[e], v) : v;
+            }
+          }
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "f"(o[0]), "f"(o[1]), "f"(o[2]),
+                       "f"(o[3])
+                       : "memory");
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (leader) {
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                  reinterpret_cast<uint64_t>(&tma_c)),
+              "r"(int(tj * TC_BN + cb * 32)), "r"(int(ti * TC_BM)), "r"(cbuf + cb * TC_CBOX_BYTES)
+              : "memory");
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+    }
+    if (leader) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  } else if (warp >= 2) {
+    // ---- epilogue, fallback: TMEM lane quadrant (warp % 4) -> rows ----
+    const int quad = warp & 3;
+    float* st = xpose + (warp - 2) * 32 * 33;
     float* C = static_cast<float*>(p.c);
     const float alpha = float(p.alpha), beta = float(p.beta);
-#pragma unroll 1
-    for (int cb = 0; cb < TC_BN / 32; ++cb) {
-      uint32_t r[32];
-      const uint32_t taddr = tmem_base + (uint32_t(quad * 32) << 16) + uint32_t(cb * 32);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-            "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-            "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-          : "r"(taddr));
+    uint32_t lt = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+      int64_t ti, tj;
+      tile_of(p, t, ti, tj);
+      const uint32_t buf = lt & 1u;
+      mbar_wait_tc(acc_full(buf), (lt >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      uint32_t r[4][32];
+      const uint32_t taddr = tmem_base + (uint32_t(quad * 32) << 16) + buf * TC_BN;
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) tmem_ld32(taddr + uint32_t(cb * 32), r[cb]);
       asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      if (gi < p.m) {
-        float old[32];
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(acc_empty(buf)) : "memory");
+      const int64_t row0 = ti * TC_BM + quad * 32;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int64_t gj = n0 + cb * 32 + j;
-          const bool ok = gj < p.n && (!p.lower_only || gi >= gj);
-          old[j] = (ok && beta != 0.f) ? C[p.c_off + gi * p.c_rs + gj * p.c_cs] : 0.f;
-        }
+      for (int cb = 0; cb < 4; ++cb) {
+        // lane holds row (row0 + lane), columns cb*32 .. cb*32+31: transpose so lanes run along columns
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int64_t gj = n0 + cb * 32 + j;
-          if (gj < p.n && (!p.lower_only || gi >= gj)) {
-            float v = alpha * __uint_as_float(r[j]);
-            if (beta != 0.f) v = fmaf(beta, old[j], v);
-            C[p.c_off + gi * p.c_rs + gj * p.c_cs] = v;
+        for (int j = 0; j < 32; ++j) st[lane * 33 + j] = __uint_as_float(r[cb][j]);
+        __syncwarp();
+        const int64_t gj = tj * TC_BN + cb * 32 + lane;
+#pragma unroll
+        for (int r8 = 0; r8 < 32; r8 += 8) {
+          float old[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int64_t gi = row0 + r8 + q;
+            const bool ok = gi < p.m && gj < p.n && (!p.lower_only || gi >= gj);
+            old[q] = (ok && beta != 0.f) ? __ldcs(C + p.c_off + gi * p.c_rs + gj * p.c_cs) : 0.f;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int64_t gi = row0 + r8 + q;
+            if (gi < p.m && gj < p.n && (!p.lower_only || gi >= gj)) {
+              float v = alpha * st[(r8 + q) * 33 + lane];
+              if (beta != 0.f) v = fmaf(beta, old[q], v);
+              __stcs(C + p.c_off + gi * p.c_rs + gj * p.c_cs, v);
+            }
           }
         }
+        __syncwarp();
       }
     }
   }
@@ -207,7 +327,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(128));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(256));
   }
 }
 
@@ -227,6 +347,18 @@ EncodeTiledFnTc encoder_tc() {
       fn = reinterpret_cast<EncodeTiledFnTc>(q);
   }
   return fn;
+}
+
+bool make_map_c32(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld) {
+  EncodeTiledFnTc enc = encoder_tc();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * 4};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool make_map_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t k, int64_t ld) {
@@ -269,11 +401,20 @@ int launch_gemm_bf16_tc(double alpha, const void* a, int64_t lda, const void* b,
   if (!make_map_bf16(&ma, a, m, k, lda) || !make_map_bf16(&mb, b, n, k, ldb)) return -3;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(gemm_bf16_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TC_SMEM)) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(gemm_bf16_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TC_SMEM)) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(gemm_bf16_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TC_SMEM)) !=
+            cudaSuccess)
       return -10;
     attr = true;
   }
+  // TMA C path: unit column stride, 16-byte aligned rows and base, and whole
+  // 16-byte row ends (a bulk store clips out-of-bounds columns per 16 bytes)
+  CUtensorMap mc;
+  const float* cbase = c + c_off;
+  const bool tmac = g_bf16_tma_c && c_cs == 1 && (reinterpret_cast<uintptr_t>(cbase) % 16 == 0) && (c_rs * 4) % 16 == 0 &&
+                    n % 4 == 0 && make_map_c32(&mc, cbase, m, n, c_rs);
+  if (!tmac) memset(&mc, 0, sizeof(mc));
   GemmParams p{};
   p.m = m;
   p.n = n;
@@ -288,10 +429,18 @@ int launch_gemm_bf16_tc(double alpha, const void* a, int64_t lda, const void* b,
   p.tiles_m = int((m + TC_BM - 1) / TC_BM);
   p.tiles_n = int((n + TC_BN - 1) / TC_BN);
   if (lower_only && (m != n)) return -1;
-  const int64_t grid = lower_only ? int64_t(p.tiles_m) * (p.tiles_m + 1) / 2 : int64_t(p.tiles_m) * p.tiles_n;
-  if (grid > 0x7fffffffLL) return -3;
+  p.num_tiles = lower_only ? int64_t(p.tiles_m) * (p.tiles_m + 1) / 2 : int64_t(p.tiles_m) * p.tiles_n;
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t grid = p.num_tiles < sms ? p.num_tiles : sms;
   note_launch();
-  gemm_bf16_tc_kernel<<<unsigned(grid), TC_THREADS, TC_SMEM, s>>>(ma, mb, p);
+  if (tmac)
+    gemm_bf16_tc_kernel<true><<<unsigned(grid), TC_THREADS, TC_SMEM, s>>>(ma, mb, mc, p);
+  else
+    gemm_bf16_tc_kernel<false><<<unsigned(grid), TC_THREADS, TC_SMEM, s>>>(ma, mb, mc, p);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 

@@ -90,6 +90,115 @@ __global__ void trsv_panel_bwd_kernel(const float* L, int64_t ld, double* x, int
   x[c] -= s;
 }
 
+// out[i] = (base ? base[i] : 0) + sign * sum_j A[i*lda + j] v[j], i < rows; one warp per row,
+// VEC floats per lane per load and 4 loads in flight per lane
+template <int VEC>
+__global__ void gemv_n_kernel(const float* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
+                              const double* __restrict__ v, const double* base, double* out, double sign) {
+  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* a = A + row * lda;
+  constexpr int STEP = 32 * VEC;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t j = int64_t(lane) * VEC;
+  for (; j + 3 * STEP < cols; j += 4 * STEP) {
+    float x[4][VEC];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if constexpr (VEC == 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(a + j + u * STEP));
+        x[u][0] = q.x;
+        x[u][1] = q.y;
+        x[u][2] = q.z;
+        x[u][3] = q.w;
+      } else {
+        x[u][0] = __ldg(a + j + u * STEP);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) s[u] = fma(double(x[u][e]), v[j + u * STEP + e], s[u]);
+  }
+  for (; j < cols; j += STEP)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) s[0] = fma(double(__ldg(a + j + e)), v[j + e], s[0]);
+  double t = (s[0] + s[1]) + (s[2] + s[3]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) out[row] = (base ? base[row] : 0.0) + sign * t;
+}
+
+// partial[c][j] = sum_{i in chunk c} A[i*lda + j] v[i]  (A^T v split over row chunks). A CTA covers
+// 256 columns with 256/VEC column threads x VEC row groups; 4 rows in flight per thread.
+template <int VEC>
+__global__ void gemv_t_partial_kernel(const float* __restrict__ A, int64_t lda, int64_t rows, int cols,
+                                      const double* __restrict__ v, double* partial, int64_t rows_per_chunk) {
+  constexpr int CT = 256 / VEC, RG = VEC;
+  __shared__ double red[RG][256];
+  const int ct = threadIdx.x % CT, rg = threadIdx.x / CT;
+  const int j0 = blockIdx.x * 256 + ct * VEC;
+  const int c = blockIdx.y;
+  const int64_t r0 = int64_t(c) * rows_per_chunk;
+  const int64_t r1 = r0 + rows_per_chunk < rows ? r0 + rows_per_chunk : rows;
+  double acc[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) acc[e] = 0.0;
+  if (j0 < cols) {
+    int64_t i = r0 + rg;
+    for (; i + 3 * RG < r1; i += 4 * RG) {
+      float x[4][VEC];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float* src = A + (i + u * RG) * lda + j0;
+        if constexpr (VEC == 4) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(src));
+          x[u][0] = q.x;
+          x[u][1] = q.y;
+          x[u][2] = q.z;
+          x[u][3] = q.w;
+        } else {
+          x[u][0] = __ldg(src);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double vi = v[i + u * RG];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[e] = fma(double(x[u][e]), vi, acc[e]);
+      }
+    }
+    for (; i < r1; i += RG) {
+      const double vi = v[i];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[e] = fma(double(__ldg(A + i * lda + j0 + e)), vi, acc[e]);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) red[rg][ct * VEC + e] = acc[e];
+  __syncthreads();
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  if (j < cols) {
+    double t = 0.0;
+#pragma unroll
+    for (int g = 0; g < RG; ++g) t += red[g][threadIdx.x];
+    partial[int64_t(c) * cols + j] = t;
+  }
+}
+
+// out[j] = (base ? base[j] : 0) + sign * sum_c partial[c][j]
+__global__ void reduce_partial_kernel(const double* partial, int chunks, int cols, const double* base, double* out,
+                                      double sign) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  double s = 0.0;
+  for (int c = 0; c < chunks; ++c) s += partial[int64_t(c) * cols + j];
+  out[j] = (base ? base[j] : 0.0) + sign * s;
+}
+
+constexpr int kPotrsMaxChunks = 128;
+
 inline int grid_for_elems(int64_t total) {
   const int64_t b = (total + 255) / 256;
   return int(b < 148 * 16 ? b : 148 * 16);
@@ -135,6 +244,74 @@ int launch_potrs_f32_f64(const float* L, int64_t ld, double* x, int64_t n, cudaS
       note_launch();
       trsv_panel_bwd_kernel<<<unsigned((lo + 255) / 256), 256, 0, s>>>(L, ld, x, lo, nb);
     }
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+// Blocked solve with the explicit inverses X_k = L_kk^-T of the diagonal
+// blocks (xinv: nblk x bs x bs fp32, X_k row-major ld bs). Every step is a
+// matrix-vector product streaming its block of L once, shaped so that the
+// long dimension is spread over the whole GPU:
+//   forward (right-looking)  y_k = X_k^T r_k;  r[k+1:] -= L[k+1:, k] y_k
+//   backward (left-looking)  x_k = X_k (y_k - L[k+1:, k]^T x[k+1:])
+// work: (kPotrsMaxChunks + 1) * bs doubles.
+int launch_potrs_blocked(const float* L, int64_t ld, const float* xinv, int64_t bs, double* x, int64_t n,
+                         double* work, cudaStream_t s) {
+  double* t = work;
+  double* partial = work + bs;
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(L) % 16 == 0) && ld % 4 == 0 && bs % 4 == 0 &&
+                      (reinterpret_cast<uintptr_t>(xinv) % 16 == 0);
+  auto gemv_t = [&](const float* A, int64_t lda, int64_t rows, int cols, const double* v, bool vec) -> int {
+    const int col_tiles = (cols + 255) / 256;
+    int64_t chunks = (rows + 31) / 32;
+    const int64_t want = (4 * 148 + col_tiles - 1) / col_tiles;
+    if (chunks > want) chunks = want;
+    if (chunks > kPotrsMaxChunks) chunks = kPotrsMaxChunks;
+    if (chunks < 1) chunks = 1;
+    const int64_t per = (rows + chunks - 1) / chunks;
+    note_launch();
+    if (vec)
+      gemv_t_partial_kernel<4><<<dim3(col_tiles, unsigned(chunks)), 256, 0, s>>>(A, lda, rows, cols, v, partial, per);
+    else
+      gemv_t_partial_kernel<1><<<dim3(col_tiles, unsigned(chunks)), 256, 0, s>>>(A, lda, rows, cols, v, partial, per);
+    return int(chunks);
+  };
+  auto gemv_n = [&](const float* A, int64_t lda, int64_t rows, int64_t cols, const double* v, const double* base,
+                    double* out, double sign, bool vec) {
+    note_launch();
+    const unsigned grid = unsigned((rows * 32 + 255) / 256);
+    if (vec)
+      gemv_n_kernel<4><<<grid, 256, 0, s>>>(A, lda, rows, cols, v, base, out, sign);
+    else
+      gemv_n_kernel<1><<<grid, 256, 0, s>>>(A, lda, rows, cols, v, base, out, sign);
+  };
+  auto reduce = [&](int chunks, int cols, const double* base, double* out, double sign) {
+    note_launch();
+    reduce_partial_kernel<<<unsigned((cols + 255) / 256), 256, 0, s>>>(partial, chunks, cols, base, out, sign);
+  };
+  const int64_t nblk = (n + bs - 1) / bs;
+  for (int64_t k = 0; k < nblk; ++k) {
+    const int64_t k0 = k * bs, k1 = k0 + bs < n ? k0 + bs : n;
+    const int b = int(k1 - k0);
+    const float* X = xinv + k * bs * bs;
+    const bool vx = vec_ok && b % 4 == 0;
+    const int ch = gemv_t(X, bs, b, b, x + k0, vx);  // y_k = X_k^T r_k
+    reduce(ch, b, nullptr, t, 1.0);
+    if (k1 < n) gemv_n(L + k1 * ld + k0, ld, n - k1, b, t, x + k1, x + k1, -1.0, vx);
+    reduce(ch, b, nullptr, x + k0, 1.0);
+  }
+  for (int64_t k = nblk - 1; k >= 0; --k) {
+    const int64_t k0 = k * bs, k1 = k0 + bs < n ? k0 + bs : n;
+    const int b = int(k1 - k0);
+    const float* X = xinv + k * bs * bs;
+    const bool vx = vec_ok && b % 4 == 0;
+    if (k1 < n) {
+      const int ch = gemv_t(L + k1 * ld + k0, ld, n - k1, b, x + k1, vx);  // L[k+1:,k]^T x[k+1:]
+      reduce(ch, b, x + k0, t, -1.0);
+    } else {
+      reduce(0, b, x + k0, t, 1.0);
+    }
+    gemv_n(X, bs, b, b, t, nullptr, x + k0, 1.0, vx);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }

@@ -41,6 +41,38 @@ def test_bf16_tcgen05_gemm_vs_torch_fp32(cuda, m, n, k, lower):
         assert (c - ref).abs().max().item() <= tol
 
 
+@pytest.mark.parametrize("tma_c", [1, 0])
+@pytest.mark.parametrize("c_off", [0, 1])
+@pytest.mark.parametrize("m", [333, 336])
+def test_bf16_gemm_epilogues_on_views(cuda, tma_c, c_off, m):
+    """TMA C-tile epilogue and the per-element fallback (forced, or picked for a
+    misaligned C view) give the same values, and leave the strict upper
+    triangle and the rest of the storage untouched."""
+    k = 192  # m=336 with c_off=0 takes the TMA path; 333 has a ragged 16-byte row end
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    a = (torch.rand(m, k, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    store = torch.rand(m + 2, 340, device="cuda", generator=g)  # 1360-byte rows
+    c = store[1:1 + m, c_off:c_off + m]
+    before = store.clone()
+    lib = _lib.lib()
+    assert lib.bf_set_option(b"bf16_tma_c", tma_c) == 0
+    try:
+        rc = lib.bf_gemm_bf16(-0.5, a.data_ptr(), k, a.data_ptr(), k, 2.0, ctypes.byref(_lib.as_bfview(from_torch(c))), k,
+                              1, torch.cuda.current_stream().cuda_stream)
+    finally:
+        lib.bf_set_option(b"bf16_tma_c", 1)
+    assert rc == 0
+    c0 = before[1:1 + m, c_off:c_off + m]
+    ref = 2.0 * c0 - 0.5 * (a.float() @ a.float().T)
+    mask = torch.tril(torch.ones(m, m, dtype=torch.bool, device="cuda"))
+    assert (c - ref)[mask].abs().max().item() <= 1e-4
+    assert torch.equal(c[~mask], c0[~mask])
+    outside = torch.ones_like(store, dtype=torch.bool)
+    outside[1:1 + m, c_off:c_off + m] = False
+    assert torch.equal(store[outside], before[outside])
+
+
 def test_bf16_gemm_rejects_unaligned_leading_dim(cuda):
     a = torch.zeros(64, 500, dtype=torch.bfloat16, device="cuda")  # 1000-byte rows: not a TMA stride
     c = torch.zeros(64, 64, device="cuda")
@@ -66,3 +98,25 @@ def test_mixed_solve_reaches_fp64_accuracy(cuda, n, bs):
     assert back <= 10 * n * eps
     x_ref = np.linalg.solve(an, bn)
     assert np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref) <= 1e-12
+
+
+def test_blocked_potrs_matches_direct_solve(cuda):
+    from paper_2604_07311_b200.mixed import cholesky_mixed
+
+    n, bs = 700, 256  # ragged last block
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    m = torch.rand(n, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    a = m @ m.T + n * torch.eye(n, dtype=torch.float64, device="cuda")
+    f = cholesky_mixed(a, bs)
+    rhs = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+    lib = _lib.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    x1, x2 = rhs.clone(), rhs.clone()
+    work = torch.empty(129 * bs, dtype=torch.float64, device="cuda")
+    assert lib.bf_potrs_f32_d(f.w.data_ptr(), n, x1.data_ptr(), n, s) == 0
+    assert lib.bf_potrs_blocked_f32_d(f.w.data_ptr(), n, f.xinv.data_ptr(), bs, x2.data_ptr(), n, work.data_ptr(), s) == 0
+    lw = torch.tril(f.w).double().cpu().numpy()
+    ref = np.linalg.solve(lw @ lw.T, rhs.cpu().numpy())
+    for x in (x1, x2):  # fp64 arithmetic on the fp32 factor; the blocked one uses fp32 inverses
+        assert np.linalg.norm(x.cpu().numpy() - ref) / np.linalg.norm(ref) <= 1e-5

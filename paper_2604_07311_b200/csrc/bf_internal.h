@@ -71,7 +71,8 @@ bool gemm_dmma_tma_eligible(const GemmParams& p);                     // TMA/mba
 int launch_gemm_dmma_tma(const GemmParams& p, cudaStream_t s);
 extern int g_use_tma;                                                 // bf_set_option("tma", 0|1)
 extern int g_tma_variant;
-extern int g_bf16_tma_c;  // bf16 GEMM: TMA C-tile epilogue (1) or per-element fallback (0)
+extern int g_bf16_tma_c;
+extern int g_trsm_warp;  // fused TRSM subtree: warp-per-32-rows kernel (1) or the 64-row CTA kernel (0)  // bf16 GEMM: TMA C-tile epilogue (1) or per-element fallback (0)
 extern int g_tiles_per_cta;                                           // bf_set_option("tiles_per_cta", t)                                             // bf_set_option("tma_variant", 0..3)
 int launch_gemm_simt_f32(const GemmParams& p, cudaStream_t s);        // f32 storage, f32 acc
 int launch_gemm_simt_f32acc64(const GemmParams& p, cudaStream_t s);   // f32 storage, f64 acc

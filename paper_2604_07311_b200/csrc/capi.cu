@@ -434,6 +434,10 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_tma_variant = int(value & 3);
     return BF_OK;
   }
+  if (name && std::strcmp(name, "trsm_warp") == 0) {
+    bf::g_trsm_warp = value != 0;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "bf16_tma_c") == 0) {
     bf::g_bf16_tma_c = value != 0;
     return BF_OK;

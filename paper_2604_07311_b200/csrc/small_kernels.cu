@@ -14,6 +14,8 @@
 
 namespace bf {
 
+int g_trsm_warp = 1;
+
 namespace {
 
 // ------------------------------------------------------------------ scale --
@@ -533,6 +535,341 @@ __global__ void __launch_bounds__(TS_THREADS) trsm_small_right_kernel(double alp
   }
 }
 
+// ---------------------------------- fused TRSM subtree, 4 warps per 32 rows --
+// Same recursion and per-element arithmetic as TrsmSmall, organised for
+// latency.  A group of four warps owns 32 rows of X * L^T = B (rows are
+// independent) and walks the tree with one named barrier per phase:
+//  * bases: warp 0, one lane per row, the row's 32 accumulators in registers,
+//    column-oriented (once x_p is final every later accumulator takes its
+//    multiply-subtract: the reference's order per element), so the serial
+//    chain is one division and one multiply-subtract per column;
+//  * folds: the output columns in 8-wide chunks spread over the 4 warps; f64
+//    on the tensor pipe (DMMA m8n8k4, 4 row tiles, k-slices zero-padded:
+//    fma(0,0,t) = t, the kc-segment chain of the reference), f32 as one SIMT
+//    chain per element (f32 products summed in f64).
+// Rows live in shared memory as sx[c][33] per group; the triangle is shared
+// by the CTA's groups.
+constexpr int TW_LD = 132;  // triangle row stride: 16-byte aligned rows
+constexpr int TW_XLD = 33;  // x column stride (padded)
+
+template <typename T>
+struct TrsmGroup {
+  T* sx;        // [128][TW_XLD]: column c of the group's 32 rows
+  const T* sl;  // [128][TW_LD] triangle
+  int lane, gw, barid;
+  int64_t kc;
+
+  __device__ __forceinline__ T& x(int c) const { return sx[c * TW_XLD + lane]; }
+  __device__ __forceinline__ T& xa(int c, int r) const { return sx[c * TW_XLD + r]; }
+  __device__ __forceinline__ void sync() const { asm volatile("bar.sync %0, 128;\n" ::"r"(barid) : "memory"); }
+
+  // Division on the serial chain: with r = rcp.rn(b) computed off the chain,
+  // q0 = a*r, e = fma(-b, q0, a), q = fma(e, r, q0) is RN(a/b) (Markstein)
+  // whenever nothing over/underflows.  Every dividend and divisor is checked
+  // to lie in a band where that holds (|x| in [2^-423, 2^423] for f64,
+  // [2^-47, 2^47] for f32; zero dividends are fine); a base that met
+  // anything else is recomputed with div.rn.
+  __device__ __forceinline__ static int expo(T v) {
+    if constexpr (sizeof(T) == 8)
+      return (__double2hiint(v) >> 20) & 0x7ff;
+    else
+      return (__float_as_int(v) >> 23) & 0xff;
+  }
+  static constexpr int kLoExp = sizeof(T) == 8 ? 600 : 80;
+  static constexpr int kHiExp = sizeof(T) == 8 ? 1446 : 174;
+  static constexpr int kMidExp = sizeof(T) == 8 ? 1023 : 127;
+  __device__ __forceinline__ static T rcp(T b) {
+    if constexpr (sizeof(T) == 8)
+      return __drcp_rn(b);
+    else
+      return __frcp_rn(b);
+  }
+
+  template <bool FULL>
+  __device__ __forceinline__ void base_impl(int lo, int n, double alpha) const {
+    const T* l = sl + lo * TW_LD + lo;
+    // lane p takes the reciprocal of diagonal p; shuffles hand them out
+    const T dl = (FULL || lane < n) ? l[lane * TW_LD + lane] : T(1);
+    const T my_rc = rcp(dl);
+    const int ed = expo(dl);
+    bool safe = __all_sync(0xffffffffu, ed >= kLoExp && ed <= kHiExp);
+    T rc[32];
+#pragma unroll
+    for (int p = 0; p < 32; ++p) rc[p] = __shfl_sync(0xffffffffu, my_rc, p);
+    T acc[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = (FULL || j < n) ? x(lo + j) : T(0);
+    if (alpha != 1.0) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = T(Ops<double>::mul(double(acc[j]), alpha));
+    }
+    int emin = kMidExp, emax = kMidExp;
+#pragma unroll
+    for (int p = 0; p < 32; ++p) {
+      if (FULL || p < n) {
+        const T a = acc[p];
+        const T q0 = Ops<T>::mul(a, rc[p]);
+        const T xp = Ops<T>::fma_(Ops<T>::fma_(-l[p * TW_LD + p], q0, a), rc[p], q0);
+        const int ea = a == T(0) ? kMidExp : expo(a);
+        emin = min(emin, ea);
+        emax = max(emax, ea);
+        acc[p] = xp;
+#pragma unroll
+        for (int q = p + 1; q < 32; ++q)
+          if (FULL || q < n) acc[q] = Ops<T>::sub(acc[q], Ops<T>::mul(xp, l[q * TW_LD + p]));
+      }
+    }
+    safe = __all_sync(0xffffffffu, safe && emin >= kLoExp && emax <= kHiExp);
+    if (safe) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (FULL || j < n) x(lo + j) = acc[j];
+    } else {  // rare: exact division throughout, in place
+      if (alpha != 1.0)
+        for (int j = 0; j < n; ++j) x(lo + j) = T(Ops<double>::mul(double(x(lo + j)), alpha));
+      for (int p = 0; p < n; ++p) {
+        const T xp = Ops<T>::div(x(lo + p), l[p * TW_LD + p]);
+        x(lo + p) = xp;
+        for (int q = p + 1; q < n; ++q) x(lo + q) = Ops<T>::sub(x(lo + q), Ops<T>::mul(xp, l[q * TW_LD + p]));
+      }
+    }
+  }
+
+  __device__ __forceinline__ void base(int lo, int hi, double alpha) const {
+    if (gw == 0) {
+      if (hi - lo == 32)
+        base_impl<true>(lo, 32, alpha);
+      else
+        base_impl<false>(lo, hi - lo, alpha);
+    }
+    sync();
+  }
+
+  // x[:, mid:hi] = beta*x[:, mid:hi] - x[:, lo:mid] * l[mid:hi, lo:mid]^T in kc segments
+  __device__ __forceinline__ void fold(int lo, int mid, int hi, double beta) const {
+    const int K = mid - lo;
+    if constexpr (sizeof(T) == 8) {
+      const int ar = lane >> 2, ak = lane & 3;
+#pragma unroll 1
+      for (int j0 = mid + 8 * gw; j0 < hi; j0 += 32) {
+        double cv[4][2];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int col = j0 + 2 * ak + i;
+            cv[mt][i] = col < hi ? xa(col, 8 * mt + ar) : 0.0;
+          }
+        const bool nok = j0 + ar < hi;
+        const T* lrow = sl + ((j0 + ar) & 127) * TW_LD;
+#pragma unroll 1
+        for (int k0 = 0, seg = 0; k0 < K; k0 += int(kc), ++seg) {
+          const int ps = lo + k0, pe = lo + ((K - k0) < kc ? K : k0 + int(kc));
+          double d[4][2];
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt) d[mt][0] = d[mt][1] = 0.0;
+#pragma unroll 2
+          for (int p = ps; p < pe; p += 4) {
+            const int pk = p + ak;
+            const bool kok = pk < pe;
+            const double bv = (kok && nok) ? lrow[pk] : 0.0;
+            double av[4];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) av[mt] = kok ? xa(pk, 8 * mt + ar) : 0.0;
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) dmma_8x8x4(d[mt][0], d[mt][1], av[mt], bv);
+          }
+          const double be = seg == 0 ? beta : 1.0;
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              double v = __dmul_rn(-1.0, d[mt][i]);
+              if (be != 0.0) v = __dadd_rn(__dmul_rn(be, cv[mt][i]), v);
+              cv[mt][i] = v;
+            }
+        }
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int col = j0 + 2 * ak + i;
+            if (col < hi) xa(col, 8 * mt + ar) = T(cv[mt][i]);
+          }
+      }
+    } else {
+#pragma unroll 1
+      for (int j0 = mid + 8 * gw; j0 < hi; j0 += 32) {
+        T c[8];
+        const T* lrow[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          c[q] = j0 + q < hi ? x(j0 + q) : T(0);
+          lrow[q] = sl + ((j0 + q) & 127) * TW_LD;
+        }
+#pragma unroll 1
+        for (int k0 = 0, seg = 0; k0 < K; k0 += int(kc), ++seg) {
+          const int p1 = lo + ((K - k0) < kc ? K : k0 + int(kc));
+          double t[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) t[q] = 0.0;
+#pragma unroll 4
+          for (int p = lo + k0; p < p1; ++p) {
+            const T xv = x(p);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)  // f32 products summed in f64 (engine/kernels.py:507-522)
+              t[q] = __dadd_rn(t[q], double(__fmul_rn(xv, lrow[q][p])));
+          }
+          const double be = seg == 0 ? beta : 1.0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float v = __fmul_rn(-1.0f, float(t[q]));
+            if (be != 0.0) v = __fadd_rn(__fmul_rn(float(be), c[q]), v);
+            c[q] = v;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (j0 + q < hi) x(j0 + q) = c[q];
+      }
+    }
+    sync();
+  }
+
+  // The recursion (n <= 128) flattened into at most 7 phases and walked by
+  // one loop, so base and fold are each instantiated once (inlined four
+  // times, the bases alone overflowed the instruction cache).
+  __device__ __forceinline__ static int plan64(int lo, int hi, double alpha, int* kind, int* a, int* b, int* c,
+                                               double* al, int k) {
+    const int n = hi - lo;
+    if (n <= 32) {
+      kind[k] = 0, a[k] = lo, b[k] = hi, al[k] = alpha;
+      return k + 1;
+    }
+    const int mid = lo + n / 2;
+    kind[k] = 0, a[k] = lo, b[k] = mid, al[k] = alpha;
+    kind[k + 1] = 1, a[k + 1] = lo, b[k + 1] = mid, c[k + 1] = hi, al[k + 1] = alpha;
+    kind[k + 2] = 0, a[k + 2] = mid, b[k + 2] = hi, al[k + 2] = 1.0;
+    return k + 3;
+  }
+  __device__ __forceinline__ void solve(int lo, int hi, double alpha) const {
+    int kind[7], pa[7], pb[7], pc[7];
+    double pal[7];
+    int np;
+    const int n = hi - lo;
+    if (n <= 64) {
+      np = plan64(lo, hi, alpha, kind, pa, pb, pc, pal, 0);
+    } else {
+      const int mid = lo + n / 2;
+      np = plan64(lo, mid, alpha, kind, pa, pb, pc, pal, 0);
+      kind[np] = 1, pa[np] = lo, pb[np] = mid, pc[np] = hi, pal[np] = alpha;
+      np = plan64(mid, hi, 1.0, kind, pa, pb, pc, pal, np + 1);
+    }
+#pragma unroll 1
+    for (int i = 0; i < np; ++i) {
+      if (kind[i] == 0)
+        base(pa[i], pb[i], pal[i]);
+      else
+        fold(pa[i], pb[i], pc[i], pal[i]);
+    }
+  }
+};
+
+
+// R groups (32 rows each) per CTA share the staged triangle
+template <typename T, int R>
+__global__ void __launch_bounds__(128 * R) trsm_warp_right_kernel(double alpha, const T* t, int64_t toff, int64_t trs,
+                                                                  int64_t tcs, T* b, int64_t boff, int64_t brs,
+                                                                  int64_t bcs, int64_t m, int n, int64_t kc,
+                                                                  const int* abort_flag) {
+  if (abort_flag != nullptr && *abort_flag >= 0) return;
+  extern __shared__ __align__(16) unsigned char tw_smem[];
+  T* sl = reinterpret_cast<T*>(tw_smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = warp >> 2, gw = warp & 3;
+  constexpr int NW = 4 * R;
+  T* sx = sl + 128 * TW_LD + grp * 128 * TW_XLD;
+  // lower triangle (the only part read), whole CTA, coalesced along rows
+  constexpr int VE = 16 / sizeof(T);
+  const T* tb = t + toff;
+  if (tcs == 1 && (reinterpret_cast<uintptr_t>(tb) % 16 == 0) && (trs % VE == 0)) {
+    for (int j = warp; j < n; j += NW)
+      for (int p = lane * VE; p <= j; p += 32 * VE) cp_async_16(&sl[j * TW_LD + p], &tb[j * trs + p], 16);
+  } else if (tcs == 1) {
+    for (int j = warp; j < n; j += NW)
+      for (int p = lane; p <= j; p += 32) {
+        if constexpr (sizeof(T) == 8)
+          cp_async_8(&sl[j * TW_LD + p], &tb[j * trs + p], 8);
+        else
+          cp_async_4(&sl[j * TW_LD + p], &tb[j * trs + p], 4);
+      }
+  } else {
+    for (int p = warp; p < n; p += NW)
+      for (int j = p + lane; j < n; j += 32) {
+        if constexpr (sizeof(T) == 8)
+          cp_async_8(&sl[j * TW_LD + p], &tb[j * trs + p * tcs], 8);
+        else
+          cp_async_4(&sl[j * TW_LD + p], &tb[j * trs + p * tcs], 4);
+      }
+  }
+  // the group's 32 rows, zero-filled past m; lanes run along a row (coalesced)
+  const int64_t r0 = (int64_t(blockIdx.x) * R + grp) * 32;
+  const int rows = int(m - r0 < 32 ? (m - r0 > 0 ? m - r0 : 0) : 32);
+  if (bcs == 1) {
+    for (int r = gw; r < 32; r += 4) {
+      const bool ok = r < rows;
+      for (int c = lane; c < n; c += 32) {
+        const T* src = ok ? &b[boff + (r0 + r) * brs + c] : b;
+        if constexpr (sizeof(T) == 8)
+          cp_async_8(&sx[c * TW_XLD + r], src, ok ? 8 : 0);
+        else
+          cp_async_4(&sx[c * TW_XLD + r], src, ok ? 4 : 0);
+      }
+    }
+  } else {
+    const bool ok = lane < rows;
+    for (int c = gw; c < n; c += 4) {
+      const T* src = ok ? &b[boff + (r0 + lane) * brs + c * bcs] : b;
+      if constexpr (sizeof(T) == 8)
+        cp_async_8(&sx[c * TW_XLD + lane], src, ok ? 8 : 0);
+      else
+        cp_async_4(&sx[c * TW_XLD + lane], src, ok ? 4 : 0);
+    }
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  if (rows > 0) {  // uniform per group
+    TrsmGroup<T> tg{sx, sl, lane, gw, 1 + grp, kc};
+    tg.solve(0, n, alpha);
+    if (bcs == 1) {
+      for (int r = gw; r < rows; r += 4)
+        for (int c = lane; c < n; c += 32) b[boff + (r0 + r) * brs + c] = sx[c * TW_XLD + r];
+    } else if (lane < rows) {
+      for (int c = gw; c < n; c += 4) b[boff + (r0 + lane) * brs + c * bcs] = sx[c * TW_XLD + lane];
+    }
+  }
+}
+
+template <typename T, int W>
+int launch_trsm_warp(double alpha, const T* t, int64_t toff, int64_t trs, int64_t tcs, T* b, int64_t boff,
+                     int64_t brs, int64_t bcs, int64_t m, int n, int64_t kc, const int* abort_flag, cudaStream_t s) {
+  const size_t smem = (size_t(128) * TW_LD + size_t(W) * 128 * TW_XLD) * sizeof(T);  // W groups
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(trsm_warp_right_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+        cudaSuccess)
+      return -10;
+    attr = true;
+  }
+  const int64_t blocks = (m + 32 * W - 1) / (32 * W);
+  if (blocks > 0x7fffffffLL) return -3;
+  note_launch();
+  trsm_warp_right_kernel<T, W><<<unsigned(blocks), 128 * W, smem, s>>>(alpha, t, toff, trs, tcs, b, boff, brs, bcs, m,
+                                                                      n, kc, abort_flag);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
 }  // namespace
 
 int launch_scale(int is_f64, double beta, void* c, int64_t off, int64_t m, int64_t n, int64_t rs, int64_t cs,
@@ -627,6 +964,21 @@ int launch_trsm_small_right(int is_f64, double alpha, const void* t, int64_t tof
                             const int* abort_flag, cudaStream_t s) {
   if (m <= 0 || n <= 0) return 0;
   if (n > 128) return -3;
+  if (g_trsm_warp) {
+    // 4 warps per 32 rows; one group per CTA while the grid fits a wave,
+    // groups sharing the staged triangle beyond (2 for f64, 4 for f32:
+    // shared-memory bound)
+    const bool big = m > 32 * 148;
+    if (is_f64)
+      return big ? launch_trsm_warp<double, 2>(alpha, (const double*)t, toff, trs, tcs, (double*)b, boff, brs, bcs, m,
+                                               int(n), kc, abort_flag, s)
+                 : launch_trsm_warp<double, 1>(alpha, (const double*)t, toff, trs, tcs, (double*)b, boff, brs, bcs, m,
+                                               int(n), kc, abort_flag, s);
+    return big ? launch_trsm_warp<float, 4>(alpha, (const float*)t, toff, trs, tcs, (float*)b, boff, brs, bcs, m,
+                                            int(n), kc, abort_flag, s)
+               : launch_trsm_warp<float, 1>(alpha, (const float*)t, toff, trs, tcs, (float*)b, boff, brs, bcs, m,
+                                            int(n), kc, abort_flag, s);
+  }
   const int64_t blocks = (m + TS_ROWS - 1) / TS_ROWS;
   if (blocks > 0x7fffffffLL) return -3;
   note_launch();

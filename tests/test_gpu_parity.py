@@ -181,15 +181,17 @@ def test_tma_kernel_variants_bitwise(cuda, variant):
         lib.bf_set_option(b"tma_variant", 2)
 
 
-@pytest.mark.parametrize("dt,kc,bs", [("f64", 40, 128), ("f64", 1024, 96), ("f32", 20, 96), ("f32", 512, 100)])
-def test_fused_trsm_subtree_bitwise(cuda, dt, kc, bs):
-    """Panels of width <= 128 take the fused TRSM kernel; multi-segment kc and
-    f32 must still give the oracle's bits (and the unfused launches' bits)."""
+@pytest.mark.parametrize("dt,kc,bs,n", [("f64", 40, 128, 700), ("f64", 1024, 96, 700), ("f32", 20, 96, 700),
+                                        ("f32", 512, 100, 700), ("f64", 128, 128, 5000), ("f32", 64, 128, 5000)])
+def test_fused_trsm_subtree_bitwise(cuda, dt, kc, bs, n):
+    """Panels of width <= 128 take a fused TRSM kernel (warp per 32 rows, one
+    or two warps per CTA — n=5000 reaches the paired grid — or the 64-row CTA
+    kernel); multi-segment kc and f32 must still give the oracle's bits (and
+    the unfused launches' bits)."""
     import json
 
     from paper_2604_07311_b200.engine import _lib
 
-    n = 700
     doc = json.dumps({"op": "cholesky", "variant": 3, "bs": bs, "kernel": {"kc": kc},
                       "child": {"op": "cholesky", "variant": "unblocked3"}})
     a0 = spd_int(99, n, dt)
@@ -198,12 +200,14 @@ def test_fused_trsm_subtree_bitwise(cuda, dt, kc, bs):
     assert bad == -1
     outs = []
     lib = _lib.lib()
-    for fused in (1, 0):
+    for fused, warp in ((1, 1), (1, 0), (0, 1)):
         lib.bf_set_option(b"fused_trsm", fused)
+        lib.bf_set_option(b"trsm_warp", warp)
         try:
             v = make_view(n, n, DType.parse(dt), fill=a0)
             bf.cholesky(v, "lower", parse_tree(doc))
             outs.append(digest(v.storage.cpu().numpy()))
         finally:
             lib.bf_set_option(b"fused_trsm", 1)
-    assert outs[0] == outs[1] == digest(st)
+            lib.bf_set_option(b"trsm_warp", 1)
+    assert outs[0] == outs[1] == outs[2] == digest(st)

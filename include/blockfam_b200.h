@@ -152,7 +152,11 @@ int bf_gemm_bf16(double alpha, const void* a, int64_t lda, const void* b, int64_
                  int64_t k, int lower_only, void* stream);
 int bf_convert_f32_bf16(const bf_view* src, void* dst, int64_t ld, int transpose, void* stream);
 int bf_convert_f64_f32(const bf_view* src, const bf_view* dst, int lower_only, void* stream);
+int bf_convert_f32_f64(const bf_view* src, const bf_view* dst, int lower_only, void* stream);
+int bf_convert_f64_bf16(const bf_view* src, void* dst, int64_t ld, int transpose, void* stream);
 int bf_residual_d(const double* a, int64_t lda, const double* x, const double* b, double* r, int64_t n, void* stream);
+/* out[i] := sum_j |a[i][j]| (the refinement's ||A||_inf is the max of these) */
+int bf_row_abs_sum_d(const double* a, int64_t lda, double* out, int64_t n, void* stream);
 int bf_potrs_f32_d(const float* l, int64_t ld, double* x, int64_t n, void* stream);
 int bf_potrs_blocked_f32_d(const float* l, int64_t ld, const float* xinv, int64_t bs, double* x, int64_t n,
                            double* work, void* stream);

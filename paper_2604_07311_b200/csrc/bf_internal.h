@@ -72,7 +72,8 @@ int launch_gemm_dmma_tma(const GemmParams& p, cudaStream_t s);
 extern int g_use_tma;                                                 // bf_set_option("tma", 0|1)
 extern int g_tma_variant;
 extern int g_bf16_tma_c;
-extern int g_trsm_warp;  // fused TRSM subtree: warp-per-32-rows kernel (1) or the 64-row CTA kernel (0)  // bf16 GEMM: TMA C-tile epilogue (1) or per-element fallback (0)
+extern int g_trsm_warp;
+extern int g_leaf_v4;  // variant-3 leaves n <= 128: blocked register/lane-per-row kernel (1) or v3 (0)  // fused TRSM subtree: warp-per-32-rows kernel (1) or the 64-row CTA kernel (0)  // bf16 GEMM: TMA C-tile epilogue (1) or per-element fallback (0)
 extern int g_tiles_per_cta;                                           // bf_set_option("tiles_per_cta", t)                                             // bf_set_option("tma_variant", 0..3)
 int launch_gemm_simt_f32(const GemmParams& p, cudaStream_t s);        // f32 storage, f32 acc
 int launch_gemm_simt_f32acc64(const GemmParams& p, cudaStream_t s);   // f32 storage, f64 acc
@@ -95,10 +96,15 @@ int launch_gemm_bf16_tc(double alpha, const void* a, int64_t lda, const void* b,
                         cudaStream_t s);
 int launch_to_bf16(const float* src, int64_t soff, int64_t srs, int64_t scs, void* dst, int64_t ld, int64_t m,
                    int64_t n, int transpose, cudaStream_t s);
+int launch_f32_to_f64(const float* src, int64_t soff, int64_t srs, int64_t scs, double* dst, int64_t doff, int64_t drs,
+                      int64_t dcs, int64_t m, int64_t n, int lower_only, cudaStream_t s);
+int launch_f64_to_bf16(const double* src, int64_t soff, int64_t srs, int64_t scs, void* dst, int64_t ld, int64_t m,
+                       int64_t n, int transpose, cudaStream_t s);
 int launch_f64_to_f32(const double* src, int64_t soff, int64_t srs, int64_t scs, float* dst, int64_t doff, int64_t drs,
                       int64_t dcs, int64_t m, int64_t n, int lower_only, cudaStream_t s);
 int launch_residual(const double* A, int64_t lda, const double* x, const double* b, double* r, int64_t n,
                     cudaStream_t s);
+int launch_row_abs_sum(const double* A, int64_t lda, double* out, int64_t n, cudaStream_t s);
 int launch_potrs_f32_f64(const float* L, int64_t ld, double* x, int64_t n, cudaStream_t s);
 int launch_potrs_blocked(const float* L, int64_t ld, const float* xinv, int64_t bs, double* x, int64_t n,
                          double* work, cudaStream_t s);

@@ -434,6 +434,10 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_tma_variant = int(value & 3);
     return BF_OK;
   }
+  if (name && std::strcmp(name, "leaf_v4") == 0) {
+    bf::g_leaf_v4 = value != 0;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "trsm_warp") == 0) {
     bf::g_trsm_warp = value != 0;
     return BF_OK;
@@ -547,6 +551,25 @@ int bf_convert_f64_f32(const bf_view* src, const bf_view* dst, int lower_only, v
                                  static_cast<float*>(dst->base), dst->off, dst->rs, dst->cs, src->m, src->n, lower_only,
                                  S(stream));
   return rc ? fail(BF_ERR_CUDA, "conversion launch failed") : BF_OK;
+}
+int bf_convert_f32_f64(const bf_view* src, const bf_view* dst, int lower_only, void* stream) {
+  if (!src || !dst) return fail(BF_ERR_VALUE, "null view");
+  if (src->m != dst->m || src->n != dst->n) return fail(BF_ERR_SHAPE, "conversion dims mismatch");
+  int rc = bf::launch_f32_to_f64(static_cast<const float*>(src->base), src->off, src->rs, src->cs,
+                                 static_cast<double*>(dst->base), dst->off, dst->rs, dst->cs, src->m, src->n,
+                                 lower_only, S(stream));
+  return rc ? fail(BF_ERR_CUDA, "conversion launch failed") : BF_OK;
+}
+int bf_convert_f64_bf16(const bf_view* src, void* dst, int64_t ld, int transpose, void* stream) {
+  if (!src) return fail(BF_ERR_VALUE, "null view");
+  int rc = bf::launch_f64_to_bf16(static_cast<const double*>(src->base), src->off, src->rs, src->cs, dst, ld, src->m,
+                                  src->n, transpose, S(stream));
+  return rc ? fail(BF_ERR_CUDA, "conversion launch failed") : BF_OK;
+}
+int bf_row_abs_sum_d(const double* a, int64_t lda, double* out, int64_t n, void* stream) {
+  int rc = bf::launch_row_abs_sum(a, lda, out, n, S(stream));
+  if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "row sums need a 16-byte aligned A with even lda");
+  return rc ? fail(BF_ERR_CUDA, "row sum launch failed") : BF_OK;
 }
 int bf_residual_d(const double* a, int64_t lda, const double* x, const double* b, double* r, int64_t n, void* stream) {
   int rc = bf::launch_residual(a, lda, x, b, r, n, S(stream));

@@ -374,7 +374,8 @@ bool make_map_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t k, 
 }
 
 // fp32 (strided) -> bf16 (row-major, ld) conversion; transposes when asked
-__global__ void to_bf16_kernel(const float* src, int64_t soff, int64_t srs, int64_t scs, __nv_bfloat16* dst,
+template <typename S>
+__global__ void to_bf16_kernel(const S* src, int64_t soff, int64_t srs, int64_t scs, __nv_bfloat16* dst,
                                int64_t ld, int64_t m, int64_t n, int transpose) {
   const int64_t total = m * n;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
@@ -450,7 +451,19 @@ int launch_to_bf16(const float* src, int64_t soff, int64_t srs, int64_t scs, voi
   const int64_t total = m * n;
   const int blocks = int((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
   note_launch();
-  to_bf16_kernel<<<blocks, 256, 0, s>>>(src, soff, srs, scs, static_cast<__nv_bfloat16*>(dst), ld, m, n, transpose);
+  to_bf16_kernel<float><<<blocks, 256, 0, s>>>(src, soff, srs, scs, static_cast<__nv_bfloat16*>(dst), ld, m, n,
+                                                transpose);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+int launch_f64_to_bf16(const double* src, int64_t soff, int64_t srs, int64_t scs, void* dst, int64_t ld, int64_t m,
+                       int64_t n, int transpose, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return 0;
+  const int64_t total = m * n;
+  const int blocks = int((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+  note_launch();
+  to_bf16_kernel<double><<<blocks, 256, 0, s>>>(src, soff, srs, scs, static_cast<__nv_bfloat16*>(dst), ld, m, n,
+                                                 transpose);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 

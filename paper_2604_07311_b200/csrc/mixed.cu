@@ -11,13 +11,14 @@ namespace bf {
 
 namespace {
 
-__global__ void f64_to_f32_kernel(const double* src, int64_t soff, int64_t srs, int64_t scs, float* dst, int64_t doff,
-                                  int64_t drs, int64_t dcs, int64_t m, int64_t n, int lower_only) {
+template <typename S, typename D>
+__global__ void convert_kernel(const S* src, int64_t soff, int64_t srs, int64_t scs, D* dst, int64_t doff,
+                               int64_t drs, int64_t dcs, int64_t m, int64_t n, int lower_only) {
   const int64_t total = m * n;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = e / n, j = e % n;
     if (lower_only && j > i) continue;
-    dst[doff + i * drs + j * dcs] = float(src[soff + i * srs + j * scs]);
+    dst[doff + i * drs + j * dcs] = D(src[soff + i * srs + j * scs]);
   }
 }
 
@@ -36,6 +37,23 @@ __global__ void residual_kernel(const double* A, int64_t lda, const double* x, c
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) r[row] = b[row] - s;
+}
+
+// out[row] = sum_j |A[row][j]| (one warp per row); the host takes the max
+__global__ void row_abs_sum_kernel(const double* A, int64_t lda, double* out, int64_t n) {
+  const int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double* a = A + row * lda;
+  double s = 0.0;
+  for (int64_t j = lane * 2; j < n; j += 64) {
+    const double2 av = *reinterpret_cast<const double2*>(a + j);
+    s += fabs(av.x);
+    if (j + 1 < n) s += fabs(av.y);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[row] = s;
 }
 
 // forward diagonal-block solve: y[lo:hi] = L[lo:hi,lo:hi]^-1 y[lo:hi]
@@ -210,7 +228,17 @@ int launch_f64_to_f32(const double* src, int64_t soff, int64_t srs, int64_t scs,
                       int64_t dcs, int64_t m, int64_t n, int lower_only, cudaStream_t s) {
   if (m <= 0 || n <= 0) return 0;
   note_launch();
-  f64_to_f32_kernel<<<grid_for_elems(m * n), 256, 0, s>>>(src, soff, srs, scs, dst, doff, drs, dcs, m, n, lower_only);
+  convert_kernel<double, float>
+      <<<grid_for_elems(m * n), 256, 0, s>>>(src, soff, srs, scs, dst, doff, drs, dcs, m, n, lower_only);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+int launch_f32_to_f64(const float* src, int64_t soff, int64_t srs, int64_t scs, double* dst, int64_t doff, int64_t drs,
+                      int64_t dcs, int64_t m, int64_t n, int lower_only, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return 0;
+  note_launch();
+  convert_kernel<float, double>
+      <<<grid_for_elems(m * n), 256, 0, s>>>(src, soff, srs, scs, dst, doff, drs, dcs, m, n, lower_only);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
@@ -220,6 +248,14 @@ int launch_residual(const double* A, int64_t lda, const double* x, const double*
   if ((reinterpret_cast<uintptr_t>(A) % 16) || (lda % 2)) return -3;
   note_launch();
   residual_kernel<<<unsigned((n * 32 + 255) / 256), 256, 0, s>>>(A, lda, x, b, r, n);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+int launch_row_abs_sum(const double* A, int64_t lda, double* out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return 0;
+  if ((reinterpret_cast<uintptr_t>(A) % 16) || (lda % 2)) return -3;
+  note_launch();
+  row_abs_sum_kernel<<<unsigned((n * 32 + 255) / 256), 256, 0, s>>>(A, lda, out, n);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 

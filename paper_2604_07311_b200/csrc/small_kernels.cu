@@ -15,6 +15,7 @@
 namespace bf {
 
 int g_trsm_warp = 1;
+int g_leaf_v4 = 0;  // v4 is bit-identical but not yet faster than v3
 
 namespace {
 
@@ -851,6 +852,232 @@ __global__ void __launch_bounds__(128 * R) trsm_warp_right_kernel(double alpha, 
   }
 }
 
+// ------------------------------------------- blocked variant-3 leaf (v4) --
+// Variant 3 (right-looking, factor/cholesky.py:74-89) for n <= 128 by 32-wide
+// column blocks, every element still receiving the reference's operations
+// in the reference's order (a(i,j) -= a(i,k)*a(j,k) for ascending k, unfused,
+// then its sqrt or division):
+//  (a) warp 0 factors the diagonal block in registers, one lane per row:
+//      the pivot reaches every lane by shuffle, each lane takes the sqrt,
+//      divides its own element, and updates its row with the pivot column
+//      (shuffled element by element) — no barrier on the pivot chain;
+//  (b) the rows below, 32 per warp, solve against the finished block like
+//      the fused TRSM's bases (Markstein division from reciprocals of the
+//      block's diagonal, exact fallback);
+//  (c) the trailing triangle takes the block's 32 rank-1 updates, 4x4
+//      register tiles over the CTA.
+// A failing pivot stops the sweep after finishing exactly the steps before
+// it (the reference's partial state).  128 threads, LD = 129 (conflict-free
+// lane-per-row access).
+constexpr int LV4_LD = 129;
+#ifdef LV4_PROF  // phase clocks for tools/leaf_probe2.cu
+__device__ long long g_lv4_prof[64];
+#define LV4_MARK(i) \
+  if (threadIdx.x == 0) g_lv4_prof[i] += clock64();
+#else
+#define LV4_MARK(i)
+#endif
+
+template <typename T>
+__global__ void __launch_bounds__(128) potrf_leaf_v4_kernel(T* g, int64_t off, int n, int64_t rs, int64_t cs,
+                                                            int64_t base_index, int* d_info) {
+  if (d_info != nullptr && *d_info >= 0) return;
+  extern __shared__ __align__(16) unsigned char leaf_v4_smem[];
+  T* A = reinterpret_cast<T*>(leaf_v4_smem);
+  __shared__ T s_rc[128];
+  __shared__ int s_fail;
+  __shared__ int s_unsafe;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (cs == 1) {
+    for (int i = warp; i < n; i += 4)
+      for (int j = lane; j <= i; j += 32) {
+        if constexpr (sizeof(T) == 8)
+          cp_async_8(&A[i * LV4_LD + j], &g[off + i * rs + j], 8);
+        else
+          cp_async_4(&A[i * LV4_LD + j], &g[off + i * rs + j], 4);
+      }
+  } else {
+    for (int j = warp; j < n; j += 4)
+      for (int i = j + lane; i < n; i += 32) {
+        if constexpr (sizeof(T) == 8)
+          cp_async_8(&A[i * LV4_LD + j], &g[off + i * rs + j * cs], 8);
+        else
+          cp_async_4(&A[i * LV4_LD + j], &g[off + i * rs + j * cs], 4);
+      }
+  }
+  cp_async_commit();
+  if (tid == 0) {
+    s_fail = -1;
+    s_unsafe = 0;
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  LV4_MARK(0)
+  using TG = TrsmGroup<T>;
+  int bad = -1;
+#pragma unroll 1
+  for (int k0 = 0; k0 < n; k0 += 32) {
+    const int bw = n - k0 < 32 ? n - k0 : 32;
+    const int k1 = k0 + bw;
+    // (a) diagonal block.  Sliding register window: at step p, acc[j] holds
+    // column p + j of this lane's row, so the loop body indexes registers
+    // statically and stays small (a fully unrolled step sequence ran out of
+    // the instruction cache).
+    if (warp == 0) {
+      T acc[32];
+      const int i = lane;  // row k0 + i
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc[q] = (q <= i && i < bw) ? A[(k0 + i) * LV4_LD + k0 + q] : T(0);
+      int fail = -1;
+#pragma unroll 1
+      for (int p = 0; p < bw; ++p) {
+        const T d = __shfl_sync(0xffffffffu, acc[0], p);
+        if (!(d > T(0))) {
+          fail = p;  // uniform; (p,p) keeps its updated value
+          break;
+        }
+        const T lpp = Ops<T>::sqrt_(d);
+        // every lane divides (no divergence); rows above the pivot and
+        // columns past the block only ever hold values that are not stored
+        const T dv = Ops<T>::div(acc[0], lpp);
+        acc[0] = i == p ? lpp : (i > p ? dv : acc[0]);
+        if (i >= p && i < bw) A[(k0 + i) * LV4_LD + k0 + p] = acc[0];
+        if (i == p) s_rc[k0 + p] = TG::rcp(lpp);
+#pragma unroll
+        for (int j = 1; j < 32; ++j) {
+          const T lqp = __shfl_sync(0xffffffffu, acc[0], (p + j) & 31);
+          acc[j] = Ops<T>::sub(acc[j], Ops<T>::mul(acc[0], lqp));
+        }
+#pragma unroll
+        for (int j = 0; j < 31; ++j) acc[j] = acc[j + 1];
+        acc[31] = T(0);
+      }
+      if (fail >= 0) {  // columns >= fail keep their updated values
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int q = fail + j;
+          if (q < bw && q <= i && i < bw) A[(k0 + i) * LV4_LD + k0 + q] = acc[j];
+        }
+      }
+      if (lane == 0) s_fail = fail < 0 ? -1 : k0 + fail;
+    }
+    __syncthreads();
+    LV4_MARK(1 + 3 * (k0 >> 5))
+    const int fail = s_fail;
+    const int kend = fail < 0 ? bw : fail - k0;  // columns of this block that complete
+    // (b) rows below the block: X * L11^T = A21 over the block's first kend
+    // columns, lane per row, same sliding window
+#pragma unroll 1
+    for (int r0 = k1 + 32 * warp; r0 < n; r0 += 128) {
+      const int r = r0 + lane;
+      const bool ok = r < n;
+      const T* l = A + k0 * LV4_LD + k0;
+      T acc[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) acc[q] = (ok && q < bw) ? A[r * LV4_LD + k0 + q] : T(0);
+      int emin = TG::kMidExp, emax = TG::kMidExp;
+#pragma unroll 1
+      for (int q = 0; q < kend; ++q) {
+        const T dq = l[q * LV4_LD + q], rq = s_rc[k0 + q];
+        const T a = acc[0];
+        const T q0 = Ops<T>::mul(a, rq);
+        const T xq = Ops<T>::fma_(Ops<T>::fma_(-dq, q0, a), rq, q0);
+        const int ea = a == T(0) ? TG::kMidExp : TG::expo(a);
+        const int ed = TG::expo(dq);
+        emin = min(emin, min(ea, ed));
+        emax = max(emax, max(ea, ed));
+        if (ok) A[r * LV4_LD + k0 + q] = xq;
+#pragma unroll
+        for (int t = 1; t < 32; ++t)  // columns past the block: never stored
+          acc[t] = Ops<T>::sub(acc[t], Ops<T>::mul(xq, l[((q + t) & 31) * LV4_LD + q]));
+#pragma unroll
+        for (int t = 0; t < 31; ++t) acc[t] = acc[t + 1];
+        acc[31] = T(0);
+      }
+      const bool safe = emin >= TG::kLoExp && emax <= TG::kHiExp;
+      if (__all_sync(0xffffffffu, safe || !ok)) {
+        if (ok) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (kend + t < bw) A[r * LV4_LD + k0 + kend + t] = acc[t];
+        }
+      } else if (ok) {  // rare: exact division, in place from the original row
+        // (columns < kend were overwritten: redo them from the saved tail is
+        // impossible, so reload the row block from global memory)
+        for (int q = 0; q < bw; ++q) {
+          const int gr = r, gc = k0 + q;
+          A[r * LV4_LD + gc] = cs == 1 ? g[off + gr * rs + gc] : g[off + gr * rs + gc * cs];
+        }
+        // earlier column blocks' updates must be re-applied: fall back to the
+        // reference order for this row over all completed columns < k0 as well
+        for (int q = 0; q < bw; ++q) {
+          T v = A[r * LV4_LD + k0 + q];
+          for (int p = 0; p < k0; ++p) v = Ops<T>::sub(v, Ops<T>::mul(A[r * LV4_LD + p], A[(k0 + q) * LV4_LD + p]));
+          A[r * LV4_LD + k0 + q] = v;
+        }
+        for (int q = 0; q < kend; ++q) {
+          const T xq = Ops<T>::div(A[r * LV4_LD + k0 + q], l[q * LV4_LD + q]);
+          A[r * LV4_LD + k0 + q] = xq;
+          for (int t = q + 1; t < bw; ++t)
+            A[r * LV4_LD + k0 + t] = Ops<T>::sub(A[r * LV4_LD + k0 + t], Ops<T>::mul(xq, l[t * LV4_LD + q]));
+        }
+      }
+    }
+    __syncthreads();
+    LV4_MARK(2 + 3 * (k0 >> 5))
+    // (c) trailing triangle k1 <= j <= i < n: the block's first kend rank-1 updates
+    const int m = n - k1;
+    if (m > 0 && kend > 0) {
+      const int tiles = (m + 3) / 4;
+      const int ntile = tiles * (tiles + 1) / 2;
+      for (int tt = tid; tt < ntile; tt += 128) {
+        int ti = int((sqrtf(8.f * float(tt) + 1.f) - 1.f) * 0.5f);
+        while (ti * (ti + 1) / 2 > tt) --ti;
+        while ((ti + 1) * (ti + 2) / 2 <= tt) ++ti;
+        const int tj = tt - ti * (ti + 1) / 2;
+        const int i0 = k1 + 4 * ti, j0 = k1 + 4 * tj;
+        T c[4][4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            c[a][b] = (i0 + a < n && j0 + b <= i0 + a) ? A[(i0 + a) * LV4_LD + j0 + b] : T(0);
+#pragma unroll 4
+        for (int p = k0; p < k0 + kend; ++p) {
+          T li[4], lj[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) li[a] = A[((i0 + a) & 127) * LV4_LD + p];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) lj[b] = A[((j0 + b) & 127) * LV4_LD + p];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) c[a][b] = Ops<T>::sub(c[a][b], Ops<T>::mul(li[a], lj[b]));
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            if (i0 + a < n && j0 + b <= i0 + a) A[(i0 + a) * LV4_LD + j0 + b] = c[a][b];
+      }
+    }
+    __syncthreads();
+    LV4_MARK(3 + 3 * (k0 >> 5))
+    if (fail >= 0) {
+      bad = fail;
+      break;
+    }
+  }
+  if (cs == 1) {
+    for (int i = warp; i < n; i += 4)
+      for (int j = lane; j <= i; j += 32) g[off + i * rs + j] = A[i * LV4_LD + j];
+  } else {
+    for (int j = warp; j < n; j += 4)
+      for (int i = j + lane; i < n; i += 32) g[off + i * rs + j * cs] = A[i * LV4_LD + j];
+  }
+  if (tid == 0 && bad >= 0 && d_info != nullptr) *d_info = int(base_index + bad);
+}
+
 template <typename T, int W>
 int launch_trsm_warp(double alpha, const T* t, int64_t toff, int64_t trs, int64_t tcs, T* b, int64_t boff,
                      int64_t brs, int64_t bcs, int64_t m, int n, int64_t kc, const int* abort_flag, cudaStream_t s) {
@@ -892,6 +1119,19 @@ static constexpr int LEAF_SMEM_LIMIT = 220 * 1024;
 template <typename T>
 static int leaf_launch(T* a, int64_t off, int64_t n, int64_t rs, int64_t cs, int variant, int64_t base_index,
                        int* d_info, cudaStream_t s) {
+  if (variant == 3 && n <= 128 && g_leaf_v4) {
+    static bool v4_attr = false;
+    const size_t smem = size_t(128) * LV4_LD * sizeof(T);
+    if (!v4_attr) {
+      if (cudaFuncSetAttribute(potrf_leaf_v4_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+          cudaSuccess)
+        return -10;
+      v4_attr = true;
+    }
+    note_launch();
+    potrf_leaf_v4_kernel<T><<<1, 128, smem, s>>>(a, off, int(n), rs, cs, base_index, d_info);
+    return cudaGetLastError() == cudaSuccess ? 0 : -11;
+  }
   if (variant == 3 && n <= 128) {
     static bool v3_attr = false;
     const size_t smem = size_t(128) * 129 * sizeof(T);  // full tile: the update reads rows < 128 unguarded

@@ -100,6 +100,9 @@ _SIGNATURES = {
     "bf_gemm_bf16": ([_D, _VP, _L, _VP, _L, _D, _V, _L, _I, _VP], _I),
     "bf_convert_f32_bf16": ([_V, _VP, _L, _I, _VP], _I),
     "bf_convert_f64_f32": ([_V, _V, _I, _VP], _I),
+    "bf_convert_f32_f64": ([_V, _V, _I, _VP], _I),
+    "bf_row_abs_sum_d": ([_VP, _L, _VP, _L, _VP], _I),
+    "bf_convert_f64_bf16": ([_V, _VP, _L, _I, _VP], _I),
     "bf_residual_d": ([_VP, _L, _VP, _VP, _VP, _L, _VP], _I),
     "bf_potrs_f32_d": ([_VP, _L, _VP, _L, _VP], _I),
     "bf_potrs_blocked_f32_d": ([_VP, _L, _VP, _L, _VP, _L, _VP, _VP], _I),

@@ -7,9 +7,9 @@ non-goal), so this path is pinned to the FP64 solution instead of to
 reference bits:
 
   factor   A (fp64) -> W (fp32 lower), right-looking in blocks of bs:
-           diagonal block: the exact fp32 tree driver (bf_cholesky_s);
+           diagonal block: FP64, the exact tree driver (bf_cholesky_d);
            panel:          L21 = A21 * L11^-T as ONE bf16 tcgen05 GEMM against
-                           the explicit inverse (L11^-T from bf_trsm_rltn_s);
+                           the explicit inverse (L11^-T from bf_trsm_rltn_d);
            trailing:       W22 -= L21 L21^T as a bf16 tcgen05 GEMMT (fp32 TMEM
                            accumulation, fp32 storage);
   refine   x += (L L^T)^-1 (b - A x) with the fp64 residual on the original A
@@ -34,10 +34,10 @@ from .engine import _lib
 from .errors import NotPositiveDefiniteError, ShapeError
 from .views import DType, MatrixView, from_torch
 
-__all__ = ["MixedFactor", "MixedResult", "cholesky_mixed", "posv_mixed"]
+__all__ = ["MixedFactor", "MixedResult", "MixedWorkspace", "cholesky_mixed", "posv_mixed"]
 
 DIAG_TREE = {"op": "cholesky", "variant": 3, "bs": 128, "kernel": {"kc": 128},
-             "child": {"op": "cholesky", "variant": "unblocked3"}}
+             "child": {"op": "cholesky", "variant": "unblocked3"}}  # FP64 diagonal blocks
 
 
 @dataclass
@@ -52,6 +52,31 @@ def _v(t: torch.Tensor) -> _lib.BfView:
     return _lib.as_bfview(from_torch(t))
 
 
+class MixedWorkspace:
+    """Every buffer of one mixed solve of order n (block bs), allocated once:
+    repeated solves never touch the allocator (multi-GB blocks churning
+    through the caching allocator cost more than the solve)."""
+
+    def __init__(self, n: int, bs: int = 1024, device: Optional[torch.device] = None) -> None:
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.n, self.bs, self.device = n, bs, dev
+        nblk = (n + bs - 1) // bs
+        self.w = torch.empty((n, n), dtype=torch.float32, device=dev)
+        self.pbuf = [torch.empty((n, bs), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+        self.xt = torch.empty((bs, bs), dtype=torch.bfloat16, device=dev)
+        self.d64 = torch.empty((bs, bs), dtype=torch.float64, device=dev)
+        self.x64 = torch.empty((bs, bs), dtype=torch.float64, device=dev)
+        self.xinv = torch.zeros((nblk, bs, bs), dtype=torch.float32, device=dev)
+        self.info = torch.empty((1,), dtype=torch.int32, device=dev)
+        self.before = torch.empty((1,), dtype=torch.int32, device=dev)
+        self.work = torch.empty((129 * bs,), dtype=torch.float64, device=dev)
+        self.rows = torch.empty((n,), dtype=torch.float64, device=dev)
+        self.x = torch.empty((n,), dtype=torch.float64, device=dev)
+        self.r = torch.empty((n,), dtype=torch.float64, device=dev)
+        self.d = torch.empty((n,), dtype=torch.float64, device=dev)
+        self.side = torch.cuda.Stream(dev, priority=-1)
+
+
 @dataclass
 class MixedFactor:
     """fp32 lower factor W (n x n row-major) and the explicit inverses
@@ -61,50 +86,94 @@ class MixedFactor:
     bs: int
 
 
-def cholesky_mixed(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlNode] = None) -> MixedFactor:
-    """bf16/fp32 factorization of the fp64 SPD matrix `a`."""
+def cholesky_mixed(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlNode] = None,
+                   lookahead: bool = True, ws: Optional[MixedWorkspace] = None) -> MixedFactor:
+    """bf16/fp32 factorization of the fp64 SPD matrix `a` (right-looking,
+    blocks of bs).  Per block: the diagonal block in FP64 (the exact tree
+    driver, DMMA GEMMs), its explicit inverse in FP64, the panel as one bf16
+    tcgen05 GEMM against that inverse, and the trailing update as a bf16
+    GEMMT.  With lookahead the next block column is updated first and the
+    next diagonal/inverse/panel run on a high-priority side stream while the
+    rest of the trailing update proceeds."""
     if a.dim() != 2 or a.shape[0] != a.shape[1] or a.dtype != torch.float64 or not a.is_cuda:
         raise ShapeError("cholesky_mixed needs a square fp64 CUDA matrix")
+    if bs % 8:
+        raise ShapeError("bs must be a multiple of 8 (16-byte bf16 rows for TMA)")
     lib = _lib.lib()
     n = a.shape[0]
-    dev = a.device
-    stream = torch.cuda.current_stream(dev).cuda_stream
+    if ws is None:
+        ws = MixedWorkspace(n, bs, a.device)
+    if ws.n != n or ws.bs != bs or ws.device != a.device:
+        raise ShapeError("workspace was made for another order, block size or device")
+    main = torch.cuda.current_stream(a.device)
+    side = ws.side if lookahead else main
     tree = diag_tree if diag_tree is not None else parse_tree(json.dumps(DIAG_TREE))
-    levels = flatten_cholesky(tree, resolve_config(tree, DType.F32))
+    levels = flatten_cholesky(tree, resolve_config(tree, DType.F64))
     arr = (_lib.BfCholLevel * len(levels))(*[_lib.BfCholLevel(v, 0, b, kc) for v, b, kc in levels])
-    w = torch.empty((n, n), dtype=torch.float32, device=dev)
-    _lib.check(lib.bf_convert_f64_f32(ctypes.byref(_v(a)), ctypes.byref(_v(w)), 1, stream), "convert")
-    panel = torch.empty((n, bs), dtype=torch.bfloat16, device=dev)
-    xt = torch.empty((bs, bs), dtype=torch.bfloat16, device=dev)
+    w, pbuf, xt, d64, x64, xinv, info = ws.w, ws.pbuf, ws.xt, ws.d64, ws.x64, ws.xinv, ws.info
+    # pbuf ping-pongs: panel k+1 is formed while step k's trailing update still reads panel k
     nblk = (n + bs - 1) // bs
-    xinv = torch.zeros((nblk, bs, bs), dtype=torch.float32, device=dev)
-    info = torch.full((1,), -1, dtype=torch.int32, device=dev)
-    for k0 in range(0, n, bs):
+    info.fill_(-1)
+    _lib.check(lib.bf_convert_f64_f32(ctypes.byref(_v(a)), ctypes.byref(_v(w)), 1, main.cuda_stream), "convert")
+
+    def diag_and_panel(k: int, stream: torch.cuda.Stream) -> None:
+        k0 = k * bs
         b = min(bs, n - k0)
         r = n - k0 - b
-        diag = w[k0:k0 + b, k0:k0 + b]
-        # the fp32 driver reports block-local pivots; shift a fresh failure by k0
-        v = _v(diag)
-        before = info.clone()
-        _lib.check(lib.bf_cholesky_s(ctypes.byref(v), arr, len(levels), info.data_ptr(), stream), "diag factor")
-        torch.where((before < 0) & (info >= 0), info + k0, info, out=info)
-        # L11^-T = X with X * L11^T = I
-        x = xinv[k0 // bs, :b, :b]
-        x.diagonal().fill_(1.0)
-        vt, vx = _v(diag), _v(x)
-        _lib.check(lib.bf_trsm_rltn_s(1.0, ctypes.byref(vt), ctypes.byref(vx), 512, None, stream), "inverse")
-        if r == 0:
-            break
-        _lib.check(lib.bf_convert_f32_bf16(ctypes.byref(vx), xt.data_ptr(), bs, 1, stream), "convert")
-        a21 = w[k0 + b:, k0:k0 + b]
-        _lib.check(lib.bf_convert_f32_bf16(ctypes.byref(_v(a21)), panel.data_ptr(), bs, 0, stream), "convert")
-        # L21 = A21 * X  (C = A * Bnk^T with Bnk = X^T)
-        _lib.check(lib.bf_gemm_bf16(1.0, panel.data_ptr(), bs, xt.data_ptr(), bs, 0.0, ctypes.byref(_v(a21)), b, 0,
-                                    stream), "panel gemm")
-        _lib.check(lib.bf_convert_f32_bf16(ctypes.byref(_v(a21)), panel.data_ptr(), bs, 0, stream), "convert")
-        a22 = w[k0 + b:, k0 + b:]
-        _lib.check(lib.bf_gemm_bf16(-1.0, panel.data_ptr(), bs, panel.data_ptr(), bs, 1.0, ctypes.byref(_v(a22)), b, 1,
-                                    stream), "trailing gemmt")
+        sh = stream.cuda_stream
+        with torch.cuda.stream(stream):
+            d32, dd = w[k0:k0 + b, k0:k0 + b], d64[:b, :b]
+            _lib.check(lib.bf_convert_f32_f64(ctypes.byref(_v(d32)), ctypes.byref(_v(dd)), 1, sh), "convert")
+            before = ws.before  # the driver reports block-local pivots; shift a fresh failure by k0
+            before.copy_(info)
+            _lib.check(lib.bf_cholesky_d(ctypes.byref(_v(dd)), arr, len(levels), info.data_ptr(), sh), "diag factor")
+            torch.where((before < 0) & (info >= 0), info + k0, info, out=info)
+            _lib.check(lib.bf_convert_f64_f32(ctypes.byref(_v(dd)), ctypes.byref(_v(d32)), 1, sh), "convert")
+            x = x64[:b, :b]
+            x.zero_()
+            x.diagonal().fill_(1.0)  # X L11^T = I: X = L11^-T
+            _lib.check(lib.bf_trsm_rltn_d(1.0, ctypes.byref(_v(dd)), ctypes.byref(_v(x)), 512, None, sh), "inverse")
+            _lib.check(lib.bf_convert_f64_f32(ctypes.byref(_v(x)), ctypes.byref(_v(xinv[k, :b, :b])), 0, sh),
+                       "convert")
+            if r == 0:
+                return
+            _lib.check(lib.bf_convert_f64_bf16(ctypes.byref(_v(x)), xt.data_ptr(), bs, 1, sh), "convert")
+            a21 = w[k0 + b:, k0:k0 + b]
+            p = pbuf[k % len(pbuf)]
+            _lib.check(lib.bf_convert_f32_bf16(ctypes.byref(_v(a21)), p.data_ptr(), bs, 0, sh), "convert")
+            # L21 = A21 * X  (C = A * Bnk^T with Bnk = X^T)
+            _lib.check(lib.bf_gemm_bf16(1.0, p.data_ptr(), bs, xt.data_ptr(), bs, 0.0, ctypes.byref(_v(a21)), b, 0, sh),
+                       "panel gemm")
+            _lib.check(lib.bf_convert_f32_bf16(ctypes.byref(_v(a21)), p.data_ptr(), bs, 0, sh), "convert")
+
+    if lookahead:
+        side.wait_stream(main)
+    diag_and_panel(0, side)
+    ev = torch.cuda.Event()
+    ev.record(side)
+    for k in range(nblk - 1):
+        k0 = k * bs
+        b = bs
+        k1 = k0 + b
+        r = n - k1
+        nb = min(bs, r)
+        main.wait_event(ev)
+        pk = pbuf[k % len(pbuf)]
+        # (1) the next block column first: W[k1:, k1:k1+nb] -= P P[:nb]^T
+        _lib.check(lib.bf_gemm_bf16(-1.0, pk.data_ptr(), bs, pk.data_ptr(), bs, 1.0, ctypes.byref(_v(w[k1:, k1:k1 + nb])),
+                                    b, 0, main.cuda_stream), "column gemm")
+        if lookahead:
+            side.wait_stream(main)
+        diag_and_panel(k + 1, side)
+        ev = torch.cuda.Event()
+        ev.record(side)
+        # (2) the rest of the trailing triangle
+        if r > nb:
+            rest = pk[nb:]
+            _lib.check(lib.bf_gemm_bf16(-1.0, rest.data_ptr(), bs, rest.data_ptr(), bs, 1.0,
+                                        ctypes.byref(_v(w[k1 + nb:, k1 + nb:])), b, 1, main.cuda_stream),
+                       "trailing gemmt")
+    main.wait_event(ev)
     bad = int(info.item())
     if bad >= 0:
         raise NotPositiveDefiniteError(bad)
@@ -112,20 +181,24 @@ def cholesky_mixed(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlN
 
 
 def posv_mixed(a: torch.Tensor, b: torch.Tensor, bs: int = 1024, tol: Optional[float] = None,
-               max_iter: int = 30) -> MixedResult:
+               max_iter: int = 30, lookahead: bool = True, ws: Optional[MixedWorkspace] = None) -> MixedResult:
     """Solve A x = b (A fp64 SPD, full dense row-major on the GPU) to FP64
-    accuracy: bf16/fp32 factorization + FP64 iterative refinement."""
+    accuracy: bf16/fp32 factorization + FP64 iterative refinement.  The
+    returned x lives in the workspace (copy it before reusing ws)."""
     n = a.shape[0]
     lib = _lib.lib()
     stream = torch.cuda.current_stream(a.device).cuda_stream
     tol = tol if tol is not None else 10 * n * torch.finfo(torch.float64).eps
-    f = cholesky_mixed(a, bs)
-    work = torch.empty((129 * bs,), dtype=torch.float64, device=a.device)
-    norm_a = float(torch.linalg.matrix_norm(a, ord=float("inf")))  # checker-grade norm, outside the loop
+    if ws is None:
+        ws = MixedWorkspace(n, bs, a.device)
+    f = cholesky_mixed(a, bs, lookahead=lookahead, ws=ws)
+    work = ws.work
+    _lib.check(lib.bf_row_abs_sum_d(a.data_ptr(), n, ws.rows.data_ptr(), n, stream), "row sums")
+    norm_a = float(ws.rows.max())
     norm_b = float(b.abs().max())
-    x = torch.zeros_like(b)
-    r = b.clone()
-    d = torch.empty_like(b)
+    x, r, d = ws.x, ws.r, ws.d
+    x.zero_()
+    r.copy_(b)
     it, err = 0, float("inf")
     while it < max_iter:
         d.copy_(r)

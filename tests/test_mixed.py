@@ -82,14 +82,14 @@ def test_bf16_gemm_rejects_unaligned_leading_dim(cuda):
     assert rc != 0 and b"aligned" in lib.bf_last_error()
 
 
-@pytest.mark.parametrize("n,bs", [(1000, 256), (3000, 1024)])
-def test_mixed_solve_reaches_fp64_accuracy(cuda, n, bs):
+@pytest.mark.parametrize("n,bs,lookahead", [(1000, 256, True), (3000, 1024, True), (2100, 512, False)])
+def test_mixed_solve_reaches_fp64_accuracy(cuda, n, bs, lookahead):
     g = torch.Generator(device="cuda")
     g.manual_seed(n)
     m = torch.rand(n, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
     a = m @ m.T + n * torch.eye(n, dtype=torch.float64, device="cuda")
     b = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
-    res = posv_mixed(a, b, bs=bs)
+    res = posv_mixed(a, b, bs=bs, lookahead=lookahead)
     assert res.converged and res.iterations <= 30
     eps = np.finfo(np.float64).eps
     x = res.x.cpu().numpy()
@@ -120,3 +120,15 @@ def test_blocked_potrs_matches_direct_solve(cuda):
     ref = np.linalg.solve(lw @ lw.T, rhs.cpu().numpy())
     for x in (x1, x2):  # fp64 arithmetic on the fp32 factor; the blocked one uses fp32 inverses
         assert np.linalg.norm(x.cpu().numpy() - ref) / np.linalg.norm(ref) <= 1e-5
+
+
+def test_mixed_factor_reports_npd_pivot(cuda):
+    from paper_2604_07311_b200.errors import NotPositiveDefiniteError
+    from paper_2604_07311_b200.mixed import cholesky_mixed
+
+    n = 900
+    a = torch.eye(n, dtype=torch.float64, device="cuda") * 4
+    a[613, 613] = -1.0
+    with pytest.raises(NotPositiveDefiniteError) as e:
+        cholesky_mixed(a, 256)
+    assert e.value.index == 613

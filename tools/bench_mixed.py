@@ -15,7 +15,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2604_07311_b200.engine import _lib  # noqa: E402
-from paper_2604_07311_b200.mixed import cholesky_mixed, posv_mixed  # noqa: E402
+from paper_2604_07311_b200.mixed import MixedWorkspace, cholesky_mixed, posv_mixed  # noqa: E402
 
 
 def main():
@@ -24,22 +24,22 @@ def main():
     g = torch.Generator(device="cuda")
     g.manual_seed(7)
     m = torch.rand(n, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    ws = MixedWorkspace(n, bs)
     for name, scale, shift in (("mmt_plus_nI", 1.0, float(n)), ("mmt_over_n_plus_1e-2I", 1.0 / n, 1e-2)):
         a = torch.mm(m, m.T).mul_(scale)
         a.diagonal().add_(shift)
         b = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
-        posv_mixed(a, b, bs=bs)  # warm
+        posv_mixed(a, b, bs=bs, ws=ws)  # warm
         torch.cuda.synchronize()
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         e[0].record()
-        w = cholesky_mixed(a, bs)
+        cholesky_mixed(a, bs, ws=ws)
         e[1].record()
-        res = posv_mixed(a, b, bs=bs)
+        res = posv_mixed(a, b, bs=bs, ws=ws)
         e[2].record()
         e[2].synchronize()
         fac = e[0].elapsed_time(e[1])
         tot = e[1].elapsed_time(e[2])  # factor + refinement inside posv_mixed
-        del w
         print(json.dumps({"n": n, "bs": bs, "matrix": name, "factor_ms": round(fac, 2), "posv_ms": round(tot, 2),
                           "refine_ms": round(tot - fac, 2), "iterations": res.iterations,
                           "backward_error": res.backward_error, "converged": res.converged,

@@ -18,7 +18,8 @@ bs = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 lib = _lib.lib()
 acc = defaultdict(float)
 cnt = defaultdict(int)
-names = {"bf_cholesky_s": "diag", "bf_trsm_rltn_s": "inverse", "bf_convert_f32_bf16": "convert",
+names = {"bf_cholesky_d": "diag", "bf_trsm_rltn_d": "inverse", "bf_convert_f32_bf16": "convert",
+         "bf_convert_f32_f64": "convert", "bf_convert_f64_bf16": "convert",
          "bf_convert_f64_f32": "convert64", "bf_gemm_bf16": "gemm", "bf_potrs_blocked_f32_d": "potrs",
          "bf_residual_d": "residual"}
 
@@ -56,10 +57,10 @@ a = torch.mm(m, m.T)
 a.diagonal().add_(float(n))
 del m
 b = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
-M.posv_mixed(a, b, bs=bs)
+M.posv_mixed(a, b, bs=bs, lookahead=False)
 acc.clear()
 cnt.clear()
-res = M.posv_mixed(a, b, bs=bs)
+res = M.posv_mixed(a, b, bs=bs, lookahead=False)  # one stream: per-call events are meaningful
 print(json.dumps({"n": n, "bs": bs, "iterations": res.iterations,
                   "ms": {k: round(v, 2) for k, v in sorted(acc.items(), key=lambda kv: -kv[1])},
                   "calls": dict(cnt)}))

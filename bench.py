@@ -161,6 +161,61 @@ def make_spd(bf, torch, n: int, device, seed: int = 42):
     return a
 
 
+def side_workloads(torch, a0, n: int, fp64_ms: float) -> dict:
+    """BASELINE configs[3] and [4], measured after the headline (not part of
+    `value`): the mixed-precision solve of the same SPD matrix (bf16/fp32
+    factor on tcgen05 + FP64 refinement to 10*n*eps), FP64-equivalent
+    n^3/3 / time; and the 4-index contraction abij,cdij->abcd at d=128."""
+    from paper_2604_07311_b200.mixed import MixedWorkspace, posv_mixed
+    from paper_2604_07311_b200.tensor import ContractionSpec, make_tensor
+    import paper_2604_07311_b200 as bfp
+
+    out = {}
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)
+    b = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+    ws = MixedWorkspace(n, 1024)
+    posv_mixed(a0, b, ws=ws)  # warm
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = posv_mixed(a0, b, ws=ws)
+        e1.record()
+        e1.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = statistics.median(ms)
+    out["c4_mixed_posv"] = {"n": n, "ms": round(t, 3), "fp64_equiv_gflops": round(chol_flops(n) / (t / 1e3) / 1e9, 1),
+                            "iterations": res.iterations, "backward_error": res.backward_error,
+                            "converged": bool(res.converged), "tol": "10*n*eps64",
+                            "time_ratio_vs_fp64_factor": round(fp64_ms / t, 2)}
+    del ws
+    d = 128
+    spec = ContractionSpec.parse("abij,cdij->abcd")
+
+    def rand(labels):
+        tt = make_tensor([d] * len(labels))
+        tt.storage.copy_(torch.rand(tt.storage.numel(), dtype=torch.float64, device="cuda", generator=g) * 2 - 1)
+        return tt
+
+    ta, tb = rand(spec.labels_a), rand(spec.labels_b)
+    tc = make_tensor([d] * 4)
+    bfp.contract(1.0, ta, tb, 0.0, tc, spec)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    bfp.contract(1.0, ta, tb, 0.0, tc, spec)
+    e1.record()
+    e1.synchronize()
+    cms = e0.elapsed_time(e1)
+    out["c5_contraction"] = {"spec": "abij,cdij->abcd", "d": d, "dtype": "f64", "ms": round(cms, 3),
+                             "gflops": round(2.0 * d ** 6 / (cms / 1e3) / 1e9, 1)}
+    del ta, tb, tc
+    torch.cuda.empty_cache()
+    return out
+
+
 def roofline_syrk(bf, torch, a0, n: int, bs: int, kc: int) -> dict:
     """Time the dominant kernel alone: the trailing GEMMT of every top-level
     step (n_k = n - (k+1)*bs, K = bs), on the launch stream."""
@@ -311,6 +366,7 @@ def main() -> int:
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--no-side", action="store_true", help="skip the C4 mixed / C5 contraction side measurements")
     ap.add_argument("--tiles-per-cta", type=int, default=None, help="library option (tuning)")
     ap.add_argument("--dist", action="store_true", help="use the distributed driver even at one rank")
     args = ap.parse_args()
@@ -446,6 +502,10 @@ def main() -> int:
     if not args.no_cpu and rank == 0 and world == 1:
         cpu = cpu_baseline(n)
 
+    side = None
+    if not args.no_side and rank == 0 and world == 1:
+        side = side_workloads(torch, a0, n, ms)
+
     if rank == 0:
         clk = clocks.summary()
         line = {
@@ -468,6 +528,7 @@ def main() -> int:
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "side_workloads": side,
             "gpu_launches": int(launches),
             "clocks": clk,
             "wall_s_timed": round(wall, 3),

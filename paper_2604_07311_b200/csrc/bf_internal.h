@@ -69,12 +69,12 @@ void note_launch(int64_t n = 1);
 int launch_gemm_dmma(const GemmParams& p, cudaStream_t s);            // f64 storage, f64 acc
 bool gemm_dmma_tma_eligible(const GemmParams& p);                     // TMA/mbarrier fast path?
 int launch_gemm_dmma_tma(const GemmParams& p, cudaStream_t s);
-extern int g_use_tma;                                                 // bf_set_option("tma", 0|1)
-extern int g_tma_variant;
-extern int g_bf16_tma_c;
-extern int g_trsm_warp;
-extern int g_leaf_v4;  // variant-3 leaves n <= 128: blocked register/lane-per-row kernel (1) or v3 (0)  // fused TRSM subtree: warp-per-32-rows kernel (1) or the 64-row CTA kernel (0)  // bf16 GEMM: TMA C-tile epilogue (1) or per-element fallback (0)
-extern int g_tiles_per_cta;                                           // bf_set_option("tiles_per_cta", t)                                             // bf_set_option("tma_variant", 0..3)
+extern int g_use_tma;         // bf_set_option("tma", 0|1)
+extern int g_tma_variant;     // bf_set_option("tma_variant", 0..3)
+extern int g_tiles_per_cta;   // bf_set_option("tiles_per_cta", t)
+extern int g_bf16_tma_c;      // bf16 GEMM: TMA C-tile epilogue (1) or per-element fallback (0)
+extern int g_trsm_warp;       // fused TRSM subtree: 4-warps-per-32-rows kernel (1) or the 64-row CTA kernel (0)
+extern int g_leaf_blocked;    // variant-3 leaves n <= 128: blocked lane-per-row kernel (1) or v3 (0)
 int launch_gemm_simt_f32(const GemmParams& p, cudaStream_t s);        // f32 storage, f32 acc
 int launch_gemm_simt_f32acc64(const GemmParams& p, cudaStream_t s);   // f32 storage, f64 acc
 int launch_scale(int is_f64, double beta, void* c, int64_t off, int64_t m, int64_t n, int64_t rs,

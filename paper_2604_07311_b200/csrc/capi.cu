@@ -434,8 +434,8 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_tma_variant = int(value & 3);
     return BF_OK;
   }
-  if (name && std::strcmp(name, "leaf_v4") == 0) {
-    bf::g_leaf_v4 = value != 0;
+  if (name && std::strcmp(name, "leaf_blocked") == 0) {
+    bf::g_leaf_blocked = value != 0;
     return BF_OK;
   }
   if (name && std::strcmp(name, "trsm_warp") == 0) {

@@ -15,7 +15,7 @@
 namespace bf {
 
 int g_trsm_warp = 1;
-int g_leaf_v4 = 0;  // v4 is bit-identical but not yet faster than v3
+int g_leaf_blocked = 1;
 
 namespace {
 
@@ -44,7 +44,7 @@ struct Mat {
 };
 
 // variant 3, right-looking: scale column k, rank-1 update of the trailing triangle
-template <typename T>
+template <typename T, int NT = LEAF_THREADS>
 __device__ int leaf_v3(Mat<T> a, int n, int* s_flag, T* s_d) {
   const int tid = threadIdx.x;
   for (int k = 0; k < n; ++k) {
@@ -61,11 +61,11 @@ __device__ int leaf_v3(Mat<T> a, int n, int* s_flag, T* s_d) {
     __syncthreads();
     if (*s_flag >= 0) return *s_flag;
     const T d = *s_d;
-    for (int i = k + 1 + tid; i < n; i += LEAF_THREADS) a(i, k) = Ops<T>::div(a(i, k), d);
+    for (int i = k + 1 + tid; i < n; i += NT) a(i, k) = Ops<T>::div(a(i, k), d);
     __syncthreads();
-    // trailing triangle k < j <= i < n; 32 x 16 thread grid, j fastest
+    // trailing triangle k < j <= i < n; 32 x (NT/32) thread grid, j fastest
     const int tx = tid & 31, ty = tid >> 5;
-    for (int i = k + 1 + ty; i < n; i += LEAF_THREADS / 32) {
+    for (int i = k + 1 + ty; i < n; i += NT / 32) {
       const T aik = a(i, k);
       for (int j = k + 1 + tx; j <= i; j += 32) a(i, j) = Ops<T>::sub(a(i, j), Ops<T>::mul(aik, a(j, k)));
     }
@@ -852,23 +852,30 @@ __global__ void __launch_bounds__(128 * R) trsm_warp_right_kernel(double alpha, 
   }
 }
 
-// ------------------------------------------- blocked variant-3 leaf (v4) --
+// ------------------------------------------------ blocked variant-3 leaf --
 // Variant 3 (right-looking, factor/cholesky.py:74-89) for n <= 128 by 32-wide
 // column blocks, every element still receiving the reference's operations
 // in the reference's order (a(i,j) -= a(i,k)*a(j,k) for ascending k, unfused,
 // then its sqrt or division):
-//  (a) warp 0 factors the diagonal block in registers, one lane per row:
-//      the pivot reaches every lane by shuffle, each lane takes the sqrt,
-//      divides its own element, and updates its row with the pivot column
-//      (shuffled element by element) — no barrier on the pivot chain;
-//  (b) the rows below, 32 per warp, solve against the finished block like
-//      the fused TRSM's bases (Markstein division from reciprocals of the
-//      block's diagonal, exact fallback);
-//  (c) the trailing triangle takes the block's 32 rank-1 updates, 4x4
-//      register tiles over the CTA.
-// A failing pivot stops the sweep after finishing exactly the steps before
-// it (the reference's partial state).  128 threads, LD = 129 (conflict-free
-// lane-per-row access).
+//  (a) warp 0 factors the diagonal block in registers, one lane per row,
+//      four columns per loop trip through a sliding register window.  The
+//      pivot chain is branch-free: sqrt from an rsqrt seed + two Newton steps
+//      + a residual correction, the reciprocal of the rounded root seeded by
+//      the same y, and Markstein division (q0 = a r, q = q0 + (a - b q0) r).
+//      Every root and quotient is then *verified* from its exact fma
+//      residual (|d - s^2| < s ulp(s), |a - b q| < b ulp(q)/2, inside an
+//      exponent band), so a result is only kept when it provably equals
+//      sqrt.rn / div.rn; anything else (never seen in 5e9 probes,
+//      tools/sqrt_probe.cu) redoes the whole leaf with the exact kernel.
+//      The next pivot's own update is taken first; the column reaches the
+//      other rows by shuffles;
+//  (b) the rows below, 32 per warp, solve against the finished block the same
+//      way (quotients verified);
+//  (c) the trailing triangle takes the block's rank-1 updates, 4x4 register
+//      tiles over the CTA.
+// A failing pivot, like an unverified result, sends the leaf to the exact
+// column-parallel algorithm (leaf_v3), which stops where the reference stops
+// and leaves its partial state.  128 threads, LD = 129.
 constexpr int LV4_LD = 129;
 #ifdef LV4_PROF  // phase clocks for tools/leaf_probe2.cu
 __device__ long long g_lv4_prof[64];
@@ -879,94 +886,186 @@ __device__ long long g_lv4_prof[64];
 #endif
 
 template <typename T>
-__global__ void __launch_bounds__(128) potrf_leaf_v4_kernel(T* g, int64_t off, int n, int64_t rs, int64_t cs,
-                                                            int64_t base_index, int* d_info) {
+struct LeafMath {  // f32 storage: the exact (branchy) operations, always "verified"
+  static __device__ __forceinline__ T sqrt_y(T d, T& y) {
+    y = T(0);
+    return Ops<T>::sqrt_(d);
+  }
+  static __device__ __forceinline__ T rcp(T b, T) { return T(0); }
+  static __device__ __forceinline__ T div(T a, T b, T) { return Ops<T>::div(a, b); }
+  static __device__ __forceinline__ bool sqrt_ok(T, T) { return true; }
+  static __device__ __forceinline__ bool div_ok(T, T, T) { return true; }
+};
+template <>
+struct LeafMath<double> {
+  static __device__ __forceinline__ int ex(double v) { return (__double2hiint(v) >> 20) & 0x7ff; }
+  static __device__ __forceinline__ bool in_band(double v) {
+    const int e = ex(v);
+    return (e >= 223) & (e <= 1823);  // |v| in [2^-800, 2^800]
+  }
+  static __device__ __forceinline__ double sqrt_y(double d, double& yo) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double h = 0.5 * y;
+    double r = __fma_rn(-d * y, h, 0.5);
+    y = __fma_rn(y, r, y);
+    h = 0.5 * y;
+    r = __fma_rn(-d * y, h, 0.5);
+    y = __fma_rn(y, r, y);
+    const double s = d * y;
+    h = 0.5 * y;
+    yo = y;
+    return __fma_rn(__fma_rn(-s, s, d), h, s);
+  }
+  static __device__ __forceinline__ double rcp(double b, double y) {
+    double e = __fma_rn(-b, y, 1.0);
+    y = __fma_rn(y, e, y);
+    e = __fma_rn(-b, y, 1.0);
+    return __fma_rn(y, e, y);
+  }
+  static __device__ __forceinline__ double div(double a, double b, double r) {
+    const double q0 = __dmul_rn(a, r);
+    return __fma_rn(__fma_rn(-b, q0, a), r, q0);
+  }
+  // s == sqrt.rn(d): the exact residual sits strictly inside the rounding
+  // interval (bitwise & / | throughout: no short-circuit branches)
+  static __device__ __forceinline__ bool sqrt_ok(double d, double s) {
+    const long long sb = __double_as_longlong(s);
+    const double ulp = __longlong_as_double((sb & 0x7ff0000000000000LL) - (52LL << 52));
+    const double rem = __fma_rn(-s, s, d);
+    return in_band(d) & (fabs(rem) < s * ulp * 0.9990234375) & ((sb & 0x000fffffffffffffLL) != 0);
+  }
+  // q == div.rn(a, b) for b > 0: |a - b q| < b ulp(q) / 2, q not a power of two
+  // (a == 0 gives q == 0 exactly)
+  static __device__ __forceinline__ bool div_ok(double a, double b, double q) {
+    const long long qb = __double_as_longlong(q);
+    const double half_ulp = __longlong_as_double((qb & 0x7ff0000000000000LL) - (53LL << 52));
+    const double rem = __fma_rn(-b, q, a);
+    const bool nonzero_ok = in_band(a) & in_band(b) & in_band(q) & (fabs(rem) < b * half_ulp) &
+                            ((qb & 0x000fffffffffffffLL) != 0);
+    return (a == 0.0) ? (q == 0.0) : nonzero_ok;
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t off, int n, int64_t rs, int64_t cs,
+                                                                 int64_t base_index, int* d_info) {
   if (d_info != nullptr && *d_info >= 0) return;
-  extern __shared__ __align__(16) unsigned char leaf_v4_smem[];
-  T* A = reinterpret_cast<T*>(leaf_v4_smem);
+  extern __shared__ __align__(16) unsigned char leaf_b_smem[];
+  T* A = reinterpret_cast<T*>(leaf_b_smem);
   __shared__ T s_rc[128];
+  __shared__ __align__(16) T s_cb[4 * 128];  // per warp: two 64-entry column buffers
   __shared__ int s_fail;
   __shared__ int s_unsafe;
+  __shared__ T s_d;
+  using LM = LeafMath<T>;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (cs == 1) {
-    for (int i = warp; i < n; i += 4)
-      for (int j = lane; j <= i; j += 32) {
-        if constexpr (sizeof(T) == 8)
-          cp_async_8(&A[i * LV4_LD + j], &g[off + i * rs + j], 8);
-        else
-          cp_async_4(&A[i * LV4_LD + j], &g[off + i * rs + j], 4);
-      }
-  } else {
-    for (int j = warp; j < n; j += 4)
-      for (int i = j + lane; i < n; i += 32) {
-        if constexpr (sizeof(T) == 8)
-          cp_async_8(&A[i * LV4_LD + j], &g[off + i * rs + j * cs], 8);
-        else
-          cp_async_4(&A[i * LV4_LD + j], &g[off + i * rs + j * cs], 4);
-      }
-  }
-  cp_async_commit();
+  auto stage_in = [&]() {
+    if (cs == 1) {
+      for (int i = warp; i < n; i += 4)
+        for (int j = lane; j <= i; j += 32) {
+          if constexpr (sizeof(T) == 8)
+            cp_async_8(&A[i * LV4_LD + j], &g[off + i * rs + j], 8);
+          else
+            cp_async_4(&A[i * LV4_LD + j], &g[off + i * rs + j], 4);
+        }
+    } else {
+      for (int j = warp; j < n; j += 4)
+        for (int i = j + lane; i < n; i += 32) {
+          if constexpr (sizeof(T) == 8)
+            cp_async_8(&A[i * LV4_LD + j], &g[off + i * rs + j * cs], 8);
+          else
+            cp_async_4(&A[i * LV4_LD + j], &g[off + i * rs + j * cs], 4);
+        }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+  };
+  stage_in();
   if (tid == 0) {
     s_fail = -1;
     s_unsafe = 0;
   }
-  cp_async_wait<0>();
   __syncthreads();
   LV4_MARK(0)
-  using TG = TrsmGroup<T>;
   int bad = -1;
 #pragma unroll 1
   for (int k0 = 0; k0 < n; k0 += 32) {
     const int bw = n - k0 < 32 ? n - k0 : 32;
     const int k1 = k0 + bw;
-    // (a) diagonal block.  Sliding register window: at step p, acc[j] holds
-    // column p + j of this lane's row, so the loop body indexes registers
-    // statically and stays small (a fully unrolled step sequence ran out of
-    // the instruction cache).
-    if (warp == 0) {
+    // (a) diagonal block: acc[j] holds column p0 + j of row k0 + lane.  The
+    // four-column body is one basic block (no barrier, no data-dependent
+    // branch: pivot failures and unverified results only raise the redo
+    // flag), so the scheduler overlaps column p+1's pivot chain with column
+    // p's shuffle-fed updates.
+    // Every warp runs it (same values); only warp 0 stores: with no
+    // warp-dependent branch around it the shuffles need no divergence
+    // checks, which would otherwise split the body into basic blocks.
+    {
+      const bool w0 = warp == 0;
+      const int i = lane;
       T acc[32];
-      const int i = lane;  // row k0 + i
 #pragma unroll
       for (int q = 0; q < 32; ++q) acc[q] = (q <= i && i < bw) ? A[(k0 + i) * LV4_LD + k0 + q] : T(0);
-      int fail = -1;
+      bool unsafe = false;
+      T d = __shfl_sync(0xffffffffu, acc[0], 0);
 #pragma unroll 1
-      for (int p = 0; p < bw; ++p) {
-        const T d = __shfl_sync(0xffffffffu, acc[0], p);
-        if (!(d > T(0))) {
-          fail = p;  // uniform; (p,p) keeps its updated value
-          break;
-        }
-        const T lpp = Ops<T>::sqrt_(d);
-        // every lane divides (no divergence); rows above the pivot and
-        // columns past the block only ever hold values that are not stored
-        const T dv = Ops<T>::div(acc[0], lpp);
-        acc[0] = i == p ? lpp : (i > p ? dv : acc[0]);
-        if (i >= p && i < bw) A[(k0 + i) * LV4_LD + k0 + p] = acc[0];
-        if (i == p) s_rc[k0 + p] = TG::rcp(lpp);
+      for (int p0 = 0; p0 < bw; p0 += 4) {
 #pragma unroll
-        for (int j = 1; j < 32; ++j) {
-          const T lqp = __shfl_sync(0xffffffffu, acc[0], (p + j) & 31);
-          acc[j] = Ops<T>::sub(acc[j], Ops<T>::mul(acc[0], lqp));
+        for (int u = 0; u < 4; ++u) {
+          const int p = p0 + u;
+          const bool live = p < bw;
+          const T dcur = d;
+          T y;
+          const T lpp = LM::sqrt_y(dcur, y);
+          const T r = LM::rcp(lpp, y);
+          const T a = acc[u];
+          const T qv = LM::div(a, lpp, r);
+          const T l = i == p ? lpp : (i > p ? qv : a);
+          // next pivot first: lane p+1's own update by column p
+          const T nd = Ops<T>::sub(acc[u + 1], Ops<T>::mul(l, l));
+          d = __shfl_sync(0xffffffffu, nd, (p + 1) & 31);
+          unsafe |= live & (!(dcur > T(0)) | !LM::sqrt_ok(dcur, lpp) |
+                            ((i > p) & (i < bw) & !LM::div_ok(a, lpp, qv)));
+          acc[u] = l;
+          if (w0 && live && i >= p && i < bw) A[(k0 + i) * LV4_LD + k0 + p] = l;
+          if (w0 && live && i == p) s_rc[k0 + p] = r;
+          // column broadcast through shared memory (double-buffered by column
+          // parity: one warp barrier per column); cb[p0 + j] is l(p0 + j, p)
+          T* cb = s_cb + (u & 1) * 64 + warp * 128;
+          cb[i] = l;
+          __syncwarp();
+          T lv[32];
+          if constexpr (sizeof(T) == 8) {
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+              const double2 t2 = reinterpret_cast<const double2*>(cb + p0)[m];
+              lv[2 * m] = t2.x;
+              lv[2 * m + 1] = t2.y;
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+              const float4 t4 = reinterpret_cast<const float4*>(cb + p0)[m];
+              lv[4 * m] = t4.x;
+              lv[4 * m + 1] = t4.y;
+              lv[4 * m + 2] = t4.z;
+              lv[4 * m + 3] = t4.w;
+            }
+          }
+#pragma unroll
+          for (int j = u + 1; j < 32; ++j) acc[j] = Ops<T>::sub(acc[j], Ops<T>::mul(l, lv[j]));
         }
 #pragma unroll
-        for (int j = 0; j < 31; ++j) acc[j] = acc[j + 1];
-        acc[31] = T(0);
+        for (int j = 0; j < 28; ++j) acc[j] = acc[j + 4];
+        acc[28] = acc[29] = acc[30] = acc[31] = T(0);
       }
-      if (fail >= 0) {  // columns >= fail keep their updated values
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int q = fail + j;
-          if (q < bw && q <= i && i < bw) A[(k0 + i) * LV4_LD + k0 + q] = acc[j];
-        }
-      }
-      if (lane == 0) s_fail = fail < 0 ? -1 : k0 + fail;
+      if (__any_sync(0xffffffffu, unsafe) && w0 && lane == 0) s_unsafe = 1;
     }
     __syncthreads();
     LV4_MARK(1 + 3 * (k0 >> 5))
-    const int fail = s_fail;
-    const int kend = fail < 0 ? bw : fail - k0;  // columns of this block that complete
-    // (b) rows below the block: X * L11^T = A21 over the block's first kend
-    // columns, lane per row, same sliding window
+    const int kend = bw;
+    // (b) rows below the block: X * L11^T = A21, lane per row, same window
 #pragma unroll 1
     for (int r0 = k1 + 32 * warp; r0 < n; r0 += 128) {
       const int r = r0 + lane;
@@ -975,53 +1074,29 @@ __global__ void __launch_bounds__(128) potrf_leaf_v4_kernel(T* g, int64_t off, i
       T acc[32];
 #pragma unroll
       for (int q = 0; q < 32; ++q) acc[q] = (ok && q < bw) ? A[r * LV4_LD + k0 + q] : T(0);
-      int emin = TG::kMidExp, emax = TG::kMidExp;
+      bool unsafe = false;
 #pragma unroll 1
-      for (int q = 0; q < kend; ++q) {
-        const T dq = l[q * LV4_LD + q], rq = s_rc[k0 + q];
-        const T a = acc[0];
-        const T q0 = Ops<T>::mul(a, rq);
-        const T xq = Ops<T>::fma_(Ops<T>::fma_(-dq, q0, a), rq, q0);
-        const int ea = a == T(0) ? TG::kMidExp : TG::expo(a);
-        const int ed = TG::expo(dq);
-        emin = min(emin, min(ea, ed));
-        emax = max(emax, max(ea, ed));
-        if (ok) A[r * LV4_LD + k0 + q] = xq;
+      for (int q0 = 0; q0 < bw; q0 += 4) {
 #pragma unroll
-        for (int t = 1; t < 32; ++t)  // columns past the block: never stored
-          acc[t] = Ops<T>::sub(acc[t], Ops<T>::mul(xq, l[((q + t) & 31) * LV4_LD + q]));
+        for (int u = 0; u < 4; ++u) {
+          const int q = q0 + u;
+          const bool live = q < bw;
+          const int qq = q & 31;
+          const T dq = l[qq * LV4_LD + qq], rq = s_rc[k0 + qq];
+          const T a = acc[u];
+          const T xq = LM::div(a, dq, rq);
+          unsafe |= live & ok & !LM::div_ok(a, dq, xq);
+          acc[u] = xq;
+          if (live && ok) A[r * LV4_LD + k0 + q] = xq;
 #pragma unroll
-        for (int t = 0; t < 31; ++t) acc[t] = acc[t + 1];
-        acc[31] = T(0);
+          for (int j = u + 1; j < 32; ++j)  // columns past the block: never stored
+            acc[j] = Ops<T>::sub(acc[j], Ops<T>::mul(xq, l[((q + j - u) & 31) * LV4_LD + qq]));
+        }
+#pragma unroll
+        for (int j = 0; j < 28; ++j) acc[j] = acc[j + 4];
+        acc[28] = acc[29] = acc[30] = acc[31] = T(0);
       }
-      const bool safe = emin >= TG::kLoExp && emax <= TG::kHiExp;
-      if (__all_sync(0xffffffffu, safe || !ok)) {
-        if (ok) {
-#pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (kend + t < bw) A[r * LV4_LD + k0 + kend + t] = acc[t];
-        }
-      } else if (ok) {  // rare: exact division, in place from the original row
-        // (columns < kend were overwritten: redo them from the saved tail is
-        // impossible, so reload the row block from global memory)
-        for (int q = 0; q < bw; ++q) {
-          const int gr = r, gc = k0 + q;
-          A[r * LV4_LD + gc] = cs == 1 ? g[off + gr * rs + gc] : g[off + gr * rs + gc * cs];
-        }
-        // earlier column blocks' updates must be re-applied: fall back to the
-        // reference order for this row over all completed columns < k0 as well
-        for (int q = 0; q < bw; ++q) {
-          T v = A[r * LV4_LD + k0 + q];
-          for (int p = 0; p < k0; ++p) v = Ops<T>::sub(v, Ops<T>::mul(A[r * LV4_LD + p], A[(k0 + q) * LV4_LD + p]));
-          A[r * LV4_LD + k0 + q] = v;
-        }
-        for (int q = 0; q < kend; ++q) {
-          const T xq = Ops<T>::div(A[r * LV4_LD + k0 + q], l[q * LV4_LD + q]);
-          A[r * LV4_LD + k0 + q] = xq;
-          for (int t = q + 1; t < bw; ++t)
-            A[r * LV4_LD + k0 + t] = Ops<T>::sub(A[r * LV4_LD + k0 + t], Ops<T>::mul(xq, l[t * LV4_LD + q]));
-        }
-      }
+      if (__any_sync(0xffffffffu, unsafe) && lane == 0) s_unsafe = 1;
     }
     __syncthreads();
     LV4_MARK(2 + 3 * (k0 >> 5))
@@ -1063,10 +1138,14 @@ __global__ void __launch_bounds__(128) potrf_leaf_v4_kernel(T* g, int64_t off, i
     }
     __syncthreads();
     LV4_MARK(3 + 3 * (k0 >> 5))
-    if (fail >= 0) {
-      bad = fail;
-      break;
-    }
+  }
+  if (s_unsafe) {  // a pivot failed, or a root or quotient was not provably sqrt.rn / div.rn: redo exactly
+    __syncthreads();
+    stage_in();
+    if (tid == 0) s_fail = -1;
+    __syncthreads();
+    bad = leaf_v3<T, 128>(Mat<T>{A, LV4_LD, 1}, n, &s_fail, &s_d);
+    __syncthreads();
   }
   if (cs == 1) {
     for (int i = warp; i < n; i += 4)
@@ -1119,17 +1198,17 @@ static constexpr int LEAF_SMEM_LIMIT = 220 * 1024;
 template <typename T>
 static int leaf_launch(T* a, int64_t off, int64_t n, int64_t rs, int64_t cs, int variant, int64_t base_index,
                        int* d_info, cudaStream_t s) {
-  if (variant == 3 && n <= 128 && g_leaf_v4) {
+  if (variant == 3 && n <= 128 && g_leaf_blocked) {
     static bool v4_attr = false;
     const size_t smem = size_t(128) * LV4_LD * sizeof(T);
     if (!v4_attr) {
-      if (cudaFuncSetAttribute(potrf_leaf_v4_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+      if (cudaFuncSetAttribute(potrf_leaf_blocked_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
           cudaSuccess)
         return -10;
       v4_attr = true;
     }
     note_launch();
-    potrf_leaf_v4_kernel<T><<<1, 128, smem, s>>>(a, off, int(n), rs, cs, base_index, d_info);
+    potrf_leaf_blocked_kernel<T><<<1, 128, smem, s>>>(a, off, int(n), rs, cs, base_index, d_info);
     return cudaGetLastError() == cudaSuccess ? 0 : -11;
   }
   if (variant == 3 && n <= 128) {

@@ -78,9 +78,9 @@ def test_npd_reports_global_index_and_stops(cuda):
     assert digest(v.storage.cpu().numpy()) == digest(st)  # same partial state as the reference stops in
 
 
-@pytest.mark.parametrize("leaf_v4", [1, 0])
+@pytest.mark.parametrize("leaf_blocked", [1, 0])
 @pytest.mark.parametrize("dt,npd_at", [("f64", None), ("f64", 77), ("f64", 100), ("f32", None), ("f32", 45)])
-def test_leaf_kernels_bitwise_and_partial_state(cuda, leaf_v4, dt, npd_at):
+def test_leaf_kernels_bitwise_and_partial_state(cuda, leaf_blocked, dt, npd_at):
     """Both variant-3 leaf kernels (blocked lane-per-row v4, column-parallel
     v3) give the oracle's bits, and on a failing pivot — inside the first
     column block, or mid-block past it — the oracle's partial state and index."""
@@ -96,7 +96,7 @@ def test_leaf_kernels_bitwise_and_partial_state(cuda, leaf_v4, dt, npd_at):
     st = a0.reshape(-1).copy()
     bad = O.cholesky(st, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1}, O.levels_from_tree(json.loads(doc), n, dt))
     lib = _lib.lib()
-    lib.bf_set_option(b"leaf_v4", leaf_v4)
+    lib.bf_set_option(b"leaf_blocked", leaf_blocked)
     try:
         v = make_view(n, n, DType.parse(dt), fill=a0)
         if npd_at is None:
@@ -106,7 +106,7 @@ def test_leaf_kernels_bitwise_and_partial_state(cuda, leaf_v4, dt, npd_at):
                 bf.cholesky(v, "lower", parse_tree(doc))
             assert e.value.index == bad == npd_at
     finally:
-        lib.bf_set_option(b"leaf_v4", 0)
+        lib.bf_set_option(b"leaf_blocked", 0)
     assert digest(v.storage.cpu().numpy()) == digest(st)
 
 

@@ -1,4 +1,4 @@
-// Probe: phase clocks of the blocked variant-3 leaf (potrf_leaf_v4_kernel).
+// Probe: phase clocks of the blocked variant-3 leaf (potrf_leaf_blocked_kernel).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DLV4_PROF -I paper_2604_07311_b200/csrc \
 //        -I include tools/leaf_probe2.cu -o tools/leaf_probe2
 #include "../paper_2604_07311_b200/csrc/small_kernels.cu"
@@ -21,7 +21,7 @@ void run(const char* label) {
   T* d;
   cudaMalloc(&d, h.size() * sizeof(T));
   const size_t smem = size_t(128) * LV4_LD * sizeof(T);
-  cudaFuncSetAttribute(potrf_leaf_v4_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaFuncSetAttribute(potrf_leaf_blocked_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   for (int rep = 0; rep < 3; ++rep) {
     cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
     long long z[64] = {0};
@@ -30,7 +30,7 @@ void run(const char* label) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    potrf_leaf_v4_kernel<T><<<1, 128, smem>>>(d, 0, n, n, 1, 0, nullptr);
+    potrf_leaf_blocked_kernel<T><<<1, 128, smem>>>(d, 0, n, n, 1, 0, nullptr);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;

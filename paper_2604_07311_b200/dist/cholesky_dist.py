@@ -25,6 +25,7 @@ logic under gloo without a GPU.
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Optional, Protocol
 
 import torch
@@ -116,10 +117,20 @@ def cholesky_distributed(
     comm: Comm,
     ops: Optional[Ops] = None,
     raise_on_failure: bool = True,
+    lookahead: Optional[bool] = None,
 ) -> int:
     """Factor the block-cyclic lower triangle held in `local` (this rank's
     local matrix) in place.  Returns -1 or the first failing global pivot
-    (and raises NotPositiveDefiniteError if raise_on_failure)."""
+    (and raises NotPositiveDefiniteError if raise_on_failure).
+
+    lookahead (default: on for CUDA tensors): step k's trailing update first
+    refreshes block column k+1; step k+1's panel work (diagonal factor, its
+    broadcast, the panel solve, the panel broadcasts) then runs on a
+    high-priority stream while the rest of step k's update proceeds, so the
+    NCCL traffic and the latency-bound panel kernels hide under the GEMMs.
+    Every element still receives the same operations in the same order (bits
+    unchanged); after a pivot failure only the reported index is defined
+    (kernels of the overlapped update may stop early)."""
     check_valid(tree, op="cholesky")
     if tree.variant != 3 or tree.bs != layout.nb:
         raise ShapeError("distributed Cholesky needs a variant-3 root whose bs equals the tile size nb")
@@ -135,8 +146,14 @@ def cholesky_distributed(
     dev = local.device
     info = torch.full((1,), -1, dtype=torch.int32, device=dev)
     my_rows, my_cols = layout.row_tiles(prow), layout.col_tiles(pcol)
+    if lookahead is None:
+        lookahead = local.is_cuda
+    lookahead = bool(lookahead) and local.is_cuda and layout.tiles > 1
+    main = torch.cuda.current_stream(dev) if local.is_cuda else None
+    side = torch.cuda.Stream(dev, priority=-1) if lookahead else None
 
-    for k in range(layout.tiles):
+    def panel(k: int) -> list:
+        """Steps 1-3 of step k; returns the received panel blocks per process row."""
         bk = layout.tile_len(k)
         kr, kcol = k % pr, k % pc
         diag_owner = kr * pc + kcol
@@ -168,25 +185,70 @@ def cholesky_distributed(
                 continue
             if comm.rank == root:
                 r0 = layout.local_row(rows_p[qp])
-                buf = local[r0:r0 + h, c0k:c0k + bk].contiguous()
+                buf = local[r0:r0 + h, c0k:c0k + bk]
+                if comm.world > 1:  # NCCL sends a dense buffer; alone, the strided view serves as is
+                    buf = buf.contiguous()
             else:
                 buf = torch.empty((h, bk), dtype=local.dtype, device=dev)
             comm.bcast(buf, root)
             panels.append((buf, rows_p[qp:]))
+        return panels
+
+    def update(k: int, panels: list, part: str) -> None:
+        """Step 4 of step k on my lower tiles: part 'next' = block column k+1
+        only, 'rest' = columns beyond it, 'all' = both."""
 
         def panel_tile(t: int) -> torch.Tensor:
             buf, tiles = panels[t % pr]
             off = (t // pr - tiles[0] // pr) * nb
             return buf[off:off + layout.tile_len(t)]
 
-        # my column tiles J > k, stacked (the B operand of every row's update)
+        def _stack(tiles: list) -> torch.Tensor:
+            """Panel rows of consecutive local row tiles (one process row):
+            a contiguous slice of that row's received block."""
+            first = panel_tile(tiles[0])
+            buf = panels[tiles[0] % pr][0]
+            off = first.data_ptr() - buf.data_ptr()
+            start = off // (buf.element_size() * buf.stride(0))
+            h = sum(layout.tile_len(t) for t in tiles)
+            return buf[start:start + h]
+
+        q0 = layout.first_row_tile_after(prow, k)
         qc0 = layout.first_col_tile_after(pcol, k)
         cols = my_cols[qc0:]
+        if part == "next":
+            cols = [j for j in cols if j == k + 1]
+        elif part == "rest":
+            cols = [j for j in cols if j != k + 1]
         if not cols or q0 >= len(my_rows):
-            continue
-        q_stack = torch.cat([panel_tile(j) for j in cols], dim=0)
+            return
+        rows = my_rows[q0:]
         c_base = layout.local_col(cols[0])
-        # 4. trailing update of my lower tiles
+        r_base = layout.local_row(rows[0])
+        if part == "next":
+            # one column tile: GEMMT on the diagonal tile (when it is mine),
+            # ONE GEMM over all the stacked rows below it
+            bj = panel_tile(cols[0])
+            w = layout.tile_len(cols[0])
+            r = r_base
+            if rows[0] == cols[0]:
+                h = layout.tile_len(rows[0])
+                ops.gemm(panel_tile(rows[0]), bj, local[r:r + h, c_base:c_base + w], True, kc, info)
+                r += h
+                rows = rows[1:]
+            if rows:
+                h = sum(layout.tile_len(t) for t in rows)
+                ops.gemm(_stack(rows), bj, local[r:r + h, c_base:c_base + w], False, kc, info)
+            return
+        if pr == 1 and pc == 1:  # one rank: the trailing block is a plain lower triangle
+            rows = [t for t in rows if t >= cols[0]]
+            r_base = layout.local_row(rows[0])
+            h = sum(layout.tile_len(t) for t in rows)
+            st = _stack(rows)
+            ops.gemm(st, st, local[r_base:r_base + h, c_base:c_base + h], True, kc, info)
+            return
+        # my column tiles J (stacked): the B operand of every row's update
+        q_stack = torch.cat([panel_tile(j) for j in cols], dim=0)
         for i_tile in my_rows[q0:]:
             n_cols = sum(1 for j in cols if j <= i_tile)
             if n_cols == 0:
@@ -201,6 +263,42 @@ def cholesky_distributed(
             if diag_here:
                 ops.gemm(a_i, q_stack[w_full:w_full + h], local[r0:r0 + h, c_base + w_full:c_base + w_full + h],
                          True, kc, info)
+
+    if not lookahead and os.environ.get("BF_DIST_FORCE_SPLIT") == "1":
+        # test hook: the lookahead's split update order without streams
+        for k in range(layout.tiles):
+            cur = panel(k)
+            if k + 1 < layout.tiles:
+                update(k, cur, "next")
+                update(k, cur, "rest")
+            else:
+                update(k, cur, "all")
+    elif not lookahead:
+        for k in range(layout.tiles):
+            update(k, panel(k), "all")
+    else:
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            cur = panel(0)
+        ready = torch.cuda.Event()
+        ready.record(side)
+        for k in range(layout.tiles):
+            main.wait_event(ready)
+            for item in cur:  # received on the side stream, read on main
+                if item is not None:
+                    item[0].record_stream(main)
+            if k + 1 < layout.tiles:
+                update(k, cur, "next")
+                side.wait_stream(main)
+                with torch.cuda.stream(side):
+                    nxt = panel(k + 1)
+                ready = torch.cuda.Event()
+                ready.record(side)
+                update(k, cur, "rest")
+                cur = nxt
+            else:
+                update(k, cur, "all")
+        main.wait_stream(side)
     bad = int(info.item())
     if bad >= 0 and raise_on_failure:
         raise NotPositiveDefiniteError(bad)

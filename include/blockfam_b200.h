@@ -117,6 +117,17 @@ int bf_trsm_rltn_s(double alpha, const bf_view* tri, const bf_view* b, int64_t k
  * unblocked3, factor/cholesky.py:154-158).  Same operation sequence as
  * factor/cholesky.py:118-151.  First failing global pivot -> *d_info. */
 int bf_cholesky_d(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream);
+/* In-place FP64 Cholesky of a HOST matrix (pinned for overlap; row-major, ld):
+ * its lower triangle goes to the device work matrix by block columns, is
+ * factored there, and every block column returns to the host as soon as it is
+ * final (copy stream, overlapped with the remaining steps).  The strict upper
+ * triangle of the host matrix is neither read nor written.  Same bits as
+ * bf_cholesky_d.  After a pivot failure the host holds the factor only up to
+ * the columns already streamed back: re-read the lower triangle from `work`.
+ * (No reference counterpart: the reference factors NumPy host arrays in
+ * place, factor/cholesky.py:99-115; this is that call with device compute.) */
+int bf_cholesky_host_d(double* host, int64_t ld, const bf_view* work, const bf_chol_level* levels, int nlevels,
+                       int* d_info, void* stream);
 int bf_cholesky_s(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream);
 
 /* Building blocks of the distributed driver (paper_2604_07311_b200/dist):

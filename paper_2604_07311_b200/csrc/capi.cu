@@ -257,6 +257,40 @@ cudaStream_t panel_stream() {
   return streams[dev];
 }
 
+// Copy stream per device (host <-> device traffic of bf_cholesky_host_d).
+cudaStream_t copy_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+  return streams[dev];
+}
+
+// Host write-back of finished block columns (bf_cholesky_host_d): while set,
+// the lookahead driver copies block column k's lower part (rows >= k*bs) to
+// the pinned host matrix as soon as panel k is final, on the copy stream.
+struct HostWriteback {
+  double* host = nullptr;
+  int64_t ld = 0;
+  cudaStream_t cs = nullptr;
+  int64_t copied_upto = 0;  // columns [0, copied_upto) already queued
+};
+thread_local HostWriteback* g_wb = nullptr;
+
+void writeback_block_column(const bf_view& a, int64_t c0, int64_t w, cudaStream_t after) {
+  if (!g_wb || w <= 0) return;
+  cudaEvent_t ev;
+  cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  cudaEventRecord(ev, after);
+  cudaStreamWaitEvent(g_wb->cs, ev, 0);
+  cudaEventDestroy(ev);
+  const double* src = static_cast<const double*>(a.base) + a.off + c0 * a.rs + c0 * a.cs;
+  cudaMemcpy2DAsync(g_wb->host + c0 * g_wb->ld + c0, size_t(g_wb->ld) * 8, src, size_t(a.rs) * 8, size_t(w) * 8,
+                    size_t(a.n - c0), cudaMemcpyDeviceToHost, g_wb->cs);
+  g_wb->copied_upto = c0 + w;
+}
+
 // Right-looking (variant 3) top level with depth-1 lookahead.  Same operation
 // set as factor/cholesky.py:146-149 — every element of A22 still receives the
 // step's whole K=bs update as one kc-segmented chain and one fold per
@@ -307,6 +341,7 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     g_tl_origin = mark(s);
   }
   int rc = panel(0, bs < n ? bs : n, s);
+  if (rc == BF_OK) writeback_block_column(a, 0, bs < n ? bs : n, s);
   for (int64_t done = 0; done < n && rc == BF_OK;) {
     const int64_t b = bs < n - done ? bs : n - done;
     const int64_t r2 = done + b, nr2 = n - r2;
@@ -331,6 +366,7 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     if (rc) break;
     if (g_timeline) ts.panel_end = mark(ps);
     cudaEventRecord(ev_panel, ps);
+    writeback_block_column(a, r2, b2, ps);  // block column k+1 is final
     // (3) the rest of the trailing update, concurrently with (2).  It belongs
     // to step k, so a pivot failure inside panel k+1 (index >= base+r2) must
     // not cancel it: the reference finishes step k before it meets that pivot.
@@ -524,6 +560,47 @@ int bf_trsm_rltn_ex_d(double alpha, const bf_view* tri, const bf_view* b, int64_
 
 int bf_cholesky_d(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream) {
   return chol_impl(MODE_D, a, levels, nlevels, d_info, S(stream));
+}
+int bf_cholesky_host_d(double* host, int64_t ld, const bf_view* work, const bf_chol_level* levels, int nlevels,
+                       int* d_info, void* stream) {
+  if (!host || !work || !levels || nlevels < 1) return fail(BF_ERR_VALUE, "null argument");
+  if (work->m != work->n) return fail(BF_ERR_SHAPE, "square matrix required");
+  if (work->cs != 1 || work->rs < work->n || ld < work->n) return fail(BF_ERR_UNSUPPORTED, "row-major work and host");
+  const int64_t n = work->n;
+  if (n == 0) return BF_OK;
+  cudaStream_t s = S(stream);
+  cudaStream_t cs = copy_stream();
+  if (!cs) return fail(BF_ERR_CUDA, "cannot create the copy stream");
+  double* dev = static_cast<double*>(work->base) + work->off;
+  // lower triangle in, by block columns of the root bs (rows >= the column's first)
+  const int64_t bs = levels[0].bs >= 1 ? levels[0].bs : n;
+  for (int64_t c0 = 0; c0 < n; c0 += bs) {
+    const int64_t w = bs < n - c0 ? bs : n - c0;
+    if (cudaMemcpy2DAsync(dev + c0 * work->rs + c0, size_t(work->rs) * 8, host + c0 * ld + c0, size_t(ld) * 8,
+                          size_t(w) * 8, size_t(n - c0), cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return fail(BF_ERR_CUDA, "host to device copy failed");
+  }
+  HostWriteback wb;
+  wb.host = host;
+  wb.ld = ld;
+  wb.cs = cs;
+  g_wb = &wb;
+  int rc = chol_impl(MODE_D, work, levels, nlevels, d_info, s);
+  g_wb = nullptr;
+  if (rc) return rc;
+  // whatever the lookahead did not stream back (the non-lookahead path, or all of it)
+  for (int64_t c0 = wb.copied_upto; c0 < n; c0 += bs) {
+    const int64_t w = bs < n - c0 ? bs : n - c0;
+    cudaMemcpy2DAsync(host + c0 * ld + c0, size_t(ld) * 8, dev + c0 * work->rs + c0, size_t(work->rs) * 8,
+                      size_t(w) * 8, size_t(n - c0), cudaMemcpyDeviceToHost, s);
+  }
+  // the caller's stream completes only after every copy
+  cudaEvent_t ev;
+  cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  cudaEventRecord(ev, cs);
+  cudaStreamWaitEvent(s, ev, 0);
+  cudaEventDestroy(ev);
+  return cudaGetLastError() == cudaSuccess ? BF_OK : fail(BF_ERR_CUDA, "host factorization copies failed");
 }
 int bf_cholesky_s(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream) {
   return chol_impl(MODE_S, a, levels, nlevels, d_info, S(stream));

@@ -94,6 +94,7 @@ _SIGNATURES = {
     "bf_trsm_rltn_d": ([_D, _V, _V, _L, _VP, _VP], _I),
     "bf_trsm_rltn_s": ([_D, _V, _V, _L, _VP, _VP], _I),
     "bf_cholesky_d": ([_V, _P(BfCholLevel), _I, _VP, _VP], _I),
+    "bf_cholesky_host_d": ([_VP, _L, _V, _P(BfCholLevel), _I, _VP, _VP], _I),
     "bf_cholesky_s": ([_V, _P(BfCholLevel), _I, _VP, _VP], _I),
     "bf_cholesky_ex_d": ([_V, _P(BfCholLevel), _I, _L, _VP, _VP], _I),
     "bf_trsm_rltn_ex_d": ([_D, _V, _V, _L, _VP, _VP, _VP], _I),

@@ -32,7 +32,7 @@ from ..engine.gemm import _launch_gemm
 from ..errors import NotPositiveDefiniteError, ShapeError
 from ..views import MatrixView, partition_steps
 
-__all__ = ["cholesky", "cholesky_async"]
+__all__ = ["cholesky", "cholesky_async", "cholesky_host"]
 
 _LEAF = {"unblocked1": 1, "unblocked2": 2, "unblocked3": 3}
 
@@ -81,6 +81,55 @@ def cholesky_async(
 
 
 # -- the tree walk, operation for operation as factor/cholesky.py:118-158 ---------
+
+
+def cholesky_host(
+    host: torch.Tensor, uplo: str = "lower", tree: Optional[ControlNode] = None,
+    work: Optional[torch.Tensor] = None, device: Optional[torch.device] = None,
+) -> None:
+    """In place on a HOST fp64 matrix (a CPU torch tensor, ideally pinned —
+    `torch.empty(..., pin_memory=True)`): the reference's call shape
+    (factor/cholesky.py:99-115 factors a NumPy array in place) with the
+    compute on the GPU.  Only the lower triangle travels (by block columns),
+    and every finished block column returns while later steps still run.
+    `work` (n x n fp64 on the device) is reused when given.  Upper is the
+    lower algorithm on the transpose, through a host-side transposed copy."""
+    if host.device.type != "cpu" or host.dtype != torch.float64 or host.dim() != 2 or host.shape[0] != host.shape[1]:
+        raise ShapeError("cholesky_host needs a square fp64 CPU tensor")
+    if uplo == "upper":
+        t = host.t().contiguous()
+        cholesky_host(t, "lower", tree, work, device)
+        host.copy_(t.t())
+        return
+    if uplo != "lower":
+        raise ValueError(f"uplo must be 'lower' or 'upper', got {uplo!r}")
+    if host.stride(1) != 1:
+        raise ShapeError("cholesky_host needs a row-major host matrix")
+    n = host.shape[0]
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if work is None:
+        work = torch.empty((n, n), dtype=torch.float64, device=dev)
+    if tuple(work.shape) != (n, n) or work.dtype != torch.float64 or work.stride(1) != 1:
+        raise ShapeError("work must be an n x n row-major fp64 device tensor")
+    from ..views import DType, from_torch
+
+    if tree is None:
+        tree = default_tree("cholesky", n, DType.F64)
+    check_valid(tree, op="cholesky")
+    levels = flatten_cholesky(tree, resolve_config(tree, DType.F64))
+    arr = (_lib.BfCholLevel * len(levels))(*[_lib.BfCholLevel(v, 0, bs, kc) for v, bs, kc in levels])
+    info = torch.full((1,), -1, dtype=torch.int32, device=work.device)
+    vw = _lib.as_bfview(from_torch(work))
+    rc = _lib.lib().bf_cholesky_host_d(host.data_ptr(), host.stride(0), ctypes.byref(vw), arr, len(levels),
+                                       info.data_ptr(), _lib.stream_ptr(work.device))
+    _lib.check(rc, "cholesky_host")
+    bad = int(info.item())
+    if bad >= 0:
+        # the reference's partial state lives in `work`: bring back its lower triangle
+        torch.cuda.synchronize(work.device)
+        low = torch.tril(work).cpu()
+        host.copy_(torch.where(torch.tril(torch.ones(n, n, dtype=torch.bool)), low, host))
+        raise NotPositiveDefiniteError(bad)
 
 
 def _leaf(a: MatrixView, variant: str, base: int, info: torch.Tensor) -> None:

@@ -243,3 +243,35 @@ def test_fused_trsm_subtree_bitwise(cuda, dt, kc, bs, n):
             lib.bf_set_option(b"fused_trsm", 1)
             lib.bf_set_option(b"trsm_warp", 1)
     assert outs[0] == outs[1] == outs[2] == digest(st)
+
+
+@pytest.mark.parametrize("n,uplo", [(1000, "lower"), (5000, "lower"), (777, "upper")])
+def test_cholesky_host_streams_back_same_bits(cuda, n, uplo):
+    """The host entry point (lower triangle in by block columns, finished
+    block columns streamed back under the remaining steps) gives exactly
+    bf.cholesky's bits and leaves the other host triangle untouched."""
+    t = TREES[1] if n < 2000 else ('{"op":"cholesky","variant":3,"bs":1024,"kernel":{"kc":1024},"child":'
+                                   '{"op":"cholesky","variant":3,"bs":128,"child":{"op":"cholesky","variant":"unblocked3"}}}')
+    a0 = spd_int(17, n)
+    host = torch.from_numpy(a0.copy()).pin_memory()
+    bf.cholesky_host(host, uplo, parse_tree(t))
+    ref = chol_gpu(a0, t, uplo).reshape(n, n)
+    got = host.numpy()
+    tri, other = (np.tril, np.triu) if uplo == "lower" else (np.triu, np.tril)
+    assert tri(got).tobytes() == tri(ref).tobytes()
+    assert other(got, 1 if uplo == "lower" else -1).tobytes() == other(a0, 1 if uplo == "lower" else -1).tobytes()
+
+
+def test_cholesky_host_npd_partial_state(cuda):
+    a0 = spd_int(9, 3000)
+    a0[2211, 2211] = -1e6
+    t = ('{"op":"cholesky","variant":3,"bs":512,"kernel":{"kc":512},"child":'
+         '{"op":"cholesky","variant":3,"bs":128,"child":{"op":"cholesky","variant":"unblocked3"}}}')
+    host = torch.from_numpy(a0.copy()).pin_memory()
+    with pytest.raises(bf.errors.NotPositiveDefiniteError) as e:
+        bf.cholesky_host(host, "lower", parse_tree(t))
+    assert e.value.index == 2211
+    v = make_view(3000, 3000, fill=a0)
+    with pytest.raises(bf.errors.NotPositiveDefiniteError):
+        bf.cholesky(v, tree=parse_tree(t))
+    assert np.tril(host.numpy()).tobytes() == np.tril(v.to_numpy()).tobytes()

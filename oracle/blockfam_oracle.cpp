@@ -328,6 +328,112 @@ int64_t chol_run(const View<T>& a, const Level* lv, int nl, int idx, int64_t bas
   return -1;
 }
 
+// ---- LU with partial pivoting (factor/lu.py:19-53, 70-103) ----------------
+// pivots (factor/pivots.py:46-61): forward = ascending swap order
+template <typename T>
+void apply_pivots(const View<T>& a, const int64_t* piv, int64_t count, bool backward) {
+  for (int64_t q = 0; q < count; ++q) {
+    const int64_t k = backward ? count - 1 - q : q;
+    const int64_t p = piv[k];
+    if (p == k) continue;
+    for (int64_t j = 0; j < a.n; ++j) std::swap(a.at(k, j), a.at(p, j));
+  }
+}
+
+// engine/trsm.py:114-125: unit lower, row by row, one ascending chain per element
+template <typename T>
+void trsm_left_base(double alpha, const View<T>& t, const View<T>& b) {
+  if (alpha != 1.0)
+    for (int64_t i = 0; i < t.n; ++i)
+      for (int64_t c = 0; c < b.n; ++c) b.at(i, c) = T(double(b.at(i, c)) * alpha);
+  for (int64_t i = 1; i < t.n; ++i)
+    for (int64_t c = 0; c < b.n; ++c) {
+      T acc = b.at(i, c);
+      for (int64_t p = 0; p < i; ++p) acc = acc - T(t.at(i, p) * b.at(p, c));
+      b.at(i, c) = acc;
+    }
+}
+
+// engine/trsm.py:71-88
+template <typename T>
+void trsm_left_rec(double alpha, const View<T>& tri, const View<T>& b, int64_t kc, int nthreads) {
+  const int64_t n = tri.n;
+  if (b.n == 0 || n == 0) return;
+  if (n <= 32) {
+    trsm_left_base(alpha, tri, b);
+    return;
+  }
+  const int64_t n1 = n / 2, n2 = n - n1;
+  trsm_left_rec(alpha, tri.sub(0, n1, 0, n1), b.sub(0, n1, 0, b.n), kc, nthreads);
+  gemm_view<T, T>(-1.0, tri.sub(n1, n2, 0, n1), b.sub(0, n1, 0, b.n), alpha, b.sub(n1, n2, 0, b.n), 0, kc, nthreads);
+  trsm_left_rec(1.0, tri.sub(n1, n2, n1, n2), b.sub(n1, n2, 0, b.n), kc, nthreads);
+}
+
+// factor/lu.py:19-53: ties keep the smallest row; a zero pivot column is skipped
+template <typename T>
+int64_t lu_leaf(const View<T>& a, int64_t* piv) {
+  const int64_t m = a.m, n = a.n, steps = m < n ? m : n;
+  int64_t sing = -1;
+  for (int64_t k = 0; k < steps; ++k) {
+    int64_t p = k;
+    T best = std::fabs(a.at(k, k));
+    for (int64_t i = k + 1; i < m; ++i) {
+      const T v = std::fabs(a.at(i, k));
+      if (v > best) {
+        best = v;
+        p = i;
+      }
+    }
+    piv[k] = p;
+    if (best == T(0)) {
+      if (sing < 0) sing = k;
+      continue;
+    }
+    if (p != k)
+      for (int64_t j = 0; j < n; ++j) std::swap(a.at(k, j), a.at(p, j));
+    const T d = a.at(k, k);
+    for (int64_t i = k + 1; i < m; ++i) a.at(i, k) = a.at(i, k) / d;
+    for (int64_t j = k + 1; j < n; ++j) {
+      const T u = a.at(k, j);
+      for (int64_t i = k + 1; i < m; ++i) a.at(i, j) = a.at(i, j) - T(a.at(i, k) * u);
+    }
+  }
+  return sing;
+}
+
+// factor/lu.py:70-103; level variant 20 = blocked, 21 = unblocked leaf
+template <typename T>
+int64_t lu_run(const View<T>& a, const Level* lv, int nl, int idx, int64_t* piv, int64_t base, int nthreads) {
+  const int64_t m = a.m, n = a.n, steps = m < n ? m : n;
+  if (steps == 0) return -1;
+  Level node = idx < nl ? lv[idx] : Level{21, 0, 0, idx > 0 ? lv[idx - 1].kc : 256};
+  if (node.variant == 21) {
+    const int64_t sing = lu_leaf(a, piv);
+    return sing < 0 ? -1 : base + sing;
+  }
+  const int64_t bs = node.bs, kc = node.kc;
+  int64_t first = -1;
+  std::vector<int64_t> local;
+  for (int64_t k = 0; k < steps; k += bs) {
+    const int64_t b = bs < steps - k ? bs : steps - k;
+    local.assign(size_t(b), 0);
+    for (int64_t q = 0; q < b; ++q) local[size_t(q)] = q;
+    const int64_t sing = lu_run(a.sub(k, m - k, k, b), lv, nl, idx + 1, local.data(), base + k, nthreads);
+    if (sing >= 0 && first < 0) first = sing;
+    for (int64_t q = 0; q < b; ++q) piv[k + q] = k + local[size_t(q)];
+    apply_pivots(a.sub(k, m - k, 0, k), local.data(), b, false);
+    apply_pivots(a.sub(k, m - k, k + b, n - k - b), local.data(), b, false);
+    if (k + b < n) {
+      const View<T> a12 = a.sub(k, b, k + b, n - k - b);
+      trsm_left_rec(1.0, a.sub(k, b, k, b), a12, kc, nthreads);
+      if (k + b < m)
+        gemm_view<T, T>(-1.0, a.sub(k + b, m - k - b, k, b), a12, 1.0, a.sub(k + b, m - k - b, k + b, n - k - b), 0,
+                        kc, nthreads);
+    }
+  }
+  return first;
+}
+
 }  // namespace
 
 struct orc_view_d {
@@ -391,6 +497,19 @@ void orc_gemm_naive_d(double alpha, const orc_view_d* a, const orc_view_d* b, do
       for (int64_t p = 0; p < A.n; ++p) acc = acc + A.at(i, p) * B.at(p, j);
       C.at(i, j) = beta == 0.0 ? alpha * acc : beta * C.at(i, j) + alpha * acc;
     }
+}
+
+int64_t orc_lu_d(const orc_view_d* a, const Level* lv, int nl, int64_t* piv, int nthreads) {
+  return lu_run(V(a), lv, nl, 0, piv, 0, nthreads);
+}
+int64_t orc_lu_s(const orc_view_s* a, const Level* lv, int nl, int64_t* piv, int nthreads) {
+  return lu_run(V(a), lv, nl, 0, piv, 0, nthreads);
+}
+void orc_trsm_llnu_d(double alpha, const orc_view_d* t, const orc_view_d* b, int64_t kc, int nthreads) {
+  trsm_left_rec(alpha, V(t), V(b), kc, nthreads);
+}
+void orc_trsm_llnu_s(double alpha, const orc_view_s* t, const orc_view_s* b, int64_t kc, int nthreads) {
+  trsm_left_rec(alpha, V(t), V(b), kc, nthreads);
 }
 
 }  // extern "C"

@@ -62,6 +62,12 @@ def lib() -> ctypes.CDLL:
         for name in ("orc_cholesky_d", "orc_cholesky_s"):
             getattr(_lib, name).argtypes = [P, ctypes.POINTER(_Level), ctypes.c_int, ctypes.c_int]
             getattr(_lib, name).restype = ctypes.c_int64
+        for name in ("orc_lu_d", "orc_lu_s"):
+            getattr(_lib, name).argtypes = [P, ctypes.POINTER(_Level), ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+            getattr(_lib, name).restype = ctypes.c_int64
+        for name in ("orc_trsm_llnu_d", "orc_trsm_llnu_s"):
+            getattr(_lib, name).argtypes = [ctypes.c_double, P, P, ctypes.c_int64, ctypes.c_int]
+            getattr(_lib, name).restype = None
         _lib.orc_gemm_naive_d.argtypes = [ctypes.c_double, P, P, ctypes.c_double, P]
         _lib.orc_gemm_naive_d.restype = None
         VP, L = ctypes.c_void_p, ctypes.c_int64
@@ -155,6 +161,40 @@ def cholesky(storage: np.ndarray, meta: dict, levels, *, uplo: str = "lower", nt
         meta = transposed(meta)
     arr = (_Level * len(levels))(*[_Level(v, 0, bs, kc) for v, bs, kc in levels])
     return int(getattr(lib(), "orc_cholesky_" + _suffix(storage))(_view(storage, meta), arr, len(levels), nthreads))
+
+
+def levels_from_tree_lu(doc: Optional[dict], n: int, dtype: str) -> list[tuple[int, int, int]]:
+    """LU tree document -> [(20 blocked | 21 leaf, bs, effective kc)]; None is
+    the reference default (control.py:212-223: unblocked up to 128, else one
+    blocked level of 128)."""
+    if doc is None:
+        doc = {"op": "lu", "variant": "unblocked"} if n <= 128 else {
+            "op": "lu", "variant": "blocked", "bs": 128, "child": {"op": "lu", "variant": "unblocked"}}
+    kc = _DEFAULT_KC[dtype]
+    out = []
+    node = doc
+    while node is not None:
+        kc = int((node.get("kernel") or {}).get("kc", kc))
+        out.append((20, int(node["bs"]), kc) if node["variant"] == "blocked" else (21, 0, kc))
+        node = node.get("child")
+    return out
+
+
+def lu(storage: np.ndarray, meta: dict, levels, *, nthreads: int = 1) -> tuple[int, np.ndarray]:
+    """In-place LU with partial pivoting (factor/lu.py:56-103): returns the
+    first exactly-zero pivot column (or -1) and the LAPACK-style swap list."""
+    steps = min(meta["m"], meta["n"])
+    piv = np.arange(max(steps, 1), dtype=np.int64)
+    arr = (_Level * len(levels))(*[_Level(v, 0, bs, kc) for v, bs, kc in levels])
+    sing = int(getattr(lib(), "orc_lu_" + _suffix(storage))(_view(storage, meta), arr, len(levels),
+                                                               piv.ctypes.data, nthreads))
+    return sing, piv[:steps]
+
+
+def trsm_llnu(alpha: float, tri, b, *, kc: int, nthreads: int = 1) -> None:
+    """unit_tril(tri) X = alpha b, b := X (engine/trsm.py:71-88,114-125)."""
+    (ts, tm), (bs_, bm) = tri, b
+    getattr(lib(), "orc_trsm_llnu_" + _suffix(bs_))(float(alpha), _view(ts, tm), _view(bs_, bm), int(kc), nthreads)
 
 
 def host_threads() -> int:

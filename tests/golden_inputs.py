@@ -64,3 +64,35 @@ def trsm_inputs(seed: int, dt: str, n: int, m: int):
 def tensor_inputs(seed: int, a_dims, b_dims, c_dims):
     rng = np.random.default_rng(seed)
     return (rng.uniform(-1, 1, a_dims), rng.uniform(-1, 1, b_dims), rng.uniform(-1, 1, c_dims))
+
+
+def lu_input(seed: int, m: int, n: int, kind: str, dt: str = "f64") -> np.ndarray:
+    """Platform-independent LU inputs (numpy default_rng values):
+    uniform  U(-1,1): real pivoting everywhere;
+    ties     small integers: equal-magnitude pivot candidates (smallest row wins);
+    diag     U(-1,1) + n I (the reference CLI's generator, cli.py:66-67): no swaps;
+    zerocol  uniform with column n//3 zeroed below the diagonal: an exactly-zero pivot."""
+    rng = np.random.default_rng(seed)
+    if kind == "uniform":
+        a = rng.uniform(-1, 1, (m, n))
+    elif kind == "ties":
+        a = rng.integers(-2, 3, (m, n)).astype(np.float64)
+    elif kind == "diag":
+        a = rng.uniform(-1, 1, (m, n)) + max(m, n) * np.eye(m, n)
+    elif kind == "zerocol":
+        a = rng.uniform(-1, 1, (m, n))
+        j = n // 3
+        a[:, j] = 0.0
+    else:
+        raise KeyError(kind)
+    return a.astype(NP[dt])
+
+
+def left_trsm_inputs(seed: int, n: int, ncols: int, dt: str = "f64"):
+    """(tri, b): unit-lower triangle (strict lower U(-1,1)/n, diagonal and
+    upper garbage that must be ignored) and a right-hand side block."""
+    rng = np.random.default_rng(seed)
+    tri = rng.uniform(-1, 1, (n, n)) / max(n, 1)
+    tri[np.triu_indices(n)] = 7.0  # never read: unit diagonal, lower only
+    b = rng.uniform(-1, 1, (n, ncols))
+    return tri.astype(NP[dt]), b.astype(NP[dt])

@@ -149,6 +149,27 @@ int bf_gemm_scatter_s(double alpha, const bf_scatter_view* a, const bf_scatter_v
 int bf_gemm_scatter_sd(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
                        const bf_scatter_view* c, int64_t kc, void* stream);
 
+/* LU with partial pivoting.
+ * bf_lu_*: replaces factor/lu.py:56-103 lu_partial/_run with the tree walk in
+ *   C++: levels are the flattened lu tree (variant 20 = blocked, bs and the
+ *   effective kc; 21 = the unblocked leaf, factor/lu.py:19-53).  d_piv
+ *   (device, min(m,n) int64) receives the LAPACK-style swap list, d_sing
+ *   (device int, preset -1) the first exactly-zero pivot column.  Bitwise the
+ *   reference.
+ * bf_trsm_llnu_*: unit_tril(tri) X = alpha B, replaces engine/trsm.py:71-88
+ *   (LEFT_LOWER_NOTRANS_UNIT), bitwise.
+ * bf_trsm_lun_*: triu(U) X = B for lu_solve (factor/lu.py:117-130 does this
+ *   with NumPy; no bitwise contract).
+ * bf_apply_pivots_*: factor/pivots.py:46-61 apply_pivots (forward/backward). */
+int bf_lu_d(const bf_view* a, const bf_chol_level* levels, int nlevels, int64_t* d_piv, int* d_sing, void* stream);
+int bf_lu_s(const bf_view* a, const bf_chol_level* levels, int nlevels, int64_t* d_piv, int* d_sing, void* stream);
+int bf_trsm_llnu_d(double alpha, const bf_view* tri, const bf_view* b, int64_t kc, void* stream);
+int bf_trsm_llnu_s(double alpha, const bf_view* tri, const bf_view* b, int64_t kc, void* stream);
+int bf_trsm_lun_d(const bf_view* u, const bf_view* b, int64_t kc, void* stream);
+int bf_trsm_lun_s(const bf_view* u, const bf_view* b, int64_t kc, void* stream);
+int bf_apply_pivots_d(const bf_view* a, const int64_t* d_piv, int64_t count, int backward, void* stream);
+int bf_apply_pivots_s(const bf_view* a, const int64_t* d_piv, int64_t count, int backward, void* stream);
+
 /* Mixed precision (BASELINE configs[3]; no reference counterpart).
  * bf_gemm_bf16: C(fp32 view) := beta*C + alpha * A * B^T on tcgen05/TMEM, with
  * A (c->m x k) and B (c->n x k) row-major bf16 (ld in elements, 16-byte aligned).

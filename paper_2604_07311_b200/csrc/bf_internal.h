@@ -74,7 +74,8 @@ extern int g_tma_variant;     // bf_set_option("tma_variant", 0..3)
 extern int g_tiles_per_cta;   // bf_set_option("tiles_per_cta", t)
 extern int g_bf16_tma_c;      // bf16 GEMM: TMA C-tile epilogue (1) or per-element fallback (0)
 extern int g_trsm_warp;       // fused TRSM subtree: 4-warps-per-32-rows kernel (1) or the 64-row CTA kernel (0)
-extern int g_leaf_blocked;    // variant-3 leaves n <= 128: blocked lane-per-row kernel (1) or v3 (0)
+extern int g_leaf_blocked;
+extern int g_lu_grid_max;   // LU leaf: cap on the cooperative grid (0 = SM-derived)    // variant-3 leaves n <= 128: blocked lane-per-row kernel (1) or v3 (0)
 int launch_gemm_simt_f32(const GemmParams& p, cudaStream_t s);        // f32 storage, f32 acc
 int launch_gemm_simt_f32acc64(const GemmParams& p, cudaStream_t s);   // f32 storage, f64 acc
 int launch_scale(int is_f64, double beta, void* c, int64_t off, int64_t m, int64_t n, int64_t rs,
@@ -104,6 +105,15 @@ int launch_f64_to_f32(const double* src, int64_t soff, int64_t srs, int64_t scs,
                       int64_t dcs, int64_t m, int64_t n, int lower_only, cudaStream_t s);
 int launch_residual(const double* A, int64_t lda, const double* x, const double* b, double* r, int64_t n,
                     cudaStream_t s);
+int launch_lu_leaf(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t n, int64_t* piv,
+                   int* d_sing, int64_t base, cudaStream_t s);
+int launch_apply_pivots(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int64_t ncols, const int64_t* piv,
+                        int64_t count, int64_t sub, int backward, cudaStream_t s);
+int launch_add_offset(int64_t* piv, int64_t count, int64_t delta, cudaStream_t s);
+int launch_trsm_left_base(int is_f64, double alpha, const void* t, int64_t toff, int64_t trs, int64_t tcs, void* b,
+                          int64_t boff, int64_t brs, int64_t bcs, int n, int64_t ncols, cudaStream_t s);
+int launch_trsm_upper_base(int is_f64, const void* u, int64_t uoff, int64_t urs, int64_t ucs, void* b, int64_t boff,
+                           int64_t brs, int64_t bcs, int n, int64_t ncols, cudaStream_t s);
 int launch_row_abs_sum(const double* A, int64_t lda, double* out, int64_t n, cudaStream_t s);
 int launch_potrs_f32_f64(const float* L, int64_t ld, double* x, int64_t n, cudaStream_t s);
 int launch_potrs_blocked(const float* L, int64_t ld, const float* xinv, int64_t bs, double* x, int64_t n,

@@ -385,6 +385,82 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
   return rc;
 }
 
+// ---- LU (factor/lu.py:56-130, engine/trsm.py:71-88) ------------------------
+// unit_tril(tri) X = alpha B, the reference's recursive halving over GEMM
+int trsm_left_rec(Mode mode, double alpha, const bf_view& tri, const bf_view& b, int64_t kc, cudaStream_t s) {
+  const int64_t n = tri.n;
+  if (b.n == 0 || n == 0) return BF_OK;
+  if (n <= 32) {
+    int rc = bf::launch_trsm_left_base(storage_is_f64(mode), alpha, tri.base, tri.off, tri.rs, tri.cs, b.base, b.off,
+                                       b.rs, b.cs, int(n), b.n, s);
+    return rc ? fail(BF_ERR_CUDA, "left trsm base launch failed") : BF_OK;
+  }
+  const int64_t n1 = n / 2, n2 = n - n1;
+  int rc = trsm_left_rec(mode, alpha, subview(tri, 0, n1, 0, n1), subview(b, 0, n1, 0, b.n), kc, s);
+  if (rc) return rc;
+  rc = gemm_impl(mode, -1.0, subview(tri, n1, n2, 0, n1), subview(b, 0, n1, 0, b.n), alpha, subview(b, n1, n2, 0, b.n),
+                 0, kc, nullptr, s);
+  if (rc) return rc;
+  return trsm_left_rec(mode, 1.0, subview(tri, n1, n2, n1, n2), subview(b, n1, n2, 0, b.n), kc, s);
+}
+
+// triu(U) X = B (non-unit), recursive: the bottom half first
+int trsm_upper_rec(Mode mode, const bf_view& u, const bf_view& b, int64_t kc, cudaStream_t s) {
+  const int64_t n = u.n;
+  if (b.n == 0 || n == 0) return BF_OK;
+  if (n <= 32) {
+    int rc = bf::launch_trsm_upper_base(storage_is_f64(mode), u.base, u.off, u.rs, u.cs, b.base, b.off, b.rs, b.cs,
+                                        int(n), b.n, s);
+    return rc ? fail(BF_ERR_CUDA, "upper trsm base launch failed") : BF_OK;
+  }
+  const int64_t n1 = n / 2, n2 = n - n1;
+  int rc = trsm_upper_rec(mode, subview(u, n1, n2, n1, n2), subview(b, n1, n2, 0, b.n), kc, s);
+  if (rc) return rc;
+  rc = gemm_impl(mode, -1.0, subview(u, 0, n1, n1, n2), subview(b, n1, n2, 0, b.n), 1.0, subview(b, 0, n1, 0, b.n), 0,
+                 kc, nullptr, s);
+  if (rc) return rc;
+  return trsm_upper_rec(mode, subview(u, 0, n1, 0, n1), subview(b, 0, n1, 0, b.n), kc, s);
+}
+
+int apply_pivots_impl(Mode mode, const bf_view& a, const int64_t* piv, int64_t count, int64_t sub, int backward,
+                      cudaStream_t s) {
+  if (a.m == 0 || a.n == 0 || count == 0) return BF_OK;
+  int rc = bf::launch_apply_pivots(storage_is_f64(mode), a.base, a.off, a.rs, a.cs, a.n, piv, count, sub, backward, s);
+  return rc ? fail(BF_ERR_CUDA, "row swap launch failed") : BF_OK;
+}
+
+// levels: variant 20 = blocked, 21 = unblocked leaf (flatten of the lu tree)
+int lu_run(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int idx, int64_t* piv, int64_t base,
+           int* d_sing, cudaStream_t s) {
+  const int64_t m = a.m, n = a.n, steps = m < n ? m : n;
+  if (steps == 0) return BF_OK;
+  const bool leaf = idx >= nl || lv[idx].variant == 21;
+  if (leaf) {
+    int rc = bf::launch_lu_leaf(storage_is_f64(mode), a.base, a.off, a.rs, a.cs, m, n, piv, d_sing, base, s);
+    return rc ? fail(BF_ERR_CUDA, "lu leaf launch failed") : BF_OK;
+  }
+  if (lv[idx].variant != 20 || lv[idx].bs < 1) return fail(BF_ERR_VALUE, "bad lu level");
+  const int64_t bs = lv[idx].bs, kc = lv[idx].kc;
+  for (int64_t k = 0; k < steps; k += bs) {
+    const int64_t b = bs < steps - k ? bs : steps - k;
+    int rc = lu_run(mode, subview(a, k, m - k, k, b), lv, nl, idx + 1, piv + k, base + k, d_sing, s);
+    if (rc) return rc;
+    rc = apply_pivots_impl(mode, subview(a, k, m - k, 0, k), piv + k, b, 0, 0, s);
+    if (!rc) rc = apply_pivots_impl(mode, subview(a, k, m - k, k + b, n - k - b), piv + k, b, 0, 0, s);
+    if (!rc && bf::launch_add_offset(piv + k, b, k, s)) rc = fail(BF_ERR_CUDA, "pivot offset launch failed");
+    if (rc) return rc;
+    if (k + b < n) {
+      const bf_view a12 = subview(a, k, b, k + b, n - k - b);
+      rc = trsm_left_rec(mode, 1.0, subview(a, k, b, k, b), a12, kc, s);
+      if (!rc && k + b < m)
+        rc = gemm_impl(mode, -1.0, subview(a, k + b, m - k - b, k, b), a12, 1.0,
+                       subview(a, k + b, m - k - b, k + b, n - k - b), 0, kc, nullptr, s);
+      if (rc) return rc;
+    }
+  }
+  return BF_OK;
+}
+
 int chol_impl(Mode mode, const bf_view* a, const bf_chol_level* lv, int nl, int* d_info, cudaStream_t s) {
   if (!a || (nl > 0 && !lv)) return fail(BF_ERR_VALUE, "null argument");
   if (a->m != a->n) return fail(BF_ERR_SHAPE, "square matrix required");
@@ -468,6 +544,10 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "tma_variant") == 0) {
     bf::g_tma_variant = int(value & 3);
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "lu_grid") == 0 && value >= 0) {
+    bf::g_lu_grid_max = int(value);
     return BF_OK;
   }
   if (name && std::strcmp(name, "leaf_blocked") == 0) {
@@ -601,6 +681,44 @@ int bf_cholesky_host_d(double* host, int64_t ld, const bf_view* work, const bf_c
   cudaStreamWaitEvent(s, ev, 0);
   cudaEventDestroy(ev);
   return cudaGetLastError() == cudaSuccess ? BF_OK : fail(BF_ERR_CUDA, "host factorization copies failed");
+}
+int bf_lu_d(const bf_view* a, const bf_chol_level* levels, int nlevels, int64_t* d_piv, int* d_sing, void* stream) {
+  if (!a || !levels || nlevels < 1 || !d_piv || !d_sing) return fail(BF_ERR_VALUE, "null argument");
+  return lu_run(MODE_D, *a, levels, nlevels, 0, d_piv, 0, d_sing, S(stream));
+}
+int bf_lu_s(const bf_view* a, const bf_chol_level* levels, int nlevels, int64_t* d_piv, int* d_sing, void* stream) {
+  if (!a || !levels || nlevels < 1 || !d_piv || !d_sing) return fail(BF_ERR_VALUE, "null argument");
+  return lu_run(MODE_S, *a, levels, nlevels, 0, d_piv, 0, d_sing, S(stream));
+}
+int bf_trsm_llnu_d(double alpha, const bf_view* tri, const bf_view* b, int64_t kc, void* stream) {
+  if (!tri || !b) return fail(BF_ERR_VALUE, "null view");
+  if (tri->m != tri->n || b->m != tri->n) return fail(BF_ERR_SHAPE, "left solve dims mismatch");
+  if (kc < 1) return fail(BF_ERR_VALUE, "kc must be >= 1");
+  return trsm_left_rec(MODE_D, alpha, *tri, *b, kc, S(stream));
+}
+int bf_trsm_llnu_s(double alpha, const bf_view* tri, const bf_view* b, int64_t kc, void* stream) {
+  if (!tri || !b) return fail(BF_ERR_VALUE, "null view");
+  if (tri->m != tri->n || b->m != tri->n) return fail(BF_ERR_SHAPE, "left solve dims mismatch");
+  if (kc < 1) return fail(BF_ERR_VALUE, "kc must be >= 1");
+  return trsm_left_rec(MODE_S, alpha, *tri, *b, kc, S(stream));
+}
+int bf_trsm_lun_d(const bf_view* u, const bf_view* b, int64_t kc, void* stream) {
+  if (!u || !b) return fail(BF_ERR_VALUE, "null view");
+  if (u->m != u->n || b->m != u->n) return fail(BF_ERR_SHAPE, "upper solve dims mismatch");
+  return trsm_upper_rec(MODE_D, *u, *b, kc < 1 ? 256 : kc, S(stream));
+}
+int bf_trsm_lun_s(const bf_view* u, const bf_view* b, int64_t kc, void* stream) {
+  if (!u || !b) return fail(BF_ERR_VALUE, "null view");
+  if (u->m != u->n || b->m != u->n) return fail(BF_ERR_SHAPE, "upper solve dims mismatch");
+  return trsm_upper_rec(MODE_S, *u, *b, kc < 1 ? 512 : kc, S(stream));
+}
+int bf_apply_pivots_d(const bf_view* a, const int64_t* d_piv, int64_t count, int backward, void* stream) {
+  if (!a || (count > 0 && !d_piv)) return fail(BF_ERR_VALUE, "null argument");
+  return apply_pivots_impl(MODE_D, *a, d_piv, count, 0, backward, S(stream));
+}
+int bf_apply_pivots_s(const bf_view* a, const int64_t* d_piv, int64_t count, int backward, void* stream) {
+  if (!a || (count > 0 && !d_piv)) return fail(BF_ERR_VALUE, "null argument");
+  return apply_pivots_impl(MODE_S, *a, d_piv, count, 0, backward, S(stream));
 }
 int bf_cholesky_s(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream) {
   return chol_impl(MODE_S, a, levels, nlevels, d_info, S(stream));

@@ -94,6 +94,14 @@ _SIGNATURES = {
     "bf_trsm_rltn_d": ([_D, _V, _V, _L, _VP, _VP], _I),
     "bf_trsm_rltn_s": ([_D, _V, _V, _L, _VP, _VP], _I),
     "bf_cholesky_d": ([_V, _P(BfCholLevel), _I, _VP, _VP], _I),
+    "bf_lu_d": ([_V, _P(BfCholLevel), _I, _VP, _VP, _VP], _I),
+    "bf_lu_s": ([_V, _P(BfCholLevel), _I, _VP, _VP, _VP], _I),
+    "bf_trsm_llnu_d": ([_D, _V, _V, _L, _VP], _I),
+    "bf_trsm_llnu_s": ([_D, _V, _V, _L, _VP], _I),
+    "bf_trsm_lun_d": ([_V, _V, _L, _VP], _I),
+    "bf_trsm_lun_s": ([_V, _V, _L, _VP], _I),
+    "bf_apply_pivots_d": ([_V, _VP, _L, _I, _VP], _I),
+    "bf_apply_pivots_s": ([_V, _VP, _L, _I, _VP], _I),
     "bf_cholesky_host_d": ([_VP, _L, _V, _P(BfCholLevel), _I, _VP, _VP], _I),
     "bf_cholesky_s": ([_V, _P(BfCholLevel), _I, _VP, _VP], _I),
     "bf_cholesky_ex_d": ([_V, _P(BfCholLevel), _I, _L, _VP, _VP], _I),

@@ -546,6 +546,10 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_tma_variant = int(value & 3);
     return BF_OK;
   }
+  if (name && std::strcmp(name, "lu_global") == 0) {
+    bf::g_lu_global = value != 0;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "lu_grid") == 0 && value >= 0) {
     bf::g_lu_grid_max = int(value);
     return BF_OK;

@@ -26,6 +26,7 @@
 namespace bf {
 
 int g_lu_grid_max = 0;  // bf_set_option("lu_grid", g): cap the leaf's cooperative grid (0 = SM-derived)
+int g_lu_global = 0;    // bf_set_option("lu_global", 1): force the global-memory leaf
 
 namespace {
 
@@ -88,29 +89,49 @@ __global__ void __launch_bounds__(LU_THREADS) lu_leaf_kernel(T* a, int64_t off, 
     grid.sync();
     // (b) every CTA combines the bands in row order from the diagonal entry,
     // exactly the sequential scan: a later band wins only with a larger value
-    double best = double(fabs(ld(k, k)));
-    int64_t p = k;
-    for (int c = 0; c < G; ++c) {
-      const int64_t ci = __ldcg(part_i + c);
-      const double cv = __ldcg(part_v + c);
-      if (ci >= 0 && cv > best) {
-        best = cv;
-        p = ci;
+    // (the partials arrive in one round trip: lane c loads band c, G <= 32;
+    // max value, smallest row among ties = the row-order combination)
+    __shared__ double s_best;
+    __shared__ int64_t s_p;
+    if (tid < 32) {
+      double cv = -1.0;
+      int64_t ci = -1;
+      if (tid < G) {
+        ci = __ldcg(part_i + tid);
+        cv = __ldcg(part_v + tid);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_down_sync(0xffffffffu, cv, o);
+        const int64_t oi = __shfl_down_sync(0xffffffffu, ci, o);
+        if (oi >= 0 && (ov > cv || (ov == cv && (ci < 0 || oi < ci)))) {
+          cv = ov;
+          ci = oi;
+        }
+      }
+      if (tid == 0) {
+        const double dkk = double(fabs(ld(k, k)));
+        const bool take = ci >= 0 && cv > dkk;
+        s_best = take ? cv : dkk;
+        s_p = take ? ci : k;
       }
     }
+    __syncthreads();
+    const double best = s_best;
+    const int64_t p = s_p;
     if (blockIdx.x == 0 && tid == 0) {
       piv[k] = p;
       if (best == 0.0 && *d_sing < 0) *d_sing = int(base + k);
     }
     const bool live = !(best == 0.0);
-    // every thread of CTA 0 has read a(k,k) before any of them overwrites it
-    // (other CTAs only need `live`, which the swap cannot change)
+    // every thread has read s_best / s_p (and thread 0 a(k,k)) before the swap
+    // overwrites row k and the next column reuses the shared words
     __syncthreads();
     // (c) the swap, by CTA 0
     if (live && p != k && blockIdx.x == 0)
       for (int64_t j = tid; j < n; j += LU_THREADS) {
-        const T t = ld(k, j);
-        at(k, j) = ld(p, j);
+        const T t = ld(k, j), u = ld(p, j);
+        at(k, j) = u;
         at(p, j) = t;
       }
     grid.sync();
@@ -120,10 +141,174 @@ __global__ void __launch_bounds__(LU_THREADS) lu_leaf_kernel(T* a, int64_t off, 
       for (int64_t i = lo + tid; i < r1; i += LU_THREADS) {
         const T lik = Ops<T>::div(ld(i, k), d);
         at(i, k) = lik;
-        for (int64_t j = k + 1; j < n; ++j) at(i, j) = Ops<T>::sub(ld(i, j), Ops<T>::mul(lik, ld(k, j)));
+        // loads batched ahead of the stores (a store may alias a later load,
+        // so a load-use-store loop would pay one L2 round trip per element)
+        for (int64_t j0 = k + 1; j0 < n; j0 += 16) {
+          T xi[16], xk[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const bool in = j0 + q < n;
+            xi[q] = in ? ld(i, j0 + q) : T(0);
+            xk[q] = in ? ld(k, j0 + q) : T(0);
+          }
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (j0 + q < n) at(i, j0 + q) = Ops<T>::sub(xi[q], Ops<T>::mul(lik, xk[q]));
+        }
       }
     }
+    // No barrier here: the next column's band search reads only this CTA's
+    // own rows (just updated by its own threads, after the block barrier);
+    // everything shared — a(k+1,k+1), the partials, the next swap — comes
+    // after the next grid barrier.
+    __syncthreads();
+  }
+}
+
+// Shared-memory variant (the usual case: a leaf panel no wider than 256):
+// each CTA keeps its band of rows in shared memory (row stride n+1), and per
+// column exactly one grid barrier separates "publish" from "use": every CTA
+// publishes its best candidate (value, row) together with that candidate's
+// whole row, and the owner of row k publishes row k; after the barrier every
+// CTA knows the pivot row's values without another round trip, performs the
+// swap on whichever of rows k / p it owns, and updates its band.  Publication
+// slots alternate by column parity, so a CTA racing ahead into column k+1
+// never overwrites what a slower one still reads for column k.
+template <typename T>
+__global__ void __launch_bounds__(LU_THREADS) lu_leaf_smem_kernel(T* a, int64_t off, int64_t rs, int64_t cs,
+                                                                int64_t m, int64_t n, int64_t* piv, int* d_sing,
+                                                                int64_t base, double* part_v, int64_t* part_i,
+                                                                T* cand_rows, T* rowk_buf) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char lu_smem[];
+  T* S = reinterpret_cast<T*>(lu_smem);
+  const int G = gridDim.x, tid = threadIdx.x, cta = blockIdx.x;
+  const int64_t ld = n + 1;
+  const int64_t chunk = (m + G - 1) / G;
+  const int64_t r0 = int64_t(cta) * chunk, r1 = r0 + chunk < m ? r0 + chunk : m;
+  const int64_t rows = r1 > r0 ? r1 - r0 : 0;
+  T* newk = S + chunk * ld;  // the pivot row's values for this column
+  const int64_t steps = m < n ? m : n;
+  __shared__ double red_v[LU_THREADS / 32];
+  __shared__ int64_t red_i[LU_THREADS / 32];
+  __shared__ double s_best;
+  __shared__ int64_t s_p;
+  __shared__ int s_src;  // band whose candidate row is the pivot row (-1: row k itself)
+  for (int64_t e = tid; e < rows * n; e += LU_THREADS) {
+    const int64_t i = e / n, j = e % n;
+    S[i * ld + j] = a[off + (r0 + i) * rs + j * cs];
+  }
+  __syncthreads();
+  for (int64_t k = 0; k < steps; ++k) {
+    const int par = int(k & 1);
+    double* pv = part_v + par * 32;
+    int64_t* pi = part_i + par * 32;
+    T* cand = cand_rows + int64_t(par) * 32 * n;
+    T* rk = rowk_buf + int64_t(par) * n;
+    // publish: this band's best candidate below k, its row, and row k
+    double bv = -1.0;
+    int64_t bi = -1;
+    const int64_t lo = r0 > k + 1 ? r0 : k + 1;
+    for (int64_t i = lo + tid; i < r1; i += LU_THREADS) {
+      const double v = double(fabs(S[(i - r0) * ld + k]));
+      if (v > bv) {
+        bv = v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_down_sync(0xffffffffu, bv, o);
+      const int64_t oi = __shfl_down_sync(0xffffffffu, bi, o);
+      if (oi >= 0 && (ov > bv || (ov == bv && (bi < 0 || oi < bi)))) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if ((tid & 31) == 0) {
+      red_v[tid >> 5] = bv;
+      red_i[tid >> 5] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < LU_THREADS / 32; ++w)
+        if (red_i[w] >= 0 && (red_v[w] > bv || (red_v[w] == bv && (bi < 0 || red_i[w] < bi)))) {
+          bv = red_v[w];
+          bi = red_i[w];
+        }
+      pv[cta] = bv;
+      pi[cta] = bi;
+      s_p = bi;
+    }
+    __syncthreads();
+    const int64_t mine = s_p;
+    if (mine >= 0)
+      for (int64_t j = tid; j < n; j += LU_THREADS) cand[int64_t(cta) * n + j] = S[(mine - r0) * ld + j];
+    if (k >= r0 && k < r1)
+      for (int64_t j = tid; j < n; j += LU_THREADS) rk[j] = S[(k - r0) * ld + j];
     grid.sync();
+    // decide: bands in row order from the diagonal entry (one warp, G <= 32)
+    if (tid < 32) {
+      double cv = -1.0;
+      int64_t ci = -1;
+      int cc = -1;
+      if (tid < G) {
+        ci = __ldcg(pi + tid);
+        cv = __ldcg(pv + tid);
+        cc = tid;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_down_sync(0xffffffffu, cv, o);
+        const int64_t oi = __shfl_down_sync(0xffffffffu, ci, o);
+        const int oc = __shfl_down_sync(0xffffffffu, cc, o);
+        if (oi >= 0 && (ov > cv || (ov == cv && (ci < 0 || oi < ci)))) {
+          cv = ov;
+          ci = oi;
+          cc = oc;
+        }
+      }
+      if (tid == 0) {
+        const double dkk = double(fabs(__ldcg(rk + k)));
+        const bool take = ci >= 0 && cv > dkk;
+        s_best = take ? cv : dkk;
+        s_p = take ? ci : k;
+        s_src = take ? cc : -1;
+        if (cta == 0) {
+          piv[k] = s_p;
+          if (s_best == 0.0 && *d_sing < 0) *d_sing = int(base + k);
+        }
+      }
+    }
+    __syncthreads();
+    const bool live = !(s_best == 0.0);
+    const int64_t p = s_p;
+    const int src = s_src;
+    if (live) {
+      // the pivot row (new row k) into shared memory; the swap where it lands
+      for (int64_t j = tid; j < n; j += LU_THREADS) {
+        const T nk = src >= 0 ? __ldcg(cand + int64_t(src) * n + j) : __ldcg(rk + j);
+        newk[j] = nk;
+        if (p != k) {
+          if (k >= r0 && k < r1) S[(k - r0) * ld + j] = nk;
+          if (p >= r0 && p < r1) S[(p - r0) * ld + j] = __ldcg(rk + j);
+        }
+      }
+      __syncthreads();
+      // divide the column by the pivot, rank-1 update of this band
+      const T d = newk[k];
+      for (int64_t i = lo + tid; i < r1; i += LU_THREADS) {
+        T* row = S + (i - r0) * ld;
+        const T lik = Ops<T>::div(row[k], d);
+        row[k] = lik;
+        for (int64_t j = k + 1; j < n; ++j) row[j] = Ops<T>::sub(row[j], Ops<T>::mul(lik, newk[j]));
+      }
+    }
+    __syncthreads();
+  }
+  for (int64_t e = tid; e < rows * n; e += LU_THREADS) {
+    const int64_t i = e / n, j = e % n;
+    a[off + (r0 + i) * rs + j * cs] = S[i * ld + j];
   }
 }
 
@@ -229,8 +414,11 @@ int launch_lu_leaf(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int
                    int* d_sing, int64_t base, cudaStream_t s) {
   const int64_t steps = m < n ? m : n;
   if (steps <= 0) return 0;
-  int G = int((m + 127) / 128);
-  const int cap = g_lu_grid_max > 0 ? g_lu_grid_max : grid_cap_lu();
+  // a few hundred rows per CTA: the leaf moves little data, and every grid
+  // barrier costs more with more CTAs
+  int G = int((m + 383) / 384);
+  // <= 32 bands: one warp combines the partials
+  const int cap = g_lu_grid_max > 0 && g_lu_grid_max < 32 ? g_lu_grid_max : (grid_cap_lu() < 32 ? grid_cap_lu() : 32);
   if (G > cap) G = cap;
   if (G < 1) G = 1;
   static double* part_v[64] = {};
@@ -247,6 +435,56 @@ int launch_lu_leaf(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int
   int64_t* pi = part_i[dev];
   note_launch();
   cudaError_t e;
+  // shared-memory bands when they fit: <= 32 bands of <= ~190 KB each
+  {
+    const size_t esz = is_f64 ? 8 : 4;
+    const int64_t max_rows = int64_t((190 * 1024) / (size_t(n + 1) * esz)) - 1;
+    int64_t Gs = max_rows > 0 ? (m + max_rows - 1) / max_rows : 1 << 30;
+    const int64_t want = (m + 255) / 256;  // ~256 rows per band when there is room
+    if (Gs < want) Gs = want;
+    if (Gs > 32) Gs = 32;
+    const int64_t chunk = (m + Gs - 1) / Gs;
+    const size_t smem = size_t(chunk + 1) * size_t(n + 1) * esz;
+    static void* cand_buf[64] = {};
+    static size_t cand_cap[64] = {};
+    const size_t need = size_t(2) * 33 * size_t(n) * esz;
+    if (n <= 4096 && chunk * (n + 1) * int64_t(esz) <= int64_t(190 * 1024) && smem <= 200 * 1024 && !g_lu_global) {
+      if (cand_cap[dev] < need) {
+        if (cand_buf[dev]) cudaFree(cand_buf[dev]);
+        if (cudaMalloc(&cand_buf[dev], need) != cudaSuccess) return -12;
+        cand_cap[dev] = need;
+      }
+      void* cand = cand_buf[dev];
+      void* rowk = static_cast<char*>(cand) + size_t(2) * 32 * size_t(n) * esz;
+      const int Gi = int(Gs);
+      if (is_f64) {
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(lu_leaf_smem_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          attr = true;
+        }
+        double* ad = static_cast<double*>(a);
+        double* cd = static_cast<double*>(cand);
+        double* rd = static_cast<double*>(rowk);
+        void* args[] = {&ad, &off, &rs, &cs, &m, &n, &piv, &d_sing, &base, &pv, &pi, &cd, &rd};
+        e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lu_leaf_smem_kernel<double>), dim3(Gi),
+                                        dim3(LU_THREADS), args, smem, s);
+      } else {
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(lu_leaf_smem_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+          attr = true;
+        }
+        float* af = static_cast<float*>(a);
+        float* cf = static_cast<float*>(cand);
+        float* rf = static_cast<float*>(rowk);
+        void* args[] = {&af, &off, &rs, &cs, &m, &n, &piv, &d_sing, &base, &pv, &pi, &cf, &rf};
+        e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lu_leaf_smem_kernel<float>), dim3(Gi),
+                                        dim3(LU_THREADS), args, smem, s);
+      }
+      return e == cudaSuccess ? 0 : -11;
+    }
+  }
   if (is_f64) {
     double* ad = static_cast<double*>(a);
     void* args[] = {&ad, &off, &rs, &cs, &m, &n, &piv, &d_sing, &base, &pv, &pi};

@@ -25,7 +25,7 @@ def test_header_is_the_reference_schema():
 
 
 @pytest.mark.parametrize("argv", [
-    ["bench", "--op", "lu", "--n", "64"],
+    ["bench", "--op", "qr", "--n", "64"],
     ["bench", "--op", "cholesky", "--n", "64", "--repeats", "2"],
     ["sweep", "--op", "qr", "--n", "64", "--out", "/tmp/x.csv"],
     ["check", "sandwich"],
@@ -62,7 +62,7 @@ def test_all_suites_pass(cuda):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("op", ["cholesky", "gemm"])
+@pytest.mark.parametrize("op", ["cholesky", "gemm", "lu"])
 def test_bench_row(cuda, op):
     rc, out = _run(["bench", "--op", op, "--n", "300"])
     assert rc == 0

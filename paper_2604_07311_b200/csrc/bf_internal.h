@@ -111,6 +111,8 @@ int launch_lu_leaf(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int
 int launch_apply_pivots(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int64_t ncols, const int64_t* piv,
                         int64_t count, int64_t sub, int backward, cudaStream_t s);
 int launch_add_offset(int64_t* piv, int64_t count, int64_t delta, cudaStream_t s);
+int launch_transpose(int is_f64, const void* src, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t n, void* dst,
+                     int64_t ld, cudaStream_t s);
 int launch_trsm_left_base(int is_f64, double alpha, const void* t, int64_t toff, int64_t trs, int64_t tcs, void* b,
                           int64_t boff, int64_t brs, int64_t bcs, int n, int64_t ncols, cudaStream_t s);
 int launch_trsm_upper_base(int is_f64, const void* u, int64_t uoff, int64_t urs, int64_t ucs, void* b, int64_t boff,

@@ -429,6 +429,27 @@ int apply_pivots_impl(Mode mode, const bf_view& a, const int64_t* piv, int64_t c
   return rc ? fail(BF_ERR_CUDA, "row swap launch failed") : BF_OK;
 }
 
+// device scratch for the LU's k-major copies (grows; one LU at a time per
+// device — the walk is single-stream)
+double* lu_scratch(size_t elems) {
+  static double* buf[64] = {};
+  static size_t cap[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (cap[dev] < elems) {
+    if (buf[dev]) {
+      cudaDeviceSynchronize();
+      cudaFree(buf[dev]);
+    }
+    buf[dev] = nullptr;
+    cap[dev] = 0;
+    if (cudaMalloc(&buf[dev], elems * sizeof(double)) != cudaSuccess) return nullptr;
+    cap[dev] = elems;
+  }
+  return buf[dev];
+}
+
 // levels: variant 20 = blocked, 21 = unblocked leaf (flatten of the lu tree)
 int lu_run(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int idx, int64_t* piv, int64_t base,
            int* d_sing, cudaStream_t s) {
@@ -452,9 +473,28 @@ int lu_run(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int idx
     if (k + b < n) {
       const bf_view a12 = subview(a, k, b, k + b, n - k - b);
       rc = trsm_left_rec(mode, 1.0, subview(a, k, b, k, b), a12, kc, s);
-      if (!rc && k + b < m)
-        rc = gemm_impl(mode, -1.0, subview(a, k + b, m - k - b, k, b), a12, 1.0,
+      if (!rc && k + b < m) {
+        // The trailing GEMM's B operand (a12, b x N) is mn-major in a row-major
+        // matrix; a k-major copy of it puts the update on the TMA kernel.
+        // Same values, same kc chains: same bits.
+        bf_view bop = a12;
+        const int64_t N = n - k - b;
+        if (mode == MODE_D && a12.rs != 1 && int64_t(b) * N >= (int64_t(1) << 16) && (b % 16 == 0)) {
+          double* scratch = lu_scratch(size_t(b) * size_t(N));
+          if (scratch && !bf::launch_transpose(1, a12.base, a12.off, a12.rs, a12.cs, b, N, scratch, b, s)) {
+            bf_view t{};
+            t.base = scratch;
+            t.off = 0;
+            t.m = N;
+            t.n = b;
+            t.rs = b;
+            t.cs = 1;
+            bop = transposed(t);
+          }
+        }
+        rc = gemm_impl(mode, -1.0, subview(a, k + b, m - k - b, k, b), bop, 1.0,
                        subview(a, k + b, m - k - b, k + b, n - k - b), 0, kc, nullptr, s);
+      }
       if (rc) return rc;
     }
   }

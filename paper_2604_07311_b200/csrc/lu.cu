@@ -396,6 +396,23 @@ __global__ void trsm_upper_base_kernel(const T* u, int64_t uoff, int64_t urs, in
     if (i < n) b[boff + i * brs + j * bcs] = x[i];
 }
 
+// dst (n x m, row-major ld) = src^T (src m x n, any strides): 32x32 tiles
+template <typename T>
+__global__ void transpose_kernel(const T* src, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t n, T* dst,
+                                 int64_t ld) {
+  __shared__ T tile[32][33];
+  const int64_t i0 = int64_t(blockIdx.y) * 32, j0 = int64_t(blockIdx.x) * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t i = i0 + r, j = j0 + threadIdx.x;
+    if (i < m && j < n) tile[r][threadIdx.x] = src[off + i * rs + j * cs];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t j = j0 + r, i = i0 + threadIdx.x;
+    if (i < m && j < n) dst[j * ld + i] = tile[threadIdx.x][r];
+  }
+}
+
 int grid_cap_lu() {
   static int cap = 0;
   if (!cap) {
@@ -510,6 +527,20 @@ int launch_apply_pivots(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs
   else
     apply_pivots_kernel<float><<<blocks, 256, 0, s>>>(static_cast<float*>(a), off, rs, cs, ncols, piv, count, sub,
                                                       backward);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+int launch_transpose(int is_f64, const void* src, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t n, void* dst,
+                     int64_t ld, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return 0;
+  note_launch();
+  const dim3 grid(unsigned((n + 31) / 32), unsigned((m + 31) / 32)), block(32, 8);
+  if (is_f64)
+    transpose_kernel<double><<<grid, block, 0, s>>>(static_cast<const double*>(src), off, rs, cs, m, n,
+                                                    static_cast<double*>(dst), ld);
+  else
+    transpose_kernel<float><<<grid, block, 0, s>>>(static_cast<const float*>(src), off, rs, cs, m, n,
+                                                   static_cast<float*>(dst), ld);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 

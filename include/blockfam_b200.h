@@ -149,6 +149,16 @@ int bf_gemm_scatter_s(double alpha, const bf_scatter_view* a, const bf_scatter_v
 int bf_gemm_scatter_sd(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
                        const bf_scatter_view* c, int64_t kc, void* stream);
 
+/* Skew sandwich: replaces engine/gemm.py:245-280
+ * sandwich_skew / gemm_scatter(..., tridiag_t): lower(C) := C - A T A^T with T
+ * skew tridiagonal (T[i+1,i] = t[i] = -T[i,i+1]), t on the device (length
+ * a->n - 1).  T A^T is formed while B tiles are staged (the reference's
+ * pack-time transform, kernels.py:93-122): no k x n intermediate.  Bitwise. */
+int bf_sandwich_skew_d(const bf_view* c, const bf_view* a, const double* d_t, int64_t kc, void* stream);
+/* f32 storage (f32 packing arithmetic, as the reference's acc dtype): W = T A^T
+ * is formed in the caller's device workspace d_w (a->n x c->n floats). */
+int bf_sandwich_skew_s(const bf_view* c, const bf_view* a, const float* d_t, float* d_w, int64_t kc, void* stream);
+
 /* LU with partial pivoting.
  * bf_lu_*: replaces factor/lu.py:56-103 lu_partial/_run with the tree walk in
  *   C++: levels are the flattened lu tree (variant 20 = blocked, bs and the

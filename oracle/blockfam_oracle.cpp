@@ -434,6 +434,72 @@ int64_t lu_run(const View<T>& a, const Level* lv, int nl, int idx, int64_t* piv,
   return first;
 }
 
+// ---- skew sandwich (engine/gemm.py:245-280, kernels.py:93-122) ------------
+template <typename T>
+void sandwich(const View<T>& c, const View<T>& a, const T* t, int64_t kc, int nthreads) {
+  const int64_t n = c.m, kt = a.n;
+  if (n == 0 || kt == 0) return;
+  std::vector<T> w(size_t(kt * n));
+  for (int64_t g = 0; g < kt; ++g)
+    for (int64_t j = 0; j < n; ++j) {
+      T acc = T(0);
+      if (g > 0) acc = acc + T(t[g - 1] * a.at(j, g - 1));
+      if (g < kt - 1) acc = acc - T(t[g] * a.at(j, g + 1));
+      w[size_t(g * n + j)] = acc;
+    }
+  View<T> wv{w.data(), 0, kt, n, n, 1};
+  gemm_view<T, T>(-1.0, a, wv, 1.0, c, 1, kc, nthreads);
+}
+
+// ---- ltlt_pivoted unblocked (factor/ltlt.py:66-88, 157-182) ----------------
+template <typename T>
+void swap_lower(const View<T>& x, int64_t a, int64_t b) {
+  if (a == b) return;
+  for (int64_t q = 0; q < a; ++q) std::swap(x.at(a, q), x.at(b, q));
+  std::vector<T> mid;
+  for (int64_t i = a + 1; i < b; ++i) mid.push_back(x.at(i, a));
+  for (int64_t i = a + 1; i < b; ++i) x.at(i, a) = -x.at(b, i);
+  for (int64_t i = a + 1; i < b; ++i) x.at(b, i) = -mid[size_t(i - a - 1)];
+  x.at(b, a) = -x.at(b, a);
+  for (int64_t i = b + 1; i < x.m; ++i) std::swap(x.at(i, a), x.at(i, b));
+}
+
+template <typename T>
+void ltlt_unblocked(const View<T>& x, int64_t* piv, T* t) {
+  const int64_t n = x.n;
+  std::vector<T> mvec(size_t(n), T(0)), wvec(size_t(n), T(0));
+  for (int64_t j = 0; j + 1 < n; ++j) {
+    int64_t p = j + 1;
+    T best = std::fabs(x.at(j + 1, j));
+    for (int64_t i = j + 2; i < n; ++i) {
+      const T v = std::fabs(x.at(i, j));
+      if (v > best) {
+        best = v;
+        p = i;
+      }
+    }
+    if (p != j + 1) {
+      swap_lower(x, j + 1, p);
+      piv[j + 1] = p;
+    }
+    const T alpha = x.at(j + 1, j);
+    t[j] = alpha;
+    if (j + 2 >= n) continue;
+    for (int64_t i = j + 2; i < n; ++i) {
+      const T m = alpha != T(0) ? x.at(i, j) / alpha : T(0);
+      mvec[size_t(i)] = m;
+      wvec[size_t(i)] = x.at(i, j + 1);
+      x.at(i, j) = m;
+    }
+    if (alpha != T(0))
+      for (int64_t c = j + 2; c < n; ++c) {
+        const T wc = wvec[size_t(c)], mc = mvec[size_t(c)];
+        for (int64_t i = c + 1; i < n; ++i)
+          x.at(i, c) = x.at(i, c) + T(T(mvec[size_t(i)] * wc) - T(wvec[size_t(i)] * mc));
+      }
+  }
+}
+
 }  // namespace
 
 struct orc_view_d {
@@ -511,5 +577,14 @@ void orc_trsm_llnu_d(double alpha, const orc_view_d* t, const orc_view_d* b, int
 void orc_trsm_llnu_s(double alpha, const orc_view_s* t, const orc_view_s* b, int64_t kc, int nthreads) {
   trsm_left_rec(alpha, V(t), V(b), kc, nthreads);
 }
+
+void orc_sandwich_d(const orc_view_d* c, const orc_view_d* a, const double* t, int64_t kc, int nthreads) {
+  sandwich(V(c), V(a), t, kc, nthreads);
+}
+void orc_sandwich_s(const orc_view_s* c, const orc_view_s* a, const float* t, int64_t kc, int nthreads) {
+  sandwich(V(c), V(a), t, kc, nthreads);
+}
+void orc_ltlt_unblocked_d(const orc_view_d* x, int64_t* piv, double* t) { ltlt_unblocked(V(x), piv, t); }
+void orc_ltlt_unblocked_s(const orc_view_s* x, int64_t* piv, float* t) { ltlt_unblocked(V(x), piv, t); }
 
 }  // extern "C"

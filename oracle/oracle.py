@@ -68,6 +68,12 @@ def lib() -> ctypes.CDLL:
         for name in ("orc_trsm_llnu_d", "orc_trsm_llnu_s"):
             getattr(_lib, name).argtypes = [ctypes.c_double, P, P, ctypes.c_int64, ctypes.c_int]
             getattr(_lib, name).restype = None
+        for name in ("orc_sandwich_d", "orc_sandwich_s"):
+            getattr(_lib, name).argtypes = [P, P, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int]
+            getattr(_lib, name).restype = None
+        for name in ("orc_ltlt_unblocked_d", "orc_ltlt_unblocked_s"):
+            getattr(_lib, name).argtypes = [P, ctypes.c_void_p, ctypes.c_void_p]
+            getattr(_lib, name).restype = None
         _lib.orc_gemm_naive_d.argtypes = [ctypes.c_double, P, P, ctypes.c_double, P]
         _lib.orc_gemm_naive_d.restype = None
         VP, L = ctypes.c_void_p, ctypes.c_int64
@@ -195,6 +201,24 @@ def trsm_llnu(alpha: float, tri, b, *, kc: int, nthreads: int = 1) -> None:
     """unit_tril(tri) X = alpha b, b := X (engine/trsm.py:71-88,114-125)."""
     (ts, tm), (bs_, bm) = tri, b
     getattr(lib(), "orc_trsm_llnu_" + _suffix(bs_))(float(alpha), _view(ts, tm), _view(bs_, bm), int(kc), nthreads)
+
+
+def sandwich(c, a, t: np.ndarray, *, kc: int, nthreads: int = 1) -> None:
+    """lower(C) -= A T A^T, T skew tridiagonal (engine/gemm.py:245-280): W = T A^T
+    formed with the reference's packing arithmetic, then the kc-segmented GEMMT."""
+    (cs_, cm), (as_, am) = c, a
+    tt = np.ascontiguousarray(t, dtype=cs_.dtype) if len(t) else np.zeros(1, dtype=cs_.dtype)
+    getattr(lib(), "orc_sandwich_" + _suffix(cs_))(_view(cs_, cm), _view(as_, am), tt.ctypes.data, int(kc), nthreads)
+
+
+def ltlt_unblocked(storage: np.ndarray, meta: dict) -> tuple[np.ndarray, np.ndarray]:
+    """factor/ltlt.py:157-182 in place; returns (piv, t)."""
+    n = meta["n"]
+    piv = np.arange(n, dtype=np.int64)
+    t = np.zeros(max(n - 1, 1), dtype=storage.dtype)
+    if n > 1:
+        getattr(lib(), "orc_ltlt_unblocked_" + _suffix(storage))(_view(storage, meta), piv.ctypes.data, t.ctypes.data)
+    return piv, t[: max(n - 1, 0)]
 
 
 def host_threads() -> int:

@@ -12,6 +12,7 @@ enum GlobalLayout : int {
   GL_KMAJOR = 0,   // unit stride along k   (row-major A, "NT" B)  -> k-major smem
   GL_MNMAJOR = 1,  // unit stride along m/n (col-major A, row-major B) -> mn-major smem
   GL_GENERIC = 2,  // arbitrary strides or block-scatter vectors     -> k-major smem, 1 element per copy
+  GL_TRIDIAG = 3,  // B read through W = T*S (skew tridiagonal T): the sandwich's pack-time transform
 };
 
 // One GEMM operand viewed as an (mn x k) matrix: A is (m x k), B^T is (n x k).
@@ -27,6 +28,8 @@ struct OperandMK {
   const int64_t* k_scat;
   int layout;  // GlobalLayout
   int vec;     // elements per vector copy along the unit-stride dim (1, or 16B/elem)
+  const double* tvec;  // GL_TRIDIAG: subdiagonal of T (length k_total - 1), device
+  int64_t k_total;     // GL_TRIDIAG: K of the product (edge terms of T dropped)
 };
 
 // C := beta*C + alpha*A*B with the reference's accumulation structure:
@@ -111,6 +114,8 @@ int launch_lu_leaf(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int
 int launch_apply_pivots(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int64_t ncols, const int64_t* piv,
                         int64_t count, int64_t sub, int backward, cudaStream_t s);
 int launch_add_offset(int64_t* piv, int64_t count, int64_t delta, cudaStream_t s);
+int launch_tridiag_form_f32(const float* a, int64_t off, int64_t rs, int64_t cs, int64_t n, int64_t kt, const float* t,
+                            float* w, cudaStream_t s);
 int launch_transpose(int is_f64, const void* src, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t n, void* dst,
                      int64_t ld, cudaStream_t s);
 int launch_trsm_left_base(int is_f64, double alpha, const void* t, int64_t toff, int64_t trs, int64_t tcs, void* b,

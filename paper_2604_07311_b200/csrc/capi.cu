@@ -764,6 +764,66 @@ int bf_apply_pivots_s(const bf_view* a, const int64_t* d_piv, int64_t count, int
   if (!a || (count > 0 && !d_piv)) return fail(BF_ERR_VALUE, "null argument");
   return apply_pivots_impl(MODE_S, *a, d_piv, count, 0, backward, S(stream));
 }
+// lower(C) := C - A T A^T, T skew tridiagonal with subdiagonal t (engine/gemm.py:245-280)
+int bf_sandwich_skew_d(const bf_view* c, const bf_view* a, const double* d_t, int64_t kc, void* stream) {
+  if (!c || !a) return fail(BF_ERR_VALUE, "null view");
+  if (c->m != c->n) return fail(BF_ERR_SHAPE, "sandwich needs square c");
+  if (a->m != c->m) return fail(BF_ERR_SHAPE, "sandwich dims mismatch");
+  if (kc < 1) return fail(BF_ERR_VALUE, "kc must be >= 1");
+  const int64_t n = c->m, kt = a->n;
+  if (n == 0 || kt == 0) return BF_OK;
+  if (kt > 1 && !d_t) return fail(BF_ERR_VALUE, "null tridiagonal vector");
+  GemmParams p{};
+  p.m = n;
+  p.n = n;
+  p.k = kt;
+  p.kc = kc;
+  p.a = classify(a->base, a->off, a->rs, a->cs, n, kt, kc, MODE_D);
+  OperandMK b{};
+  b.base = a->base;  // B = T * A^T: B's (n, k) source element is a(n, k)
+  b.off = a->off;
+  b.s_mn = a->rs;
+  b.s_k = a->cs;
+  b.layout = bf::GL_TRIDIAG;
+  b.vec = 1;
+  b.tvec = d_t;
+  b.k_total = kt;
+  p.b = b;
+  p.c = c->base;
+  p.c_off = c->off;
+  p.c_rs = c->rs;
+  p.c_cs = c->cs;
+  p.alpha = -1.0;
+  p.beta = 1.0;
+  p.lower_only = 1;
+  p.abort_flag = nullptr;
+  p.abort_limit = -1;
+  const int rc = bf::launch_gemm_dmma(p, S(stream));
+  return rc ? fail(BF_ERR_CUDA, "sandwich launch failed") : BF_OK;
+}
+
+// f32 storage: the reference packs W in f32 (acc dtype f32); W is formed in a
+// device workspace (w: kt x n floats, caller-provided) and fed to the f32 GEMMT
+int bf_sandwich_skew_s(const bf_view* c, const bf_view* a, const float* d_t, float* d_w, int64_t kc, void* stream) {
+  if (!c || !a) return fail(BF_ERR_VALUE, "null view");
+  if (c->m != c->n) return fail(BF_ERR_SHAPE, "sandwich needs square c");
+  if (a->m != c->m) return fail(BF_ERR_SHAPE, "sandwich dims mismatch");
+  if (kc < 1) return fail(BF_ERR_VALUE, "kc must be >= 1");
+  const int64_t n = c->m, kt = a->n;
+  if (n == 0 || kt == 0) return BF_OK;
+  if (!d_w || (kt > 1 && !d_t)) return fail(BF_ERR_VALUE, "null tridiagonal vector or workspace");
+  cudaStream_t s = S(stream);
+  if (bf::launch_tridiag_form_f32(static_cast<const float*>(a->base), a->off, a->rs, a->cs, n, kt, d_t, d_w, s))
+    return fail(BF_ERR_CUDA, "sandwich transform launch failed");
+  bf_view w{};
+  w.base = d_w;
+  w.off = 0;
+  w.m = kt;
+  w.n = n;
+  w.rs = n;
+  w.cs = 1;
+  return gemm_impl(MODE_S, -1.0, *a, w, 1.0, *c, 1, kc, nullptr, s);
+}
 int bf_cholesky_s(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream) {
   return chol_impl(MODE_S, a, levels, nlevels, d_info, S(stream));
 }

@@ -105,6 +105,32 @@ __device__ __forceinline__ void load_tile(double* s, const OperandMK& op, int64_
     }
     return;
   }
+  if constexpr (LAYOUT == GL_TRIDIAG) {
+    // The skew sandwich's B operand, formed while it is staged (engine/
+    // kernels.py:93-122 pack_b_block_tridiag): row g of W = T*S combines two
+    // source rows, W[g,j] = (0 + t[g-1]*S[g-1,j]) - t[g]*S[g+1,j], edge terms
+    // dropped, each product and sum rounded like the reference's packing.
+    // No W ever exists outside shared memory.
+    constexpr int ELEMS = BMN * BK;
+#pragma unroll
+    for (int it = 0; it < (ELEMS + THREADS - 1) / THREADS; ++it) {
+      const int q = tid + it * THREADS;
+      if (ELEMS % THREADS == 0 || q < ELEMS) {
+        const int mn = q / BK, k = q % BK;
+        const int64_t gm = mn0 + mn, gk = k_lo + k;
+        double w = 0.0;
+        if (gm < MN && gk < k_hi) {
+          const double* row = g + op.off + gm * op.s_mn;
+          double acc = 0.0;
+          if (gk > 0) acc = __dadd_rn(acc, __dmul_rn(__ldg(op.tvec + gk - 1), __ldg(row + (gk - 1) * op.s_k)));
+          if (gk < op.k_total - 1) acc = __dsub_rn(acc, __dmul_rn(__ldg(op.tvec + gk), __ldg(row + (gk + 1) * op.s_k)));
+          w = acc;
+        }
+        s[sidx<false, BMN, BK>(mn, k)] = w;
+      }
+    }
+    return;
+  }
   // k-major unaligned, generic strided, or block-scatter: element copies, k fastest.
   constexpr int ELEMS = BMN * BK;
   if constexpr (THREADS % BK == 0 && ELEMS % THREADS == 0) {
@@ -351,6 +377,9 @@ int launch_gemm_dmma(const GemmParams& p, cudaStream_t s) {
   BF_CASE(GL_GENERIC, GL_KMAJOR)
   BF_CASE(GL_GENERIC, GL_MNMAJOR)
   BF_CASE(GL_GENERIC, GL_GENERIC)
+  BF_CASE(GL_KMAJOR, GL_TRIDIAG)
+  BF_CASE(GL_MNMAJOR, GL_TRIDIAG)
+  BF_CASE(GL_GENERIC, GL_TRIDIAG)
 #undef BF_CASE
   return -3;
 }

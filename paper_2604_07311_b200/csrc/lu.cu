@@ -413,6 +413,20 @@ __global__ void transpose_kernel(const T* src, int64_t off, int64_t rs, int64_t 
   }
 }
 
+// W (kt x n, row-major) = T * A^T with the reference's packing arithmetic in T
+template <typename T>
+__global__ void tridiag_form_kernel(const T* a, int64_t off, int64_t rs, int64_t cs, int64_t n, int64_t kt,
+                                    const T* t, T* w) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n * kt) return;
+  const int64_t g = e / n, j = e % n;
+  const T* row = a + off + j * rs;
+  T acc = T(0);
+  if (g > 0) acc = Ops<T>::add(acc, Ops<T>::mul(t[g - 1], row[(g - 1) * cs]));
+  if (g < kt - 1) acc = Ops<T>::sub(acc, Ops<T>::mul(t[g], row[(g + 1) * cs]));
+  w[g * n + j] = acc;
+}
+
 int grid_cap_lu() {
   static int cap = 0;
   if (!cap) {
@@ -541,6 +555,14 @@ int launch_transpose(int is_f64, const void* src, int64_t off, int64_t rs, int64
   else
     transpose_kernel<float><<<grid, block, 0, s>>>(static_cast<const float*>(src), off, rs, cs, m, n,
                                                    static_cast<float*>(dst), ld);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+int launch_tridiag_form_f32(const float* a, int64_t off, int64_t rs, int64_t cs, int64_t n, int64_t kt, const float* t,
+                            float* w, cudaStream_t s) {
+  if (n <= 0 || kt <= 0) return 0;
+  note_launch();
+  tridiag_form_kernel<float><<<unsigned((n * kt + 255) / 256), 256, 0, s>>>(a, off, rs, cs, n, kt, t, w);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 

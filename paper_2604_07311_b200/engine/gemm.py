@@ -31,6 +31,7 @@ __all__ = [
     "gemm",
     "gemmt_lower",
     "syrk_lower",
+    "sandwich_skew",
 ]
 
 
@@ -142,6 +143,47 @@ def syrk_lower(
 ) -> None:
     """tril(c) := beta*tril(c) + alpha*a*a^T (reference engine/gemm.py:233-242)."""
     gemmt_lower(alpha, a, a.transposed(), beta, c, cfg=cfg, ways=ways)
+
+
+def sandwich_skew(
+    c: MatrixView,
+    a: MatrixView,
+    t: np.ndarray,
+    cfg: Optional[KernelConfig] = None,
+    ways: int = 1,
+) -> None:
+    """Lower triangle of c := c - a * T * a^T with T skew tridiagonal
+    (T[i+1,i] = t[i] = -T[i,i+1]) — reference engine/gemm.py:245-280.
+
+    f64: T*a^T is formed while the B tiles are staged (GL_TRIDIAG loader of
+    the DMMA kernel), so no k x n intermediate exists, and every W element is
+    rounded as the reference's pack_b_block_tridiag rounds it: bit-identical.
+    f32: W is formed once in a device workspace with the reference's f32
+    packing arithmetic, then the f32 GEMMT (same bits)."""
+    if c.m != c.n:
+        raise ShapeError(f"sandwich needs square c, got {c.shape}")
+    if a.m != c.m:
+        raise ShapeError(f"sandwich dims mismatch: c {c.shape}, a {a.shape}")
+    kt = a.n
+    t = np.asarray(t, dtype=np.float64)
+    if t.shape != (max(kt - 1, 0),):
+        raise ShapeError(f"tridiag vector length {t.size} != k - 1 = {kt - 1}")
+    _check_operands(c, a)
+    cfg = _cfg_for(cfg, c.dtype)
+    if kt == 0 or c.m == 0:
+        return
+    _lib.require_cuda(c, a)
+    vc, va = _lib.as_bfview(c), _lib.as_bfview(a)
+    stream = _lib.stream_ptr(c.device)
+    if c.dtype.value == "f64":
+        d_t = torch.as_tensor(t if t.size else np.zeros(1), dtype=torch.float64).to(c.device)
+        rc = _lib.lib().bf_sandwich_skew_d(ctypes.byref(vc), ctypes.byref(va), d_t.data_ptr(), int(cfg.kc), stream)
+    else:
+        d_t = torch.as_tensor(t.astype(np.float32) if t.size else np.zeros(1, np.float32)).to(c.device)
+        d_w = torch.empty(kt * c.m, dtype=torch.float32, device=c.device)
+        rc = _lib.lib().bf_sandwich_skew_s(ctypes.byref(vc), ctypes.byref(va), d_t.data_ptr(), d_w.data_ptr(),
+                                           int(cfg.kc), stream)
+    _lib.check(rc, "sandwich_skew")
 
 
 def _dev_vec(x: np.ndarray, device) -> torch.Tensor:

@@ -6,7 +6,9 @@ caller's kc) and the base-case substitution run natively in the sm_100a
 library in the reference's exact operation order, so the solution is
 bit-identical.  A zero diagonal raises SingularMatrixError with the
 base-local column index, as the reference does (engine/trsm.py:128-135).
-LEFT_LOWER_NOTRANS_UNIT belongs to LU, which is outside this build's scope.
+LEFT_LOWER_NOTRANS_UNIT solves unit_tril(T) * X = alpha*B in place (the
+LU's case, engine/trsm.py:71-88,114-125): the same halving, a base case one
+thread per column, bit-identical.
 """
 from __future__ import annotations
 
@@ -39,7 +41,15 @@ def trsm(
     if case == LEFT_LOWER_NOTRANS_UNIT:
         if b.m != tri.n:
             raise ShapeError(f"left solve dims mismatch: b {b.shape}, tri {tri.shape}")
-        raise NotImplementedError("left_lower_notrans_unit (LU) is outside the B200 hot path")
+        if b.n == 0 or tri.n == 0:
+            return
+        cfg = cfg if cfg is not None else default_config(b.dtype)
+        _lib.require_cuda(tri, b)
+        fn = getattr(_lib.lib(), "bf_trsm_llnu_" + ("d" if b.dtype.value == "f64" else "s"))
+        rc = fn(float(alpha), ctypes.byref(_lib.as_bfview(tri)), ctypes.byref(_lib.as_bfview(b)), int(cfg.kc),
+                _lib.stream_ptr(b.device))
+        _lib.check(rc, "trsm")
+        return
     if case != RIGHT_LOWER_TRANS_NONUNIT:
         raise ValueError(f"unknown trsm case {case!r}")
     if b.n != tri.n:

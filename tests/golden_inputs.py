@@ -96,3 +96,23 @@ def left_trsm_inputs(seed: int, n: int, ncols: int, dt: str = "f64"):
     tri[np.triu_indices(n)] = 7.0  # never read: unit diagonal, lower only
     b = rng.uniform(-1, 1, (n, ncols))
     return tri.astype(NP[dt]), b.astype(NP[dt])
+
+
+def sandwich_inputs(seed: int, n: int, k: int, dt: str = "f64", a_layout: str = "row"):
+    """(c0, a, t) for lower(C) -= A T A^T: U(-1,1) values; a stored row-major
+    or as the transpose of a row-major (k x n) block."""
+    rng = np.random.default_rng(seed)
+    c0 = rng.uniform(-1, 1, (n, n)).astype(NP[dt])
+    a = rng.uniform(-1, 1, (n, k)).astype(NP[dt])
+    t = rng.uniform(-1, 1, max(k - 1, 0))
+    return c0, a, t
+
+
+def skew_input(seed: int, n: int, kind: str = "uniform", dt: str = "f64") -> np.ndarray:
+    """Skew-symmetric X = M - M^T (the reference CLI's ltlt generator)."""
+    rng = np.random.default_rng(seed)
+    if kind == "ties":
+        m = rng.integers(-2, 3, (n, n)).astype(np.float64)
+    else:
+        m = rng.uniform(-1, 1, (n, n))
+    return (m - m.T).astype(NP[dt])

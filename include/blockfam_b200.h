@@ -159,6 +159,18 @@ int bf_sandwich_skew_d(const bf_view* c, const bf_view* a, const double* d_t, in
  * is formed in the caller's device workspace d_w (a->n x c->n floats). */
 int bf_sandwich_skew_s(const bf_view* c, const bf_view* a, const float* d_t, float* d_w, int64_t kc, void* stream);
 
+/* Pivoted LTL^T of a skew-symmetric matrix (factor/ltlt.py), eliminations
+ * [j0, j1) on the stored lower triangle: blocked = 0 runs the unblocked
+ * right-looking stepper (ltlt.py:157-182; d_m/d_w: n-element workspaces;
+ * bitwise); blocked = 1 runs one panel of the blocked form starting at k
+ * (ltlt.py:131-147; w: the n x wld history, swapped with the rows; the
+ * trailing update is then bf_sandwich_skew_*).  d_piv (n, preset 0..n-1) and
+ * d_t (n-1) receive the swaps and T's subdiagonal. */
+int bf_ltlt_d(const bf_view* x, int64_t j0, int64_t j1, int blocked, int64_t k, double* w, int64_t wld,
+              int64_t* d_piv, double* d_t, double* d_m, double* d_w, void* stream);
+int bf_ltlt_s(const bf_view* x, int64_t j0, int64_t j1, int blocked, int64_t k, float* w, int64_t wld,
+              int64_t* d_piv, float* d_t, float* d_m, float* d_w, void* stream);
+
 /* LU with partial pivoting.
  * bf_lu_*: replaces factor/lu.py:56-103 lu_partial/_run with the tree walk in
  *   C++: levels are the flattened lu tree (variant 20 = blocked, bs and the

@@ -122,6 +122,9 @@ int launch_trsm_left_base(int is_f64, double alpha, const void* t, int64_t toff,
                           int64_t boff, int64_t brs, int64_t bcs, int n, int64_t ncols, cudaStream_t s);
 int launch_trsm_upper_base(int is_f64, const void* u, int64_t uoff, int64_t urs, int64_t ucs, void* b, int64_t boff,
                            int64_t brs, int64_t bcs, int n, int64_t ncols, cudaStream_t s);
+int launch_ltlt(int is_f64, void* x, int64_t off, int64_t rs, int64_t cs, int64_t n, int64_t j0, int64_t j1,
+                int blocked, int64_t k, void* w, int64_t wld, int64_t* piv, void* t, void* mvec, void* wvec,
+                cudaStream_t s);
 int launch_row_abs_sum(const double* A, int64_t lda, double* out, int64_t n, cudaStream_t s);
 int launch_potrs_f32_f64(const float* L, int64_t ld, double* x, int64_t n, cudaStream_t s);
 int launch_potrs_blocked(const float* L, int64_t ld, const float* xinv, int64_t bs, double* x, int64_t n,

@@ -824,6 +824,24 @@ int bf_sandwich_skew_s(const bf_view* c, const bf_view* a, const float* d_t, flo
   w.cs = 1;
   return gemm_impl(MODE_S, -1.0, *a, w, 1.0, *c, 1, kc, nullptr, s);
 }
+static int ltlt_entry(int is_f64, const bf_view* x, int64_t j0, int64_t j1, int blocked, int64_t k, void* w,
+                      int64_t wld, int64_t* d_piv, void* d_t, void* d_m, void* d_w, void* stream) {
+  if (!x || !d_piv || !d_t) return fail(BF_ERR_VALUE, "null argument");
+  if (x->m != x->n) return fail(BF_ERR_SHAPE, "square matrix required");
+  if (j0 < 0 || j1 > x->n - 1 || j0 > j1) return fail(BF_ERR_VALUE, "bad elimination range");
+  if (blocked ? (!w || wld < 1) : (!d_m || !d_w)) return fail(BF_ERR_VALUE, "null workspace");
+  int rc = bf::launch_ltlt(is_f64, x->base, x->off, x->rs, x->cs, x->n, j0, j1, blocked, k, w, wld, d_piv, d_t, d_m,
+                           d_w, S(stream));
+  return rc ? fail(BF_ERR_CUDA, "ltlt launch failed") : BF_OK;
+}
+int bf_ltlt_d(const bf_view* x, int64_t j0, int64_t j1, int blocked, int64_t k, double* w, int64_t wld,
+              int64_t* d_piv, double* d_t, double* d_m, double* d_w, void* stream) {
+  return ltlt_entry(1, x, j0, j1, blocked, k, w, wld, d_piv, d_t, d_m, d_w, stream);
+}
+int bf_ltlt_s(const bf_view* x, int64_t j0, int64_t j1, int blocked, int64_t k, float* w, int64_t wld,
+              int64_t* d_piv, float* d_t, float* d_m, float* d_w, void* stream) {
+  return ltlt_entry(0, x, j0, j1, blocked, k, w, wld, d_piv, d_t, d_m, d_w, stream);
+}
 int bf_cholesky_s(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream) {
   return chol_impl(MODE_S, a, levels, nlevels, d_info, S(stream));
 }

@@ -96,6 +96,8 @@ _SIGNATURES = {
     "bf_cholesky_d": ([_V, _P(BfCholLevel), _I, _VP, _VP], _I),
     "bf_sandwich_skew_d": ([_V, _V, _VP, _L, _VP], _I),
     "bf_sandwich_skew_s": ([_V, _V, _VP, _VP, _L, _VP], _I),
+    "bf_ltlt_d": ([_V, _L, _L, _I, _L, _VP, _L, _VP, _VP, _VP, _VP, _VP], _I),
+    "bf_ltlt_s": ([_V, _L, _L, _I, _L, _VP, _L, _VP, _VP, _VP, _VP, _VP], _I),
     "bf_lu_d": ([_V, _P(BfCholLevel), _I, _VP, _VP, _VP], _I),
     "bf_lu_s": ([_V, _P(BfCholLevel), _I, _VP, _VP, _VP], _I),
     "bf_trsm_llnu_d": ([_D, _V, _V, _L, _VP], _I),

@@ -186,6 +186,22 @@ def sandwich_skew(
     _lib.check(rc, "sandwich_skew")
 
 
+def _sandwich_dev(c: MatrixView, a: MatrixView, d_t: torch.Tensor, cfg: KernelConfig) -> None:
+    """sandwich_skew with T's subdiagonal already on the device (length a.n-1,
+    c's element type): the blocked LTL^T's trailing update, no host round trip."""
+    if a.n == 0 or c.m == 0:
+        return
+    vc, va = _lib.as_bfview(c), _lib.as_bfview(a)
+    stream = _lib.stream_ptr(c.device)
+    if c.dtype.value == "f64":
+        rc = _lib.lib().bf_sandwich_skew_d(ctypes.byref(vc), ctypes.byref(va), d_t.data_ptr(), int(cfg.kc), stream)
+    else:
+        d_w = torch.empty(a.n * c.m, dtype=torch.float32, device=c.device)
+        rc = _lib.lib().bf_sandwich_skew_s(ctypes.byref(vc), ctypes.byref(va), d_t.data_ptr(), d_w.data_ptr(),
+                                           int(cfg.kc), stream)
+    _lib.check(rc, "sandwich_skew")
+
+
 def _dev_vec(x: np.ndarray, device) -> torch.Tensor:
     return torch.as_tensor(np.ascontiguousarray(x, dtype=np.int64)).to(device)
 

@@ -76,3 +76,79 @@ def test_cuda_sandwich_strict_upper_untouched_and_large(cuda):
     cs = c0.reshape(-1).copy()
     O.sandwich((cs, _meta(n, n)), (a.reshape(-1).copy(), _meta(n, k)), t, kc=256)
     assert digest(got) == digest(cs)
+
+
+def _gpu_view(x, dt="f64"):
+    import paper_2604_07311_b200 as bf
+    from paper_2604_07311_b200.views import DType
+
+    return bf.make_view(x.shape[0], x.shape[1], DType.parse(dt), fill=x)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [c for c in CASES if c["kind"] == "ltlt_unblocked"], ids=lambda c: c["id"])
+def test_cuda_ltlt_unblocked_matches_reference(cuda, case):
+    import paper_2604_07311_b200 as bf
+    from paper_2604_07311_b200.control import ControlNode
+
+    x0 = skew_input(case["seed"], case["n"], case["input"], case["dtype"])
+    v = _gpu_view(x0, case["dtype"])
+    piv, tri = bf.ltlt_pivoted(v, ControlNode("ltlt", "unblocked"))
+    assert list(piv.piv) == case["piv"]
+    assert digest(v.to_numpy()) == case["sha256"]
+    assert digest(np.asarray(tri.t)) == case["t_sha256"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [c for c in CASES if c["kind"] == "ltlt_blocked"], ids=lambda c: c["id"])
+def test_cuda_ltlt_blocked_matches_reference_to_rounding(cuda, case):
+    import paper_2604_07311_b200 as bf
+    from paper_2604_07311_b200.control import ControlNode
+
+    n = case["n"]
+    x0 = skew_input(case["seed"], n)
+    v = _gpu_view(x0)
+    piv, tri = bf.ltlt_pivoted(v, ControlNode("ltlt", "blocked", bs=case["bs"], child=ControlNode("ltlt", "unblocked")))
+    assert list(piv.piv) == case["piv"]
+    assert np.abs(np.asarray(tri.t) - np.asarray(case["t"])).max() <= 1e-10 * max(1.0, np.abs(case["t"]).max())
+    ell = bf.unit_lower_from_storage(v)
+    perm = piv.permutation(n)
+    err = np.linalg.norm(x0[perm][:, perm] - ell @ tri.to_dense() @ ell.T) / np.linalg.norm(x0)
+    assert err < 1e-12
+    assert np.triu(v.to_numpy(), 1).tobytes() == np.triu(x0, 1).tobytes()  # strict upper never touched
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", [c for c in CASES if c["kind"] == "pfaffian"], ids=lambda c: c["id"])
+def test_cuda_pfaffian_matches_reference(cuda, case):
+    import paper_2604_07311_b200 as bf
+
+    x0 = skew_input(case["seed"], case["n"])
+    got = bf.pfaffian(_gpu_view(x0))
+    ref = case["value"]
+    assert abs(got - ref) <= 1e-9 * max(1.0, abs(ref))
+
+
+@pytest.mark.gpu
+def test_cuda_ltlt_larger(cuda):
+    """Unblocked at n=300 bitwise against the oracle; blocked at n=1000
+    reconstructs; pf(X)^2 = det(X)."""
+    import paper_2604_07311_b200 as bf
+    from paper_2604_07311_b200.control import ControlNode
+
+    x0 = skew_input(31337, 300)
+    v = _gpu_view(x0)
+    piv, tri = bf.ltlt_pivoted(v, ControlNode("ltlt", "unblocked"))
+    st = x0.reshape(-1).copy()
+    opiv, ot = O.ltlt_unblocked(st, _meta(300, 300))
+    assert list(piv.piv) == list(opiv) and digest(v.to_numpy()) == digest(st)
+    n = 1000
+    x1 = skew_input(4, n)
+    v1 = _gpu_view(x1)
+    piv1, tri1 = bf.ltlt_pivoted(v1, ControlNode("ltlt", "blocked", bs=96, child=ControlNode("ltlt", "unblocked")))
+    ell = bf.unit_lower_from_storage(v1)
+    perm = piv1.permutation(n)
+    assert np.linalg.norm(x1[perm][:, perm] - ell @ tri1.to_dense() @ ell.T) / np.linalg.norm(x1) < 1e-11
+    x2 = skew_input(5, 12)
+    pf = bf.pfaffian(_gpu_view(x2))
+    assert abs(pf * pf - np.linalg.det(x2)) <= 1e-9 * abs(np.linalg.det(x2))

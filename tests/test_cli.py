@@ -28,7 +28,7 @@ def test_header_is_the_reference_schema():
     ["bench", "--op", "qr", "--n", "64"],
     ["bench", "--op", "cholesky", "--n", "64", "--repeats", "2"],
     ["sweep", "--op", "qr", "--n", "64", "--out", "/tmp/x.csv"],
-    ["check", "sandwich"],
+    ["check", "qr"],
     ["check", "nosuch"],
 ])
 def test_usage_errors_exit_2(argv):
@@ -62,7 +62,7 @@ def test_all_suites_pass(cuda):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("op", ["cholesky", "gemm", "lu"])
+@pytest.mark.parametrize("op", ["cholesky", "gemm", "lu", "ltlt"])
 def test_bench_row(cuda, op):
     rc, out = _run(["bench", "--op", op, "--n", "300"])
     assert rc == 0

@@ -171,6 +171,22 @@ int bf_ltlt_d(const bf_view* x, int64_t j0, int64_t j1, int blocked, int64_t k, 
 int bf_ltlt_s(const bf_view* x, int64_t j0, int64_t j1, int blocked, int64_t k, float* w, int64_t wld,
               int64_t* d_piv, float* d_t, float* d_m, float* d_w, void* stream);
 
+/* Householder QR (factor/qr.py).  The reference
+ * uses NumPy/BLAS for every panel operation, so these agree with it to
+ * rounding (its own tests are tolerance tests).
+ * bf_qr_panel_*: the unblocked column sweep (qr.py:58-76) on an m x b view
+ *   (m >= b), taus to d_taus (b).
+ * bf_qr_t_*: the panel's compact-WY T (b x b upper, qr.py:79-92) and the
+ *   explicit V (m x b, unit diagonal, qr.py:95-100); b <= 128.
+ * bf_reflector_apply_*: c := H_j c, H_j = I - tau v v^T with v stored in
+ *   column j of a below the diagonal (apply_q, qr.py:124-140). */
+int bf_qr_panel_d(const bf_view* a, double* d_taus, void* stream);
+int bf_qr_panel_s(const bf_view* a, float* d_taus, void* stream);
+int bf_qr_t_d(const bf_view* panel, const double* d_taus, double* d_t, double* d_v, void* stream);
+int bf_qr_t_s(const bf_view* panel, const float* d_taus, float* d_t, float* d_v, void* stream);
+int bf_reflector_apply_d(const bf_view* a, int64_t j, double tau, const bf_view* c, void* stream);
+int bf_reflector_apply_s(const bf_view* a, int64_t j, double tau, const bf_view* c, void* stream);
+
 /* LU with partial pivoting.
  * bf_lu_*: replaces factor/lu.py:56-103 lu_partial/_run with the tree walk in
  *   C++: levels are the flattened lu tree (variant 20 = blocked, bs and the

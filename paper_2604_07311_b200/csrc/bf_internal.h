@@ -125,6 +125,15 @@ int launch_trsm_upper_base(int is_f64, const void* u, int64_t uoff, int64_t urs,
 int launch_ltlt(int is_f64, void* x, int64_t off, int64_t rs, int64_t cs, int64_t n, int64_t j0, int64_t j1,
                 int blocked, int64_t k, void* w, int64_t wld, int64_t* piv, void* t, void* mvec, void* wvec,
                 cudaStream_t s);
+int launch_qr_panel(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t b, void* taus,
+                    cudaStream_t s);
+int launch_qr_t(int is_f64, const void* a, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t b,
+                const void* taus, void* t, cudaStream_t s);
+int launch_explicit_v(int is_f64, const void* a, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t b, void* v,
+                      cudaStream_t s);
+int launch_reflector_apply(int is_f64, const void* a, int64_t aoff, int64_t ars, int64_t acs, int64_t m, int64_t j,
+                           double tau, void* c, int64_t coff, int64_t crs, int64_t ccs, int64_t ncols,
+                           cudaStream_t s);
 int launch_row_abs_sum(const double* A, int64_t lda, double* out, int64_t n, cudaStream_t s);
 int launch_potrs_f32_f64(const float* L, int64_t ld, double* x, int64_t n, cudaStream_t s);
 int launch_potrs_blocked(const float* L, int64_t ld, const float* xinv, int64_t bs, double* x, int64_t n,

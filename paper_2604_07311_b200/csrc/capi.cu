@@ -842,6 +842,44 @@ int bf_ltlt_s(const bf_view* x, int64_t j0, int64_t j1, int blocked, int64_t k, 
               int64_t* d_piv, float* d_t, float* d_m, float* d_w, void* stream) {
   return ltlt_entry(0, x, j0, j1, blocked, k, w, wld, d_piv, d_t, d_m, d_w, stream);
 }
+// ---- Householder QR (factor/qr.py) -----------------------------------------
+static int qr_panel_entry(int is_f64, const bf_view* a, void* d_taus, void* stream) {
+  if (!a || !d_taus) return fail(BF_ERR_VALUE, "null argument");
+  if (a->m < a->n) return fail(BF_ERR_SHAPE, "qr requires m >= n");
+  int rc = bf::launch_qr_panel(is_f64, a->base, a->off, a->rs, a->cs, a->m, a->n, d_taus, S(stream));
+  return rc ? fail(BF_ERR_CUDA, "qr panel launch failed") : BF_OK;
+}
+int bf_qr_panel_d(const bf_view* a, double* d_taus, void* stream) { return qr_panel_entry(1, a, d_taus, stream); }
+int bf_qr_panel_s(const bf_view* a, float* d_taus, void* stream) { return qr_panel_entry(0, a, d_taus, stream); }
+static int qr_t_entry(int is_f64, const bf_view* panel, const void* d_taus, void* d_t, void* d_v, void* stream) {
+  if (!panel || !d_taus || !d_t || !d_v) return fail(BF_ERR_VALUE, "null argument");
+  int rc = bf::launch_qr_t(is_f64, panel->base, panel->off, panel->rs, panel->cs, panel->m, panel->n, d_taus, d_t,
+                           S(stream));
+  if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "qr panel wider than 128");
+  if (!rc)
+    rc = bf::launch_explicit_v(is_f64, panel->base, panel->off, panel->rs, panel->cs, panel->m, panel->n, d_v,
+                               S(stream));
+  return rc ? fail(BF_ERR_CUDA, "qr T launch failed") : BF_OK;
+}
+int bf_qr_t_d(const bf_view* panel, const double* d_taus, double* d_t, double* d_v, void* stream) {
+  return qr_t_entry(1, panel, d_taus, d_t, d_v, stream);
+}
+int bf_qr_t_s(const bf_view* panel, const float* d_taus, float* d_t, float* d_v, void* stream) {
+  return qr_t_entry(0, panel, d_taus, d_t, d_v, stream);
+}
+static int reflector_entry(int is_f64, const bf_view* a, int64_t j, double tau, const bf_view* c, void* stream) {
+  if (!a || !c) return fail(BF_ERR_VALUE, "null view");
+  if (c->m != a->m) return fail(BF_ERR_SHAPE, "c rows != a rows");
+  int rc = bf::launch_reflector_apply(is_f64, a->base, a->off, a->rs, a->cs, a->m, j, tau, c->base, c->off, c->rs,
+                                      c->cs, c->n, S(stream));
+  return rc ? fail(BF_ERR_CUDA, "reflector launch failed") : BF_OK;
+}
+int bf_reflector_apply_d(const bf_view* a, int64_t j, double tau, const bf_view* c, void* stream) {
+  return reflector_entry(1, a, j, tau, c, stream);
+}
+int bf_reflector_apply_s(const bf_view* a, int64_t j, double tau, const bf_view* c, void* stream) {
+  return reflector_entry(0, a, j, tau, c, stream);
+}
 int bf_cholesky_s(const bf_view* a, const bf_chol_level* levels, int nlevels, int* d_info, void* stream) {
   return chol_impl(MODE_S, a, levels, nlevels, d_info, S(stream));
 }

@@ -177,13 +177,20 @@ int bf_ltlt_s(const bf_view* x, int64_t j0, int64_t j1, int blocked, int64_t k, 
  * bf_qr_panel_*: the unblocked column sweep (qr.py:58-76) on an m x b view
  *   (m >= b), taus to d_taus (b).
  * bf_qr_t_*: the panel's compact-WY T (b x b upper, qr.py:79-92) and the
- *   explicit V (m x b, unit diagonal, qr.py:95-100); b <= 128.
+ *   explicit V (m x b, unit diagonal, qr.py:95-100); d_gram: b x b workspace
+ *   (V^T V by the split-K GEMM, feeds T's recursion).
+ * bf_gemm_splitk_*: c = alpha a b + beta c for the reflector products of the
+ *   blocked update (V^T C, qr.py:103-121, NumPy '@' in the reference): the K
+ *   range is split over concurrent streams when the output has few tiles.
+ *   To rounding only — never a substitute for bf_gemm_* on bitwise paths.
  * bf_reflector_apply_*: c := H_j c, H_j = I - tau v v^T with v stored in
  *   column j of a below the diagonal (apply_q, qr.py:124-140). */
 int bf_qr_panel_d(const bf_view* a, double* d_taus, void* stream);
 int bf_qr_panel_s(const bf_view* a, float* d_taus, void* stream);
-int bf_qr_t_d(const bf_view* panel, const double* d_taus, double* d_t, double* d_v, void* stream);
-int bf_qr_t_s(const bf_view* panel, const float* d_taus, float* d_t, float* d_v, void* stream);
+int bf_qr_t_d(const bf_view* panel, const double* d_taus, double* d_t, double* d_v, double* d_gram, void* stream);
+int bf_qr_t_s(const bf_view* panel, const float* d_taus, float* d_t, float* d_v, float* d_gram, void* stream);
+int bf_gemm_splitk_d(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c, void* stream);
+int bf_gemm_splitk_s(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c, void* stream);
 int bf_reflector_apply_d(const bf_view* a, int64_t j, double tau, const bf_view* c, void* stream);
 int bf_reflector_apply_s(const bf_view* a, int64_t j, double tau, const bf_view* c, void* stream);
 

@@ -77,9 +77,10 @@ extern int g_tma_variant;     // bf_set_option("tma_variant", 0..3)
 extern int g_tiles_per_cta;   // bf_set_option("tiles_per_cta", t)
 extern int g_bf16_tma_c;      // bf16 GEMM: TMA C-tile epilogue (1) or per-element fallback (0)
 extern int g_trsm_warp;       // fused TRSM subtree: 4-warps-per-32-rows kernel (1) or the 64-row CTA kernel (0)
-extern int g_leaf_blocked;
-extern int g_lu_grid_max;
-extern int g_lu_global;     // LU leaf: force the global-memory kernel   // LU leaf: cap on the cooperative grid (0 = SM-derived)    // variant-3 leaves n <= 128: blocked lane-per-row kernel (1) or v3 (0)
+extern int g_leaf_blocked;    // variant-3 leaves n <= 128: blocked lane-per-row kernel (1) or v3 (0)
+extern int g_lu_grid_max;     // LU leaf: cap on the cooperative grid (0 = SM-derived)
+extern int g_lu_global;       // LU leaf: force the global-memory kernel
+extern int g_qr_global;       // QR panel: force the global-memory sweep
 int launch_gemm_simt_f32(const GemmParams& p, cudaStream_t s);        // f32 storage, f32 acc
 int launch_gemm_simt_f32acc64(const GemmParams& p, cudaStream_t s);   // f32 storage, f64 acc
 int launch_scale(int is_f64, double beta, void* c, int64_t off, int64_t m, int64_t n, int64_t rs,
@@ -127,8 +128,9 @@ int launch_ltlt(int is_f64, void* x, int64_t off, int64_t rs, int64_t cs, int64_
                 cudaStream_t s);
 int launch_qr_panel(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t b, void* taus,
                     cudaStream_t s);
-int launch_qr_t(int is_f64, const void* a, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t b,
-                const void* taus, void* t, cudaStream_t s);
+int launch_qr_t(int is_f64, const void* gram, int64_t b, const void* taus, void* t, cudaStream_t s);
+int launch_splitk_reduce(int is_f64, const void* ws, int S, int64_t m, int64_t n, double alpha, double beta, void* c,
+                         int64_t off, int64_t rs, int64_t cs, cudaStream_t s);
 int launch_explicit_v(int is_f64, const void* a, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t b, void* v,
                       cudaStream_t s);
 int launch_reflector_apply(int is_f64, const void* a, int64_t aoff, int64_t ars, int64_t acs, int64_t m, int64_t j,

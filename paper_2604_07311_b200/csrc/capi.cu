@@ -586,6 +586,10 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_tma_variant = int(value & 3);
     return BF_OK;
   }
+  if (name && std::strcmp(name, "qr_global") == 0) {
+    bf::g_qr_global = value != 0;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "lu_global") == 0) {
     bf::g_lu_global = value != 0;
     return BF_OK;
@@ -842,6 +846,85 @@ int bf_ltlt_s(const bf_view* x, int64_t j0, int64_t j1, int blocked, int64_t k, 
               int64_t* d_piv, float* d_t, float* d_m, float* d_w, void* stream) {
   return ltlt_entry(0, x, j0, j1, blocked, k, w, wld, d_piv, d_t, d_m, d_w, stream);
 }
+// ---- split-K GEMM (QR's reflector products) ---------------------------------
+// For the tall-K products of the QR path (V^T V, V^T C: a handful of output
+// tiles, K = the panel height) the K range is cut into S slices that run
+// concurrently on forked streams into a workspace, then summed in slice
+// order.  The reference forms these with NumPy/BLAS (factor/qr.py:81-121),
+// so they are parity-to-rounding products, never used on a bitwise path.
+static int gemm_splitk_impl(Mode mode, double alpha, const bf_view& a, const bf_view& b, double beta,
+                            const bf_view& c, cudaStream_t s) {
+  constexpr int SMAX = 8;
+  const int64_t m = c.m, n = c.n, k = a.n;
+  if (a.n != b.m || c.m != a.m || c.n != b.n) return fail(BF_ERR_SHAPE, "gemm dims mismatch");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return fail(BF_ERR_CUDA, "device index");
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tiles = ((m + 127) / 128) * ((n + 127) / 128);
+  int64_t S = tiles > 0 ? sms / tiles : 1;
+  if (S > SMAX) S = SMAX;
+  if (S > k / 512) S = k / 512;
+  if (S <= 1 || m == 0 || n == 0) return gemm_impl(mode, alpha, a, b, beta, c, 0, int64_t(1) << 40, nullptr, s);
+  static cudaStream_t side[64][SMAX] = {};
+  static cudaEvent_t ev[64][SMAX + 1] = {};
+  static void* ws[64] = {};
+  static size_t ws_bytes[64] = {};
+  if (!side[dev][0]) {
+    for (int i = 0; i < SMAX; ++i) {
+      cudaStreamCreateWithFlags(&side[dev][i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&ev[dev][i], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&ev[dev][SMAX], cudaEventDisableTiming);
+  }
+  const size_t need = size_t(S) * size_t(m) * size_t(n) * size_t(elem_bytes(mode));
+  if (need > ws_bytes[dev]) {
+    if (ws[dev]) {
+      cudaStreamSynchronize(s);
+      cudaFree(ws[dev]);
+    }
+    ws[dev] = nullptr;
+    ws_bytes[dev] = 0;
+    if (cudaMalloc(&ws[dev], need) != cudaSuccess) return fail(BF_ERR_CUDA, "split-K workspace");
+    ws_bytes[dev] = need;
+  }
+  cudaEventRecord(ev[dev][SMAX], s);
+  const int64_t slice = (k + S - 1) / S;
+  for (int64_t q = 0; q < S; ++q) {
+    const int64_t k0 = q * slice, kn = k0 + slice < k ? slice : k - k0;
+    cudaStream_t sq = side[dev][q];
+    cudaStreamWaitEvent(sq, ev[dev][SMAX], 0);
+    bf_view w{};
+    w.base = ws[dev];
+    w.off = q * m * n;
+    w.m = m;
+    w.n = n;
+    w.rs = n;
+    w.cs = 1;
+    int rc = gemm_impl(mode, 1.0, subview(a, 0, m, k0, kn), subview(b, k0, kn, 0, n), 0.0, w, 0, int64_t(1) << 40,
+                       nullptr, sq);
+    if (rc) return rc;
+    cudaEventRecord(ev[dev][q], sq);
+    cudaStreamWaitEvent(s, ev[dev][q], 0);
+  }
+  double al = alpha, be = beta;
+  if (mode == MODE_S) {
+    al = double(float(alpha));
+    be = double(float(beta));
+  }
+  int rc = bf::launch_splitk_reduce(storage_is_f64(mode), ws[dev], int(S), m, n, al, be, c.base, c.off, c.rs, c.cs, s);
+  return rc ? fail(BF_ERR_CUDA, "split-K reduce launch failed") : BF_OK;
+}
+int bf_gemm_splitk_d(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c, void* stream) {
+  if (!a || !b || !c) return fail(BF_ERR_VALUE, "null view");
+  return gemm_splitk_impl(MODE_D, alpha, *a, *b, beta, *c, S(stream));
+}
+int bf_gemm_splitk_s(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c, void* stream) {
+  if (!a || !b || !c) return fail(BF_ERR_VALUE, "null view");
+  return gemm_splitk_impl(MODE_S, alpha, *a, *b, beta, *c, S(stream));
+}
+
 // ---- Householder QR (factor/qr.py) -----------------------------------------
 static int qr_panel_entry(int is_f64, const bf_view* a, void* d_taus, void* stream) {
   if (!a || !d_taus) return fail(BF_ERR_VALUE, "null argument");
@@ -851,21 +934,39 @@ static int qr_panel_entry(int is_f64, const bf_view* a, void* d_taus, void* stre
 }
 int bf_qr_panel_d(const bf_view* a, double* d_taus, void* stream) { return qr_panel_entry(1, a, d_taus, stream); }
 int bf_qr_panel_s(const bf_view* a, float* d_taus, void* stream) { return qr_panel_entry(0, a, d_taus, stream); }
-static int qr_t_entry(int is_f64, const bf_view* panel, const void* d_taus, void* d_t, void* d_v, void* stream) {
-  if (!panel || !d_taus || !d_t || !d_v) return fail(BF_ERR_VALUE, "null argument");
-  int rc = bf::launch_qr_t(is_f64, panel->base, panel->off, panel->rs, panel->cs, panel->m, panel->n, d_taus, d_t,
-                           S(stream));
-  if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "qr panel wider than 128");
-  if (!rc)
-    rc = bf::launch_explicit_v(is_f64, panel->base, panel->off, panel->rs, panel->cs, panel->m, panel->n, d_v,
-                               S(stream));
+static int qr_t_entry(int is_f64, const bf_view* panel, const void* d_taus, void* d_t, void* d_v, void* d_gram,
+                      void* stream) {
+  if (!panel || !d_taus || !d_t || !d_v || !d_gram) return fail(BF_ERR_VALUE, "null argument");
+  const int64_t m = panel->m, b = panel->n;
+  cudaStream_t s = S(stream);
+  int rc = bf::launch_explicit_v(is_f64, panel->base, panel->off, panel->rs, panel->cs, m, b, d_v, s);
+  if (rc) return fail(BF_ERR_CUDA, "qr V launch failed");
+  // G = V^T V (b x b) on the engine GEMM; T from G
+  bf_view v{};
+  v.base = d_v;
+  v.off = 0;
+  v.m = m;
+  v.n = b;
+  v.rs = b;
+  v.cs = 1;
+  bf_view g{};
+  g.base = d_gram;
+  g.off = 0;
+  g.m = b;
+  g.n = b;
+  g.rs = b;
+  g.cs = 1;
+  const Mode mode = is_f64 ? MODE_D : MODE_S;
+  rc = gemm_splitk_impl(mode, 1.0, transposed(v), v, 0.0, g, s);
+  if (rc) return rc;
+  rc = bf::launch_qr_t(is_f64, d_gram, b, d_taus, d_t, s);
   return rc ? fail(BF_ERR_CUDA, "qr T launch failed") : BF_OK;
 }
-int bf_qr_t_d(const bf_view* panel, const double* d_taus, double* d_t, double* d_v, void* stream) {
-  return qr_t_entry(1, panel, d_taus, d_t, d_v, stream);
+int bf_qr_t_d(const bf_view* panel, const double* d_taus, double* d_t, double* d_v, double* d_gram, void* stream) {
+  return qr_t_entry(1, panel, d_taus, d_t, d_v, d_gram, stream);
 }
-int bf_qr_t_s(const bf_view* panel, const float* d_taus, float* d_t, float* d_v, void* stream) {
-  return qr_t_entry(0, panel, d_taus, d_t, d_v, stream);
+int bf_qr_t_s(const bf_view* panel, const float* d_taus, float* d_t, float* d_v, float* d_gram, void* stream) {
+  return qr_t_entry(0, panel, d_taus, d_t, d_v, d_gram, stream);
 }
 static int reflector_entry(int is_f64, const bf_view* a, int64_t j, double tau, const bf_view* c, void* stream) {
   if (!a || !c) return fail(BF_ERR_VALUE, "null view");

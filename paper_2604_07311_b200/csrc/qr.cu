@@ -6,7 +6,8 @@
 //    then w = a(j, j+1:) + v^T a(j+1:, j+1:) (per-column grid reductions)
 //    and the rank-1 update.  The reference computes these with NumPy/BLAS
 //    (np.linalg.norm, @, np.outer), so the factor agrees to rounding.
-//  * qr_t_kernel — the compact-WY T of a panel (qr.py:79-92), one CTA.
+//  * qr_t_kernel — the compact-WY T of a panel (qr.py:79-92) from the
+//    panel's Gram matrix V^T V (one engine GEMM), one CTA.
 //  * explicit_v_kernel — V with its unit diagonal and zeros above (qr.py:95-100).
 //  * reflector_apply_kernel — c := H_j c for one reflector (apply_q, qr.py:124-140).
 #include "bf_common.cuh"
@@ -15,6 +16,8 @@
 #include <cooperative_groups.h>
 
 namespace bf {
+
+int g_qr_global = 0;  // 1: the global-memory panel sweep only (tests / A-B)
 
 namespace {
 
@@ -30,8 +33,8 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(T* a, int64_t off,
   const int G = gridDim.x, tid = threadIdx.x, cta = blockIdx.x;
   auto A = [&](int64_t i, int64_t j) -> T& { return a[off + i * rs + j * cs]; };
   __shared__ double red[QR_THREADS / 32][QR_MAXB + 1];
-  __shared__ double s_w[QR_MAXB];
-  __shared__ double s_rowj[QR_MAXB];
+  __shared__ double s_w[QR_THREADS];
+  __shared__ double s_rowj[QR_THREADS];
   __shared__ double s_beta, s_tau, s_scale;
   __shared__ int s_skip;
   const int64_t steps = m < b ? m : b;
@@ -78,88 +81,222 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(T* a, int64_t off,
     for (int64_t i = lo + tid; i < r1; i += QR_THREADS) A(i, j) = T(double(A(i, j)) / s_scale);
     grid.sync();
     if (cta == 0 && tid == 0) A(j, j) = T(s_beta);
-    // (3) w_c = a(j, c) + sum_{i>j} v_i a(i, c), c in (j, b)
+    // (3) w_c = a(j, c) + sum_{i>j} v_i a(i, c), c in (j, b): one thread per
+    // column (coalesced along the row), rows of this band in a loop
     const int64_t nc = b - j - 1;
-    if (nc > 0) {
-      for (int64_t c0 = 0; c0 < nc; c0 += QR_MAXB) {
-        const int64_t cn = nc - c0 < QR_MAXB ? nc - c0 : QR_MAXB;
-        for (int64_t cc = 0; cc < cn; ++cc) {
-          double acc = 0.0;
-          for (int64_t i = lo + tid; i < r1; i += QR_THREADS)
-            acc = fma(double(A(i, j)), double(A(i, j + 1 + c0 + cc)), acc);
-#pragma unroll
-          for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-          if ((tid & 31) == 0) red[tid >> 5][cc] = acc;
-        }
-        __syncthreads();
-        for (int64_t cc = tid; cc < cn; cc += QR_THREADS) {
-          double t = 0.0;
-          for (int w = 0; w < QR_THREADS / 32; ++w) t += red[w][cc];
-          part[int64_t(cta) * QR_MAXB + cc] = t;
-          s_rowj[cc] = double(A(j, j + 1 + c0 + cc));  // read before CTA 0 may rewrite row j
-        }
-        grid.sync();
-        for (int64_t cc = tid; cc < cn; cc += QR_THREADS) {
-          double t = s_rowj[cc];
-          for (int c = 0; c < G; ++c) t += part[int64_t(c) * QR_MAXB + cc];
-          s_w[cc] = t;
-        }
-        __syncthreads();
-        // (4) a(j, c) -= tau w_c ; a(i, c) -= tau v_i w_c
-        const double tau = s_tau;
-        if (cta == 0)
-          for (int64_t cc = tid; cc < cn; cc += QR_THREADS) {
-            const int64_t c = j + 1 + c0 + cc;
-            A(j, c) = T(double(A(j, c)) - tau * s_w[cc]);
-          }
-        for (int64_t i = lo + tid; i < r1; i += QR_THREADS) {
-          const double vi = double(A(i, j));
-          for (int64_t cc = 0; cc < cn; ++cc) {
-            const int64_t c = j + 1 + c0 + cc;
-            A(i, c) = T(double(A(i, c)) - tau * vi * s_w[cc]);
-          }
-        }
-        grid.sync();
+    for (int64_t c0 = 0; c0 < nc; c0 += QR_THREADS) {
+      const int64_t cn = nc - c0 < QR_THREADS ? nc - c0 : QR_THREADS;
+      const int64_t c = j + 1 + c0 + tid;
+      if (tid < cn) {
+        double acc = 0.0;
+#pragma unroll 4
+        for (int64_t i = lo; i < r1; ++i) acc = fma(double(A(i, j)), double(A(i, c)), acc);
+        part[int64_t(cta) * QR_THREADS + tid] = acc;
+        s_rowj[tid] = double(A(j, c));  // read before CTA 0 may rewrite row j
       }
-    } else {
+      grid.sync();
+      if (tid < cn) {
+        double t = s_rowj[tid];
+        for (int q = 0; q < G; ++q) t += part[int64_t(q) * QR_THREADS + tid];
+        s_w[tid] = t;
+      }
+      // (4) a(j, c) -= tau w_c ; a(i, c) -= tau v_i w_c
+      const double tau = s_tau;
+      if (tid < cn) {
+        const double wc = s_w[tid];
+        if (cta == 0) A(j, c) = T(double(A(j, c)) - tau * wc);
+#pragma unroll 4
+        for (int64_t i = lo; i < r1; ++i) A(i, c) = T(double(A(i, c)) - tau * double(A(i, j)) * wc);
+      }
       grid.sync();
     }
+    if (nc <= 0) grid.sync();
   }
 }
 
-// T (b x b, row-major ld b, upper): T[j,j] = tau_j, T[:j, j] = -tau_j T[:j,:j] (V[:, :j]^T v_j)
+// The same sweep with every CTA's row band of the panel resident in shared
+// memory (static bands of `chunk` rows): two grid barriers per column.  The
+// norm partials of column j+1 and its diagonal entry are published by the
+// update of column j; w's partials are combined in CTA order, so every CTA
+// forms the same w.
 template <typename T>
-__global__ void qr_t_kernel(const T* a, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t b, const T* taus,
-                            T* t) {
-  __shared__ double z[QR_MAXB];
-  const int tid = threadIdx.x;
-  auto V = [&](int64_t i, int64_t j) -> double {  // explicit unit-lower V of the panel
-    return i == j ? 1.0 : (i > j ? double(a[off + i * rs + j * cs]) : 0.0);
+__global__ void __launch_bounds__(QR_THREADS) qr_panel_smem_kernel(T* a, int64_t off, int64_t rs, int64_t cs,
+                                                                 int64_t m, int64_t b, T* taus, double* part,
+                                                                 double* npart, double* diag, int chunk) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char qr_smem[];
+  T* S = reinterpret_cast<T*>(qr_smem);  // chunk x b, row-major
+  const int G = gridDim.x, tid = threadIdx.x, cta = blockIdx.x;
+  const int64_t R0 = int64_t(cta) * chunk;
+  const int64_t R1 = R0 + chunk < m ? R0 + chunk : m;
+  const int nr = R1 > R0 ? int(R1 - R0) : 0;
+  const int bb = int(b);
+  __shared__ double red[QR_THREADS / 32];
+  __shared__ double s_w[QR_MAXB];
+  __shared__ double s_half[QR_MAXB];
+  __shared__ double s_beta, s_tau, s_scale;
+  __shared__ int s_skip;
+  for (int e = tid; e < nr * bb; e += QR_THREADS) {
+    const int r = e / bb, c = e - r * bb;
+    S[e] = a[off + (R0 + r) * rs + int64_t(c) * cs];
+  }
+  __syncthreads();
+  // norm partial of column j over band rows >= j, and the diagonal entry
+  auto publish_norm = [&](int64_t j) {
+    const int64_t lo = R0 > j ? R0 : j;
+    double ss = 0.0;
+    for (int64_t i = lo + tid; i < R1; i += QR_THREADS) {
+      const double v = double(S[(i - R0) * bb + j]);
+      ss = fma(v, v, ss);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_down_sync(0xffffffffu, ss, o);
+    if ((tid & 31) == 0) red[tid >> 5] = ss;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < QR_THREADS / 32; ++w) t += red[w];
+      npart[cta] = t;
+      if (j >= R0 && j < R1) diag[j & 1] = double(S[(j - R0) * bb + j]);
+    }
   };
-  for (int64_t e = tid; e < b * b; e += blockDim.x) t[e] = T(0);
+  const int64_t steps = m < b ? m : b;
+  if (steps > 0) publish_norm(0);
+  grid.sync();
+  for (int64_t j = 0; j < steps; ++j) {
+    if (tid < 32) {
+      // lane-strided partial sums, then a fixed shuffle tree: the same order in every CTA
+      double t = 0.0;
+      for (int q = tid; q < G; q += 32) t += __ldcg(npart + q);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (tid == 0) red[0] = t;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double nrm = sqrt(red[0]);
+      const double x0 = __ldcg(diag + (j & 1));
+      s_skip = nrm == 0.0;
+      const double beta = -copysign(nrm, x0);
+      s_beta = beta;
+      s_tau = nrm == 0.0 ? 0.0 : (beta - x0) / beta;
+      s_scale = x0 - beta;
+      if (cta == 0) taus[j] = T(s_tau);
+    }
+    __syncthreads();
+    const bool skip = s_skip;
+    const int64_t lo = R0 > j ? R0 : j;  // band rows taking part in this column
+    const int nc = int(b - j - 1);
+    if (!skip) {
+      // (2) the reflector: v_i = a(i, j) / scale below the diagonal, beta on it
+      for (int64_t i = (R0 > j + 1 ? R0 : j + 1) + tid; i < R1; i += QR_THREADS) {
+        T& x = S[(i - R0) * bb + j];
+        x = T(double(x) / s_scale);
+      }
+      __syncthreads();
+      // (3) partial w_c = sum_{i >= j} v_i a(i, c), v_j = 1; two row halves per column
+      const int cc = tid & (QR_MAXB - 1), half = tid >> 7;
+      double acc = 0.0;
+      if (cc < nc) {
+        const int c = int(j) + 1 + cc;
+        for (int64_t i = lo + half; i < R1; i += 2) {
+          const double v = i == j ? 1.0 : double(S[(i - R0) * bb + j]);
+          acc = fma(v, double(S[(i - R0) * bb + c]), acc);
+        }
+      }
+      if (half) s_half[cc] = acc;
+      __syncthreads();
+      if (!half && cc < nc) part[int64_t(cta) * QR_MAXB + cc] = acc + s_half[cc];
+      if (j >= R0 && j < R1 && tid == 0) S[(j - R0) * bb + j] = T(s_beta);
+    }
+    grid.sync();
+    if (!skip) {
+      // w_c (row j's own a(j, c) is the v_j = 1 term); then a(i, c) -= tau v_i w_c
+      {
+        const int cc = tid & (QR_MAXB - 1), half = tid >> 7;
+        double t = 0.0;
+        if (cc < nc)
+          for (int q0 = half; q0 < G; q0 += 16) {  // 8 independent loads in flight, summed in order
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int q = q0 + 2 * u;
+              v[u] = q < G ? __ldcg(part + int64_t(q) * QR_MAXB + cc) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t += v[u];
+          }
+        if (half) s_half[cc] = t;
+        __syncthreads();
+        if (!half && cc < nc) s_w[cc] = t + s_half[cc];
+        __syncthreads();
+      }
+      const double tau = s_tau;
+      const int cc = tid & (QR_MAXB - 1), half = tid >> 7;
+      if (cc < nc) {
+        const int c = int(j) + 1 + cc;
+        const double wc = s_w[cc];
+        for (int64_t i = lo + half; i < R1; i += 2) {
+          T& x = S[(i - R0) * bb + c];
+          if (i == j)
+            x = T(double(x) - tau * wc);
+          else
+            x = T(double(x) - tau * double(S[(i - R0) * bb + j]) * wc);
+        }
+      }
+      __syncthreads();
+    }
+    if (j + 1 < steps) publish_norm(j + 1);
+    grid.sync();
+  }
+  __syncthreads();
+  for (int e = tid; e < nr * bb; e += QR_THREADS) {
+    const int r = e / bb, c = e - r * bb;
+    a[off + (R0 + r) * rs + int64_t(c) * cs] = S[e];
+  }
+}
+
+// T (b x b, row-major ld b, upper): T[j,j] = tau_j, T[:j, j] = -tau_j T[:j,:j] z with
+// z = V[:, :j]^T v_j = G[j, :j] (G = V^T V is symmetric, formed beforehand by
+// one split-K GEMM).  T lives in shared memory; one warp per row of T.
+template <typename T>
+__global__ void __launch_bounds__(256) qr_t_kernel(const T* gram, int64_t b, const T* taus, T* t) {
+  extern __shared__ __align__(16) unsigned char qt_smem[];
+  double* Ts = reinterpret_cast<double*>(qt_smem);  // b x (b + 1)
+  double* z = Ts + b * (b + 1);                     // b
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ld = b + 1;
+  for (int64_t e = tid; e < b * ld; e += blockDim.x) Ts[e] = 0.0;
   __syncthreads();
   for (int64_t j = 0; j < b; ++j) {
     const double tau = double(taus[j]);
-    if (tid == 0) t[j * b + j] = T(tau);
-    if (j > 0 && tau != 0.0) {
-      // z_q = V[:, q]^T v_j over rows j.., q < j (warp per q)
-      const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
-      for (int64_t q = warp; q < j; q += nw) {
+    for (int64_t q = tid; q < j; q += blockDim.x) z[q] = double(gram[j * b + q]);
+    if (tid == 0) Ts[j * ld + j] = tau;
+    __syncthreads();
+    if (j > 0 && tau != 0.0)
+      for (int64_t r = warp; r < j; r += blockDim.x / 32) {
         double acc = 0.0;
-        for (int64_t i = j + lane; i < m; i += 32) acc = fma(V(i, q), V(i, j), acc);
+        for (int64_t q = r + lane; q < j; q += 32) acc = fma(Ts[r * ld + q], z[q], acc);
 #pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-        if (lane == 0) z[q] = acc;
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) Ts[r * ld + j] = -tau * acc;
       }
-      __syncthreads();
-      for (int64_t r = tid; r < j; r += blockDim.x) {
-        double acc = 0.0;
-        for (int64_t q = r; q < j; ++q) acc = fma(double(t[r * b + q]), z[q], acc);
-        t[r * b + j] = T(-tau * acc);
-      }
-    }
     __syncthreads();
   }
+  for (int64_t e = tid; e < b * b; e += blockDim.x) t[e] = T(Ts[(e / b) * ld + e % b]);
+}
+
+// c = alpha * sum_s ws[s] + beta * c, slices summed in order (split-K GEMM)
+template <typename T>
+__global__ void splitk_reduce_kernel(const T* ws, int S, int64_t m, int64_t n, double alpha, double beta, T* c,
+                                     int64_t off, int64_t rs, int64_t cs) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= m * n) return;
+  const int64_t i = e / n, j = e - i * n;
+  double acc = 0.0;
+  for (int q = 0; q < S; ++q) acc += double(ws[int64_t(q) * m * n + e]);
+  T& x = c[off + i * rs + j * cs];
+  x = T(beta == 0.0 ? alpha * acc : alpha * acc + beta * double(x));
 }
 
 template <typename T>
@@ -193,11 +330,47 @@ int launch_qr_panel(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, in
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return -3;
-  if (!part[dev] && cudaMalloc(&part[dev], 32 * QR_MAXB * sizeof(double)) != cudaSuccess) return -12;
-  int G = int((m + 511) / 512);
-  if (G > 32) G = 32;
-  if (G < 1) G = 1;
+  // w partials (160 x 128) + norm partials (160) + diag (2)
+  if (!part[dev] && cudaMalloc(&part[dev], (160 * QR_THREADS + 256) * sizeof(double)) != cudaSuccess) return -12;
   double* pp = part[dev];
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const size_t esz = is_f64 ? sizeof(double) : sizeof(float);
+  if (!g_qr_global && b <= QR_MAXB) {
+    // resident bands of ~128 rows (fewer, taller bands once the grid is full)
+    int G = int((m + 127) / 128);
+    if (G > sms) G = sms;
+    if (G > 160) G = 160;
+    if (G < 1) G = 1;
+    int chunk = int((m + G - 1) / G);
+    const size_t smem = size_t(chunk) * size_t(b) * esz;
+    if (smem <= 200 * 1024) {
+      double* np = pp + 160 * QR_MAXB;
+      double* dg = np + 160;
+      note_launch();
+      cudaError_t e;
+      if (is_f64) {
+        auto k = qr_panel_smem_kernel<double>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        double* ad = static_cast<double*>(a);
+        double* td = static_cast<double*>(taus);
+        void* args[] = {&ad, &off, &rs, &cs, &m, &b, &td, &pp, &np, &dg, &chunk};
+        e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k), dim3(G), dim3(QR_THREADS), args, smem, s);
+      } else {
+        auto k = qr_panel_smem_kernel<float>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        float* af = static_cast<float*>(a);
+        float* tf = static_cast<float*>(taus);
+        void* args[] = {&af, &off, &rs, &cs, &m, &b, &tf, &pp, &np, &dg, &chunk};
+        e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k), dim3(G), dim3(QR_THREADS), args, smem, s);
+      }
+      return e == cudaSuccess ? 0 : -11;
+    }
+  }
+  // ~64 rows per CTA: the column loops are latency-bound, so spread them
+  int G = int((m + 63) / 64);
+  if (G > 128) G = 128;
+  if (G < 1) G = 1;
   note_launch();
   cudaError_t e;
   if (is_f64) {
@@ -216,17 +389,34 @@ int launch_qr_panel(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, in
   return e == cudaSuccess ? 0 : -11;
 }
 
-int launch_qr_t(int is_f64, const void* a, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t b,
-                const void* taus, void* t, cudaStream_t s) {
+int launch_qr_t(int is_f64, const void* gram, int64_t b, const void* taus, void* t, cudaStream_t s) {
   if (b <= 0) return 0;
-  if (b > QR_MAXB) return -3;
+  const size_t smem = size_t(b * (b + 1) + b) * sizeof(double);
+  if (smem > 220 * 1024) return -3;
   note_launch();
+  if (is_f64) {
+    cudaFuncSetAttribute(qr_t_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    qr_t_kernel<double><<<1, 256, smem, s>>>(static_cast<const double*>(gram), b, static_cast<const double*>(taus),
+                                             static_cast<double*>(t));
+  } else {
+    cudaFuncSetAttribute(qr_t_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    qr_t_kernel<float><<<1, 256, smem, s>>>(static_cast<const float*>(gram), b, static_cast<const float*>(taus),
+                                            static_cast<float*>(t));
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+int launch_splitk_reduce(int is_f64, const void* ws, int S, int64_t m, int64_t n, double alpha, double beta, void* c,
+                         int64_t off, int64_t rs, int64_t cs, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return 0;
+  note_launch();
+  const unsigned blocks = unsigned((m * n + 255) / 256);
   if (is_f64)
-    qr_t_kernel<double><<<1, 256, 0, s>>>(static_cast<const double*>(a), off, rs, cs, m, b,
-                                          static_cast<const double*>(taus), static_cast<double*>(t));
+    splitk_reduce_kernel<double><<<blocks, 256, 0, s>>>(static_cast<const double*>(ws), S, m, n, alpha, beta,
+                                                        static_cast<double*>(c), off, rs, cs);
   else
-    qr_t_kernel<float><<<1, 256, 0, s>>>(static_cast<const float*>(a), off, rs, cs, m, b,
-                                         static_cast<const float*>(taus), static_cast<float*>(t));
+    splitk_reduce_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(ws), S, m, n, alpha, beta,
+                                                       static_cast<float*>(c), off, rs, cs);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 

@@ -99,9 +99,11 @@ _SIGNATURES = {
     "bf_ltlt_d": ([_V, _L, _L, _I, _L, _VP, _L, _VP, _VP, _VP, _VP, _VP], _I),
     "bf_ltlt_s": ([_V, _L, _L, _I, _L, _VP, _L, _VP, _VP, _VP, _VP, _VP], _I),
     "bf_qr_panel_d": ([_V, _VP, _VP], _I),
+    "bf_gemm_splitk_d": ([_D, _V, _V, _D, _V, _VP], _I),
+    "bf_gemm_splitk_s": ([_D, _V, _V, _D, _V, _VP], _I),
     "bf_qr_panel_s": ([_V, _VP, _VP], _I),
-    "bf_qr_t_d": ([_V, _VP, _VP, _VP, _VP], _I),
-    "bf_qr_t_s": ([_V, _VP, _VP, _VP, _VP], _I),
+    "bf_qr_t_d": ([_V, _VP, _VP, _VP, _VP, _VP], _I),
+    "bf_qr_t_s": ([_V, _VP, _VP, _VP, _VP, _VP], _I),
     "bf_reflector_apply_d": ([_V, _L, _D, _V, _VP], _I),
     "bf_reflector_apply_s": ([_V, _L, _D, _V, _VP], _I),
     "bf_lu_d": ([_V, _P(BfCholLevel), _I, _VP, _VP, _VP], _I),

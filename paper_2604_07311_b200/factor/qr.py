@@ -69,16 +69,20 @@ def qr_householder(a: MatrixView, tree: Optional[ControlNode] = None) -> Reflect
         _lib.check(panel_fn(ctypes.byref(_lib.as_bfview(panel)), tk.data_ptr(), stream), "qr panel")
         t_mat = torch.empty((b, b), dtype=tdt, device=a.device)
         v = torch.empty((m - k, b), dtype=tdt, device=a.device)
+        gram = torch.empty((b, b), dtype=tdt, device=a.device)
         _lib.check(getattr(lib, "bf_qr_t_" + _sfx(a))(ctypes.byref(_lib.as_bfview(panel)), tk.data_ptr(),
-                                                       t_mat.data_ptr(), v.data_ptr(), stream), "qr T")
+                                                       t_mat.data_ptr(), v.data_ptr(), gram.data_ptr(), stream), "qr T")
         panels.append((k, t_mat))
         if step.r2.len > 0:
             # trailing := trailing - V (T^T (V^T trailing))   (qr.py:103-121)
             trailing = a.subview(rows, step.r2)
             vv = from_torch(v)
-            w = torch.zeros((b, step.r2.len), dtype=tdt, device=a.device)
+            w = torch.empty((b, step.r2.len), dtype=tdt, device=a.device)
             wv = from_torch(w)
-            gemm(1.0, vv.transposed(), trailing, 0.0, wv, cfg=cfg, ways=tree.ways)
+            # V^T C has b x n outputs and K = m - k: split-K over side streams
+            _lib.check(getattr(lib, "bf_gemm_splitk_" + _sfx(a))(
+                1.0, ctypes.byref(_lib.as_bfview(vv.transposed())), ctypes.byref(_lib.as_bfview(trailing)), 0.0,
+                ctypes.byref(_lib.as_bfview(wv)), stream), "qr V^T C")
             w2 = torch.zeros_like(w)
             gemm(1.0, from_torch(t_mat).transposed(), wv, 0.0, from_torch(w2), cfg=cfg, ways=tree.ways)
             gemm(-1.0, vv, from_torch(w2), 1.0, trailing, cfg=cfg, ways=tree.ways)

@@ -1,30 +1,25 @@
-"""Summarise an ncu --metrics gpu__time_duration.sum launch list (skips the
-input-generation SYRK, the first TMA launch, when asked)."""
+"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list: total
+ms, share, launches and mean us per kernel."""
 import collections
 import csv
 import sys
 
-path = sys.argv[1]
-skip_first = "--skip-first" in sys.argv
-rows = list(csv.reader(open(path)))
-hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
-hdr = rows[hdr_i]
-ki, mi = hdr.index("Kernel Name"), hdr.index("Metric Value")
-tot, cnt, mx = collections.defaultdict(float), collections.Counter(), collections.defaultdict(float)
-first = skip_first
-for r in rows[hdr_i + 1:]:
-    if len(r) <= mi:
+d = collections.defaultdict(lambda: [0, 0.0])
+h = None
+for r in csv.reader(open(sys.argv[1])):
+    if "Kernel Name" in r:
+        h = r
         continue
-    v = float(r[mi].replace(",", "")) / 1e6
-    name = r[ki].split("(")[0][:80]
-    if first and "gemm_dmma" in name:
-        first = False
-        continue
-    tot[name] += v
-    cnt[name] += 1
-    mx[name] = max(mx[name], v)
-T = sum(tot.values())
-print(f"{'ms':>9} {'share':>6} {'launches':>8} {'max ms':>8}  kernel")
-for k, v in sorted(tot.items(), key=lambda x: -x[1])[:12]:
-    print(f"{v:9.2f} {100 * v / T:5.1f}% {cnt[k]:8d} {mx[k]:8.3f}  {k}")
-print(f"{T:9.2f}  total over {sum(cnt.values())} launches (cold-cache, serialised by ncu)")
+    if h and len(r) == len(h):
+        x = dict(zip(h, r))
+        if x["Metric Name"] != "gpu__time_duration.sum":
+            continue
+        v = float(x["Metric Value"].replace(",", ""))
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(x["Metric Unit"], 1.0)
+        k = x["Kernel Name"][: int(sys.argv[2]) if len(sys.argv) > 2 else 70]
+        d[k][0] += 1
+        d[k][1] += v
+tot = sum(v[1] for v in d.values())
+print(f"total {tot / 1e3:.2f} ms over {sum(v[0] for v in d.values())} launches")
+for k, v in sorted(d.items(), key=lambda t: -t[1][1])[:15]:
+    print(f"{v[1] / 1e3:9.2f} ms {100 * v[1] / tot:5.1f}% {v[0]:5d} {v[1] / v[0]:10.1f} us  {k}")

@@ -854,7 +854,7 @@ int bf_ltlt_s(const bf_view* x, int64_t j0, int64_t j1, int blocked, int64_t k, 
 // so they are parity-to-rounding products, never used on a bitwise path.
 static int gemm_splitk_impl(Mode mode, double alpha, const bf_view& a, const bf_view& b, double beta,
                             const bf_view& c, cudaStream_t s) {
-  constexpr int SMAX = 8;
+  constexpr int SMAX = 16;
   const int64_t m = c.m, n = c.n, k = a.n;
   if (a.n != b.m || c.m != a.m || c.n != b.n) return fail(BF_ERR_SHAPE, "gemm dims mismatch");
   int dev = 0;

@@ -115,14 +115,19 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_kernel(T* a, int64_t off,
 }
 
 // The same sweep with every CTA's row band of the panel resident in shared
-// memory (static bands of `chunk` rows): two grid barriers per column.  The
-// norm partials of column j+1 and its diagonal entry are published by the
-// update of column j; w's partials are combined in CTA order, so every CTA
-// forms the same w.
+// memory (static bands of `chunk` rows) and ONE grid barrier per column:
+// before the barrier each CTA publishes, for the coming column j, the raw
+// partial dots u_c = sum_{i>j} a(i,j) a(i,c), c >= j, over its band (u_j is
+// the norm's tail), and the owner of row j publishes a(j, j:).  After it,
+// every CTA derives beta/tau/scale from the same sums and forms
+// w_c = a(j,c) + u_c / scale (= a(j,c) + v^T a(j+1:, c) with v = a(j+1:,j) /
+// scale), scales its part of the reflector, applies the rank-1 update to its
+// rows and publishes the partials of column j+1.  Partial sums are combined
+// in CTA order (identical in every CTA); buffers alternate by column parity.
 template <typename T>
 __global__ void __launch_bounds__(QR_THREADS) qr_panel_smem_kernel(T* a, int64_t off, int64_t rs, int64_t cs,
                                                                  int64_t m, int64_t b, T* taus, double* part,
-                                                                 double* npart, double* diag, int chunk) {
+                                                                 double* rowbuf, int chunk) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char qr_smem[];
   T* S = reinterpret_cast<T*>(qr_smem);  // chunk x b, row-major
@@ -131,8 +136,9 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_smem_kernel(T* a, int64_t
   const int64_t R1 = R0 + chunk < m ? R0 + chunk : m;
   const int nr = R1 > R0 ? int(R1 - R0) : 0;
   const int bb = int(b);
-  __shared__ double red[QR_THREADS / 32];
-  __shared__ double s_w[QR_MAXB];
+  const int cc = tid & (QR_MAXB - 1), half = tid >> 7;
+  __shared__ double s_u[QR_MAXB];
+  __shared__ double s_row[QR_MAXB];
   __shared__ double s_half[QR_MAXB];
   __shared__ double s_beta, s_tau, s_scale;
   __shared__ int s_skip;
@@ -141,41 +147,50 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_smem_kernel(T* a, int64_t
     S[e] = a[off + (R0 + r) * rs + int64_t(c) * cs];
   }
   __syncthreads();
-  // norm partial of column j over band rows >= j, and the diagonal entry
-  auto publish_norm = [&](int64_t j) {
-    const int64_t lo = R0 > j ? R0 : j;
-    double ss = 0.0;
-    for (int64_t i = lo + tid; i < R1; i += QR_THREADS) {
-      const double v = double(S[(i - R0) * bb + j]);
-      ss = fma(v, v, ss);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) ss += __shfl_down_sync(0xffffffffu, ss, o);
-    if ((tid & 31) == 0) red[tid >> 5] = ss;
+  // partials of column j: u_c over band rows i > j, c in [j, b); row j if owned
+  auto publish = [&](int64_t j) {
+    const int par = int(j & 1);
+    const int nc = bb - int(j);
+    const int64_t lo = R0 > j + 1 ? R0 : j + 1;
+    double acc = 0.0;
+    if (cc < nc)
+      for (int64_t i = lo + half; i < R1; i += 2) {
+        const T* row = S + (i - R0) * bb;
+        acc = fma(double(row[j]), double(row[j + cc]), acc);
+      }
+    if (half) s_half[cc] = acc;
     __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int w = 0; w < QR_THREADS / 32; ++w) t += red[w];
-      npart[cta] = t;
-      if (j >= R0 && j < R1) diag[j & 1] = double(S[(j - R0) * bb + j]);
-    }
+    if (!half && cc < nc) part[(int64_t(par) * 160 + cta) * QR_MAXB + cc] = acc + s_half[cc];
+    if (j >= R0 && j < R1 && half && cc < nc) rowbuf[par * QR_MAXB + cc] = double(S[(j - R0) * bb + j + cc]);
   };
   const int64_t steps = m < b ? m : b;
-  if (steps > 0) publish_norm(0);
+  if (steps > 0) publish(0);
   grid.sync();
   for (int64_t j = 0; j < steps; ++j) {
-    if (tid < 32) {
-      // lane-strided partial sums, then a fixed shuffle tree: the same order in every CTA
+    const int par = int(j & 1);
+    const int nc = bb - int(j);
+    {
       double t = 0.0;
-      for (int q = tid; q < G; q += 32) t += __ldcg(npart + q);
+      if (cc < nc)
+        for (int q0 = half; q0 < G; q0 += 32) {  // 16 independent loads in flight, summed in order
+          double v[16];
 #pragma unroll
-      for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (tid == 0) red[0] = t;
+          for (int u = 0; u < 16; ++u) {
+            const int q = q0 + 2 * u;
+            v[u] = q < G ? __ldcg(part + (int64_t(par) * 160 + q) * QR_MAXB + cc) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 16; ++u) t += v[u];
+        }
+      if (half) s_half[cc] = t;
+      else if (cc < nc) s_row[cc] = __ldcg(rowbuf + par * QR_MAXB + cc);
+      __syncthreads();
+      if (!half && cc < nc) s_u[cc] = t + s_half[cc];
+      __syncthreads();
     }
-    __syncthreads();
     if (tid == 0) {
-      const double nrm = sqrt(red[0]);
-      const double x0 = __ldcg(diag + (j & 1));
+      const double x0 = s_row[0];
+      const double nrm = sqrt(fma(x0, x0, s_u[0]));
       s_skip = nrm == 0.0;
       const double beta = -copysign(nrm, x0);
       s_beta = beta;
@@ -184,69 +199,30 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_smem_kernel(T* a, int64_t
       if (cta == 0) taus[j] = T(s_tau);
     }
     __syncthreads();
-    const bool skip = s_skip;
-    const int64_t lo = R0 > j ? R0 : j;  // band rows taking part in this column
-    const int nc = int(b - j - 1);
-    if (!skip) {
-      // (2) the reflector: v_i = a(i, j) / scale below the diagonal, beta on it
+    if (!s_skip) {
+      const double scale = s_scale, tau = s_tau;
+      // the reflector below the diagonal (own rows), beta on the diagonal
       for (int64_t i = (R0 > j + 1 ? R0 : j + 1) + tid; i < R1; i += QR_THREADS) {
         T& x = S[(i - R0) * bb + j];
-        x = T(double(x) / s_scale);
+        x = T(double(x) / scale);
       }
       __syncthreads();
-      // (3) partial w_c = sum_{i >= j} v_i a(i, c), v_j = 1; two row halves per column
-      const int cc = tid & (QR_MAXB - 1), half = tid >> 7;
-      double acc = 0.0;
-      if (cc < nc) {
-        const int c = int(j) + 1 + cc;
-        for (int64_t i = lo + half; i < R1; i += 2) {
-          const double v = i == j ? 1.0 : double(S[(i - R0) * bb + j]);
-          acc = fma(v, double(S[(i - R0) * bb + c]), acc);
+      if (cc >= 1 && cc < nc) {
+        const int64_t c = j + cc;
+        const double wc = s_row[cc] + s_u[cc] / scale;
+        if (half == 0 && j >= R0 && j < R1) {
+          T& x = S[(j - R0) * bb + c];
+          x = T(double(x) - tau * wc);
+        }
+        for (int64_t i = (R0 > j + 1 ? R0 : j + 1) + half; i < R1; i += 2) {
+          T* row = S + (i - R0) * bb;
+          row[c] = T(double(row[c]) - tau * double(row[j]) * wc);
         }
       }
-      if (half) s_half[cc] = acc;
-      __syncthreads();
-      if (!half && cc < nc) part[int64_t(cta) * QR_MAXB + cc] = acc + s_half[cc];
-      if (j >= R0 && j < R1 && tid == 0) S[(j - R0) * bb + j] = T(s_beta);
-    }
-    grid.sync();
-    if (!skip) {
-      // w_c (row j's own a(j, c) is the v_j = 1 term); then a(i, c) -= tau v_i w_c
-      {
-        const int cc = tid & (QR_MAXB - 1), half = tid >> 7;
-        double t = 0.0;
-        if (cc < nc)
-          for (int q0 = half; q0 < G; q0 += 16) {  // 8 independent loads in flight, summed in order
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int q = q0 + 2 * u;
-              v[u] = q < G ? __ldcg(part + int64_t(q) * QR_MAXB + cc) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) t += v[u];
-          }
-        if (half) s_half[cc] = t;
-        __syncthreads();
-        if (!half && cc < nc) s_w[cc] = t + s_half[cc];
-        __syncthreads();
-      }
-      const double tau = s_tau;
-      const int cc = tid & (QR_MAXB - 1), half = tid >> 7;
-      if (cc < nc) {
-        const int c = int(j) + 1 + cc;
-        const double wc = s_w[cc];
-        for (int64_t i = lo + half; i < R1; i += 2) {
-          T& x = S[(i - R0) * bb + c];
-          if (i == j)
-            x = T(double(x) - tau * wc);
-          else
-            x = T(double(x) - tau * double(S[(i - R0) * bb + j]) * wc);
-        }
-      }
+      if (tid == 0 && j >= R0 && j < R1) S[(j - R0) * bb + j] = T(s_beta);
       __syncthreads();
     }
-    if (j + 1 < steps) publish_norm(j + 1);
+    if (j + 1 < steps) publish(j + 1);
     grid.sync();
   }
   __syncthreads();
@@ -256,34 +232,73 @@ __global__ void __launch_bounds__(QR_THREADS) qr_panel_smem_kernel(T* a, int64_t
   }
 }
 
-// T (b x b, row-major ld b, upper): T[j,j] = tau_j, T[:j, j] = -tau_j T[:j,:j] z with
-// z = V[:, :j]^T v_j = G[j, :j] (G = V^T V is symmetric, formed beforehand by
-// one split-K GEMM).  T lives in shared memory; one warp per row of T.
+// T (b x b, row-major ld b, upper) of the compact-WY form I - V T V^T
+// (qr.py:79-92 builds it column by column: T[:j, j] = -tau_j T[:j,:j] V^T v_j).
+// Here the same T is formed recursively from G = V^T V (one split-K GEMM):
+// 32-column leaves run that column recursion (one warp each, lane per row),
+// then T12 = -T11 G12 T22 merges blocks pairwise (equal to the column
+// recursion up to rounding).  T and the G blocks live in shared memory.
+constexpr int QT_LEAF = 32;
+constexpr int QT_XLD = 65;
+
 template <typename T>
 __global__ void __launch_bounds__(256) qr_t_kernel(const T* gram, int64_t b, const T* taus, T* t) {
   extern __shared__ __align__(16) unsigned char qt_smem[];
+  const int bb = int(b), ld = bb + 1;
   double* Ts = reinterpret_cast<double*>(qt_smem);  // b x (b + 1)
-  double* z = Ts + b * (b + 1);                     // b
+  double* X = Ts + bb * ld;                         // 64 x 65 scratch (leaf G blocks, then G12 T22)
+  double* G12 = X + 4 * QT_LEAF * 33;               // 64 x 65: the off-diagonal G block of a merge
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t ld = b + 1;
-  for (int64_t e = tid; e < b * ld; e += blockDim.x) Ts[e] = 0.0;
-  __syncthreads();
-  for (int64_t j = 0; j < b; ++j) {
-    const double tau = double(taus[j]);
-    for (int64_t q = tid; q < j; q += blockDim.x) z[q] = double(gram[j * b + q]);
-    if (tid == 0) Ts[j * ld + j] = tau;
-    __syncthreads();
-    if (j > 0 && tau != 0.0)
-      for (int64_t r = warp; r < j; r += blockDim.x / 32) {
-        double acc = 0.0;
-        for (int64_t q = r + lane; q < j; q += 32) acc = fma(Ts[r * ld + q], z[q], acc);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) Ts[r * ld + j] = -tau * acc;
-      }
-    __syncthreads();
+  for (int e = tid; e < bb * ld; e += blockDim.x) Ts[e] = 0.0;
+  // leaf diagonal blocks of G, leaf w at X + w * 32 * 33
+  const int nleaf = (bb + QT_LEAF - 1) / QT_LEAF;
+  for (int e = tid; e < nleaf * QT_LEAF * QT_LEAF; e += blockDim.x) {
+    const int w = e / (QT_LEAF * QT_LEAF), q = (e / QT_LEAF) % QT_LEAF, c = e % QT_LEAF;
+    const int r0 = w * QT_LEAF;
+    X[w * QT_LEAF * 33 + q * 33 + c] = (r0 + q < bb && r0 + c < bb) ? double(gram[int64_t(r0 + q) * b + r0 + c]) : 0.0;
   }
-  for (int64_t e = tid; e < b * b; e += blockDim.x) t[e] = T(Ts[(e / b) * ld + e % b]);
+  __syncthreads();
+  if (warp < nleaf) {
+    const int r0 = warp * QT_LEAF, sz = bb - r0 < QT_LEAF ? bb - r0 : QT_LEAF;
+    const double* Gl = X + warp * QT_LEAF * 33;
+    for (int jj = 0; jj < sz; ++jj) {
+      const double tau = double(taus[r0 + jj]);
+      if (lane == jj) Ts[(r0 + jj) * ld + r0 + jj] = tau;
+      if (lane < jj && tau != 0.0) {
+        double acc = 0.0;
+        for (int q = lane; q < jj; ++q) acc = fma(Ts[(r0 + lane) * ld + r0 + q], Gl[q * 33 + jj], acc);
+        Ts[(r0 + lane) * ld + r0 + jj] = -tau * acc;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int sz = QT_LEAF; sz < bb; sz *= 2)
+    for (int r0 = 0; r0 + sz < bb; r0 += 2 * sz) {
+      const int s1 = sz, s2 = bb - r0 - sz < sz ? bb - r0 - sz : sz, c0 = r0 + s1;
+      for (int e = tid; e < s1 * s2; e += blockDim.x) {
+        const int q = e / s2, c = e % s2;
+        G12[q * QT_XLD + c] = double(gram[int64_t(r0 + q) * b + c0 + c]);
+      }
+      __syncthreads();
+      // X = G12 T22  (T22 upper: p <= c)
+      for (int e = tid; e < s1 * s2; e += blockDim.x) {
+        const int q = e / s2, c = e % s2;
+        double acc = 0.0;
+        for (int p = 0; p <= c; ++p) acc = fma(G12[q * QT_XLD + p], Ts[(c0 + p) * ld + c0 + c], acc);
+        X[q * QT_XLD + c] = acc;
+      }
+      __syncthreads();
+      // T12 = -T11 X  (T11 upper: p >= q)
+      for (int e = tid; e < s1 * s2; e += blockDim.x) {
+        const int q = e / s2, c = e % s2;
+        double acc = 0.0;
+        for (int p = q; p < s1; ++p) acc = fma(Ts[(r0 + q) * ld + r0 + p], X[p * QT_XLD + c], acc);
+        Ts[(r0 + q) * ld + c0 + c] = -acc;
+      }
+      __syncthreads();
+    }
+  for (int e = tid; e < bb * bb; e += blockDim.x) t[e] = T(Ts[(e / bb) * ld + e % bb]);
 }
 
 // c = alpha * sum_s ws[s] + beta * c, slices summed in order (split-K GEMM)
@@ -330,8 +345,9 @@ int launch_qr_panel(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, in
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return -3;
-  // w partials (160 x 128) + norm partials (160) + diag (2)
-  if (!part[dev] && cudaMalloc(&part[dev], (160 * QR_THREADS + 256) * sizeof(double)) != cudaSuccess) return -12;
+  // 2 x (160 x 128) dot partials (by column parity) + 2 x 128 published rows
+  if (!part[dev] && cudaMalloc(&part[dev], (2 * 160 * QR_MAXB + 2 * QR_MAXB) * sizeof(double)) != cudaSuccess)
+    return -12;
   double* pp = part[dev];
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -345,8 +361,7 @@ int launch_qr_panel(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, in
     int chunk = int((m + G - 1) / G);
     const size_t smem = size_t(chunk) * size_t(b) * esz;
     if (smem <= 200 * 1024) {
-      double* np = pp + 160 * QR_MAXB;
-      double* dg = np + 160;
+      double* rb = pp + 2 * 160 * QR_MAXB;
       note_launch();
       cudaError_t e;
       if (is_f64) {
@@ -354,14 +369,14 @@ int launch_qr_panel(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, in
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         double* ad = static_cast<double*>(a);
         double* td = static_cast<double*>(taus);
-        void* args[] = {&ad, &off, &rs, &cs, &m, &b, &td, &pp, &np, &dg, &chunk};
+        void* args[] = {&ad, &off, &rs, &cs, &m, &b, &td, &pp, &rb, &chunk};
         e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k), dim3(G), dim3(QR_THREADS), args, smem, s);
       } else {
         auto k = qr_panel_smem_kernel<float>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         float* af = static_cast<float*>(a);
         float* tf = static_cast<float*>(taus);
-        void* args[] = {&af, &off, &rs, &cs, &m, &b, &tf, &pp, &np, &dg, &chunk};
+        void* args[] = {&af, &off, &rs, &cs, &m, &b, &tf, &pp, &rb, &chunk};
         e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k), dim3(G), dim3(QR_THREADS), args, smem, s);
       }
       return e == cudaSuccess ? 0 : -11;
@@ -391,8 +406,8 @@ int launch_qr_panel(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, in
 
 int launch_qr_t(int is_f64, const void* gram, int64_t b, const void* taus, void* t, cudaStream_t s) {
   if (b <= 0) return 0;
-  const size_t smem = size_t(b * (b + 1) + b) * sizeof(double);
-  if (smem > 220 * 1024) return -3;
+  if (b > QR_MAXB) return -3;
+  const size_t smem = size_t(b * (b + 1) + 4 * QT_LEAF * 33 + 64 * QT_XLD) * sizeof(double);
   note_launch();
   if (is_f64) {
     cudaFuncSetAttribute(qr_t_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);

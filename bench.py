@@ -167,7 +167,8 @@ def side_workloads(torch, a0, n: int, fp64_ms: float) -> dict:
     """BASELINE configs[3] and [4], measured after the headline (not part of
     `value`): the mixed-precision solve of the same SPD matrix (bf16/fp32
     factor on tcgen05 + FP64 refinement to 10*n*eps), FP64-equivalent
-    n^3/3 / time; and the 4-index contraction abij,cdij->abcd at d=128."""
+    n^3/3 / time; the FP32 factorization of that matrix on the tensor cores
+    (3xTF32); and the 4-index contraction abij,cdij->abcd at d=128."""
     from paper_2604_07311_b200.mixed import MixedWorkspace, posv_mixed
     from paper_2604_07311_b200.tensor import ContractionSpec, make_tensor
     import paper_2604_07311_b200 as bfp
@@ -193,6 +194,33 @@ def side_workloads(torch, a0, n: int, fp64_ms: float) -> dict:
                             "converged": bool(res.converged), "tol": "10*n*eps64",
                             "time_ratio_vs_fp64_factor": round(fp64_ms / t, 2)}
     del ws
+    # FP32 Cholesky of the same matrix on the tensor cores (3xTF32 tcgen05)
+    from paper_2604_07311_b200.mixed import F32TcWorkspace, cholesky_f32_tc
+
+    a32 = a0.float()
+    w32 = torch.empty_like(a32)
+    ws32 = F32TcWorkspace(n, 1024)
+    ms = []
+    for i in range(4):
+        w32.copy_(a32)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        cholesky_f32_tc(w32, bs=1024, ws=ws32)
+        e1.record()
+        e1.synchronize()
+        if i:
+            ms.append(e0.elapsed_time(e1))
+    t = statistics.median(ms)
+    xv = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    lf = torch.tril(w32).double()
+    ax = a0 @ xv + a0.T @ xv - a0.diagonal() * xv  # a0 holds the lower triangle only
+    rr = float(torch.linalg.vector_norm(ax - lf @ (lf.T @ xv)) / torch.linalg.vector_norm(ax))
+    out["c2_f32_tensor_core"] = {"n": n, "ms": round(t, 3), "gflops": round(chol_flops(n) / (t / 1e3) / 1e9, 1),
+                                 "method": "3xTF32 tcgen05 GEMMs, FP64 diagonal blocks (mixed.cholesky_f32_tc)",
+                                 "rel_residual_Ax_vs_LLtx": rr}
+    del a32, w32, ws32, lf, ax
+    torch.cuda.empty_cache()
     d = 128
     spec = ContractionSpec.parse("abij,cdij->abcd")
 

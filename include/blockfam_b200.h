@@ -228,6 +228,24 @@ int bf_apply_pivots_s(const bf_view* a, const int64_t* d_piv, int64_t count, int
 int bf_gemm_bf16(double alpha, const void* a, int64_t lda, const void* b, int64_t ldb, double beta, const bf_view* c,
                  int64_t k, int lower_only, void* stream);
 int bf_convert_f32_bf16(const bf_view* src, void* dst, int64_t ld, int transpose, void* stream);
+/* FP32 on the tensor cores (3xTF32; no reference counterpart — the
+ * reference's f32 GEMM is engine/gemm.py:179-201 with f32 or f64
+ * accumulation, which tcgen05 cannot reproduce bit for bit; this is the
+ * fp32-accurate tensor-core alternative, to rounding).
+ * bf_split_tf32_{s,d}: row i of src (m x k, fp32 / fp64) -> dst row i =
+ *   [hi | hi | lo | hi], four parts of kp >= k columns (zero padded),
+ *   hi = tf32(x) (round to nearest), lo = x - hi; ld >= 4 kp.
+ * bf_gemm_tf32: C(fp32 view) := beta*C + alpha * A * B^T with A (c->m x k),
+ *   B (c->n x k) row-major fp32 read as tf32 (kind::tf32, TMEM accumulation).
+ *   With A = split[:, 0:3kp] and B = split[:, kp:4kp], k = 3kp: the 3xTF32 product.
+ * bf_gemm_f32_tc: C := beta*C + alpha * A * B for fp32 views, both splits and
+ *   the K = 3k tf32 GEMM in one call (lower_only: GEMMT). */
+int bf_split_tf32_s(const bf_view* src, float* dst, int64_t ld, int64_t kp, void* stream);
+int bf_split_tf32_d(const bf_view* src, float* dst, int64_t ld, int64_t kp, void* stream);
+int bf_gemm_tf32(double alpha, const float* a, int64_t lda, const float* b, int64_t ldb, double beta, const bf_view* c,
+                 int64_t k, int lower_only, void* stream);
+int bf_gemm_f32_tc(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c, int lower_only,
+                   void* stream);
 int bf_convert_f64_f32(const bf_view* src, const bf_view* dst, int lower_only, void* stream);
 int bf_convert_f32_f64(const bf_view* src, const bf_view* dst, int lower_only, void* stream);
 int bf_convert_f64_bf16(const bf_view* src, void* dst, int64_t ld, int transpose, void* stream);

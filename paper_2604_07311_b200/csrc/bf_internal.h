@@ -97,6 +97,11 @@ int launch_trsm_small_right(int is_f64, double alpha, const void* t, int64_t tof
                             int64_t boff, int64_t brs, int64_t bcs, int64_t m, int64_t n, int64_t kc,
                             const int* abort_flag, cudaStream_t s);
 
+int launch_gemm_tf32_tc(double alpha, const float* a, int64_t lda, const float* b, int64_t ldb, double beta, float* c,
+                        int64_t c_off, int64_t c_rs, int64_t c_cs, int64_t m, int64_t n, int64_t k, int lower_only,
+                        cudaStream_t s);
+int launch_split_tf32(int src_f64, const void* src, int64_t soff, int64_t srs, int64_t scs, float* dst, int64_t ld,
+                      int64_t m, int64_t k, int64_t kp, cudaStream_t s);
 int launch_gemm_bf16_tc(double alpha, const void* a, int64_t lda, const void* b, int64_t ldb, double beta, float* c,
                         int64_t c_off, int64_t c_rs, int64_t c_cs, int64_t m, int64_t n, int64_t k, int lower_only,
                         cudaStream_t s);

@@ -994,6 +994,67 @@ int bf_gemm_bf16(double alpha, const void* a, int64_t lda, const void* b, int64_
   if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "bf16 gemm: operands must be 16-byte aligned k-contiguous bf16");
   return rc ? fail(BF_ERR_CUDA, "bf16 gemm launch failed") : BF_OK;
 }
+int bf_gemm_tf32(double alpha, const float* a, int64_t lda, const float* b, int64_t ldb, double beta, const bf_view* c,
+                 int64_t k, int lower_only, void* stream) {
+  if (!c) return fail(BF_ERR_VALUE, "null view");
+  if (lower_only && c->m != c->n) return fail(BF_ERR_SHAPE, "gemmt needs square c");
+  int rc = bf::launch_gemm_tf32_tc(alpha, a, lda, b, ldb, beta, static_cast<float*>(c->base), c->off, c->rs, c->cs,
+                                   c->m, c->n, k, lower_only, S(stream));
+  if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "tf32 gemm: operands must be 16-byte aligned k-contiguous fp32");
+  return rc ? fail(BF_ERR_CUDA, "tf32 gemm launch failed") : BF_OK;
+}
+static int split_entry(int f64, const bf_view* src, float* dst, int64_t ld, int64_t kp, void* stream) {
+  if (!src || !dst) return fail(BF_ERR_VALUE, "null argument");
+  if (kp < src->n || ld < 4 * kp) return fail(BF_ERR_SHAPE, "split needs kp >= k and ld >= 4 kp");
+  int rc = bf::launch_split_tf32(f64, src->base, src->off, src->rs, src->cs, dst, ld, src->m, src->n, kp, S(stream));
+  return rc ? fail(BF_ERR_CUDA, "split launch failed") : BF_OK;
+}
+int bf_split_tf32_s(const bf_view* src, float* dst, int64_t ld, int64_t kp, void* stream) {
+  return split_entry(0, src, dst, ld, kp, stream);
+}
+int bf_split_tf32_d(const bf_view* src, float* dst, int64_t ld, int64_t kp, void* stream) {
+  return split_entry(1, src, dst, ld, kp, stream);
+}
+// C(f32) := beta C + alpha A B (A m x k, B k x n fp32 views) as ONE K = 3k
+// tf32 GEMM over the split operands (workspace owned by the library)
+int bf_gemm_f32_tc(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c, int lower_only,
+                   void* stream) {
+  if (!a || !b || !c) return fail(BF_ERR_VALUE, "null view");
+  if (a->n != b->m || c->m != a->m || c->n != b->n) return fail(BF_ERR_SHAPE, "gemm dims mismatch");
+  if (lower_only && c->m != c->n) return fail(BF_ERR_SHAPE, "gemmt needs square c");
+  const int64_t m = c->m, n = c->n, k = a->n;
+  if (m == 0 || n == 0) return BF_OK;
+  cudaStream_t s = S(stream);
+  if (k == 0 || alpha == 0.0) return scale_impl(MODE_S, beta, *c, lower_only, s);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return fail(BF_ERR_CUDA, "device index");
+  static float* ws[64] = {};
+  static size_t ws_bytes[64] = {};
+  const int64_t kp = (k + 3) / 4 * 4, ld = 4 * kp;
+  const size_t need = size_t(m + n) * size_t(ld) * sizeof(float);
+  if (need > ws_bytes[dev]) {
+    if (ws[dev]) {
+      cudaDeviceSynchronize();
+      cudaFree(ws[dev]);
+    }
+    ws[dev] = nullptr;
+    ws_bytes[dev] = 0;
+    if (cudaMalloc(&ws[dev], need) != cudaSuccess) return fail(BF_ERR_CUDA, "tf32 split workspace");
+    ws_bytes[dev] = need;
+  }
+  float* sa = ws[dev];
+  float* sb = sa + m * ld;
+  int rc = bf::launch_split_tf32(0, a->base, a->off, a->rs, a->cs, sa, ld, m, k, kp, s);
+  const bf_view bt = transposed(*b);  // rows of B^T: the k-contiguous N x K operand
+  if (!rc) rc = bf::launch_split_tf32(0, bt.base, bt.off, bt.rs, bt.cs, sb, ld, n, k, kp, s);
+  if (rc) return fail(BF_ERR_CUDA, "split launch failed");
+  // A' = [hi hi lo] (columns 0..3kp of sa), B' = [hi lo hi] (columns kp..4kp of sb)
+  rc = bf::launch_gemm_tf32_tc(alpha, sa, ld, sb + kp, ld, beta, static_cast<float*>(c->base), c->off, c->rs, c->cs, m,
+                               n, 3 * kp, lower_only, s);
+  if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "tf32 gemm: unsupported layout");
+  return rc ? fail(BF_ERR_CUDA, "tf32 gemm launch failed") : BF_OK;
+}
 int bf_convert_f32_bf16(const bf_view* src, void* dst, int64_t ld, int transpose, void* stream) {
   if (!src) return fail(BF_ERR_VALUE, "null view");
   int rc = bf::launch_to_bf16(static_cast<const float*>(src->base), src->off, src->rs, src->cs, dst, ld, src->m,

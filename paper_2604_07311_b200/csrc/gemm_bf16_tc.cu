@@ -1,5 +1,7 @@
 // bf16 x bf16 -> fp32 GEMM / GEMMT on the 5th-generation tensor cores
-// (tcgen05.mma kind::f16, accumulator in TMEM), operands staged by TMA.
+// (tcgen05.mma kind::f16, accumulator in TMEM), operands staged by TMA; the
+// same kernel with kind::tf32 on fp32 operands backs the 3xTF32 FP32 GEMM
+// (split_tf32_kernel: A B^T = hi hi^T + hi lo^T + lo hi^T as one K = 3k GEMM).
 //
 // The trailing update of the mixed-precision Cholesky (BASELINE configs[3]):
 // C(fp32) := beta*C + alpha * A * B^T with A (M x K) and B (N x K) bf16,
@@ -87,6 +89,10 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int m, int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
 }
+// kind::tf32 instruction descriptor: D f32, A/B tf32 (format 2), both K-major
+__host__ __device__ constexpr uint32_t idesc_tf32_f32(int m, int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(m >> 4) << 24);
+}
 
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -94,6 +100,15 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
@@ -125,7 +140,10 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 
-template <bool TMAC>
+// TF32 = 0: bf16 operands (kind::f16, 64 k per 128-byte row);
+// TF32 = 1: fp32 operands read as tf32 (kind::tf32, 32 k per row).  The smem
+// geometry, descriptors and the 4 MMAs per stage (32 bytes of k each) are the same.
+template <bool TMAC, int TF32>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                         const __grid_constant__ CUtensorMap tma_c, const GemmParams p) {
@@ -165,7 +183,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint32_t tmem_base;
   asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(tmem_base) : "r"(tmem_slot));
 
-  const int ktiles = int((p.k + TC_BK - 1) / TC_BK);
+  constexpr int BK = TF32 ? 32 : TC_BK;  // k elements per 128-byte swizzle row
+  const int ktiles = int((p.k + BK - 1) / BK);
   const int64_t ntiles = p.num_tiles;
   if (warp == 0 && lane == 0) {
     // ---- TMA producer ----
@@ -178,13 +197,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_wait_tc(empty(s), ((it / TC_STAGES) & 1u) ^ 1u);
         const uint32_t sa = tiles + s * TC_STAGE_BYTES;
         mbar_expect_tx_tc(full(s), TC_STAGE_BYTES);
-        tma_load_2d_tc(sa, &tma_a, kt * TC_BK, int(ti * TC_BM), full(s));
-        tma_load_2d_tc(sa + TC_A_BYTES, &tma_b, kt * TC_BK, int(tj * TC_BN), full(s));
+        tma_load_2d_tc(sa, &tma_a, kt * BK, int(ti * TC_BM), full(s));
+        tma_load_2d_tc(sa + TC_A_BYTES, &tma_b, kt * BK, int(tj * TC_BN), full(s));
       }
     }
   } else if (warp == 1 && lane == 0) {
     // ---- MMA issuer ----
-    constexpr uint32_t idesc = idesc_bf16_f32(TC_BM, TC_BN);
+    constexpr uint32_t idesc = TF32 ? idesc_tf32_f32(TC_BM, TC_BN) : idesc_bf16_f32(TC_BM, TC_BN);
     uint32_t it = 0, lt = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
       const uint32_t buf = lt & 1u;
@@ -198,8 +217,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const uint32_t sa = tiles + s * TC_STAGE_BYTES;
         const uint64_t da = umma_desc_sw128(sa), db = umma_desc_sw128(sa + TC_A_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < TC_BK / 16; ++kk)  // K=16 per MMA: advance 32 bytes inside the swizzle row
-          umma_bf16(dst, da + uint64_t(2 * kk), db + uint64_t(2 * kk), idesc, (kt | kk) != 0);
+        for (int kk = 0; kk < 4; ++kk) {  // 32 bytes of k per MMA (16 bf16 / 8 tf32): advance inside the swizzle row
+          if (TF32)
+            umma_tf32(dst, da + uint64_t(2 * kk), db + uint64_t(2 * kk), idesc, (kt | kk) != 0);
+          else
+            umma_bf16(dst, da + uint64_t(2 * kk), db + uint64_t(2 * kk), idesc, (kt | kk) != 0);
+        }
         umma_commit(empty(s));
       }
       umma_commit(acc_full(buf));
@@ -361,6 +384,18 @@ bool make_map_c32(CUtensorMap* map, const float* base, int64_t rows, int64_t col
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool make_map_f32k(CUtensorMap* map, const float* base, int64_t rows, int64_t k, int64_t ld) {
+  EncodeTiledFnTc enc = encoder_tc();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cuuint64_t(k), cuuint64_t(rows)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * 4};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t k, int64_t ld) {
   EncodeTiledFnTc enc = encoder_tc();
   if (!enc) return false;
@@ -388,24 +423,70 @@ __global__ void to_bf16_kernel(const S* src, int64_t soff, int64_t srs, int64_t 
   }
 }
 
+// 3xTF32 operand split: row i of the (m x k) fp32 source becomes
+// [hi | hi | lo | hi] in dst (4 parts of kp >= k columns, zero padded), with
+// hi = x rounded to tf32 and lo = x - hi (exact).  A' = dst[:, 0:3kp] and
+// B' = dst[:, kp:4kp] then give A'B'^T = hi hi^T + hi lo^T + lo hi^T.
+template <typename S>
+__global__ void split_tf32_kernel(const S* src, int64_t soff, int64_t srs, int64_t scs, float* dst, int64_t ld,
+                                  int64_t m, int64_t k, int64_t kp) {
+  const int64_t total = m * kp;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / kp, j = e % kp;
+    const float x = j < k ? float(src[soff + i * srs + j * scs]) : 0.f;
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(h) : "f"(x));
+    const float hi = __uint_as_float(h), lo = x - hi;
+    float* row = dst + i * ld;
+    row[j] = hi;
+    row[kp + j] = hi;
+    row[2 * kp + j] = lo;
+    row[3 * kp + j] = hi;
+  }
+}
+
 }  // namespace
 
-// C(fp32 view) = beta*C + alpha * A(bf16 m x k, row stride lda) * B(bf16 n x k, ldb)^T
-int launch_gemm_bf16_tc(double alpha, const void* a, int64_t lda, const void* b, int64_t ldb, double beta, float* c,
-                        int64_t c_off, int64_t c_rs, int64_t c_cs, int64_t m, int64_t n, int64_t k, int lower_only,
-                        cudaStream_t s) {
+int launch_split_tf32(int src_f64, const void* src, int64_t soff, int64_t srs, int64_t scs, float* dst, int64_t ld,
+                      int64_t m, int64_t k, int64_t kp, cudaStream_t s) {
+  if (m <= 0 || kp <= 0) return 0;
+  const int64_t total = m * kp;
+  const int blocks = int((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+  note_launch();
+  if (src_f64)
+    split_tf32_kernel<double><<<blocks, 256, 0, s>>>(static_cast<const double*>(src), soff, srs, scs, dst, ld, m, k, kp);
+  else
+    split_tf32_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(src), soff, srs, scs, dst, ld, m, k, kp);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+namespace {
+int launch_tc(int tf32, double alpha, const void* a, int64_t lda, const void* b, int64_t ldb, double beta, float* c,
+              int64_t c_off, int64_t c_rs, int64_t c_cs, int64_t m, int64_t n, int64_t k, int lower_only,
+              cudaStream_t s) {
   if (m <= 0 || n <= 0) return 0;
-  if ((reinterpret_cast<uintptr_t>(a) % 16) || (reinterpret_cast<uintptr_t>(b) % 16) || (lda * 2) % 16 ||
-      (ldb * 2) % 16 || k < 1)
+  const int esz = tf32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(a) % 16) || (reinterpret_cast<uintptr_t>(b) % 16) || (lda * esz) % 16 ||
+      (ldb * esz) % 16 || k < 1)
     return -3;
   CUtensorMap ma, mb;
-  if (!make_map_bf16(&ma, a, m, k, lda) || !make_map_bf16(&mb, b, n, k, ldb)) return -3;
+  if (tf32) {
+    if (!make_map_f32k(&ma, static_cast<const float*>(a), m, k, lda) ||
+        !make_map_f32k(&mb, static_cast<const float*>(b), n, k, ldb))
+      return -3;
+  } else if (!make_map_bf16(&ma, a, m, k, lda) || !make_map_bf16(&mb, b, n, k, ldb)) {
+    return -3;
+  }
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(gemm_bf16_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TC_SMEM)) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(gemm_bf16_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TC_SMEM)) !=
-            cudaSuccess)
+    if (cudaFuncSetAttribute(gemm_bf16_tc_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(TC_SMEM)) != cudaSuccess ||
+        cudaFuncSetAttribute(gemm_bf16_tc_kernel<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(TC_SMEM)) != cudaSuccess ||
+        cudaFuncSetAttribute(gemm_bf16_tc_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(TC_SMEM)) != cudaSuccess ||
+        cudaFuncSetAttribute(gemm_bf16_tc_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(TC_SMEM)) != cudaSuccess)
       return -10;
     attr = true;
   }
@@ -438,11 +519,33 @@ int launch_gemm_bf16_tc(double alpha, const void* a, int64_t lda, const void* b,
   }
   const int64_t grid = p.num_tiles < sms ? p.num_tiles : sms;
   note_launch();
-  if (tmac)
-    gemm_bf16_tc_kernel<true><<<unsigned(grid), TC_THREADS, TC_SMEM, s>>>(ma, mb, mc, p);
-  else
-    gemm_bf16_tc_kernel<false><<<unsigned(grid), TC_THREADS, TC_SMEM, s>>>(ma, mb, mc, p);
+  if (tf32) {
+    if (tmac)
+      gemm_bf16_tc_kernel<true, 1><<<unsigned(grid), TC_THREADS, TC_SMEM, s>>>(ma, mb, mc, p);
+    else
+      gemm_bf16_tc_kernel<false, 1><<<unsigned(grid), TC_THREADS, TC_SMEM, s>>>(ma, mb, mc, p);
+  } else {
+    if (tmac)
+      gemm_bf16_tc_kernel<true, 0><<<unsigned(grid), TC_THREADS, TC_SMEM, s>>>(ma, mb, mc, p);
+    else
+      gemm_bf16_tc_kernel<false, 0><<<unsigned(grid), TC_THREADS, TC_SMEM, s>>>(ma, mb, mc, p);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+}  // namespace
+
+// C(fp32 view) = beta*C + alpha * A(bf16 m x k, row stride lda) * B(bf16 n x k, ldb)^T
+int launch_gemm_bf16_tc(double alpha, const void* a, int64_t lda, const void* b, int64_t ldb, double beta, float* c,
+                        int64_t c_off, int64_t c_rs, int64_t c_cs, int64_t m, int64_t n, int64_t k, int lower_only,
+                        cudaStream_t s) {
+  return launch_tc(0, alpha, a, lda, b, ldb, beta, c, c_off, c_rs, c_cs, m, n, k, lower_only, s);
+}
+
+// The same with fp32 operands consumed as tf32 (kind::tf32)
+int launch_gemm_tf32_tc(double alpha, const float* a, int64_t lda, const float* b, int64_t ldb, double beta, float* c,
+                        int64_t c_off, int64_t c_rs, int64_t c_cs, int64_t m, int64_t n, int64_t k, int lower_only,
+                        cudaStream_t s) {
+  return launch_tc(1, alpha, a, lda, b, ldb, beta, c, c_off, c_rs, c_cs, m, n, k, lower_only, s);
 }
 
 int launch_to_bf16(const float* src, int64_t soff, int64_t srs, int64_t scs, void* dst, int64_t ld, int64_t m,

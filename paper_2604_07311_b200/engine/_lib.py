@@ -119,6 +119,10 @@ _SIGNATURES = {
     "bf_cholesky_ex_d": ([_V, _P(BfCholLevel), _I, _L, _VP, _VP], _I),
     "bf_trsm_rltn_ex_d": ([_D, _V, _V, _L, _VP, _VP, _VP], _I),
     "bf_gemm_bf16": ([_D, _VP, _L, _VP, _L, _D, _V, _L, _I, _VP], _I),
+    "bf_split_tf32_s": ([_V, _VP, _L, _L, _VP], _I),
+    "bf_split_tf32_d": ([_V, _VP, _L, _L, _VP], _I),
+    "bf_gemm_tf32": ([_D, _VP, _L, _VP, _L, _D, _V, _L, _I, _VP], _I),
+    "bf_gemm_f32_tc": ([_D, _V, _V, _D, _V, _I, _VP], _I),
     "bf_convert_f32_bf16": ([_V, _VP, _L, _I, _VP], _I),
     "bf_convert_f64_f32": ([_V, _V, _I, _VP], _I),
     "bf_convert_f32_f64": ([_V, _V, _I, _VP], _I),

@@ -34,7 +34,8 @@ from .engine import _lib
 from .errors import NotPositiveDefiniteError, ShapeError
 from .views import DType, MatrixView, from_torch
 
-__all__ = ["MixedFactor", "MixedResult", "MixedWorkspace", "cholesky_mixed", "posv_mixed"]
+__all__ = ["F32TcWorkspace", "MixedFactor", "MixedResult", "MixedWorkspace", "cholesky_f32_tc", "cholesky_mixed",
+           "posv_mixed"]
 
 DIAG_TREE = {"op": "cholesky", "variant": 3, "bs": 128, "kernel": {"kc": 128},
              "child": {"op": "cholesky", "variant": "unblocked3"}}  # FP64 diagonal blocks
@@ -211,3 +212,123 @@ def posv_mixed(a: torch.Tensor, b: torch.Tensor, bs: int = 1024, tol: Optional[f
         if err <= tol:
             break
     return MixedResult(x, it, err, err <= tol)
+
+
+# --------------------------------------------------------------------------
+# FP32 Cholesky on the tensor cores (3xTF32)
+#
+# The reference's FP32 path (f32 storage, f32 or f64 accumulation,
+# engine/config.py:21,39) is reproduced bit for bit by the DMMA/SIMT engine
+# (bf_cholesky_s).  This is the tensor-core alternative at FP32 accuracy, to
+# rounding: every GEMM runs as ONE tcgen05 kind::tf32 GEMM over operands split
+# into tf32 hi/lo parts (A B^T = hi hi^T + hi lo^T + lo hi^T, K = 3k, fp32
+# accumulation in TMEM).  Per block of bs: the diagonal block in FP64 (exact
+# tree driver) and its explicit inverse, the panel L21 = A21 L11^-T as a 3xTF32
+# GEMM, the trailing update as a 3xTF32 GEMMT; lookahead as in cholesky_mixed.
+# --------------------------------------------------------------------------
+class F32TcWorkspace:
+    """Buffers of one FP32 tensor-core factorization of order n (block bs)."""
+
+    def __init__(self, n: int, bs: int = 1024, device: Optional[torch.device] = None) -> None:
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.n, self.bs, self.device = n, bs, dev
+        self.kp = (bs + 3) // 4 * 4
+        # split panels [hi | hi | lo | hi] (ping-pong: panel k+1 forms while step k's update reads panel k)
+        self.pbuf = [torch.empty((n, 4 * self.kp), dtype=torch.float32, device=dev) for _ in range(2)]
+        self.d64 = torch.empty((bs, bs), dtype=torch.float64, device=dev)
+        self.x64 = torch.empty((bs, bs), dtype=torch.float64, device=dev)
+        self.x32 = torch.empty((bs, bs), dtype=torch.float32, device=dev)
+        self.info = torch.empty((1,), dtype=torch.int32, device=dev)
+        self.before = torch.empty((1,), dtype=torch.int32, device=dev)
+        self.side = torch.cuda.Stream(dev, priority=-1)
+
+
+def cholesky_f32_tc(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlNode] = None,
+                    lookahead: bool = True, ws: Optional[F32TcWorkspace] = None) -> torch.Tensor:
+    """In-place lower Cholesky of the fp32 SPD matrix `a` (square, row-major,
+    CUDA) with 3xTF32 tensor-core GEMMs; the strict upper triangle is left
+    untouched.  Returns the device pivot flag (-1 = success) after raising
+    NotPositiveDefiniteError for a failed pivot."""
+    if a.dim() != 2 or a.shape[0] != a.shape[1] or a.dtype != torch.float32 or not a.is_cuda:
+        raise ShapeError("cholesky_f32_tc needs a square fp32 CUDA matrix")
+    if a.stride(1) != 1 or a.stride(0) % 4:
+        raise ShapeError("cholesky_f32_tc needs a row-major matrix with 16-byte rows")
+    lib = _lib.lib()
+    n = a.shape[0]
+    if ws is None:
+        ws = F32TcWorkspace(n, bs, a.device)
+    if ws.n != n or ws.bs != bs or ws.device != a.device:
+        raise ShapeError("workspace was made for another order, block size or device")
+    main = torch.cuda.current_stream(a.device)
+    side = ws.side if lookahead else main
+    tree = diag_tree if diag_tree is not None else parse_tree(json.dumps(DIAG_TREE))
+    levels = flatten_cholesky(tree, resolve_config(tree, DType.F64))
+    arr = (_lib.BfCholLevel * len(levels))(*[_lib.BfCholLevel(v, 0, b, kc) for v, b, kc in levels])
+    kp, info = ws.kp, ws.info
+    ld = 4 * kp
+    nblk = (n + bs - 1) // bs
+    info.fill_(-1)
+
+    def diag_and_panel(k: int, stream: torch.cuda.Stream) -> None:
+        k0 = k * bs
+        b = min(bs, n - k0)
+        r = n - k0 - b
+        sh = stream.cuda_stream
+        with torch.cuda.stream(stream):
+            d32, dd = a[k0:k0 + b, k0:k0 + b], ws.d64[:b, :b]
+            _lib.check(lib.bf_convert_f32_f64(ctypes.byref(_v(d32)), ctypes.byref(_v(dd)), 1, sh), "convert")
+            ws.before.copy_(info)
+            _lib.check(lib.bf_cholesky_d(ctypes.byref(_v(dd)), arr, len(levels), info.data_ptr(), sh), "diag factor")
+            torch.where((ws.before < 0) & (info >= 0), info + k0, info, out=info)
+            _lib.check(lib.bf_convert_f64_f32(ctypes.byref(_v(dd)), ctypes.byref(_v(d32)), 1, sh), "convert")
+            if r == 0:
+                return
+            x = ws.x64[:b, :b]
+            x.zero_()
+            x.diagonal().fill_(1.0)  # X L11^T = I: X = L11^-T
+            _lib.check(lib.bf_trsm_rltn_d(1.0, ctypes.byref(_v(dd)), ctypes.byref(_v(x)), 512, None, sh), "inverse")
+            x32 = ws.x32[:b, :b]
+            _lib.check(lib.bf_convert_f64_f32(ctypes.byref(_v(x)), ctypes.byref(_v(x32)), 0, sh), "convert")
+            a21 = a[k0 + b:, k0:k0 + b]
+            # L21 = A21 X (3xTF32), then its split for the trailing updates
+            _lib.check(lib.bf_gemm_f32_tc(1.0, ctypes.byref(_v(a21)), ctypes.byref(_v(x32)), 0.0,
+                                          ctypes.byref(_v(a21)), 0, sh), "panel gemm")
+            p = ws.pbuf[k % 2]
+            _lib.check(lib.bf_split_tf32_s(ctypes.byref(_v(a21)), p.data_ptr(), ld, kp, sh), "split")
+
+    def syrk(p: torch.Tensor, c: torch.Tensor, lower: int) -> None:
+        # C -= P P^T with A' = p[:, 0:3kp], B' = p[:, kp:4kp]
+        _lib.check(lib.bf_gemm_tf32(-1.0, p.data_ptr(), ld, p[:, kp:].data_ptr(), ld, 1.0, ctypes.byref(_v(c)),
+                                    3 * kp, lower, main.cuda_stream), "trailing gemm")
+
+    if lookahead:
+        side.wait_stream(main)
+    diag_and_panel(0, side)
+    ev = torch.cuda.Event()
+    ev.record(side)
+    for k in range(nblk - 1):
+        k1 = (k + 1) * bs
+        r = n - k1
+        nb = min(bs, r)
+        main.wait_event(ev)
+        pk = ws.pbuf[k % 2][: n - k * bs - bs]
+        # (1) the next block column first (its diagonal block lower-only: the
+        # strict upper triangle is never written), (2) the next panel on the
+        # side stream, (3) the rest
+        syrk(pk[:nb], a[k1:k1 + nb, k1:k1 + nb], 1)
+        if r > nb:
+            _lib.check(lib.bf_gemm_tf32(-1.0, pk[nb:].data_ptr(), ld, pk[:nb, kp:].data_ptr(), ld, 1.0,
+                                        ctypes.byref(_v(a[k1 + nb:, k1:k1 + nb])), 3 * kp, 0, main.cuda_stream),
+                       "column gemm")
+        if lookahead:
+            side.wait_stream(main)
+        diag_and_panel(k + 1, side)
+        ev = torch.cuda.Event()
+        ev.record(side)
+        if r > nb:
+            syrk(pk[nb:], a[k1 + nb:, k1 + nb:], 1)
+    main.wait_event(ev)
+    bad = int(info.item())
+    if bad >= 0:
+        raise NotPositiveDefiniteError(bad)
+    return info

@@ -58,13 +58,18 @@ class MixedWorkspace:
     repeated solves never touch the allocator (multi-GB blocks churning
     through the caching allocator cost more than the solve)."""
 
-    def __init__(self, n: int, bs: int = 1024, device: Optional[torch.device] = None) -> None:
+    def __init__(self, n: int, bs: int = 1024, device: Optional[torch.device] = None,
+                 precision: str = "bf16") -> None:
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.n, self.bs, self.device = n, bs, dev
+        if precision not in ("bf16", "tf32"):
+            raise ValueError(f"precision must be 'bf16' or 'tf32', got {precision!r}")
+        self.n, self.bs, self.device, self.precision = n, bs, dev, precision
         nblk = (n + bs - 1) // bs
+        # panel operands of the tensor-core GEMMs: bf16 copies, or fp32 read as tf32
+        pdt = torch.bfloat16 if precision == "bf16" else torch.float32
         self.w = torch.empty((n, n), dtype=torch.float32, device=dev)
-        self.pbuf = [torch.empty((n, bs), dtype=torch.bfloat16, device=dev) for _ in range(2)]
-        self.xt = torch.empty((bs, bs), dtype=torch.bfloat16, device=dev)
+        self.pbuf = [torch.empty((n, bs), dtype=pdt, device=dev) for _ in range(2)]
+        self.xt = torch.empty((bs, bs), dtype=pdt, device=dev)
         self.d64 = torch.empty((bs, bs), dtype=torch.float64, device=dev)
         self.x64 = torch.empty((bs, bs), dtype=torch.float64, device=dev)
         self.xinv = torch.zeros((nblk, bs, bs), dtype=torch.float32, device=dev)
@@ -88,14 +93,17 @@ class MixedFactor:
 
 
 def cholesky_mixed(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlNode] = None,
-                   lookahead: bool = True, ws: Optional[MixedWorkspace] = None) -> MixedFactor:
+                   lookahead: bool = True, ws: Optional[MixedWorkspace] = None,
+                   precision: Optional[str] = None) -> MixedFactor:
     """bf16/fp32 factorization of the fp64 SPD matrix `a` (right-looking,
     blocks of bs).  Per block: the diagonal block in FP64 (the exact tree
     driver, DMMA GEMMs), its explicit inverse in FP64, the panel as one bf16
     tcgen05 GEMM against that inverse, and the trailing update as a bf16
     GEMMT.  With lookahead the next block column is updated first and the
     next diagonal/inverse/panel run on a high-priority side stream while the
-    rest of the trailing update proceeds."""
+    rest of the trailing update proceeds.  precision "tf32" runs the panel and
+    trailing GEMMs as tcgen05 kind::tf32 on the fp32 data itself (no bf16
+    copies; ~2^-11 instead of ~2^-8 per product, so fewer refinement steps)."""
     if a.dim() != 2 or a.shape[0] != a.shape[1] or a.dtype != torch.float64 or not a.is_cuda:
         raise ShapeError("cholesky_mixed needs a square fp64 CUDA matrix")
     if bs % 8:
@@ -103,9 +111,15 @@ def cholesky_mixed(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlN
     lib = _lib.lib()
     n = a.shape[0]
     if ws is None:
-        ws = MixedWorkspace(n, bs, a.device)
+        ws = MixedWorkspace(n, bs, a.device, precision or "bf16")
     if ws.n != n or ws.bs != bs or ws.device != a.device:
         raise ShapeError("workspace was made for another order, block size or device")
+    if precision is not None and precision != ws.precision:
+        raise ShapeError(f"workspace was made for precision {ws.precision!r}")
+    tf32 = ws.precision == "tf32"
+    if tf32 and n % 4:
+        raise ShapeError("precision 'tf32' needs n % 4 == 0 (16-byte fp32 rows for TMA)")
+    tc_gemm = lib.bf_gemm_tf32 if tf32 else lib.bf_gemm_bf16
     main = torch.cuda.current_stream(a.device)
     side = ws.side if lookahead else main
     tree = diag_tree if diag_tree is not None else parse_tree(json.dumps(DIAG_TREE))
@@ -138,9 +152,18 @@ def cholesky_mixed(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlN
                        "convert")
             if r == 0:
                 return
-            _lib.check(lib.bf_convert_f64_bf16(ctypes.byref(_v(x)), xt.data_ptr(), bs, 1, sh), "convert")
             a21 = w[k0 + b:, k0:k0 + b]
             p = pbuf[k % len(pbuf)]
+            if tf32:
+                # L21 = A21 * X straight from W (C = A * Bnk^T, Bnk = X^T in fp32), into the panel buffer
+                xtv = _lib.BfView(xt.data_ptr(), 0, b, b, 1, bs)  # X^T: transposed fp32 store
+                _lib.check(lib.bf_convert_f64_f32(ctypes.byref(_v(x)), ctypes.byref(xtv), 0, sh), "convert")
+                pv = p[:r, :b]
+                _lib.check(lib.bf_gemm_tf32(1.0, a21.data_ptr(), n, xt.data_ptr(), bs, 0.0, ctypes.byref(_v(pv)), b, 0,
+                                            sh), "panel gemm")
+                a21.copy_(pv)
+                return
+            _lib.check(lib.bf_convert_f64_bf16(ctypes.byref(_v(x)), xt.data_ptr(), bs, 1, sh), "convert")
             _lib.check(lib.bf_convert_f32_bf16(ctypes.byref(_v(a21)), p.data_ptr(), bs, 0, sh), "convert")
             # L21 = A21 * X  (C = A * Bnk^T with Bnk = X^T)
             _lib.check(lib.bf_gemm_bf16(1.0, p.data_ptr(), bs, xt.data_ptr(), bs, 0.0, ctypes.byref(_v(a21)), b, 0, sh),
@@ -161,8 +184,8 @@ def cholesky_mixed(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlN
         main.wait_event(ev)
         pk = pbuf[k % len(pbuf)]
         # (1) the next block column first: W[k1:, k1:k1+nb] -= P P[:nb]^T
-        _lib.check(lib.bf_gemm_bf16(-1.0, pk.data_ptr(), bs, pk.data_ptr(), bs, 1.0, ctypes.byref(_v(w[k1:, k1:k1 + nb])),
-                                    b, 0, main.cuda_stream), "column gemm")
+        _lib.check(tc_gemm(-1.0, pk.data_ptr(), bs, pk.data_ptr(), bs, 1.0, ctypes.byref(_v(w[k1:, k1:k1 + nb])),
+                           b, 0, main.cuda_stream), "column gemm")
         if lookahead:
             side.wait_stream(main)
         diag_and_panel(k + 1, side)
@@ -171,8 +194,8 @@ def cholesky_mixed(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlN
         # (2) the rest of the trailing triangle
         if r > nb:
             rest = pk[nb:]
-            _lib.check(lib.bf_gemm_bf16(-1.0, rest.data_ptr(), bs, rest.data_ptr(), bs, 1.0,
-                                        ctypes.byref(_v(w[k1 + nb:, k1 + nb:])), b, 1, main.cuda_stream),
+            _lib.check(tc_gemm(-1.0, rest.data_ptr(), bs, rest.data_ptr(), bs, 1.0,
+                               ctypes.byref(_v(w[k1 + nb:, k1 + nb:])), b, 1, main.cuda_stream),
                        "trailing gemmt")
     main.wait_event(ev)
     bad = int(info.item())
@@ -182,7 +205,8 @@ def cholesky_mixed(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlN
 
 
 def posv_mixed(a: torch.Tensor, b: torch.Tensor, bs: int = 1024, tol: Optional[float] = None,
-               max_iter: int = 30, lookahead: bool = True, ws: Optional[MixedWorkspace] = None) -> MixedResult:
+               max_iter: int = 30, lookahead: bool = True, ws: Optional[MixedWorkspace] = None,
+               precision: Optional[str] = None) -> MixedResult:
     """Solve A x = b (A fp64 SPD, full dense row-major on the GPU) to FP64
     accuracy: bf16/fp32 factorization + FP64 iterative refinement.  The
     returned x lives in the workspace (copy it before reusing ws)."""
@@ -191,8 +215,8 @@ def posv_mixed(a: torch.Tensor, b: torch.Tensor, bs: int = 1024, tol: Optional[f
     stream = torch.cuda.current_stream(a.device).cuda_stream
     tol = tol if tol is not None else 10 * n * torch.finfo(torch.float64).eps
     if ws is None:
-        ws = MixedWorkspace(n, bs, a.device)
-    f = cholesky_mixed(a, bs, lookahead=lookahead, ws=ws)
+        ws = MixedWorkspace(n, bs, a.device, precision or "bf16")
+    f = cholesky_mixed(a, bs, lookahead=lookahead, ws=ws, precision=precision)
     work = ws.work
     _lib.check(lib.bf_row_abs_sum_d(a.data_ptr(), n, ws.rows.data_ptr(), n, stream), "row sums")
     norm_a = float(ws.rows.max())

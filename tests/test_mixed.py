@@ -82,22 +82,24 @@ def test_bf16_gemm_rejects_unaligned_leading_dim(cuda):
     assert rc != 0 and b"aligned" in lib.bf_last_error()
 
 
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
 @pytest.mark.parametrize("n,bs,lookahead", [(1000, 256, True), (3000, 1024, True), (2100, 512, False)])
-def test_mixed_solve_reaches_fp64_accuracy(cuda, n, bs, lookahead):
+def test_mixed_solve_reaches_fp64_accuracy(cuda, n, bs, lookahead, precision):
     g = torch.Generator(device="cuda")
     g.manual_seed(n)
     m = torch.rand(n, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
     a = m @ m.T + n * torch.eye(n, dtype=torch.float64, device="cuda")
     b = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
-    res = posv_mixed(a, b, bs=bs, lookahead=lookahead)
-    assert res.converged and res.iterations <= 30
+    res = posv_mixed(a, b, bs=bs, lookahead=lookahead, precision=precision)
+    assert res.converged and res.iterations <= (30 if precision == "bf16" else 8)
     eps = np.finfo(np.float64).eps
     x = res.x.cpu().numpy()
     an, bn = a.cpu().numpy(), b.cpu().numpy()
     back = np.abs(bn - an @ x).max() / (np.abs(an).sum(1).max() * np.abs(x).max() + np.abs(bn).max())
     assert back <= 10 * n * eps
     x_ref = np.linalg.solve(an, bn)
-    assert np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref) <= 1e-12
+    # forward error <= cond(A) * backward error; cond(M M^T + n I) is ~2-3
+    assert np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref) <= 100 * n * eps
 
 
 def test_blocked_potrs_matches_direct_solve(cuda):

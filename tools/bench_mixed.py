@@ -1,7 +1,7 @@
 """Mixed-precision SPD solve benchmark (BASELINE configs[3]): n=32768,
 bf16/fp32 factorization + FP64 iterative refinement.
 
-    python tools/bench_mixed.py [n] [bs]
+    python tools/bench_mixed.py [n] [bs] [bf16|tf32]
 
 Prints one JSON line: factor / refine ms (CUDA events, inputs resident),
 iterations, backward error, and FP64-equivalent GFLOP/s = (n^3/3) / total.
@@ -21,10 +21,11 @@ from paper_2604_07311_b200.mixed import MixedWorkspace, cholesky_mixed, posv_mix
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
     bs = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+    prec = sys.argv[3] if len(sys.argv) > 3 else "bf16"
     g = torch.Generator(device="cuda")
     g.manual_seed(7)
     m = torch.rand(n, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
-    ws = MixedWorkspace(n, bs)
+    ws = MixedWorkspace(n, bs, precision=prec)
     for name, scale, shift in (("mmt_plus_nI", 1.0, float(n)), ("mmt_over_n_plus_1e-2I", 1.0 / n, 1e-2)):
         a = torch.mm(m, m.T).mul_(scale)
         a.diagonal().add_(shift)
@@ -40,7 +41,7 @@ def main():
         e[2].synchronize()
         fac = e[0].elapsed_time(e[1])
         tot = e[1].elapsed_time(e[2])  # factor + refinement inside posv_mixed
-        print(json.dumps({"n": n, "bs": bs, "matrix": name, "factor_ms": round(fac, 2), "posv_ms": round(tot, 2),
+        print(json.dumps({"n": n, "bs": bs, "precision": prec, "matrix": name, "factor_ms": round(fac, 2), "posv_ms": round(tot, 2),
                           "refine_ms": round(tot - fac, 2), "iterations": res.iterations,
                           "backward_error": res.backward_error, "converged": res.converged,
                           "fp64_equiv_gflops": round(n ** 3 / 3 / (tot / 1e3) / 1e9, 1),

@@ -25,9 +25,14 @@ using bf::GemmParams;
 using bf::OperandMK;
 
 thread_local std::string g_last_error;
-int g_lookahead = 1;
-int g_group = 8;
-int g_fused_trsm = 1;  // bf_set_option("fused_trsm", 0) keeps every recursion level a separate launch  // bf_set_option("group", g): raster group height in tiles  // bf_set_option("lookahead", 0) restores the plain reference schedule
+int g_lookahead = 1;      // bf_set_option("lookahead", 0) restores the plain reference schedule
+int g_group = 8;          // bf_set_option("group", g): raster group height in tiles
+int g_fused_trsm = 1;     // bf_set_option("fused_trsm", 0) keeps every recursion level a separate launch
+// bf_set_option("pipeline_first", c): step 0 of the lookahead schedule in ~c
+// row chunks of the first panel (0/1: off).  Bitwise-neutral; measured no
+// faster at n=32768 (the chunked TRSM competes with the SYRK for the same
+// SMs), so off by default.
+int g_pipeline_first = 0;
 
 int fail(int code, const char* msg) {
   g_last_error = msg;
@@ -257,6 +262,16 @@ cudaStream_t panel_stream() {
   return streams[dev];
 }
 
+// Auxiliary stream per device (the pipelined first step's trailing update).
+cudaStream_t aux_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+  return streams[dev];
+}
+
 // Copy stream per device (host <-> device traffic of bf_cholesky_host_d).
 cudaStream_t copy_stream() {
   static cudaStream_t streams[64] = {};
@@ -340,9 +355,93 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     if (g_tl_origin) cudaEventDestroy(g_tl_origin);
     g_tl_origin = mark(s);
   }
-  int rc = panel(0, bs < n ? bs : n, s);
-  if (rc == BF_OK) writeback_block_column(a, 0, bs < n ? bs : n, s);
-  for (int64_t done = 0; done < n && rc == BF_OK;) {
+  int64_t start = 0;
+  int rc = BF_OK;
+  if (g_pipeline_first > 1 && n > 3 * bs) {
+    // Step 0, pipelined by row chunks of the panel: the first panel has no
+    // earlier SYRK to hide under, so its TRSM (rows independent) runs chunk
+    // by chunk on the panel stream while the main stream applies each
+    // finished chunk to block column 1 and the aux stream applies its part
+    // of the rest of the trailing update.  Every element still receives the
+    // same single K = bs update (same kernel, same kc chain): bitwise the
+    // unpipelined schedule.
+    // chunks: about g_pipeline_first of them, whole multiples of the next panel width
+    const int64_t b = bs, r2 = bs, nr2 = n - bs, b2 = bs < nr2 ? bs : nr2;
+    const int64_t want = (nr2 + g_pipeline_first - 1) / g_pipeline_first;
+    const int64_t C = ((want + b2 - 1) / b2) * b2;
+    const int64_t chunks = (nr2 + C - 1) / C;
+    cudaStream_t xs = aux_stream();
+    if (!xs) return fail(BF_ERR_CUDA, "cannot create the aux stream");
+    bf_view a11 = subview(a, 0, b, 0, b);
+    bf_view l21 = subview(a, r2, nr2, 0, b);
+    bf_view l21_top = subview(l21, 0, b2, 0, b);
+    rc = chol_run(mode, a11, lv, nl, 1, base, d_info, s);
+    if (rc) return rc;
+    std::vector<cudaEvent_t> ev_chunk(static_cast<size_t>(chunks));
+    for (auto& e : ev_chunk) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEvent_t ev_col, ev_rest;
+    cudaEventCreateWithFlags(&ev_col, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming);
+    cudaEventRecord(ev_main, s);
+    cudaStreamWaitEvent(ps, ev_main, 0);
+    for (int64_t i = 0; i < chunks && !rc; ++i) {
+      const int64_t r0 = i * C, rn = C < nr2 - r0 ? C : nr2 - r0;
+      rc = trsm_rec(mode, 1.0, a11, subview(l21, r0, rn, 0, b), kc, nullptr, d_info, ps);
+      cudaEventRecord(ev_chunk[size_t(i)], ps);
+    }
+    if (!rc) writeback_block_column(a, 0, b, ps);
+    // block column 1 (l21 columns [0, b2) of the trailing matrix), chunk by chunk (main stream)
+    for (int64_t i = 0; i < chunks && !rc; ++i) {
+      const int64_t r0 = i * C, rn = C < nr2 - r0 ? C : nr2 - r0;
+      cudaStreamWaitEvent(s, ev_chunk[size_t(i)], 0);
+      int64_t g0 = r0;  // first row of this chunk taking a full-width GEMM
+      if (i == 0) {
+        rc = gemm_impl(mode, -1.0, l21_top, transposed(l21_top), 1.0, subview(a, r2, b2, r2, b2), 1, kc, d_info, s);
+        g0 = b2;
+      }
+      if (!rc && r0 + rn > g0)
+        rc = gemm_impl(mode, -1.0, subview(l21, g0, r0 + rn - g0, 0, b), transposed(l21_top), 1.0,
+                       subview(a, r2 + g0, r0 + rn - g0, r2, b2), 0, kc, d_info, s);
+    }
+    // the rest of step 0's trailing update (l21 rows and columns >= b2), chunk
+    // by chunk on the aux stream: the chunk's rows against every column before
+    // them (GEMM), then its own diagonal block (GEMMT)
+    cudaStreamWaitEvent(xs, ev_main, 0);
+    for (int64_t i = 0; i < chunks && !rc; ++i) {
+      const int64_t r0 = i * C, rn = C < nr2 - r0 ? C : nr2 - r0;
+      const int64_t q0 = r0 > b2 ? r0 : b2, qn = r0 + rn - q0;  // rows of this chunk in the rest
+      if (qn <= 0) continue;
+      cudaStreamWaitEvent(xs, ev_chunk[size_t(i)], 0);
+      bf_view li = subview(l21, q0, qn, 0, b);
+      if (q0 > b2) {
+        bf_view mid = subview(l21, b2, q0 - b2, 0, b);
+        rc = gemm_impl(mode, -1.0, li, transposed(mid), 1.0, subview(a, r2 + q0, qn, r2 + b2, q0 - b2), 0, kc, d_info,
+                       xs, base + r2);
+      }
+      if (!rc)
+        rc = gemm_impl(mode, -1.0, li, transposed(li), 1.0, subview(a, r2 + q0, qn, r2 + q0, qn), 1, kc, d_info, xs,
+                       base + r2);
+    }
+    cudaEventRecord(ev_rest, xs);
+    // panel 1 once block column 1 is complete
+    if (!rc) {
+      cudaEventRecord(ev_col, s);
+      cudaStreamWaitEvent(ps, ev_col, 0);
+      rc = panel(r2, b2, ps);
+      if (!rc) writeback_block_column(a, r2, b2, ps);
+      cudaEventRecord(ev_panel, ps);
+      cudaStreamWaitEvent(s, ev_panel, 0);
+    }
+    cudaStreamWaitEvent(s, ev_rest, 0);
+    for (auto& e : ev_chunk) cudaEventDestroy(e);
+    cudaEventDestroy(ev_col);
+    cudaEventDestroy(ev_rest);
+    start = r2;
+  } else {
+    rc = panel(0, bs < n ? bs : n, s);
+    if (rc == BF_OK) writeback_block_column(a, 0, bs < n ? bs : n, s);
+  }
+  for (int64_t done = start; done < n && rc == BF_OK;) {
     const int64_t b = bs < n - done ? bs : n - done;
     const int64_t r2 = done + b, nr2 = n - r2;
     if (nr2 == 0) break;
@@ -584,6 +683,10 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "tma_variant") == 0) {
     bf::g_tma_variant = int(value & 3);
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "pipeline_first") == 0) {
+    g_pipeline_first = value < 0 ? 0 : int(value);
     return BF_OK;
   }
   if (name && std::strcmp(name, "qr_global") == 0) {

@@ -78,6 +78,51 @@ def test_npd_reports_global_index_and_stops(cuda):
     assert digest(v.storage.cpu().numpy()) == digest(st)  # same partial state as the reference stops in
 
 
+@pytest.mark.parametrize("pipeline", [2, 4, 15])
+@pytest.mark.parametrize("tree", TREES[:2])
+def test_pipelined_first_step_bitwise_vs_oracle(cuda, tree, pipeline):
+    from paper_2604_07311_b200.engine import _lib
+
+    lib = _lib.lib()
+    a0 = spd_int(778, 2000)
+    assert lib.bf_set_option(b"pipeline_first", pipeline) == 0
+    try:
+        got = chol_gpu(a0, tree)
+    finally:
+        lib.bf_set_option(b"pipeline_first", 0)
+    assert digest(got) == digest(chol_oracle(a0, tree))
+
+
+@pytest.mark.parametrize("npd_at", [100, 700, 1300])
+@pytest.mark.parametrize("pipeline", [4, 0, 15, 2])
+def test_lookahead_pipelined_first_step_npd_partial_state(cuda, npd_at, pipeline):
+    """The row-chunked first step (panel TRSM chunks on the panel stream, the
+    chunk's block-column and rest updates on two more streams) stops in the
+    reference's partial state for a failure in step 0's diagonal block, in
+    panel 1, and later."""
+    import json
+
+    from paper_2604_07311_b200.engine import _lib
+
+    n = 2000
+    a0 = spd_int(31, n)
+    a0[npd_at, npd_at] = -1e9
+    lib = _lib.lib()
+    assert lib.bf_set_option(b"pipeline_first", pipeline) == 0
+    try:
+        v = make_view(n, n, fill=a0)
+        with pytest.raises(bf.errors.NotPositiveDefiniteError) as e:
+            bf.cholesky(v, tree=parse_tree(TREES[1]))
+    finally:
+        lib.bf_set_option(b"pipeline_first", 0)
+    assert e.value.index == npd_at
+    st = a0.reshape(-1).copy()
+    bad = O.cholesky(st, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1},
+                     O.levels_from_tree(json.loads(TREES[1]), n, "f64"), nthreads=O.host_threads())
+    assert bad == npd_at
+    assert digest(v.storage.cpu().numpy()) == digest(st)
+
+
 @pytest.mark.parametrize("leaf_blocked", [1, 0])
 @pytest.mark.parametrize("dt,npd_at", [("f64", None), ("f64", 77), ("f64", 100), ("f32", None), ("f32", 45)])
 def test_leaf_kernels_bitwise_and_partial_state(cuda, leaf_blocked, dt, npd_at):

@@ -40,7 +40,7 @@ struct LtArgs {
   T* t;
   T* mvec;          // unblocked: length n
   T* wvec;
-  double* part_v;   // >= 32
+  double* part_v;   // >= gridDim.x
   int64_t* part_i;
 };
 
@@ -49,6 +49,8 @@ __global__ void __launch_bounds__(LT_THREADS) ltlt_kernel(LtArgs<T> A) {
   cg::grid_group grid = cg::this_grid();
   const int G = gridDim.x, tid = threadIdx.x, cta = blockIdx.x;
   const int64_t gt = int64_t(cta) * LT_THREADS + tid, GT = int64_t(G) * LT_THREADS;
+  const int lane = tid & 31;
+  const int64_t gw = gt >> 5, GW = GT >> 5;  // global warp index / count
   const int64_t n = A.n;
   auto X = [&](int64_t i, int64_t j) -> T& { return A.x[A.off + i * A.rs + j * A.cs]; };
   auto W = [&](int64_t i, int64_t q) -> T& { return A.w[i * A.wld + q]; };
@@ -97,9 +99,13 @@ __global__ void __launch_bounds__(LT_THREADS) ltlt_kernel(LtArgs<T> A) {
     if (tid < 32) {
       double cv = -1.0;
       int64_t ci = -1;
-      if (tid < G) {
-        ci = A.part_i[tid];
-        cv = A.part_v[tid];
+      for (int q = tid; q < G; q += 32) {  // ties resolve by index: any scan order gives the first maximum
+        const int64_t oi = __ldcg(A.part_i + q);
+        const double ov = __ldcg(A.part_v + q);
+        if (oi >= 0 && (ov > cv || (ov == cv && (ci < 0 || oi < ci)))) {
+          cv = ov;
+          ci = oi;
+        }
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) {
@@ -148,13 +154,19 @@ __global__ void __launch_bounds__(LT_THREADS) ltlt_kernel(LtArgs<T> A) {
     const int64_t h = j - A.k;
     if (A.blocked && h > 0 && j + 2 <= n - 1) {
       // bring column j+1 current: += x(i, k:j) . w(j+1, :h) ; -= w(i, :h) . x(j+1, k:j)
-      for (int64_t i = j + 2 + gt; i < n; i += GT) {
+      // (BLAS products in the reference: to rounding); one warp per row, lanes along the row
+      for (int64_t i = j + 2 + gw; i < n; i += GW) {
         T s1 = T(0), s2 = T(0);
-        for (int64_t q = 0; q < h; ++q) {
+        for (int64_t q = lane; q < h; q += 32) {
           s1 = Ops<T>::fma_(X(i, A.k + q), W(j + 1, q), s1);
           s2 = Ops<T>::fma_(W(i, q), X(j + 1, A.k + q), s2);
         }
-        X(i, j + 1) = Ops<T>::sub(Ops<T>::add(X(i, j + 1), s1), s2);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+          s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        }
+        if (lane == 0) X(i, j + 1) = Ops<T>::sub(Ops<T>::add(X(i, j + 1), s1), s2);
       }
       grid.sync();
     }
@@ -175,11 +187,13 @@ __global__ void __launch_bounds__(LT_THREADS) ltlt_kernel(LtArgs<T> A) {
       }
       if (!A.blocked && nz) {
         grid.sync();
-        // right-looking rank-2 update of the trailing lower triangle
-        for (int64_t i = j + 3 + gt; i < n; i += GT) {
-          const T mi = A.mvec[i], wi = A.wvec[i];
-          for (int64_t c = j + 2; c < i; ++c)
-            X(i, c) = Ops<T>::add(X(i, c), Ops<T>::sub(Ops<T>::mul(mi, A.wvec[c]), Ops<T>::mul(wi, A.mvec[c])));
+        // right-looking rank-2 update of the trailing lower triangle (elementwise,
+        // each element rounded like the reference's loop); one warp per row
+        for (int64_t i = j + 3 + gw; i < n; i += GW) {
+          const T mi = __ldcg(A.mvec + i), wi = __ldcg(A.wvec + i);
+          for (int64_t c = j + 2 + lane; c < i; c += 32)
+            X(i, c) = Ops<T>::add(X(i, c), Ops<T>::sub(Ops<T>::mul(mi, __ldcg(A.wvec + c)),
+                                                       Ops<T>::mul(wi, __ldcg(A.mvec + c))));
         }
       }
     }
@@ -199,15 +213,16 @@ int launch_ltlt(int is_f64, void* x, int64_t off, int64_t rs, int64_t cs, int64_
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return -3;
   if (!pv[dev]) {
-    if (cudaMalloc(&pv[dev], 64 * sizeof(double)) != cudaSuccess) return -12;
-    if (cudaMalloc(&pi[dev], 64 * sizeof(int64_t)) != cudaSuccess) return -12;
+    if (cudaMalloc(&pv[dev], 256 * sizeof(double)) != cudaSuccess) return -12;
+    if (cudaMalloc(&pi[dev], 256 * sizeof(int64_t)) != cudaSuccess) return -12;
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int G = int((n * n / 2 + 65535) / 65536);  // ~64K trailing elements per CTA
+  // one warp per trailing row at most ~2 rows per warp: up to one CTA per SM
+  int G = int((n + 15) / 16);
   if (G < 1) G = 1;
-  if (G > 32) G = 32;
   if (G > sms) G = sms;
+  if (G > 256) G = 256;
   note_launch();
   cudaError_t e;
   if (is_f64) {

@@ -530,26 +530,65 @@ int apply_pivots_impl(Mode mode, const bf_view& a, const int64_t* piv, int64_t c
 
 // device scratch for the LU's k-major copies (grows; one LU at a time per
 // device — the walk is single-stream)
-double* lu_scratch(size_t elems) {
-  static double* buf[64] = {};
-  static size_t cap[64] = {};
+// one buffer per device and stream role: the lookahead's panel stream runs
+// child-level GEMMs concurrently with the main stream's trailing update
+double* lu_scratch(size_t elems, cudaStream_t s) {
+  static double* buf[64][2] = {};
+  static size_t cap[64][2] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return nullptr;
-  if (cap[dev] < elems) {
-    if (buf[dev]) {
+  const int slot = s != nullptr && s == panel_stream() ? 1 : 0;
+  if (cap[dev][slot] < elems) {
+    if (buf[dev][slot]) {
       cudaDeviceSynchronize();
-      cudaFree(buf[dev]);
+      cudaFree(buf[dev][slot]);
     }
-    buf[dev] = nullptr;
-    cap[dev] = 0;
-    if (cudaMalloc(&buf[dev], elems * sizeof(double)) != cudaSuccess) return nullptr;
-    cap[dev] = elems;
+    buf[dev][slot] = nullptr;
+    cap[dev][slot] = 0;
+    if (cudaMalloc(&buf[dev][slot], elems * sizeof(double)) != cudaSuccess) return nullptr;
+    cap[dev][slot] = elems;
   }
-  return buf[dev];
+  return buf[dev][slot];
 }
 
 // levels: variant 20 = blocked, 21 = unblocked leaf (flatten of the lu tree)
+// a22 -= a21 * a12 for the columns [c0, c0 + nc) of a12 / a22 (k-major copy of
+// a12's part for the TMA kernel when it pays; same values, same kc chains)
+static int lu_update(Mode mode, const bf_view& a21, const bf_view& a12, const bf_view& a22, int64_t c0, int64_t nc,
+                     int64_t kc, cudaStream_t s) {
+  if (nc <= 0 || a21.m == 0) return BF_OK;
+  const bf_view b12 = subview(a12, 0, a12.m, c0, nc);
+  bf_view bop = b12;
+  const int64_t b = a12.m;
+  if (mode == MODE_D && b12.rs != 1 && int64_t(b) * nc >= (int64_t(1) << 16) && (b % 16 == 0)) {
+    double* scratch = lu_scratch(size_t(b) * size_t(nc), s);
+    if (scratch && !bf::launch_transpose(1, b12.base, b12.off, b12.rs, b12.cs, b, nc, scratch, b, s)) {
+      bf_view t{};
+      t.base = scratch;
+      t.off = 0;
+      t.m = nc;
+      t.n = b;
+      t.rs = b;
+      t.cs = 1;
+      bop = transposed(t);
+    }
+  }
+  return gemm_impl(mode, -1.0, a21, bop, 1.0, subview(a22, 0, a22.m, c0, nc), 0, kc, nullptr, s);
+}
+
+// swaps of panel k to the left and right parts, global pivot offsets, and
+// the TRSM of the block row (factor/lu.py:80-99)
+static int lu_after_panel(Mode mode, const bf_view& a, int64_t k, int64_t b, int64_t* piv, int64_t kc,
+                          cudaStream_t s) {
+  const int64_t m = a.m, n = a.n;
+  int rc = apply_pivots_impl(mode, subview(a, k, m - k, 0, k), piv + k, b, 0, 0, s);
+  if (!rc) rc = apply_pivots_impl(mode, subview(a, k, m - k, k + b, n - k - b), piv + k, b, 0, 0, s);
+  if (!rc && bf::launch_add_offset(piv + k, b, k, s)) rc = fail(BF_ERR_CUDA, "pivot offset launch failed");
+  if (!rc && k + b < n) rc = trsm_left_rec(mode, 1.0, subview(a, k, b, k, b), subview(a, k, b, k + b, n - k - b), kc, s);
+  return rc;
+}
+
 int lu_run(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int idx, int64_t* piv, int64_t base,
            int* d_sing, cudaStream_t s) {
   const int64_t m = a.m, n = a.n, steps = m < n ? m : n;
@@ -564,40 +603,55 @@ int lu_run(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int idx
   for (int64_t k = 0; k < steps; k += bs) {
     const int64_t b = bs < steps - k ? bs : steps - k;
     int rc = lu_run(mode, subview(a, k, m - k, k, b), lv, nl, idx + 1, piv + k, base + k, d_sing, s);
+    if (!rc) rc = lu_after_panel(mode, a, k, b, piv, kc, s);
+    if (!rc && k + b < n && k + b < m)
+      rc = lu_update(mode, subview(a, k + b, m - k - b, k, b), subview(a, k, b, k + b, n - k - b),
+                     subview(a, k + b, m - k - b, k + b, n - k - b), 0, n - k - b, kc, s);
     if (rc) return rc;
-    rc = apply_pivots_impl(mode, subview(a, k, m - k, 0, k), piv + k, b, 0, 0, s);
-    if (!rc) rc = apply_pivots_impl(mode, subview(a, k, m - k, k + b, n - k - b), piv + k, b, 0, 0, s);
-    if (!rc && bf::launch_add_offset(piv + k, b, k, s)) rc = fail(BF_ERR_CUDA, "pivot offset launch failed");
-    if (rc) return rc;
-    if (k + b < n) {
-      const bf_view a12 = subview(a, k, b, k + b, n - k - b);
-      rc = trsm_left_rec(mode, 1.0, subview(a, k, b, k, b), a12, kc, s);
-      if (!rc && k + b < m) {
-        // The trailing GEMM's B operand (a12, b x N) is mn-major in a row-major
-        // matrix; a k-major copy of it puts the update on the TMA kernel.
-        // Same values, same kc chains: same bits.
-        bf_view bop = a12;
-        const int64_t N = n - k - b;
-        if (mode == MODE_D && a12.rs != 1 && int64_t(b) * N >= (int64_t(1) << 16) && (b % 16 == 0)) {
-          double* scratch = lu_scratch(size_t(b) * size_t(N));
-          if (scratch && !bf::launch_transpose(1, a12.base, a12.off, a12.rs, a12.cs, b, N, scratch, b, s)) {
-            bf_view t{};
-            t.base = scratch;
-            t.off = 0;
-            t.m = N;
-            t.n = b;
-            t.rs = b;
-            t.cs = 1;
-            bop = transposed(t);
-          }
-        }
-        rc = gemm_impl(mode, -1.0, subview(a, k + b, m - k - b, k, b), bop, 1.0,
-                       subview(a, k + b, m - k - b, k + b, n - k - b), 0, kc, nullptr, s);
-      }
-      if (rc) return rc;
-    }
   }
   return BF_OK;
+}
+
+// Top-level blocked LU with depth-1 lookahead: per step the next block
+// column's share of the trailing GEMM runs first, then panel k+1 (its own
+// columns only) factors on the high-priority panel stream while the main
+// stream applies the rest of step k's update; panel k+1's row swaps touch
+// the other columns only after that join.  Same operations per element as
+// lu_run (a column split of one GEMM): bitwise the same factor.
+int lu_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int64_t* piv, int* d_sing,
+                 cudaStream_t s) {
+  const int64_t m = a.m, n = a.n, steps = m < n ? m : n;
+  const int64_t bs = lv[0].bs, kc = lv[0].kc;
+  cudaStream_t ps = panel_stream();
+  if (!ps) return fail(BF_ERR_CUDA, "cannot create the panel stream");
+  cudaEvent_t ev_main, ev_panel;
+  cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming);
+  int rc = lu_run(mode, subview(a, 0, m, 0, bs < steps ? bs : steps), lv, nl, 1, piv, 0, d_sing, s);
+  for (int64_t k = 0; k < steps && !rc; k += bs) {
+    const int64_t b = bs < steps - k ? bs : steps - k;
+    rc = lu_after_panel(mode, a, k, b, piv, kc, s);
+    if (rc) break;
+    const int64_t k1 = k + b;
+    if (k1 >= n || k1 >= m) {
+      if (k1 < steps) rc = fail(BF_ERR_VALUE, "lu lookahead: bad step");
+      break;
+    }
+    const bf_view a21 = subview(a, k1, m - k1, k, b), a12 = subview(a, k, b, k1, n - k1),
+                  a22 = subview(a, k1, m - k1, k1, n - k1);
+    const int64_t b2 = k1 < steps ? (bs < steps - k1 ? bs : steps - k1) : 0;
+    rc = lu_update(mode, a21, a12, a22, 0, b2 > 0 ? b2 : n - k1, kc, s);
+    if (rc || b2 == 0) break;
+    cudaEventRecord(ev_main, s);
+    cudaStreamWaitEvent(ps, ev_main, 0);
+    rc = lu_run(mode, subview(a, k1, m - k1, k1, b2), lv, nl, 1, piv + k1, k1, d_sing, ps);
+    cudaEventRecord(ev_panel, ps);
+    if (!rc) rc = lu_update(mode, a21, a12, a22, b2, n - k1 - b2, kc, s);
+    cudaStreamWaitEvent(s, ev_panel, 0);
+  }
+  cudaEventDestroy(ev_main);
+  cudaEventDestroy(ev_panel);
+  return rc;
 }
 
 int chol_impl(Mode mode, const bf_view* a, const bf_chol_level* lv, int nl, int* d_info, cudaStream_t s) {
@@ -835,10 +889,16 @@ int bf_cholesky_host_d(double* host, int64_t ld, const bf_view* work, const bf_c
 }
 int bf_lu_d(const bf_view* a, const bf_chol_level* levels, int nlevels, int64_t* d_piv, int* d_sing, void* stream) {
   if (!a || !levels || nlevels < 1 || !d_piv || !d_sing) return fail(BF_ERR_VALUE, "null argument");
+  if (g_lookahead && nlevels >= 1 && levels[0].variant == 20 && levels[0].bs >= 1 &&
+      (a->m < a->n ? a->m : a->n) > 2 * levels[0].bs)
+    return lu_lookahead(MODE_D, *a, levels, nlevels, d_piv, d_sing, S(stream));
   return lu_run(MODE_D, *a, levels, nlevels, 0, d_piv, 0, d_sing, S(stream));
 }
 int bf_lu_s(const bf_view* a, const bf_chol_level* levels, int nlevels, int64_t* d_piv, int* d_sing, void* stream) {
   if (!a || !levels || nlevels < 1 || !d_piv || !d_sing) return fail(BF_ERR_VALUE, "null argument");
+  if (g_lookahead && nlevels >= 1 && levels[0].variant == 20 && levels[0].bs >= 1 &&
+      (a->m < a->n ? a->m : a->n) > 2 * levels[0].bs)
+    return lu_lookahead(MODE_S, *a, levels, nlevels, d_piv, d_sing, S(stream));
   return lu_run(MODE_S, *a, levels, nlevels, 0, d_piv, 0, d_sing, S(stream));
 }
 int bf_trsm_llnu_d(double alpha, const bf_view* tri, const bf_view* b, int64_t kc, void* stream) {

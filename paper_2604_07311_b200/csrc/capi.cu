@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 namespace bf {
@@ -1030,36 +1031,54 @@ static int gemm_splitk_impl(Mode mode, double alpha, const bf_view& a, const bf_
   if (S > SMAX) S = SMAX;
   if (S > k / 512) S = k / 512;
   if (S <= 1 || m == 0 || n == 0) return gemm_impl(mode, alpha, a, b, beta, c, 0, int64_t(1) << 40, nullptr, s);
-  static cudaStream_t side[64][SMAX] = {};
-  static cudaEvent_t ev[64][SMAX + 1] = {};
-  static void* ws[64] = {};
-  static size_t ws_bytes[64] = {};
-  if (!side[dev][0]) {
-    for (int i = 0; i < SMAX; ++i) {
-      cudaStreamCreateWithFlags(&side[dev][i], cudaStreamNonBlocking);
-      cudaEventCreateWithFlags(&ev[dev][i], cudaEventDisableTiming);
+  // side streams, events and workspace per (device, calling stream): QR's
+  // lookahead issues split-K products from two streams at once
+  struct Ctx {
+    int dev;
+    cudaStream_t owner;
+    cudaStream_t side[SMAX];
+    cudaEvent_t ev[SMAX + 1];
+    void* ws;
+    size_t bytes;
+  };
+  static std::vector<Ctx*> ctxs;
+  static std::mutex mu;
+  Ctx* cx = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (Ctx* c : ctxs)
+      if (c->dev == dev && c->owner == s) cx = c;
+    if (!cx) {
+      cx = new Ctx{};
+      cx->dev = dev;
+      cx->owner = s;
+      for (int i = 0; i < SMAX; ++i) {
+        cudaStreamCreateWithFlags(&cx->side[i], cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&cx->ev[i], cudaEventDisableTiming);
+      }
+      cudaEventCreateWithFlags(&cx->ev[SMAX], cudaEventDisableTiming);
+      ctxs.push_back(cx);
     }
-    cudaEventCreateWithFlags(&ev[dev][SMAX], cudaEventDisableTiming);
   }
   const size_t need = size_t(S) * size_t(m) * size_t(n) * size_t(elem_bytes(mode));
-  if (need > ws_bytes[dev]) {
-    if (ws[dev]) {
+  if (need > cx->bytes) {
+    if (cx->ws) {
       cudaStreamSynchronize(s);
-      cudaFree(ws[dev]);
+      cudaFree(cx->ws);
     }
-    ws[dev] = nullptr;
-    ws_bytes[dev] = 0;
-    if (cudaMalloc(&ws[dev], need) != cudaSuccess) return fail(BF_ERR_CUDA, "split-K workspace");
-    ws_bytes[dev] = need;
+    cx->ws = nullptr;
+    cx->bytes = 0;
+    if (cudaMalloc(&cx->ws, need) != cudaSuccess) return fail(BF_ERR_CUDA, "split-K workspace");
+    cx->bytes = need;
   }
-  cudaEventRecord(ev[dev][SMAX], s);
+  cudaEventRecord(cx->ev[SMAX], s);
   const int64_t slice = (k + S - 1) / S;
   for (int64_t q = 0; q < S; ++q) {
     const int64_t k0 = q * slice, kn = k0 + slice < k ? slice : k - k0;
-    cudaStream_t sq = side[dev][q];
-    cudaStreamWaitEvent(sq, ev[dev][SMAX], 0);
+    cudaStream_t sq = cx->side[q];
+    cudaStreamWaitEvent(sq, cx->ev[SMAX], 0);
     bf_view w{};
-    w.base = ws[dev];
+    w.base = cx->ws;
     w.off = q * m * n;
     w.m = m;
     w.n = n;
@@ -1068,15 +1087,15 @@ static int gemm_splitk_impl(Mode mode, double alpha, const bf_view& a, const bf_
     int rc = gemm_impl(mode, 1.0, subview(a, 0, m, k0, kn), subview(b, k0, kn, 0, n), 0.0, w, 0, int64_t(1) << 40,
                        nullptr, sq);
     if (rc) return rc;
-    cudaEventRecord(ev[dev][q], sq);
-    cudaStreamWaitEvent(s, ev[dev][q], 0);
+    cudaEventRecord(cx->ev[q], sq);
+    cudaStreamWaitEvent(s, cx->ev[q], 0);
   }
   double al = alpha, be = beta;
   if (mode == MODE_S) {
     al = double(float(alpha));
     be = double(float(beta));
   }
-  int rc = bf::launch_splitk_reduce(storage_is_f64(mode), ws[dev], int(S), m, n, al, be, c.base, c.off, c.rs, c.cs, s);
+  int rc = bf::launch_splitk_reduce(storage_is_f64(mode), cx->ws, int(S), m, n, al, be, c.base, c.off, c.rs, c.cs, s);
   return rc ? fail(BF_ERR_CUDA, "split-K reduce launch failed") : BF_OK;
 }
 int bf_gemm_splitk_d(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c, void* stream) {

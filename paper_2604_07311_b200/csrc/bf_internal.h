@@ -80,6 +80,7 @@ extern int g_trsm_warp;       // fused TRSM subtree: 4-warps-per-32-rows kernel 
 extern int g_leaf_blocked;    // variant-3 leaves n <= 128: blocked lane-per-row kernel (1) or v3 (0)
 extern int g_lu_grid_max;     // LU leaf: cap on the cooperative grid (0 = SM-derived)
 extern int g_lu_global;       // LU leaf: force the global-memory kernel
+extern int g_lu_noprefetch;   // LU leaf: no candidate-row prefetch
 extern int g_qr_global;       // QR panel: force the global-memory sweep
 int launch_gemm_simt_f32(const GemmParams& p, cudaStream_t s);        // f32 storage, f32 acc
 int launch_gemm_simt_f32acc64(const GemmParams& p, cudaStream_t s);   // f32 storage, f64 acc

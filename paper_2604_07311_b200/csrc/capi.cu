@@ -748,6 +748,10 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_qr_global = value != 0;
     return BF_OK;
   }
+  if (name && std::strcmp(name, "lu_noprefetch") == 0) {
+    bf::g_lu_noprefetch = value != 0;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "lu_global") == 0) {
     bf::g_lu_global = value != 0;
     return BF_OK;

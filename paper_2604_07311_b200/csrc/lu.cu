@@ -27,6 +27,7 @@ namespace bf {
 
 int g_lu_grid_max = 0;  // bf_set_option("lu_grid", g): cap the leaf's cooperative grid (0 = SM-derived)
 int g_lu_global = 0;    // bf_set_option("lu_global", 1): force the global-memory leaf
+int g_lu_noprefetch = 0;  // bf_set_option("lu_noprefetch", 1): fetch the pivot row after the decision
 
 namespace {
 
@@ -178,7 +179,7 @@ template <typename T>
 __global__ void __launch_bounds__(LU_THREADS) lu_leaf_smem_kernel(T* a, int64_t off, int64_t rs, int64_t cs,
                                                                 int64_t m, int64_t n, int64_t* piv, int* d_sing,
                                                                 int64_t base, double* part_v, int64_t* part_i,
-                                                                T* cand_rows, T* rowk_buf) {
+                                                                T* cand_rows, T* rowk_buf, int pre) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char lu_smem[];
   T* S = reinterpret_cast<T*>(lu_smem);
@@ -188,6 +189,10 @@ __global__ void __launch_bounds__(LU_THREADS) lu_leaf_smem_kernel(T* a, int64_t 
   const int64_t r0 = int64_t(cta) * chunk, r1 = r0 + chunk < m ? r0 + chunk : m;
   const int64_t rows = r1 > r0 ? r1 - r0 : 0;
   T* newk = S + chunk * ld;  // the pivot row's values for this column
+  // pre: every band's candidate row and row k are fetched together with the
+  // partial maxima (one L2 round trip after the barrier instead of two)
+  T* cand_s = newk + ld;     // G x n (pre only)
+  T* rk_s = cand_s + int64_t(G) * n;
   const int64_t steps = m < n ? m : n;
   __shared__ double red_v[LU_THREADS / 32];
   __shared__ int64_t red_i[LU_THREADS / 32];
@@ -247,6 +252,11 @@ __global__ void __launch_bounds__(LU_THREADS) lu_leaf_smem_kernel(T* a, int64_t 
     if (k >= r0 && k < r1)
       for (int64_t j = tid; j < n; j += LU_THREADS) rk[j] = S[(k - r0) * ld + j];
     grid.sync();
+    if (pre) {
+      for (int64_t e = tid; e < int64_t(G) * n; e += LU_THREADS) cand_s[e] = __ldcg(cand + e);
+      for (int64_t j = tid; j < n; j += LU_THREADS) rk_s[j] = __ldcg(rk + j);
+      __syncthreads();
+    }
     // decide: bands in row order from the diagonal entry (one warp, G <= 32)
     if (tid < 32) {
       double cv = -1.0;
@@ -269,7 +279,7 @@ __global__ void __launch_bounds__(LU_THREADS) lu_leaf_smem_kernel(T* a, int64_t 
         }
       }
       if (tid == 0) {
-        const double dkk = double(fabs(__ldcg(rk + k)));
+        const double dkk = double(fabs(pre ? rk_s[k] : __ldcg(rk + k)));
         const bool take = ci >= 0 && cv > dkk;
         s_best = take ? cv : dkk;
         s_p = take ? ci : k;
@@ -287,11 +297,12 @@ __global__ void __launch_bounds__(LU_THREADS) lu_leaf_smem_kernel(T* a, int64_t 
     if (live) {
       // the pivot row (new row k) into shared memory; the swap where it lands
       for (int64_t j = tid; j < n; j += LU_THREADS) {
-        const T nk = src >= 0 ? __ldcg(cand + int64_t(src) * n + j) : __ldcg(rk + j);
+        const T nk = pre ? (src >= 0 ? cand_s[int64_t(src) * n + j] : rk_s[j])
+                         : (src >= 0 ? __ldcg(cand + int64_t(src) * n + j) : __ldcg(rk + j));
         newk[j] = nk;
         if (p != k) {
           if (k >= r0 && k < r1) S[(k - r0) * ld + j] = nk;
-          if (p >= r0 && p < r1) S[(p - r0) * ld + j] = __ldcg(rk + j);
+          if (p >= r0 && p < r1) S[(p - r0) * ld + j] = pre ? rk_s[j] : __ldcg(rk + j);
         }
       }
       __syncthreads();
@@ -475,7 +486,8 @@ int launch_lu_leaf(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int
     if (Gs < want) Gs = want;
     if (Gs > 32) Gs = 32;
     const int64_t chunk = (m + Gs - 1) / Gs;
-    const size_t smem = size_t(chunk + 1) * size_t(n + 1) * esz;
+    int pre = n <= 128 && !g_lu_noprefetch;
+    const size_t smem = size_t(chunk + 1) * size_t(n + 1) * esz + (pre ? size_t(Gs + 1) * size_t(n) * esz : 0);
     static void* cand_buf[64] = {};
     static size_t cand_cap[64] = {};
     const size_t need = size_t(2) * 33 * size_t(n) * esz;
@@ -497,7 +509,7 @@ int launch_lu_leaf(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int
         double* ad = static_cast<double*>(a);
         double* cd = static_cast<double*>(cand);
         double* rd = static_cast<double*>(rowk);
-        void* args[] = {&ad, &off, &rs, &cs, &m, &n, &piv, &d_sing, &base, &pv, &pi, &cd, &rd};
+        void* args[] = {&ad, &off, &rs, &cs, &m, &n, &piv, &d_sing, &base, &pv, &pi, &cd, &rd, &pre};
         e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lu_leaf_smem_kernel<double>), dim3(Gi),
                                         dim3(LU_THREADS), args, smem, s);
       } else {
@@ -509,7 +521,7 @@ int launch_lu_leaf(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int
         float* af = static_cast<float*>(a);
         float* cf = static_cast<float*>(cand);
         float* rf = static_cast<float*>(rowk);
-        void* args[] = {&af, &off, &rs, &cs, &m, &n, &piv, &d_sing, &base, &pv, &pi, &cf, &rf};
+        void* args[] = {&af, &off, &rs, &cs, &m, &n, &piv, &d_sing, &base, &pv, &pi, &cf, &rf, &pre};
         e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lu_leaf_smem_kernel<float>), dim3(Gi),
                                         dim3(LU_THREADS), args, smem, s);
       }

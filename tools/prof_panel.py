@@ -42,9 +42,11 @@ def t(fn, reps=3):
 
 a = a0.clone()
 out = {"bs": bs}
-out["diag_factor_ms"] = t(lambda: (a.copy_(a0), lib.bf_cholesky_ex_d(  # leaves `a` factored for the TRSMsctypes.byref(_lib.as_bfview(from_torch(a))), arr,
+# (leaves `a` factored for the TRSMs)
+out["diag_factor_ms"] = t(lambda: (a.copy_(a0), lib.bf_cholesky_ex_d(ctypes.byref(_lib.as_bfview(from_torch(a))), arr,
                                                                      len(levels), 0, info.data_ptr(), s)))
-for mm in (30720, 16384, 8192, 2048):
+assert int(info.item()) == -1
+for mm in [int(x) for x in (sys.argv[2].split(',') if len(sys.argv) > 2 else ('30720', '16384', '8192', '2048'))]:
     b0 = torch.rand(mm, bs, dtype=torch.float64, device="cuda", generator=g)
     b = b0.clone()
     out[f"trsm_{mm}_ms"] = t(lambda: (b.copy_(b0), lib.bf_trsm_rltn_ex_d(1.0, ctypes.byref(_lib.as_bfview(from_torch(a))),

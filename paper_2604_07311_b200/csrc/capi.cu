@@ -34,6 +34,9 @@ int g_fused_trsm = 1;     // bf_set_option("fused_trsm", 0) keeps every recursio
 // faster at n=32768 (the chunked TRSM competes with the SYRK for the same
 // SMs), so off by default.
 int g_pipeline_first = 0;
+// bf_set_option("overlap_h2d", 0): bf_cholesky_host_d loads the whole lower
+// triangle before factoring instead of overlapping the load with step 0
+int g_overlap_h2d = 1;
 
 int fail(int code, const char* msg) {
   g_last_error = msg;
@@ -273,6 +276,16 @@ cudaStream_t aux_stream() {
   return streams[dev];
 }
 
+// Host-to-device stream per device (the overlapped load of bf_cholesky_host_d).
+cudaStream_t h2d_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+  return streams[dev];
+}
+
 // Copy stream per device (host <-> device traffic of bf_cholesky_host_d).
 cudaStream_t copy_stream() {
   static cudaStream_t streams[64] = {};
@@ -293,6 +306,22 @@ struct HostWriteback {
   int64_t copied_upto = 0;  // columns [0, copied_upto) already queued
 };
 thread_local HostWriteback* g_wb = nullptr;
+
+// Host load of bf_cholesky_host_d: while set, block column j of the lower
+// triangle (columns [j*bs, (j+1)*bs), rows >= j*bs) is on the device once
+// ev[j] has fired; step 0 of the lookahead driver waits per block column, so
+// the host->device copy overlaps the first panel and step 0's update.
+struct HostLoad {
+  int64_t bs = 0;
+  std::vector<cudaEvent_t> ev;
+};
+thread_local HostLoad* g_h2d = nullptr;
+
+void wait_column(cudaStream_t st, int64_t c0) {
+  if (!g_h2d || g_h2d->bs <= 0) return;
+  const size_t j = size_t(c0 / g_h2d->bs);
+  if (j < g_h2d->ev.size()) cudaStreamWaitEvent(st, g_h2d->ev[j], 0);
+}
 
 void writeback_block_column(const bf_view& a, int64_t c0, int64_t w, cudaStream_t after) {
   if (!g_wb || w <= 0) return;
@@ -439,6 +468,7 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     cudaEventDestroy(ev_rest);
     start = r2;
   } else {
+    wait_column(s, 0);
     rc = panel(0, bs < n ? bs : n, s);
     if (rc == BF_OK) writeback_block_column(a, 0, bs < n ? bs : n, s);
   }
@@ -451,6 +481,8 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     bf_view l21_top = subview(l21, 0, b2, 0, b);
     bf_view l21_rest = subview(l21, b2, nr2 - b2, 0, b);
     // (1) next block column, on the main stream
+    const bool loading = g_h2d && done == 0;  // step 0 of a host factorization: columns still arriving
+    if (loading) wait_column(s, r2);
     rc = gemm_impl(mode, -1.0, l21_top, transposed(l21_top), 1.0, subview(a, r2, b2, r2, b2), 1, kc, d_info, s);
     if (!rc && nr2 > b2)
       rc = gemm_impl(mode, -1.0, l21_rest, transposed(l21_top), 1.0, subview(a, r2 + b2, nr2 - b2, r2, b2), 0, kc,
@@ -470,9 +502,24 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     // (3) the rest of the trailing update, concurrently with (2).  It belongs
     // to step k, so a pivot failure inside panel k+1 (index >= base+r2) must
     // not cancel it: the reference finishes step k before it meets that pivot.
-    if (nr2 > b2)
+    if (nr2 > b2 && loading) {
+      // block column by block column as each arrives: the same GEMMT split by
+      // columns (diagonal block lower-only, the rows below it full)
+      for (int64_t c0 = r2 + b2; c0 < n && !rc; c0 += bs) {
+        const int64_t w = bs < n - c0 ? bs : n - c0;
+        wait_column(s, c0);
+        bf_view lc = subview(a, c0, w, done, b);
+        rc = gemm_impl(mode, -1.0, lc, transposed(lc), 1.0, subview(a, c0, w, c0, w), 1, kc, d_info, s, base + r2);
+        if (!rc && c0 + w < n) {
+          bf_view lb = subview(a, c0 + w, n - c0 - w, done, b);
+          rc = gemm_impl(mode, -1.0, lb, transposed(lc), 1.0, subview(a, c0 + w, n - c0 - w, c0, w), 0, kc, d_info,
+                         s, base + r2);
+        }
+      }
+    } else if (nr2 > b2) {
       rc = gemm_impl(mode, -1.0, l21_rest, transposed(l21_rest), 1.0, subview(a, r2 + b2, nr2 - b2, r2 + b2, nr2 - b2),
                      1, kc, d_info, s, base + r2);
+    }
     if (g_timeline) {
       ts.main_rest = mark(s);
       g_tl.push_back(ts);
@@ -740,6 +787,10 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_tma_variant = int(value & 3);
     return BF_OK;
   }
+  if (name && std::strcmp(name, "overlap_h2d") == 0) {
+    g_overlap_h2d = value != 0;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "pipeline_first") == 0) {
     g_pipeline_first = value < 0 ? 0 : int(value);
     return BF_OK;
@@ -862,21 +913,52 @@ int bf_cholesky_host_d(double* host, int64_t ld, const bf_view* work, const bf_c
   cudaStream_t cs = copy_stream();
   if (!cs) return fail(BF_ERR_CUDA, "cannot create the copy stream");
   double* dev = static_cast<double*>(work->base) + work->off;
-  // lower triangle in, by block columns of the root bs (rows >= the column's first)
+  // lower triangle in, by block columns of the root bs (rows >= the column's
+  // first).  With the lookahead driver the copies run on their own stream and
+  // step 0 consumes each block column as it lands; otherwise in stream order.
   const int64_t bs = levels[0].bs >= 1 ? levels[0].bs : n;
+  const bool overlap = g_lookahead && g_overlap_h2d && levels[0].variant == 3 && n > 2 * bs && !g_pipeline_first;
+  cudaStream_t hs = overlap ? h2d_stream() : s;
+  if (overlap && !hs) return fail(BF_ERR_CUDA, "cannot create the h2d stream");
+  HostLoad hl;
+  hl.bs = bs;
+  if (overlap) {
+    cudaEvent_t start;
+    cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+    cudaEventRecord(start, s);  // the work buffer is free once the caller's prior work is done
+    cudaStreamWaitEvent(hs, start, 0);
+    cudaEventDestroy(start);
+  }
   for (int64_t c0 = 0; c0 < n; c0 += bs) {
     const int64_t w = bs < n - c0 ? bs : n - c0;
     if (cudaMemcpy2DAsync(dev + c0 * work->rs + c0, size_t(work->rs) * 8, host + c0 * ld + c0, size_t(ld) * 8,
-                          size_t(w) * 8, size_t(n - c0), cudaMemcpyHostToDevice, s) != cudaSuccess)
+                          size_t(w) * 8, size_t(n - c0), cudaMemcpyHostToDevice, hs) != cudaSuccess)
       return fail(BF_ERR_CUDA, "host to device copy failed");
+    if (overlap) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      cudaEventRecord(e, hs);
+      hl.ev.push_back(e);
+    }
   }
   HostWriteback wb;
   wb.host = host;
   wb.ld = ld;
   wb.cs = cs;
   g_wb = &wb;
+  g_h2d = overlap ? &hl : nullptr;
   int rc = chol_impl(MODE_D, work, levels, nlevels, d_info, s);
   g_wb = nullptr;
+  g_h2d = nullptr;
+  if (overlap) {
+    // every copy is complete before the caller's stream moves on
+    cudaEvent_t done;
+    cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+    cudaEventRecord(done, hs);
+    cudaStreamWaitEvent(s, done, 0);
+    cudaEventDestroy(done);
+    for (auto e : hl.ev) cudaEventDestroy(e);
+  }
   if (rc) return rc;
   // whatever the lookahead did not stream back (the non-lookahead path, or all of it)
   for (int64_t c0 = wb.copied_upto; c0 < n; c0 += bs) {

@@ -307,15 +307,18 @@ def test_cholesky_host_streams_back_same_bits(cuda, n, uplo):
     assert other(got, 1 if uplo == "lower" else -1).tobytes() == other(a0, 1 if uplo == "lower" else -1).tobytes()
 
 
-def test_cholesky_host_npd_partial_state(cuda):
+@pytest.mark.parametrize("npd_at", [2211, 100, 1100])
+def test_cholesky_host_npd_partial_state(cuda, npd_at):
+    """Failures after, inside and during the overlapped host load (step 0
+    consumes block columns as they land) leave the reference's partial state."""
     a0 = spd_int(9, 3000)
-    a0[2211, 2211] = -1e6
+    a0[npd_at, npd_at] = -1e6
     t = ('{"op":"cholesky","variant":3,"bs":512,"kernel":{"kc":512},"child":'
          '{"op":"cholesky","variant":3,"bs":128,"child":{"op":"cholesky","variant":"unblocked3"}}}')
     host = torch.from_numpy(a0.copy()).pin_memory()
     with pytest.raises(bf.errors.NotPositiveDefiniteError) as e:
         bf.cholesky_host(host, "lower", parse_tree(t))
-    assert e.value.index == 2211
+    assert e.value.index == npd_at
     v = make_view(3000, 3000, fill=a0)
     with pytest.raises(bf.errors.NotPositiveDefiniteError):
         bf.cholesky(v, tree=parse_tree(t))

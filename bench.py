@@ -13,7 +13,8 @@ flop count n^3/3 (cli.py:78-79).
              the pristine input is restored between steps outside the events.
 * e2e        the same metric through the public API from HOST memory:
              cholesky_host() on a pinned host matrix (its lower triangle goes
-             to HBM by block columns, each finished block column of the
+             to HBM by block columns on a copy stream while step 0 consumes
+             each column as it lands, each finished block column of the
              factor comes back while later steps run), all inside the timed
              region.
 * roofline   the dominant kernel (the DMMA GEMMT/SYRK of the trailing update),
@@ -520,7 +521,8 @@ def main() -> int:
         e2e = {"value": round(chol_flops(n) * world / (ems / 1e3) / 1e9, 3), "unit": "GFLOP/s",
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(ems, 3),
                "path": "paper_2604_07311_b200.cholesky_host(pinned host matrix): lower triangle to HBM by block "
-                       "columns, factor, each finished block column back to the host under the remaining steps"}
+                       "columns overlapped with step 0, factor, each finished block column back to the host under "
+                       "the remaining steps"}
         del host, pristine
 
     roof = None

@@ -81,6 +81,8 @@ extern int g_leaf_blocked;    // variant-3 leaves n <= 128: blocked lane-per-row
 extern int g_lu_grid_max;     // LU leaf: cap on the cooperative grid (0 = SM-derived)
 extern int g_lu_global;       // LU leaf: force the global-memory kernel
 extern int g_lu_noprefetch;   // LU leaf: no candidate-row prefetch
+extern int g_lu_nocluster;    // LU leaf: never the single-cluster kernel
+extern int g_lu_cluster_max;  // LU leaf: largest cluster
 extern int g_qr_global;       // QR panel: force the global-memory sweep
 int launch_gemm_simt_f32(const GemmParams& p, cudaStream_t s);        // f32 storage, f32 acc
 int launch_gemm_simt_f32acc64(const GemmParams& p, cudaStream_t s);   // f32 storage, f64 acc

@@ -799,6 +799,14 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_qr_global = value != 0;
     return BF_OK;
   }
+  if (name && std::strcmp(name, "lu_nocluster") == 0) {
+    bf::g_lu_nocluster = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "lu_cluster") == 0 && value >= 1 && value <= 16) {
+    bf::g_lu_cluster_max = int(value);
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "lu_noprefetch") == 0) {
     bf::g_lu_noprefetch = value != 0;
     return BF_OK;

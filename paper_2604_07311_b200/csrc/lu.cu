@@ -10,6 +10,9 @@
 //    the reference's order for every element (a(i,j) -= a(i,k)*a(k,j),
 //    unfused, ascending k).  An exactly-zero pivot column is recorded and
 //    skipped like the reference.
+//  * lu_leaf_cluster_kernel — the same leaf on one thread-block cluster when
+//    the panel fits in its shared memory: cluster barrier + DSMEM instead of
+//    a grid barrier + L2 (used first; the grid kernels take taller panels).
 //  * apply_pivots_kernel — LAPACK-style swap list, one thread per column,
 //    swaps in list order (factor/pivots.py:46-61).
 //  * trsm_left_base_kernel — unit-lower X = T^-1 (alpha B) for n <= 32, one
@@ -28,6 +31,8 @@ namespace bf {
 int g_lu_grid_max = 0;  // bf_set_option("lu_grid", g): cap the leaf's cooperative grid (0 = SM-derived)
 int g_lu_global = 0;    // bf_set_option("lu_global", 1): force the global-memory leaf
 int g_lu_noprefetch = 0;  // bf_set_option("lu_noprefetch", 1): fetch the pivot row after the decision
+int g_lu_nocluster = 0;   // bf_set_option("lu_nocluster", 1): never the single-cluster leaf
+int g_lu_cluster_max = 16;  // bf_set_option("lu_cluster", c): largest cluster for the leaf (1..16)
 
 namespace {
 
@@ -323,6 +328,190 @@ __global__ void __launch_bounds__(LU_THREADS) lu_leaf_smem_kernel(T* a, int64_t 
   }
 }
 
+// The same leaf on ONE thread-block cluster (<= 16 CTAs) whose bands hold the
+// whole panel in shared memory: per column every CTA publishes its band's
+// best candidate (value, row, the row itself) and, for the owner, row k in
+// its OWN shared memory (slots alternate by column parity), one cluster
+// barrier (~0.2 us instead of a grid barrier), then every CTA reads the
+// partials and the winning row straight from its peers' shared memory
+// (DSMEM).  No global traffic inside the column loop; identical arithmetic.
+__device__ __forceinline__ uint32_t dsmem_map(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double dsmem_ld_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float dsmem_ld_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ int64_t dsmem_ld_s64(uint32_t addr) {
+  int64_t v;
+  asm volatile("ld.shared::cluster.s64 %0, [%1];\n" : "=l"(v) : "r"(addr));
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T dsmem_ld(uint32_t addr);
+template <>
+__device__ __forceinline__ double dsmem_ld<double>(uint32_t addr) {
+  return dsmem_ld_f64(addr);
+}
+template <>
+__device__ __forceinline__ float dsmem_ld<float>(uint32_t addr) {
+  return dsmem_ld_f32(addr);
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(LU_THREADS) lu_leaf_cluster_kernel(T* a, int64_t off, int64_t rs, int64_t cs,
+                                                                   int64_t m, int64_t n, int64_t* piv, int* d_sing,
+                                                                   int64_t base, int chunk) {
+  extern __shared__ __align__(16) unsigned char lc_smem[];
+  const int C = gridDim.x, tid = threadIdx.x;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+  const int64_t ld = n + 1;
+  // [pub_v 2][pub_i 2] | band chunk x ld | newk n | pub_row 2 x n | rowk 2 x n
+  double* pub_v = reinterpret_cast<double*>(lc_smem);
+  int64_t* pub_i = reinterpret_cast<int64_t*>(lc_smem + 16);
+  T* S = reinterpret_cast<T*>(lc_smem + 32);
+  T* newk = S + int64_t(chunk) * ld;
+  T* pub_row = newk + n;
+  T* rowk = pub_row + 2 * n;
+  const uint32_t base_v = smem_u32(pub_v), base_i = smem_u32(pub_i), base_row = smem_u32(pub_row),
+                 base_rk = smem_u32(rowk);
+  const int64_t r0 = int64_t(rank) * chunk, r1 = r0 + chunk < m ? r0 + chunk : m;
+  const int64_t rows = r1 > r0 ? r1 - r0 : 0;
+  const int64_t steps = m < n ? m : n;
+  __shared__ double red_v[LU_THREADS / 32];
+  __shared__ int64_t red_i[LU_THREADS / 32];
+  __shared__ double s_best;
+  __shared__ int64_t s_p;
+  __shared__ int s_src;
+  for (int64_t e = tid; e < rows * n; e += LU_THREADS) {
+    const int64_t i = e / n, j = e % n;
+    S[i * ld + j] = a[off + (r0 + i) * rs + j * cs];
+  }
+  __syncthreads();
+  for (int64_t k = 0; k < steps; ++k) {
+    const int par = int(k & 1);
+    double bv = -1.0;
+    int64_t bi = -1;
+    const int64_t lo = r0 > k + 1 ? r0 : k + 1;
+    for (int64_t i = lo + tid; i < r1; i += LU_THREADS) {
+      const double v = double(fabs(S[(i - r0) * ld + k]));
+      if (v > bv) {
+        bv = v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_down_sync(0xffffffffu, bv, o);
+      const int64_t oi = __shfl_down_sync(0xffffffffu, bi, o);
+      if (oi >= 0 && (ov > bv || (ov == bv && (bi < 0 || oi < bi)))) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if ((tid & 31) == 0) {
+      red_v[tid >> 5] = bv;
+      red_i[tid >> 5] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < LU_THREADS / 32; ++w)
+        if (red_i[w] >= 0 && (red_v[w] > bv || (red_v[w] == bv && (bi < 0 || red_i[w] < bi)))) {
+          bv = red_v[w];
+          bi = red_i[w];
+        }
+      pub_v[par] = bv;
+      pub_i[par] = bi;
+      s_p = bi;
+    }
+    __syncthreads();
+    const int64_t mine = s_p;
+    if (mine >= 0)
+      for (int64_t j = tid; j < n; j += LU_THREADS) pub_row[par * n + j] = S[(mine - r0) * ld + j];
+    if (k >= r0 && k < r1)
+      for (int64_t j = tid; j < n; j += LU_THREADS) rowk[par * n + j] = S[(k - r0) * ld + j];
+    cluster_barrier();
+    const uint32_t owner_k = uint32_t(k / chunk);
+    // decide from the peers' partials, bands in rank (= row) order
+    if (tid < 32) {
+      double cv = -1.0;
+      int64_t ci = -1;
+      int cc = -1;
+      if (tid < C) {
+        cv = dsmem_ld_f64(dsmem_map(base_v + 8u * par, uint32_t(tid)));
+        ci = dsmem_ld_s64(dsmem_map(base_i + 8u * par, uint32_t(tid)));
+        cc = tid;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_down_sync(0xffffffffu, cv, o);
+        const int64_t oi = __shfl_down_sync(0xffffffffu, ci, o);
+        const int oc = __shfl_down_sync(0xffffffffu, cc, o);
+        if (oi >= 0 && (ov > cv || (ov == cv && (ci < 0 || oi < ci)))) {
+          cv = ov;
+          ci = oi;
+          cc = oc;
+        }
+      }
+      if (tid == 0) {
+        const double dkk =
+            double(fabs(dsmem_ld<T>(dsmem_map(base_rk + uint32_t((par * n + k) * sizeof(T)), owner_k))));
+        const bool take = ci >= 0 && cv > dkk;
+        s_best = take ? cv : dkk;
+        s_p = take ? ci : k;
+        s_src = take ? cc : -1;
+        if (rank == 0) {
+          piv[k] = s_p;
+          if (s_best == 0.0 && *d_sing < 0) *d_sing = int(base + k);
+        }
+      }
+    }
+    __syncthreads();
+    const bool live = !(s_best == 0.0);
+    const int64_t p = s_p;
+    const int src = s_src;
+    if (live) {
+      for (int64_t j = tid; j < n; j += LU_THREADS) {
+        const T rkj = dsmem_ld<T>(dsmem_map(base_rk + uint32_t((par * n + j) * sizeof(T)), owner_k));
+        const T nk = src >= 0 ? dsmem_ld<T>(dsmem_map(base_row + uint32_t((par * n + j) * sizeof(T)), uint32_t(src)))
+                              : rkj;
+        newk[j] = nk;
+        if (p != k) {
+          if (k >= r0 && k < r1) S[(k - r0) * ld + j] = nk;
+          if (p >= r0 && p < r1) S[(p - r0) * ld + j] = rkj;
+        }
+      }
+      __syncthreads();
+      const T d = newk[k];
+      for (int64_t i = lo + tid; i < r1; i += LU_THREADS) {
+        T* row = S + (i - r0) * ld;
+        const T lik = Ops<T>::div(row[k], d);
+        row[k] = lik;
+        for (int64_t j = k + 1; j < n; ++j) row[j] = Ops<T>::sub(row[j], Ops<T>::mul(lik, newk[j]));
+      }
+    }
+    __syncthreads();
+  }
+  for (int64_t e = tid; e < rows * n; e += LU_THREADS) {
+    const int64_t i = e / n, j = e % n;
+    a[off + (r0 + i) * rs + j * cs] = S[i * ld + j];
+  }
+  cluster_barrier();  // no CTA leaves while a peer may still read its shared memory
+}
+
 template <typename T>
 __global__ void apply_pivots_kernel(T* a, int64_t off, int64_t rs, int64_t cs, int64_t ncols, const int64_t* piv,
                                     int64_t count, int64_t sub, int backward) {
@@ -475,6 +664,59 @@ int launch_lu_leaf(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int
   if (G > 4096) G = 4096;
   double* pv = part_v[dev];
   int64_t* pi = part_i[dev];
+  // one cluster when the whole panel fits in its shared memory
+  if (!g_lu_global && !g_lu_nocluster && n <= 1024) {
+    const size_t esz = is_f64 ? 8 : 4;
+    const size_t budget = 200 * 1024;
+    const size_t fixed = 32 + size_t(5 * n) * esz;  // partial slots, newk, 2 published rows, 2 rows k
+    const int64_t max_rows = budget > fixed ? int64_t((budget - fixed) / (size_t(n + 1) * esz)) : 0;
+    int64_t Cn = max_rows > 0 ? (m + max_rows - 1) / max_rows : 1 << 30;
+    const int64_t want = (m + 383) / 384;  // a few hundred rows per CTA
+    if (Cn < want) Cn = want;
+    if (Cn < 1) Cn = 1;
+    if (Cn <= g_lu_cluster_max) {
+      const int C = int(Cn);
+      const int chunk = int((m + C - 1) / C);
+      const size_t smem = fixed + size_t(chunk) * size_t(n + 1) * esz;
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(C);
+      cfg.blockDim = dim3(LU_THREADS);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = C;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaError_t e;
+      if (is_f64) {
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(lu_leaf_cluster_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+          cudaFuncSetAttribute(lu_leaf_cluster_kernel<double>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+          attr = true;
+        }
+        e = cudaLaunchKernelEx(&cfg, lu_leaf_cluster_kernel<double>, static_cast<double*>(a), off, rs, cs, m, n, piv,
+                               d_sing, base, chunk);
+      } else {
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(lu_leaf_cluster_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+          cudaFuncSetAttribute(lu_leaf_cluster_kernel<float>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+          attr = true;
+        }
+        e = cudaLaunchKernelEx(&cfg, lu_leaf_cluster_kernel<float>, static_cast<float*>(a), off, rs, cs, m, n, piv,
+                               d_sing, base, chunk);
+      }
+      if (e == cudaSuccess) {
+        note_launch();
+        return 0;
+      }
+      (void)cudaGetLastError();  // not schedulable as one cluster here: the grid kernels below
+    }
+  }
   note_launch();
   cudaError_t e;
   // shared-memory bands when they fit: <= 32 bands of <= ~190 KB each

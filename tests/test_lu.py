@@ -87,24 +87,23 @@ def test_cuda_left_trsm_matches_reference(cuda, case):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("leaf_opt", [None, "lu_noprefetch", "lu_global"])
-@pytest.mark.parametrize("n,m_rows,tree", [(1500, 1500, [256, 32]), (600, 2000, [128, 16]), (3000, 3000, [512, 64, 16])])
-def test_cuda_lu_bitwise_vs_oracle_larger(cuda, n, m_rows, tree, leaf_opt):
+@pytest.mark.parametrize("leaf_opts", [(), ("lu_nocluster",), ("lu_nocluster", "lu_noprefetch"), ("lu_global",)])
+@pytest.mark.parametrize("n,m_rows,tree", [(1500, 1500, [256, 32]), (600, 2000, [128, 16]), (3000, 3000, [512, 64, 16]),
+                                           (128, 9000, [64, 32])])
+def test_cuda_lu_bitwise_vs_oracle_larger(cuda, n, m_rows, tree, leaf_opts):
     """Sizes past the golden set (tall, square, three levels) against the
-    oracle, for each leaf kernel path (shared-memory bands with and without
-    the candidate-row prefetch, global memory); then lu_solve to rounding
-    against numpy."""
-    import paper_2604_07311_b200 as bf
-    from paper_2604_07311_b200.control import parse_tree
+    oracle, for each leaf kernel path (one cluster with DSMEM, shared-memory
+    bands on a cooperative grid with and without the candidate-row prefetch,
+    global memory); then lu_solve to rounding against numpy."""
     from paper_2604_07311_b200.engine import _lib
 
-    if leaf_opt is not None:
-        assert _lib.lib().bf_set_option(leaf_opt.encode(), 1) == 0
+    for o in leaf_opts:
+        assert _lib.lib().bf_set_option(o.encode(), 1) == 0
     try:
         _lu_larger(n, m_rows, tree)
     finally:
-        if leaf_opt is not None:
-            _lib.lib().bf_set_option(leaf_opt.encode(), 0)
+        for o in leaf_opts:
+            _lib.lib().bf_set_option(o.encode(), 0)
 
 
 def _lu_larger(n, m_rows, tree):

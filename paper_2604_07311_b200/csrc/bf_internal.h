@@ -84,6 +84,7 @@ extern int g_lu_noprefetch;   // LU leaf: no candidate-row prefetch
 extern int g_lu_nocluster;    // LU leaf: never the single-cluster kernel
 extern int g_lu_cluster_max;  // LU leaf: largest cluster
 extern int g_qr_global;       // QR panel: force the global-memory sweep
+extern int g_ltlt_grid_max;   // LTL^T stepper: cap on the cooperative grid
 int launch_gemm_simt_f32(const GemmParams& p, cudaStream_t s);        // f32 storage, f32 acc
 int launch_gemm_simt_f32acc64(const GemmParams& p, cudaStream_t s);   // f32 storage, f64 acc
 int launch_scale(int is_f64, double beta, void* c, int64_t off, int64_t m, int64_t n, int64_t rs,

@@ -795,6 +795,10 @@ int bf_set_option(const char* name, int64_t value) {
     g_pipeline_first = value < 0 ? 0 : int(value);
     return BF_OK;
   }
+  if (name && std::strcmp(name, "ltlt_grid") == 0 && value >= 0) {
+    bf::g_ltlt_grid_max = int(value);
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "qr_global") == 0) {
     bf::g_qr_global = value != 0;
     return BF_OK;

@@ -21,6 +21,8 @@
 
 namespace bf {
 
+int g_ltlt_grid_max = 0;  // bf_set_option("ltlt_grid", g): cap the stepper's cooperative grid (0 = one CTA per SM)
+
 namespace {
 
 namespace cg = cooperative_groups;
@@ -223,6 +225,7 @@ int launch_ltlt(int is_f64, void* x, int64_t off, int64_t rs, int64_t cs, int64_
   if (G < 1) G = 1;
   if (G > sms) G = sms;
   if (G > 256) G = 256;
+  if (g_ltlt_grid_max > 0 && G > g_ltlt_grid_max) G = g_ltlt_grid_max;
   note_launch();
   cudaError_t e;
   if (is_f64) {

@@ -17,6 +17,9 @@ m = rng.uniform(-1, 1, (n, n))
 x0 = np.tril(m - m.T)
 tree = ControlNode("ltlt", "unblocked") if bs == 0 else ControlNode("ltlt", "blocked", bs=bs,
                                                                      child=ControlNode("ltlt", "unblocked"))
+if len(args) > 3:
+    from paper_2604_07311_b200.engine import _lib
+    _lib.lib().bf_set_option(b"ltlt_grid", args[3])
 v = bf.make_view(n, n, fill=x0)
 src = v.storage.clone()
 for _ in range(reps):
@@ -27,4 +30,4 @@ for _ in range(reps):
     bf.ltlt_pivoted(v, tree)
     e1.record()
     e1.synchronize()
-    print(f"ltlt n={n} bs={bs} ms {e0.elapsed_time(e1):.2f}")
+    print(f"ltlt n={n} bs={bs} grid_cap={args[3] if len(args) > 3 else 0} ms {e0.elapsed_time(e1):.2f}")

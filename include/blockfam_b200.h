@@ -80,8 +80,9 @@ const char* bf_last_error(void);
 int bf_set_option(const char* name, int64_t value);
 int bf_device_sm_count(void);
 /* With bf_set_option("timeline", 1): per top-level step of the last lookahead
- * factorization, 4 floats (ms): next-column update done, trailing update done,
- * panel start, panel end.  Returns the number of steps. */
+ * factorization, 5 floats (ms): next-column update done, trailing update done,
+ * panel start, panel end, diagonal factor of the panel done.  Returns the
+ * number of steps. */
 int bf_timeline(float* out, int max_steps);
 
 /* C := beta*C + alpha*A*B (lower_only: only i >= j of C is read or written).

@@ -51,6 +51,7 @@ struct GemmParams {
   int tiles_m, tiles_n;
   int group;              // raster group height in tiles
   int tiles_per_cta;      // TMA kernel: contiguous raster tiles per CTA
+  int tile_stride;        // TMA kernel: 0, or CTA b owns raster tiles b, b + tile_stride, ... (persistent grid)
   int64_t num_tiles;
   const int* abort_flag;  // skip all work when non-null and 0 <= *abort_flag < abort_limit
   int64_t abort_limit;    // a failure at a pivot >= abort_limit happened "later" in the
@@ -74,6 +75,8 @@ bool gemm_dmma_tma_eligible(const GemmParams& p);                     // TMA/mba
 int launch_gemm_dmma_tma(const GemmParams& p, cudaStream_t s);
 extern int g_use_tma;         // bf_set_option("tma", 0|1)
 extern int g_tma_variant;     // bf_set_option("tma_variant", 0..3)
+extern int g_reserve_strided;
+extern thread_local int t_reserve_sms;  // gemm_dmma_tma.cu: SMs left free by the next launch
 extern int g_tiles_per_cta;   // bf_set_option("tiles_per_cta", t)
 extern int g_bf16_tma_c;      // bf16 GEMM: TMA C-tile epilogue (1) or per-element fallback (0)
 extern int g_trsm_warp;       // fused TRSM subtree: 4-warps-per-32-rows kernel (1) or the 64-row CTA kernel (0)

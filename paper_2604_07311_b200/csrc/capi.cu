@@ -34,6 +34,18 @@ int g_fused_trsm = 1;     // bf_set_option("fused_trsm", 0) keeps every recursio
 // faster at n=32768 (the chunked TRSM competes with the SYRK for the same
 // SMs), so off by default.
 int g_pipeline_first = 0;
+// Lookahead SM reservation: the rest of each step's trailing update runs as a
+// persistent grid on all but g_tail_reserve SMs, so the panel stream's chain
+// of small launches (diagonal factor, TRSM) finds SMs free at once instead of
+// waiting for 128x128xbs tiles to retire.  Measured at n=32768 (bench tree):
+// 0 -> 390 ms, 8 -> 384, 12 -> 383, 16 -> 382, 20 -> 385, 24 -> 392
+// (tools/gpu_tail_sweep.sh).  Grid shape only: the bits are unchanged.
+int g_tail_reserve = 16;     // bf_set_option("tail_reserve", r): SMs left to the panel stream
+int64_t g_tail_rows = 32768;  // bf_set_option("tail_rows", t): ... when the rest of the update is <= t rows
+                              // (larger updates keep the 1-tile CTAs: at n=131072 a persistent grid
+                              // over the whole trailing matrix loses L2 locality, 22.1 -> 23.0 s)
+int g_diag_reserve = 0;      // bf_set_option("diag_reserve", r): SMs left to the panel stream while ...
+int64_t g_diag_rows = 0;     // bf_set_option("diag_rows", h): ... the first h rows of the rest are updated
 // bf_set_option("overlap_h2d", 0): bf_cholesky_host_d loads the whole lower
 // triangle before factoring instead of overlapping the load with step 0
 int g_overlap_h2d = 1;
@@ -347,7 +359,7 @@ void writeback_block_column(const bf_view& a, int64_t c0, int64_t w, cudaStream_
 // per step, events after the next-column update, after the rest of the
 // trailing update, and around the panel on the side stream.
 struct TimelineStep {
-  cudaEvent_t main_col, main_rest, panel_begin, panel_end;
+  cudaEvent_t main_col, main_rest, panel_begin, panel_end, panel_diag;
 };
 int g_timeline = 0;
 std::vector<TimelineStep> g_tl;
@@ -361,10 +373,15 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
   cudaEvent_t ev_main, ev_panel;
   cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming);
+  cudaEvent_t* diag_mark = nullptr;  // timeline: event after the diagonal factor of the next panel
   auto panel = [&](int64_t done, int64_t b, cudaStream_t st) {
     bf_view a11 = subview(a, done, b, done, b);
     bf_view a21 = subview(a, done + b, n - done - b, done, b);
     int rc = chol_run(mode, a11, lv, nl, 1, base + done, d_info, st);
+    if (diag_mark) {
+      cudaEventCreate(diag_mark);
+      cudaEventRecord(*diag_mark, st);
+    }
     if (!rc) rc = trsm_rec(mode, 1.0, a11, a21, kc, nullptr, d_info, st);
     return rc;
   };
@@ -373,6 +390,7 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     cudaEventDestroy(st.main_rest);
     cudaEventDestroy(st.panel_begin);
     cudaEventDestroy(st.panel_end);
+    if (st.panel_diag) cudaEventDestroy(st.panel_diag);
   }
   g_tl.clear();
   auto mark = [&](cudaStream_t st) {
@@ -493,8 +511,12 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     // (2) next panel on the side stream once (1) has landed
     cudaEventRecord(ev_main, s);
     cudaStreamWaitEvent(ps, ev_main, 0);
-    if (g_timeline) ts.panel_begin = mark(ps);
+    if (g_timeline) {
+      ts.panel_begin = mark(ps);
+      diag_mark = &ts.panel_diag;
+    }
     rc = panel(r2, b2, ps);
+    diag_mark = nullptr;
     if (rc) break;
     if (g_timeline) ts.panel_end = mark(ps);
     cudaEventRecord(ev_panel, ps);
@@ -517,8 +539,33 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
         }
       }
     } else if (nr2 > b2) {
-      rc = gemm_impl(mode, -1.0, l21_rest, transposed(l21_rest), 1.0, subview(a, r2 + b2, nr2 - b2, r2 + b2, nr2 - b2),
-                     1, kc, d_info, s, base + r2);
+      // tail steps (the panel chain is the critical path): optionally keep
+      // g_tail_reserve SMs free of this update so the panel kernels start at once
+      const int64_t m = nr2 - b2, r3 = r2 + b2;
+      if (g_tail_reserve > 0 && m <= g_tail_rows) bf::t_reserve_sms = g_tail_reserve;
+      // diagonal-factor window: the first h1 rows of the rest leave
+      // g_diag_reserve SMs to the panel stream (its diagonal factor is a chain
+      // of small launches that otherwise waits for trailing tiles to retire);
+      // the rows below follow on the whole GPU.  Same per-element chains.
+      const int64_t h1 = g_diag_reserve > 0 ? (m < g_diag_rows ? m : g_diag_rows) : 0;
+      if (h1 > 0) {
+        if (!bf::t_reserve_sms) bf::t_reserve_sms = g_diag_reserve;
+        bf_view l1 = subview(l21_rest, 0, h1, 0, b);
+        rc = gemm_impl(mode, -1.0, l1, transposed(l1), 1.0, subview(a, r3, h1, r3, h1), 1, kc, d_info, s, base + r2);
+        if (m <= g_tail_rows) bf::t_reserve_sms = g_tail_reserve; else bf::t_reserve_sms = 0;
+        if (!rc && m > h1) {
+          bf_view l2 = subview(l21_rest, h1, m - h1, 0, b);
+          rc = gemm_impl(mode, -1.0, l2, transposed(l1), 1.0, subview(a, r3 + h1, m - h1, r3, h1), 0, kc, d_info, s,
+                         base + r2);
+          if (!rc)
+            rc = gemm_impl(mode, -1.0, l2, transposed(l2), 1.0, subview(a, r3 + h1, m - h1, r3 + h1, m - h1), 1, kc,
+                           d_info, s, base + r2);
+        }
+      } else {
+        rc = gemm_impl(mode, -1.0, l21_rest, transposed(l21_rest), 1.0, subview(a, r3, m, r3, m), 1, kc, d_info, s,
+                       base + r2);
+      }
+      bf::t_reserve_sms = 0;
     }
     if (g_timeline) {
       ts.main_rest = mark(s);
@@ -791,6 +838,26 @@ int bf_set_option(const char* name, int64_t value) {
     g_overlap_h2d = value != 0;
     return BF_OK;
   }
+  if (name && std::strcmp(name, "tail_reserve") == 0 && value >= 0) {
+    g_tail_reserve = int(value);
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "reserve_strided") == 0) {
+    bf::g_reserve_strided = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "diag_reserve") == 0 && value >= 0) {
+    g_diag_reserve = int(value);
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "diag_rows") == 0 && value >= 0) {
+    g_diag_rows = value;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "tail_rows") == 0 && value >= 0) {
+    g_tail_rows = value;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "pipeline_first") == 0) {
     g_pipeline_first = value < 0 ? 0 : int(value);
     return BF_OK;
@@ -839,17 +906,19 @@ int bf_set_option(const char* name, int64_t value) {
 }
 
 int bf_timeline(float* out, int max_steps) {
-  // out[4*i + 0..3] = ms from the start to: next-column update done, rest of
-  // the trailing update done, panel start, panel end (step i of the last
-  // lookahead factorization).  Synchronises on the recorded events.
+  // out[5*i + 0..4] = ms from the start to: next-column update done, rest of
+  // the trailing update done, panel start, panel end, diagonal factor of the
+  // panel done (step i of the last lookahead factorization).  Synchronises on
+  // the recorded events.
   int nsteps = int(g_tl.size());
   if (!out || !g_tl_origin) return nsteps;
   for (int i = 0; i < nsteps && i < max_steps; ++i) {
-    cudaEvent_t ev[4] = {g_tl[i].main_col, g_tl[i].main_rest, g_tl[i].panel_begin, g_tl[i].panel_end};
-    for (int q = 0; q < 4; ++q) {
+    cudaEvent_t ev[5] = {g_tl[i].main_col, g_tl[i].main_rest, g_tl[i].panel_begin, g_tl[i].panel_end,
+                         g_tl[i].panel_diag};
+    for (int q = 0; q < 5; ++q) {
       float ms = -1.f;
       if (ev[q] && cudaEventSynchronize(ev[q]) == cudaSuccess) cudaEventElapsedTime(&ms, g_tl_origin, ev[q]);
-      out[4 * i + q] = ms;
+      out[5 * i + q] = ms;
     }
   }
   return nsteps;

@@ -156,11 +156,15 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   // enough to overlap a tile's fold with the next tile's first loads, short
   // enough that CTAs retire every few hundred microseconds and the
   // high-priority panel stream of the Cholesky lookahead gets SMs promptly.
-  const int64_t first_tile = int64_t(blockIdx.x) * p.tiles_per_cta;
-  const int W = int(p.num_tiles - first_tile < p.tiles_per_cta ? p.num_tiles - first_tile : p.tiles_per_cta);
+  // A persistent grid (p.tile_stride > 0) strides instead, so the tiles in
+  // flight at any moment stay neighbours in the L2-friendly raster order.
+  const int64_t tstep = p.tile_stride > 0 ? p.tile_stride : 1;
+  const int64_t first_tile = p.tile_stride > 0 ? int64_t(blockIdx.x) : int64_t(blockIdx.x) * p.tiles_per_cta;
+  const int64_t owned = p.tile_stride > 0 ? (p.num_tiles - first_tile + tstep - 1) / tstep : p.num_tiles - first_tile;
+  const int W = int(owned < p.tiles_per_cta ? owned : p.tiles_per_cta);
   for (int w = tid; w < W; w += TM_THREADS) {
     int64_t ti, tj;
-    tile_coords_tma(p, first_tile + w, tri, ti, tj);
+    tile_coords_tma(p, first_tile + w * tstep, tri, ti, tj);
     tile_tab[w] = (uint32_t(ti) << 16) | uint32_t(tj);
   }
   if (tid == 0) {
@@ -413,6 +417,8 @@ bool gemm_dmma_tma_eligible(const GemmParams& p) {
 }
 
 int g_tiles_per_cta = 1;
+thread_local int t_reserve_sms = 0;
+int g_reserve_strided = 0;  // bf_set_option("reserve_strided", 0/1): tile order of the reserved persistent grid  // set around a launch: persistent grid leaving this many SMs free
 int g_tma_variant = 2;  // 0: m8n8k4/1 box/6 stages, 1: m16n8k8/1/6, 2: m8n8k4/2 boxes/3, 3: m16n8k8/2/3
 
 template <int MMAK, int KBOX, int STAGES>
@@ -430,10 +436,17 @@ static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensor
   }
   // tiles per CTA: g_tiles_per_cta (0 = fully persistent, one CTA per SM)
   int64_t tpc = g_tiles_per_cta > 0 ? g_tiles_per_cta : (p.num_tiles + sms - 1) / sms;
+  if (t_reserve_sms > 0 && t_reserve_sms < sms) {
+    // persistent CTAs on all but t_reserve_sms SMs: the high-priority panel
+    // stream always finds SMs free instead of waiting for tiles to retire
+    const int64_t ctas = sms - t_reserve_sms;
+    tpc = (p.num_tiles + ctas - 1) / ctas;
+  }
   while (tpc * 4 + base_smem > max_smem) tpc /= 2;  // the tile table must fit
   if (tpc < 1) tpc = 1;
   p.tiles_per_cta = int(tpc);
   const int64_t grid = (p.num_tiles + tpc - 1) / tpc;
+  if (t_reserve_sms > 0 && g_reserve_strided) p.tile_stride = int(grid);
   if (grid > 0x7fffffffLL) return -3;
   if (p.m >= (1 << 16) * int64_t(TM_BM) || p.n >= (1 << 16) * int64_t(TM_BN)) return -3;
   const size_t smem = base_smem + size_t(tpc) * 4;

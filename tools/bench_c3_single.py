@@ -22,6 +22,11 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 131072
 bs = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
 RB = 2048
 dev = torch.device("cuda:0")
+import os  # noqa: E402
+from paper_2604_07311_b200.engine import _lib  # noqa: E402
+for kv in filter(None, os.environ.get("BF_OPTS", "").split(",")):  # e.g. BF_OPTS=tail_reserve=0
+    k, v = kv.split("=")
+    assert _lib.lib().bf_set_option(k.encode(), int(v)) == 0, kv
 tree_doc = {"op": "cholesky", "variant": 3, "bs": bs, "kernel": {"kc": bs},
             "child": {"op": "cholesky", "variant": 3, "bs": 128, "kernel": {"kc": 128},
                       "child": {"op": "cholesky", "variant": "unblocked3"}}}

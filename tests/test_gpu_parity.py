@@ -123,6 +123,51 @@ def test_lookahead_pipelined_first_step_npd_partial_state(cuda, npd_at, pipeline
     assert digest(v.storage.cpu().numpy()) == digest(st)
 
 
+RESERVE_TREE = ('{"op": "cholesky", "variant": 3, "bs": 256, "kernel": {"kc": 256}, "child": {"op": "cholesky", '
+                '"variant": 3, "bs": 64, "kernel": {"kc": 64}, "child": {"op": "cholesky", "variant": "unblocked3"}}}')
+
+
+@pytest.mark.parametrize("opts", [
+    {"tail_reserve": 0},                                     # 1-tile CTAs on the whole GPU
+    {"tail_reserve": 16, "tail_rows": 1 << 40},              # default grid shape on every step
+    {"tail_reserve": 40, "tail_rows": 1 << 40, "reserve_strided": 1},
+    {"tail_reserve": 0, "diag_reserve": 24, "diag_rows": 700},  # two-phase rest update
+    {"tail_reserve": 16, "tail_rows": 1024, "diag_reserve": 8, "diag_rows": 384},
+])
+@pytest.mark.parametrize("npd_at", [None, 1500])
+def test_lookahead_sm_reservation_bitwise(cuda, opts, npd_at):
+    """The SM-reservation options of the lookahead schedule (persistent grid
+    leaving SMs to the panel stream, strided tile order, the two-phase rest
+    update) only change grid shapes and launch splits: the factor, and the
+    partial state after a pivot failure, stay the reference's bits.  n=2304
+    with bs=256 puts up to 28 tile rows (406 tiles > one per SM) in the rest
+    update, so the persistent grid really holds several tiles per CTA."""
+    import json
+
+    from paper_2604_07311_b200.engine import _lib
+
+    n = 2304
+    a0 = spd_int(4242, n)
+    if npd_at is not None:
+        a0[npd_at, npd_at] = -1e9
+    lib = _lib.lib()
+    defaults = {"tail_reserve": 16, "tail_rows": 32768, "diag_reserve": 0, "diag_rows": 0, "reserve_strided": 0}
+    try:
+        for key, val in opts.items():
+            assert lib.bf_set_option(key.encode(), int(val)) == 0
+        v = make_view(n, n, fill=a0)
+        bad = int(bf.cholesky_async(v, "lower", parse_tree(RESERVE_TREE)).item())
+    finally:
+        for key, val in defaults.items():
+            lib.bf_set_option(key.encode(), val)
+    st = a0.reshape(-1).copy()
+    ref_bad = O.cholesky(st, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1},
+                         O.levels_from_tree(json.loads(RESERVE_TREE), n, "f64"), nthreads=O.host_threads())
+    assert ref_bad == (-1 if npd_at is None else npd_at)
+    assert bad == ref_bad
+    assert digest(v.storage.cpu().numpy()) == digest(st)
+
+
 @pytest.mark.parametrize("leaf_blocked", [1, 0])
 @pytest.mark.parametrize("dt,npd_at", [("f64", None), ("f64", 77), ("f64", 100), ("f32", None), ("f32", 45)])
 def test_leaf_kernels_bitwise_and_partial_state(cuda, leaf_blocked, dt, npd_at):

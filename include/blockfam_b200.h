@@ -76,7 +76,11 @@ const char* bf_last_error(void);
  * bf_cholesky_*; "tma" / "tma_variant" / "tiles_per_cta" / "group" select the
  * FP64 GEMM kernel and its tile schedule; "fused_trsm" the single-kernel TRSM
  * subtree; "timeline" records per-step events; "bf16_tma_c" the TMA C-tile
- * epilogue of the bf16 GEMM. */
+ * epilogue of the bf16 GEMM; "tail_reserve" (default 16) / "tail_rows"
+ * (default 32768) run the lookahead's rest-of-step update as a persistent grid
+ * leaving that many SMs to the panel stream when the update is <= tail_rows
+ * rows; "reserve_strided" its tile order; "diag_reserve" / "diag_rows" an
+ * optional two-phase split of that update (off). */
 int bf_set_option(const char* name, int64_t value);
 int bf_device_sm_count(void);
 /* With bf_set_option("timeline", 1): per top-level step of the last lookahead

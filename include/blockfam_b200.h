@@ -151,6 +151,12 @@ int bf_gemm_scatter_d(double alpha, const bf_scatter_view* a, const bf_scatter_v
                       const bf_scatter_view* c, int64_t kc, void* stream);
 int bf_gemm_scatter_s(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
                       const bf_scatter_view* c, int64_t kc, void* stream);
+/* Operand staging (the whole-operand form of engine/kernels.py:24-90
+ * pack_a_block / pack_b_block): out (m x n, or n x m when transpose != 0,
+ * row-major, device) := src[rscat[i] + cscat[j]].  tensor/contract.py stages a
+ * large permuted facade k-contiguous with it so the TMA DMMA GEMM can read it;
+ * values are copied exactly, so the contraction's bits do not change. */
+int bf_pack_scatter_d(const bf_scatter_view* src, int transpose, double* out, void* stream);
 int bf_gemm_scatter_sd(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
                        const bf_scatter_view* c, int64_t kc, void* stream);
 

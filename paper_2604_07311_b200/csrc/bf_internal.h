@@ -73,6 +73,9 @@ void note_launch(int64_t n = 1);
 int launch_gemm_dmma(const GemmParams& p, cudaStream_t s);            // f64 storage, f64 acc
 bool gemm_dmma_tma_eligible(const GemmParams& p);                     // TMA/mbarrier fast path?
 int launch_gemm_dmma_tma(const GemmParams& p, cudaStream_t s);
+// pack.cu: out[r*cols + c] = src[row_scat[r] + col_scat[c]] (contraction operand staging)
+int launch_pack_scatter(int is_f64, const void* src, const int64_t* row_scat, const int64_t* col_scat, int64_t rows,
+                        int64_t cols, void* out, cudaStream_t s);
 extern int g_use_tma;         // bf_set_option("tma", 0|1)
 extern int g_tma_variant;     // bf_set_option("tma_variant", 0..3)
 extern int g_reserve_strided;

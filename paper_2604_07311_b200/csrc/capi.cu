@@ -1457,6 +1457,15 @@ int bf_gemm_scatter_d(double alpha, const bf_scatter_view* a, const bf_scatter_v
                       const bf_scatter_view* c, int64_t kc, void* stream) {
   return scatter_impl(MODE_D, alpha, a, b, beta, c, kc, S(stream));
 }
+int bf_pack_scatter_d(const bf_scatter_view* src, int transpose, double* out, void* stream) {
+  if (!src || !out) return fail(BF_ERR_VALUE, "null argument");
+  if (src->m < 0 || src->n < 0) return fail(BF_ERR_SHAPE, "negative extent");
+  if (src->m == 0 || src->n == 0) return BF_OK;
+  if (!src->rscat || !src->cscat) return fail(BF_ERR_VALUE, "scatter vectors required");
+  const int rc = transpose ? bf::launch_pack_scatter(1, src->base, src->cscat, src->rscat, src->n, src->m, out, S(stream))
+                           : bf::launch_pack_scatter(1, src->base, src->rscat, src->cscat, src->m, src->n, out, S(stream));
+  return rc ? fail(BF_ERR_CUDA, "pack launch failed") : BF_OK;
+}
 int bf_gemm_scatter_s(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
                       const bf_scatter_view* c, int64_t kc, void* stream) {
   return scatter_impl(MODE_S, alpha, a, b, beta, c, kc, S(stream));

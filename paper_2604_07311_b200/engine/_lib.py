@@ -132,6 +132,7 @@ _SIGNATURES = {
     "bf_potrs_f32_d": ([_VP, _L, _VP, _L, _VP], _I),
     "bf_potrs_blocked_f32_d": ([_VP, _L, _VP, _L, _VP, _L, _VP, _VP], _I),
     "bf_gemm_scatter_d": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
+    "bf_pack_scatter_d": ([_SV, _I, _VP, _VP], _I),
     "bf_gemm_scatter_s": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
     "bf_gemm_scatter_sd": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
 }

@@ -5,9 +5,10 @@ aibj,cjdi->abcd that exercises the gathered (block-scatter) operand path.
     python tools/bench_contract.py [d ...]
 
 Prints one JSON line per (spec, d): GFLOP/s (2*M*N*K per contraction, device
-time, inputs resident), and whether fold on/off give identical bits (the
-folded run uses the strided TMA GEMM, the unfolded one the gather kernel, and
-both must sum k in the reference's order).
+time, inputs resident) for fold on/off x stage auto/never (auto: permuted
+operands staged k-contiguous for the TMA GEMM when large; never: the
+element-gathering GEMM), and whether every path gave identical bits (all must
+sum k in the reference's order).
 """
 import hashlib
 import json
@@ -36,21 +37,24 @@ def run(spec_text: str, d: int, reps: int = 3):
     flops = 2.0 * d ** (len(set(spec.labels_a + spec.labels_b)))
     out = {}
     for fold in (True, False):
-        bf.contract(1.0, a, b, 0.0, c, spec, fold=fold)  # warm
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps):
-            bf.contract(1.0, a, b, 0.0, c, spec, fold=fold)
-        e1.record()
-        e1.synchronize()
-        ms = e0.elapsed_time(e1) / reps
-        out[fold] = (flops / (ms / 1e3) / 1e9, ms, hashlib.sha256(c.storage.cpu().numpy().tobytes()).hexdigest())
-    print(json.dumps({"spec": spec_text, "d": d, "flops": flops,
-                      "gflops_fold": round(out[True][0], 1), "ms_fold": round(out[True][1], 3),
-                      "gflops_nofold": round(out[False][0], 1), "ms_nofold": round(out[False][1], 3),
-                      "fold_bitwise_equal": out[True][2] == out[False][2]}), flush=True)
-
+        for stage in ("auto", "never"):
+            bf.contract(1.0, a, b, 0.0, c, spec, fold=fold, stage=stage)  # warm
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                bf.contract(1.0, a, b, 0.0, c, spec, fold=fold, stage=stage)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            key = ("fold" if fold else "nofold") + "_" + stage
+            out[key] = (flops / (ms / 1e3) / 1e9, ms, hashlib.sha256(c.storage.cpu().numpy().tobytes()).hexdigest())
+    line = {"spec": spec_text, "d": d, "flops": flops}
+    for key, (gf, ms, _) in out.items():
+        line["gflops_" + key] = round(gf, 1)
+        line["ms_" + key] = round(ms, 3)
+    line["all_paths_bitwise_equal"] = len({h for _, _, h in out.values()}) == 1
+    print(json.dumps(line), flush=True)
 
 if __name__ == "__main__":
     dims = [int(x) for x in sys.argv[1:]] or [64, 128]

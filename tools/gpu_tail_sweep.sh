@@ -1,7 +1,7 @@
 #!/bin/bash
 # Sweep of the SM-reservation options of the lookahead schedule (timeline + plain timings at n=32768).
 mkdir -p gpurun_out
-for o in "" "tail_reserve=16,tail_rows=40000,reserve_strided=0" "tail_reserve=12,tail_rows=40000" "tail_reserve=16,tail_rows=40000" "tail_reserve=20,tail_rows=40000" "tail_reserve=24,tail_rows=40000" "tail_reserve=32,tail_rows=40000"; do
+for o in "" "pipeline_first=2" "pipeline_first=4" "pipeline_first=8" "tail_reserve=16,tail_rows=40000"; do
   f=gpurun_out/tail_$(echo "$o" | tr ',=' '__').log
   BF_OPTS="$o" timeout 300 python tools/timeline.py 32768 > $f 2>&1
   grep -E "^opts|^total" $f

@@ -224,11 +224,18 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  // k tile at which segment sg prefetches C (4 tiles before its fold), or -1
+  auto pf_next = [&](int sg) -> int {
+    if (sg >= nseg) return -1;
+    const int len = sg < nseg - 1 ? tps : tps_last;
+    return sg * tps + (len >= 4 ? len - 4 : 0);
+  };
   int s = 0, round = 0, f = 0;
   for (int w = 0; w < W; ++w) {
     const uint32_t tt = tile_tab[w];
     const int64_t m0 = int64_t(tt >> 16) * TM_BM, n0 = int64_t(tt & 0xffffu) * TM_BN;
     int seg = 0, sub = 0;
+    int pf_kt = pf_next(p.beta != 0.0 ? 0 : 1);
     for (int kt = 0; kt < ntiles; ++kt, ++f) {
       mbar_wait(full(s), uint32_t(round & 1));
       const uint32_t sa = tiles + s * STAGE_BYTES;
@@ -308,8 +315,11 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         s = 0;
         ++round;
       }
-      if (kt == ntiles - 4 || (ntiles < 4 && kt == 0)) {
-        // warm L2 with this warp's 32x32 block of C before the fold reads it
+      if (kt == pf_kt) {
+        pf_kt = pf_next(kt / tps + 1);
+        // warm L2 with this warp's 32x32 block of C before this segment's fold
+        // reads it (with kc < K the folds recur, and the operand streams evict
+        // C from L2 between them: d=128 contraction, 64 folds per tile)
         const int64_t r = m0 + wm * 32 + lane, c0 = n0 + wn * 32;
         if (r < p.m && c0 < p.n) {
           const double* rowp = C + p.c_off + r * p.c_rs + c0 * p.c_cs;

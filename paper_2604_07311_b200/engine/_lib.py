@@ -8,6 +8,7 @@ check that every declared entry point is exported.
 from __future__ import annotations
 
 import ctypes
+import os
 import re
 import threading
 from pathlib import Path
@@ -33,7 +34,7 @@ __all__ = [
 ]
 
 _PKG = Path(__file__).resolve().parents[1]
-_LIB_PATH = _PKG / "_lib" / "libblockfam_b200.so"
+_LIB_PATH = Path(os.environ["BF_LIB_PATH"]) if os.environ.get("BF_LIB_PATH") else _PKG / "_lib" / "libblockfam_b200.so"
 _HEADER = _PKG.parent / "include" / "blockfam_b200.h"
 
 BF_OK = 0

@@ -5,3 +5,7 @@ for r in 1 2; do
   BF_LIB_PATH=$OLD timeout 300 python tools/timeline.py 32768 | grep opts | sed "s/^/old /"
   timeout 300 python tools/timeline.py 32768 | grep opts | sed "s/^/new /"
 done
+if [ -n "$AB_CONTRACT" ]; then
+  BF_LIB_PATH=$OLD timeout 300 python tools/bench_contract.py 128 | sed "s/^/old /"
+  timeout 300 python tools/bench_contract.py 128 | sed "s/^/new /"
+fi

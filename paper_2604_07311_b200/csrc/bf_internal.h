@@ -56,6 +56,7 @@ struct GemmParams {
   const int* abort_flag;  // skip all work when non-null and 0 <= *abort_flag < abort_limit
   int64_t abort_limit;    // a failure at a pivot >= abort_limit happened "later" in the
                           // reference's order and must not cancel this launch
+  int red_fold;           // TMA kernel: beta_eff == 1 folds as L2 reductions (C += alpha*acc)
 };
 
 __device__ __forceinline__ bool aborted(const GemmParams& p) {
@@ -78,6 +79,7 @@ int launch_pack_scatter(int is_f64, const void* src, const int64_t* row_scat, co
                         int64_t cols, void* out, cudaStream_t s);
 extern int g_use_tma;         // bf_set_option("tma", 0|1)
 extern int g_tma_variant;     // bf_set_option("tma_variant", 0..3)
+extern int g_red_fold;        // bf_set_option("red_fold", 0|1): TMA kernel folds with red.global.add.f64
 extern int g_reserve_strided;
 extern thread_local int t_reserve_sms;  // gemm_dmma_tma.cu: SMs left free by the next launch
 extern int g_tiles_per_cta;   // bf_set_option("tiles_per_cta", t)

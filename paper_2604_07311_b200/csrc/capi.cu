@@ -830,6 +830,10 @@ int bf_set_option(const char* name, int64_t value) {
     g_group = int(value);
     return BF_OK;
   }
+  if (name && std::strcmp(name, "red_fold") == 0) {
+    bf::g_red_fold = value != 0;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "tma_variant") == 0) {
     bf::g_tma_variant = int(value & 3);
     return BF_OK;

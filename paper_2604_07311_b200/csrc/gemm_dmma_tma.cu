@@ -333,6 +333,31 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         // serialise one L2 round trip per element; instead each half of the
         // thread's 32 elements has all its reads in flight before its writes.
         const double beta_eff = seg == 0 ? p.beta : 1.0;
+        if (beta_eff == 1.0 && p.red_fold) {
+          // C := C + round(alpha*acc) is one correctly rounded add whichever
+          // unit performs it: hand it to L2 as a fire-and-forget reduction
+          // (red.global.add.f64, round-to-nearest, subnormals kept) instead of
+          // a load -> add -> store round trip that stalls the warp before the
+          // next segment's DMMAs.  Each element has one owning thread and its
+          // folds stay in program order (same-address coherence), so the
+          // sequence of adds, and the bits, are those of the load/store fold.
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int64_t gi = m0 + wm * 32 + i * 8 + pg;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
+                const double v = __dmul_rn(p.alpha, acc[i][j][h]);
+                if (gi < p.m && gj < p.n && (!p.lower_only || gi >= gj))
+                  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(C + p.c_off + gi * p.c_rs + gj * p.c_cs),
+                               "d"(v)
+                               : "memory");
+                acc[i][j][h] = 0.0;
+              }
+          }
+        } else
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           double cold[2][4][2];
@@ -429,6 +454,7 @@ bool gemm_dmma_tma_eligible(const GemmParams& p) {
 int g_tiles_per_cta = 1;
 thread_local int t_reserve_sms = 0;
 int g_reserve_strided = 0;  // bf_set_option("reserve_strided", 0/1): tile order of the reserved persistent grid  // set around a launch: persistent grid leaving this many SMs free
+int g_red_fold = 1;
 int g_tma_variant = 2;  // 0: m8n8k4/1 box/6 stages, 1: m16n8k8/1/6, 2: m8n8k4/2 boxes/3, 3: m16n8k8/2/3
 
 template <int MMAK, int KBOX, int STAGES>
@@ -474,6 +500,7 @@ static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensor
 
 int launch_gemm_dmma_tma(const GemmParams& p_in, cudaStream_t s) {
   GemmParams p = p_in;
+  p.red_fold = g_red_fold;
   CUtensorMap ma, mb;
   if (!make_map(&ma, p.a, p.m, p.k) || !make_map(&mb, p.b, p.n, p.k)) return -3;
   p.tiles_m = int((p.m + TM_BM - 1) / TM_BM);

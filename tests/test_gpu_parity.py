@@ -303,6 +303,40 @@ def test_tma_kernel_variants_bitwise(cuda, variant):
         lib.bf_set_option(b"tma_variant", 2)
 
 
+@pytest.mark.parametrize("beta", [0.0, 1.0, -0.75])
+@pytest.mark.parametrize("lower", [False, True])
+def test_tma_red_fold_bitwise(cuda, beta, lower):
+    """The TMA kernel folds every segment with beta_eff == 1 as L2 reductions
+    (red.global.add.f64): same bits as the load/add/store fold and the oracle,
+    over many segments (kc=64 -> 12 folds), ragged edges, and lower-only C."""
+    from paper_2604_07311_b200.engine import _lib
+
+    lib = _lib.lib()
+    rng = np.random.default_rng(77 + int(lower))
+    m, n, k, kc = 700, 650, 768, 64
+    if lower:
+        n = m
+    a = rng.uniform(-1, 1, (m, k))
+    bt = rng.uniform(-1, 1, (n, k))
+    c0 = rng.uniform(-1, 1, (m, n))
+    cst = c0.reshape(-1).copy()
+    O.gemm(-1.25, (a.reshape(-1).copy(), {"off": 0, "m": m, "n": k, "rs": k, "cs": 1}),
+           (bt.reshape(-1).copy(), {"off": 0, "m": k, "n": n, "rs": 1, "cs": k}), beta,
+           (cst, {"off": 0, "m": m, "n": n, "rs": n, "cs": 1}), kc=kc, lower_only=lower)
+    cfg = KernelConfig(8, 6, 64, kc, 2048, F64, F64)
+    outs = []
+    try:
+        for mode in (1, 0):
+            lib.bf_set_option(b"red_fold", mode)
+            va, vb, vc = make_view(m, k, fill=a), make_view(n, k, fill=bt), make_view(m, n, fill=c0)
+            fn = bf.gemmt_lower if lower else bf.gemm
+            fn(-1.25, va, vb.transposed(), beta, vc, cfg=cfg)
+            outs.append(digest(vc.storage.cpu().numpy()))
+    finally:
+        lib.bf_set_option(b"red_fold", 1)
+    assert outs[0] == outs[1] == digest(cst)
+
+
 @pytest.mark.parametrize("dt,kc,bs,n", [("f64", 40, 128, 700), ("f64", 1024, 96, 700), ("f32", 20, 96, 700),
                                         ("f32", 512, 100, 700), ("f64", 128, 128, 5000), ("f32", 64, 128, 5000)])
 def test_fused_trsm_subtree_bitwise(cuda, dt, kc, bs, n):

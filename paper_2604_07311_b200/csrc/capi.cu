@@ -830,6 +830,10 @@ int bf_set_option(const char* name, int64_t value) {
     g_group = int(value);
     return BF_OK;
   }
+  if (name && std::strcmp(name, "persist") == 0) {
+    bf::g_persist = value != 0;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "red_fold") == 0) {
     bf::g_red_fold = value != 0;
     return BF_OK;

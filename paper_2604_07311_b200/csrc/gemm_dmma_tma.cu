@@ -455,6 +455,7 @@ int g_tiles_per_cta = 1;
 thread_local int t_reserve_sms = 0;
 int g_reserve_strided = 0;  // bf_set_option("reserve_strided", 0/1): tile order of the reserved persistent grid  // set around a launch: persistent grid leaving this many SMs free
 int g_red_fold = 1;
+int g_persist = 0;
 int g_tma_variant = 2;  // 0: m8n8k4/1 box/6 stages, 1: m16n8k8/1/6, 2: m8n8k4/2 boxes/3, 3: m16n8k8/2/3
 
 template <int MMAK, int KBOX, int STAGES>
@@ -478,11 +479,17 @@ static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensor
     const int64_t ctas = sms - t_reserve_sms;
     tpc = (p.num_tiles + ctas - 1) / ctas;
   }
+  // g_persist: one CTA per SM striding over the raster (CTA b owns tiles b,
+  // b + grid, ...), so each wave of concurrent tiles is one raster window
+  // walking k in lockstep and its shared A/B strips are read from HBM once
+  // per wave instead of once per staggered CTA (long-K GEMMs: the C5 contraction)
+  const bool persist = g_persist && t_reserve_sms == 0 && p.num_tiles >= int64_t(4) * sms && p.k >= 4096;
+  if (persist) tpc = (p.num_tiles + sms - 1) / sms;
   while (tpc * 4 + base_smem > max_smem) tpc /= 2;  // the tile table must fit
   if (tpc < 1) tpc = 1;
   p.tiles_per_cta = int(tpc);
   const int64_t grid = (p.num_tiles + tpc - 1) / tpc;
-  if (t_reserve_sms > 0 && g_reserve_strided) p.tile_stride = int(grid);
+  if ((t_reserve_sms > 0 && g_reserve_strided) || persist) p.tile_stride = int(grid);
   if (grid > 0x7fffffffLL) return -3;
   if (p.m >= (1 << 16) * int64_t(TM_BM) || p.n >= (1 << 16) * int64_t(TM_BN)) return -3;
   const size_t smem = base_smem + size_t(tpc) * 4;

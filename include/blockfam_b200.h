@@ -80,7 +80,9 @@ const char* bf_last_error(void);
  * (default 32768) run the lookahead's rest-of-step update as a persistent grid
  * leaving that many SMs to the panel stream when the update is <= tail_rows
  * rows; "reserve_strided" its tile order; "diag_reserve" / "diag_rows" an
- * optional two-phase split of that update (off). */
+ * optional two-phase split of that update (off); "red_fold" (default 1) folds
+ * the TMA GEMM's beta == 1 segments as red.global.add.f64 L2 reductions (0:
+ * load/add/store); "persist" a strided one-CTA-per-SM grid for long-K GEMMs (off). */
 int bf_set_option(const char* name, int64_t value);
 int bf_device_sm_count(void);
 /* With bf_set_option("timeline", 1): per top-level step of the last lookahead

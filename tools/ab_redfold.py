@@ -5,6 +5,7 @@ Cholesky (bench tree).  Prints times and whether both modes give identical bits.
     python tools/ab_redfold.py [d] [n]
 """
 import hashlib
+import os
 import json
 import sys
 from pathlib import Path
@@ -21,6 +22,7 @@ from paper_2604_07311_b200.tensor import ContractionSpec, contract, make_tensor 
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
 dev = torch.device("cuda")
+modes = [int(x) for x in os.environ.get("MODES", "0,1").split(",")] * 2
 
 
 def sha(t):
@@ -53,7 +55,7 @@ def rand():
 
 
 ta, tb, tc = rand(), rand(), make_tensor([d] * 4)
-for mode in (0, 1, 0, 1):
+for mode in modes:
     _lib.lib().bf_set_option(b"red_fold", mode)
     contract(1.0, ta, tb, 0.0, tc, spec)
     ts = timed(lambda: contract(1.0, ta, tb, 0.0, tc, spec))
@@ -64,7 +66,7 @@ torch.cuda.empty_cache()
 tree = parse_tree(json.dumps(bench.GPU_TREE))
 a0 = bench.make_spd(bf, torch, n, dev)
 a = torch.empty_like(a0)
-for mode in (0, 1, 0, 1):
+for mode in modes:
     _lib.lib().bf_set_option(b"red_fold", mode)
     ts = []
     for _ in range(3):

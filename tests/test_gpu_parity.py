@@ -337,6 +337,32 @@ def test_tma_red_fold_bitwise(cuda, beta, lower):
     assert outs[0] == outs[1] == digest(cst)
 
 
+def test_tma_persist_grid_bitwise(cuda):
+    """The strided persistent grid (option "persist", long-K GEMMs with at
+    least 4 tiles per SM) only reorders tiles: same bits as the default grid."""
+    from paper_2604_07311_b200.engine import _lib
+
+    lib = _lib.lib()
+    torch.manual_seed(5)
+    m, n, k, kc = 3200, 3072, 4096, 1024
+    a = torch.rand(m, k, dtype=torch.float64, device="cuda") - 0.5
+    bt = torch.rand(n, k, dtype=torch.float64, device="cuda") - 0.5
+    c0 = torch.rand(m, n, dtype=torch.float64, device="cuda") - 0.5
+    cfg = KernelConfig(8, 6, 64, kc, 2048, F64, F64)
+    outs = []
+    try:
+        for persist in (0, 1):
+            lib.bf_set_option(b"persist", persist)
+            c = c0.clone()
+            bf.gemm(0.5, bf.from_torch(a), bf.from_torch(bt).transposed(), 1.0, bf.from_torch(c), cfg=cfg)
+            torch.cuda.synchronize()
+            outs.append(c)
+    finally:
+        lib.bf_set_option(b"persist", 0)
+    assert torch.equal(outs[0], outs[1])
+    assert not torch.equal(outs[0], c0)
+
+
 @pytest.mark.parametrize("dt,kc,bs,n", [("f64", 40, 128, 700), ("f64", 1024, 96, 700), ("f32", 20, 96, 700),
                                         ("f32", 512, 100, 700), ("f64", 128, 128, 5000), ("f32", 64, 128, 5000)])
 def test_fused_trsm_subtree_bitwise(cuda, dt, kc, bs, n):

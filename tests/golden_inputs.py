@@ -42,9 +42,43 @@ def gemm_inputs(seed: int, op: str, dt: str, m: int, n: int, k: int, kinds: tupl
 
 def spd_int(seed: int, n: int, dt: str = "f64") -> np.ndarray:
     """A = M M^T + n I with small-integer M: exact in any summation order."""
+    if n > 4096:
+        return spd_int_large(seed, n).astype(NP[dt], copy=False)
     rng = np.random.default_rng(seed)
     m = rng.integers(-4, 5, (n, n)).astype(np.float64)
     return (m @ m.T + n * np.eye(n)).astype(NP[dt])
+
+
+def spd_int_large(seed: int, n: int, block: int = 4096) -> np.ndarray:
+    """spd_int for large n, bit-identical to the small-n formula.
+
+    Every entry of M M^T is a sum of n integer products in [-16, 16], so its
+    magnitude stays below 16 n < 2^24 for n < 2^20: float32 arithmetic forms
+    it exactly, in any order.  Row blocks avoid OpenBLAS's n=32768 fp64 SYRK
+    crash."""
+    assert 16 * n < 2**24
+    rng = np.random.default_rng(seed)
+    m = rng.integers(-4, 5, (n, n)).astype(np.float32)
+    mt = np.ascontiguousarray(m.T)
+    out = np.empty((n, n), dtype=np.float64)
+    for i in range(0, n, block):
+        out[i : i + block] = m[i : i + block] @ mt
+    del mt, m
+    out[np.diag_indices(n)] += n
+    return out
+
+
+def spd_int_torch(seed: int, n: int, device="cuda"):
+    """spd_int(seed, n) as a float64 torch tensor formed on `device` (same bits:
+    the integer products are exact in any summation order)."""
+    import torch
+
+    rng = np.random.default_rng(seed)
+    m = torch.from_numpy(rng.integers(-4, 5, (n, n)).astype(np.float32)).to(device).double()
+    a = m @ m.T
+    del m
+    a.diagonal().add_(n)
+    return a
 
 
 def spd_float(seed: int, n: int) -> np.ndarray:

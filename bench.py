@@ -288,43 +288,43 @@ def roofline_syrk(bf, torch, a0, n: int, bs: int, kc: int) -> dict:
             "syrk_ms_total": round(ms, 3), "peak_source": FP64_PEAK_SOURCE}
 
 
-DIST_TREE = {
-    "op": "cholesky", "variant": 3, "bs": 1024, "kernel": {"kc": 1024},
-    "child": {"op": "cholesky", "variant": 3, "bs": 128, "kernel": {"kc": 128},
-              "child": {"op": "cholesky", "variant": "unblocked3"}},
-}
+def dist_tree(world: int) -> dict:
+    """Tile size of the 2D block-cyclic layout = the root bs: 2048 (the bench
+    tree) up to 2 GPUs, 1024 beyond, so the per-step panel chain (diagonal
+    factor + panel TRSM + broadcasts) stays under each step's share of the
+    trailing update on 4-8 GPUs."""
+    doc = json.loads(json.dumps(GPU_TREE))
+    if world > 2:
+        doc["bs"], doc["kernel"]["kc"] = 1024, 1024
+    return doc
 
 
 def run_distributed(args, bf, torch, dist, dev, world: int, rank: int, n: int) -> int:
-    """All ranks factor one n x n matrix: 2D block-cyclic, NCCL broadcasts."""
+    """All ranks factor ONE n x n matrix with the native NCCL driver
+    (bf_chol_dist_d): lower tiles only, 2D block-cyclic over grid_for(world),
+    each rank generating its own tiles (no rank ever holds the whole matrix),
+    row/column communicators, panel broadcasts under the trailing updates.
+    At one rank (--dist) it is the same NCCL path on a 1x1 grid."""
     from paper_2604_07311_b200.control import parse_tree
-    from paper_2604_07311_b200.dist import BlockCyclic2D, TorchComm, cholesky_distributed, grid_for
+    from paper_2604_07311_b200.dist import native
     from paper_2604_07311_b200.engine import _lib
 
-    tree_doc = DIST_TREE if args.tree == json.dumps(GPU_TREE) else json.loads(args.tree)
+    tree_doc = dist_tree(world) if args.tree == json.dumps(GPU_TREE) else json.loads(args.tree)
     tree = parse_tree(json.dumps(tree_doc))
-    pr, pc = grid_for(world)
-    layout = BlockCyclic2D(n, tree.bs, pr, pc)
-    prow, pcol = layout.coords(rank)
-    a0 = make_spd(bf, torch, n, dev)
-    rows = torch.cat([torch.arange(t * layout.nb, t * layout.nb + layout.tile_len(t), device=dev)
-                      for t in layout.row_tiles(prow)])
-    cols = torch.cat([torch.arange(t * layout.nb, t * layout.nb + layout.tile_len(t), device=dev)
-                      for t in layout.col_tiles(pcol)])
-    local0 = a0.index_select(0, rows).index_select(1, cols).contiguous()
-    del a0, rows, cols
-    torch.cuda.empty_cache()
+    ctx = native.DistContext.from_torch_distributed()
+    lp = ctx.layout(n, tree.bs)
+    local0 = torch.empty(lp.local_elems(), dtype=torch.float64, device=dev)
+    native.fill_synthetic(ctx, local0, n, tree.bs, seed=42)
     work = torch.empty_like(local0)
-    comm = TorchComm()
     stream = torch.cuda.current_stream()
 
     def one(timed):
-        work.copy_(local0)
+        work.copy_(local0)  # restore outside the events
         dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        bad = cholesky_distributed(work, layout, tree, comm)
+        bad = native.cholesky_dist(ctx, work, n, tree)
         e1.record(stream)
         e1.synchronize()
         assert bad == -1
@@ -346,7 +346,7 @@ def run_distributed(args, bf, torch, dist, dev, world: int, rank: int, n: int) -
     value = chol_flops(n) / (ms / 1e3) / 1e9
     e2e = None
     if not args.no_e2e:
-        host = torch.empty_like(local0, device="cpu").pin_memory()
+        host = torch.empty(local0.numel(), dtype=torch.float64, pin_memory=True)
         host.copy_(local0)
         out = torch.empty_like(host).pin_memory()
         e2e_ms = []
@@ -356,7 +356,7 @@ def run_distributed(args, bf, torch, dist, dev, world: int, rank: int, n: int) -
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             work.copy_(host, non_blocking=True)
-            cholesky_distributed(work, layout, tree, comm)
+            native.cholesky_dist(ctx, work, n, tree)
             out.copy_(work, non_blocking=True)
             e1.record(stream)
             e1.synchronize()
@@ -367,22 +367,27 @@ def run_distributed(args, bf, torch, dist, dev, world: int, rank: int, n: int) -
         nbytes = local0.numel() * 8
         e2e = {"value": round(chol_flops(n) / (float(t2.item()) / 1e3) / 1e9, 3), "unit": "GFLOP/s",
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "ms_per_step": round(float(t2.item()), 3),
-               "path": "per rank: pinned host local block -> HBM, cholesky_distributed(), HBM -> pinned host"}
+               "path": "per rank: pinned host lower panels -> HBM, bf_chol_dist_d (NCCL), HBM -> pinned host"}
+        del host, out
     if rank == 0:
         line = {
             "metric": "Cholesky GFLOP/s (n=32768 FP64)", "value": round(value, 3), "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic: A = M M^T + n I, M ~ U(-1,1) seed 42, formed on device",
-            "config": {"workload": f"FP64 blocked Cholesky n={n}, 2D block-cyclic over {pr}x{pc} GPUs (BASELINE configs[1]/[2])",
-                       "n": n, "tree": tree_doc, "parallelism": f"2D block-cyclic {pr}x{pc}, NCCL panel broadcasts",
-                       "l2": "matrix >> L2"},
+            "data": "synthetic SPD: A = S + n I, S symmetric U[-1,1) from a counter hash, each rank generating "
+                    "its own lower tiles on device (bf_dist_fill_synthetic_d)",
+            "config": {"workload": f"FP64 blocked Cholesky n={n}, 2D block-cyclic over {ctx.pr}x{ctx.pc} GPUs "
+                                   "(BASELINE configs[1]/[2])",
+                       "n": n, "tree": tree_doc, "parallelism": f"2D block-cyclic {ctx.pr}x{ctx.pc}, lower tiles "
+                       "only, NCCL row/column broadcasts (bf_chol_dist_d)",
+                       "local_elems_rank0": lp.local_elems(), "l2": "matrix >> L2"},
             "pct_of_fp64_peak": round(100 * value / world / 1e3 / FP64_PEAK_TFLOPS, 2),
             "roofline": None, "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks.summary(),
+            "clocks": clocks.summary(), "step_ms": [round(x, 3) for x in timed],
         }
         print(json.dumps(line), flush=True)
     dist.barrier()
+    ctx.close()
     dist.destroy_process_group()
     return 0
 

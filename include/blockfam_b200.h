@@ -269,6 +269,43 @@ int bf_potrs_f32_d(const float* l, int64_t ld, double* x, int64_t n, void* strea
 int bf_potrs_blocked_f32_d(const float* l, int64_t ld, const float* xinv, int64_t bs, double* x, int64_t n,
                            double* work, void* stream);
 
+/* ---- multi-GPU Cholesky (the reference has no
+ * distribution) --------------------------------------------------
+ * One process per GPU; NCCL over NVLink/NVSwitch.  The matrix is held as the
+ * LOWER tiles of a 2D block-cyclic layout over a pr x pc process grid, tile
+ * size nb = the root bs of the control tree: rank (prow, pcol) = (rank / pc,
+ * rank % pc) owns tiles (I, J), I >= J, with I mod pr = prow and J mod pc =
+ * pcol, stored as one row-major panel per local column tile J (its row tiles
+ * I >= J stacked, leading dimension tile_len(J)), panels in J order
+ * (paper_2604_07311_b200/csrc/dist_layout.h).  The root `ways` of a control
+ * tree (control.py:47-71; the reference threads it into every level-3 call,
+ * factor/cholesky.py:128-149) selects this path with ways = pr * pc ranks. */
+typedef struct bf_dist bf_dist;
+int bf_dist_available(void);                 /* 1 if NCCL could be loaded */
+int bf_dist_unique_id_bytes(void);           /* sizeof(ncclUniqueId) */
+int bf_dist_unique_id(void* out);            /* ncclGetUniqueId (rank 0), to be shared with every rank */
+/* world communicator from the id, then ncclCommSplit into row / column communicators */
+int bf_dist_init(const void* nccl_unique_id, int rank, int nranks, int pr, int pc, bf_dist** out);
+int bf_dist_set_option(bf_dist* d, const char* name, int64_t value); /* "reserve", "fan", "lookahead" */
+int bf_dist_finalize(bf_dist* d);
+int64_t bf_dist_local_elems(int64_t n, int64_t nb, int pr, int pc, int rank);            /* host only */
+int64_t bf_dist_panel_offset(int64_t n, int64_t nb, int pr, int pc, int rank, int64_t q); /* host only */
+/* synthetic SPD input A = S + n I (S symmetric, entries U[-1,1) from a counter
+ * hash of (max(i,j), min(i,j), seed)): a rank fills its own tiles, so no rank
+ * ever holds the whole matrix; bf_fill_synthetic_d fills a full view with the
+ * same values (the one-GPU comparison) */
+int bf_dist_fill_synthetic_d(int64_t n, int64_t nb, int pr, int pc, int rank, double* local, uint64_t seed,
+                             void* stream);
+int bf_fill_synthetic_d(const bf_view* a, uint64_t seed, void* stream);
+/* factor this rank's panels in place (factor/cholesky.py:118-151 at a
+ * variant-3 root, distributed); levels[0] = root (variant 3, bs = nb, kc),
+ * levels[1..] = the diagonal tiles' tree.  Bit-identical to bf_cholesky_d on
+ * one GPU with the same tree.  Synchronises `stream`. */
+int bf_chol_dist_d(bf_dist* d, double* local, int64_t n, const bf_chol_level* levels, int nlevels, int* d_info,
+                   void* stream);
+int bf_cholesky_dist_d(bf_dist* d, double* local, int64_t n, const bf_chol_level* levels, int nlevels, int* d_info,
+                       void* stream); /* alias of bf_chol_dist_d */
+
 #ifdef __cplusplus
 }
 #endif

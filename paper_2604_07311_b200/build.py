@@ -21,6 +21,23 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include"), "-I", str(CSRC)]
 
 
+def _nccl_include() -> list[str]:
+    """NCCL headers for dist.cu (types only: the library dlopens libnccl.so.2 at
+    run time).  The venv's NCCL 2.28 is the one torch loads."""
+    try:
+        import nvidia.nccl
+
+        inc = Path(list(nvidia.nccl.__path__)[0]) / "include"
+        if (inc / "nccl.h").exists():
+            return ["-I", str(inc)]
+    except ImportError:
+        pass
+    return []
+
+
+FLAGS += _nccl_include()
+
+
 def sources() -> list[Path]:
     return sorted(CSRC.glob("*.cu"))
 
@@ -53,7 +70,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
                 if verbose:
                     sys.stderr.write(res.stderr)
     if jobs or not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart", "-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             sys.stderr.write(res.stdout + res.stderr)

@@ -800,6 +800,15 @@ inline cudaStream_t S(void* p) { return static_cast<cudaStream_t>(p); }
 
 }  // namespace
 
+namespace bf {
+// bridges for the other translation units (dist.cu)
+int gemm_d_limited(double alpha, const bf_view& a, const bf_view& b, double beta, const bf_view& c, int lower_only,
+                   int64_t kc, const int* d_abort, int64_t abort_limit, cudaStream_t s) {
+  return gemm_impl(MODE_D, alpha, a, b, beta, c, lower_only, kc, d_abort, s, abort_limit);
+}
+int set_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace bf
+
 extern "C" {
 
 int bf_abi_version(void) { return 1; }

@@ -112,3 +112,71 @@ class BlockCyclic2D:
                     h, w = self.tile_len(i), self.tile_len(j)
                     full[i * self.nb:i * self.nb + h, j * self.nb:j * self.nb + w] = loc[r0:r0 + h, c0:c0 + w]
         return full
+
+
+@dataclass(frozen=True)
+class LowerPanels:
+    """Lower column-panel storage of one rank (mirror of csrc/dist_layout.h, the
+    layout the native NCCL driver bf_chol_dist_d factors).
+
+    Rank (prow, pcol) keeps, for each of its column tiles J = pcol + q*pc, ONE
+    row-major panel holding its row tiles I >= J stacked (leading dimension
+    tile_len(J)); panels follow each other in q order.  Only lower tiles are
+    stored: about n^2 / (2P) elements per rank."""
+
+    n: int
+    nb: int
+    pr: int
+    pc: int
+    rank: int
+
+    @property
+    def base(self) -> BlockCyclic2D:
+        return BlockCyclic2D(self.n, self.nb, self.pr, self.pc)
+
+    @property
+    def prow(self) -> int:
+        return self.rank // self.pc
+
+    @property
+    def pcol(self) -> int:
+        return self.rank % self.pc
+
+    def first_row_geq(self, p: int, t: int) -> int:
+        return 0 if t <= p else (t - p + self.pr - 1) // self.pr
+
+    def rows_of(self, p: int, i0: int, i1: int) -> int:
+        b = self.base
+        return sum(b.tile_len(p + i * self.pr) for i in range(i0, i1))
+
+    def panels(self) -> list[tuple[int, int, int, int, int]]:
+        """[(J, first local row-tile index, height, width, element offset)]."""
+        b = self.base
+        out, off = [], 0
+        nrt = len(b.row_tiles(self.prow))
+        for J in b.col_tiles(self.pcol):
+            i0 = self.first_row_geq(self.prow, J)
+            h, w = self.rows_of(self.prow, i0, nrt), b.tile_len(J)
+            out.append((J, i0, h, w, off))
+            off += h * w
+        return out
+
+    def local_elems(self) -> int:
+        return sum(h * w for _, _, h, w, _ in self.panels())
+
+    def _rows(self, i0: int, h: int) -> np.ndarray:
+        """Global row indices of a panel's h rows starting at local row tile i0."""
+        r = np.arange(h)
+        return (self.prow + (i0 + r // self.nb) * self.pr) * self.nb + r % self.nb
+
+    def scatter(self, full: np.ndarray) -> np.ndarray:
+        out = np.zeros(self.local_elems(), dtype=full.dtype)
+        for J, i0, h, w, off in self.panels():
+            rows = self._rows(i0, h)
+            out[off:off + h * w] = full[rows, J * self.nb:J * self.nb + w].reshape(-1)
+        return out
+
+    def gather_into(self, local: np.ndarray, full: np.ndarray) -> None:
+        for J, i0, h, w, off in self.panels():
+            rows = self._rows(i0, h)
+            full[rows, J * self.nb:J * self.nb + w] = local[off:off + h * w].reshape(h, w)

@@ -136,6 +136,18 @@ _SIGNATURES = {
     "bf_pack_scatter_d": ([_SV, _I, _VP, _VP], _I),
     "bf_gemm_scatter_s": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
     "bf_gemm_scatter_sd": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
+    "bf_dist_available": ([], _I),
+    "bf_dist_unique_id_bytes": ([], _I),
+    "bf_dist_unique_id": ([_VP], _I),
+    "bf_dist_init": ([_VP, _I, _I, _I, _I, _P(_VP)], _I),
+    "bf_dist_set_option": ([_VP, ctypes.c_char_p, _L], _I),
+    "bf_dist_finalize": ([_VP], _I),
+    "bf_dist_local_elems": ([_L, _L, _I, _I, _I], _L),
+    "bf_dist_panel_offset": ([_L, _L, _I, _I, _I, _L], _L),
+    "bf_dist_fill_synthetic_d": ([_L, _L, _I, _I, _I, _VP, ctypes.c_uint64, _VP], _I),
+    "bf_fill_synthetic_d": ([_V, ctypes.c_uint64, _VP], _I),
+    "bf_chol_dist_d": ([_VP, _VP, _L, _P(BfCholLevel), _I, _VP, _VP], _I),
+    "bf_cholesky_dist_d": ([_VP, _VP, _L, _P(BfCholLevel), _I, _VP, _VP], _I),
 }
 
 

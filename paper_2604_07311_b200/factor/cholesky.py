@@ -66,6 +66,15 @@ def cholesky_async(
     if a.n == 0:
         return info
     _lib.require_cuda(a)
+    if engine == "native" and _distributed_ways(tree):
+        # root ways = the ranks of the default process group: the tiles are
+        # factored over them by the NCCL driver and every rank gets the factor
+        from ..dist.native import cholesky_replicated
+
+        full = a.storage.as_strided((a.n, a.n), (a.rs, a.cs), a.offset)
+        bad = cholesky_replicated(full, tree, _dist_context())
+        info.fill_(bad)
+        return info
     if engine == "native":
         levels = flatten_cholesky(tree, cfg)
         arr = (_lib.BfCholLevel * len(levels))(*[_lib.BfCholLevel(v, 0, bs, kc) for v, bs, kc in levels])
@@ -78,6 +87,31 @@ def cholesky_async(
     else:
         raise ValueError(f"unknown engine {engine!r}")
     return info
+
+
+_DIST_CTX = None
+
+
+def _distributed_ways(tree: ControlNode) -> bool:
+    """Root `ways` > 1 selects the multi-GPU driver when torch.distributed is
+    initialised with exactly that many ranks (one process per GPU).  Otherwise
+    `ways` keeps its single-GPU meaning: a parallel width the CTA grid already
+    covers (results are identical for every width)."""
+    ways = tree.ways or 1
+    if ways <= 1 or tree.variant != 3 or not tree.bs:
+        return False
+    import torch.distributed as dist
+
+    return dist.is_available() and dist.is_initialized() and dist.get_world_size() == ways
+
+
+def _dist_context():
+    global _DIST_CTX
+    if _DIST_CTX is None:
+        from ..dist.native import DistContext
+
+        _DIST_CTX = DistContext.from_torch_distributed()
+    return _DIST_CTX
 
 
 # -- the tree walk, operation for operation as factor/cholesky.py:118-158 ---------

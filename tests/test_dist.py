@@ -1,6 +1,6 @@
 """Multi-rank 2D block-cyclic Cholesky.
 
-CPU: world_size 2 and 4 under gloo, the distribution/communication logic
+CPU: world_size 2, 4 and 8 (grids 1x2, 2x2, 2x4) under gloo, the distribution/communication logic
 driven with the oracle as the per-tile compute (test-side stand-in), checked
 bit for bit against the single-process oracle factorization.
 GPU: the 1x1 grid against bf.cholesky, and 2 ranks sharing one GPU with a
@@ -132,7 +132,7 @@ def test_layout_roundtrip_and_ownership():
     assert [grid_for(p) for p in (1, 2, 4, 8)] == [(1, 1), (1, 2), (2, 2), (2, 4)]
 
 
-@pytest.mark.parametrize("world,n", [(1, 150), (2, 200), (4, 250)])
+@pytest.mark.parametrize("world,n", [(1, 150), (2, 200), (4, 250), (8, 400)])
 def test_distributed_bitwise_equals_single_process_cpu(tmp_path, world, n):
     full, bads = _run(world, n, 48, tmp_path)
     ref, bad = _oracle_full(n)

@@ -12,7 +12,7 @@
 //     cut into kc segments; every C element's segment sum is an ascending fma
 //     chain from +0 (micro-kernel compiled with fastmath={"contract"},
 //     engine/kernels.py:169-172); the segment is folded into C with the
-//     unfused C = beta_eff*C + alpha*t (engine/kernels.py:585-610).
+//     unfused C = beta_eff*C + alpha*t (engine/kernels.py:228-253).
 //   * leaves: factor/cholesky.py:31-89 with numba's typing (sums that start
 //     at the literal 0.0 are f64 even for f32 storage).
 //   * trsm: engine/trsm.py:51-68 recursion, base engine/trsm.py:96-111.

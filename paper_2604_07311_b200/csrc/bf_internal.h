@@ -70,6 +70,13 @@ __device__ __forceinline__ bool aborted(const GemmParams& p) {
 // kernels ran in a timed region.
 void note_launch(int64_t n = 1);
 
+// Raise a kernel's dynamic shared-memory limit on the CURRENT device, once per
+// (kernel, device): cudaFuncSetAttribute only applies to the calling device's
+// context, so a process-wide "done" flag would skip every other GPU.
+bool smem_attr(const void* kern, int bytes);
+// device scratch keyed by (tag, current device, stream); grows on demand
+void* stream_scratch(int tag, size_t bytes, cudaStream_t s);
+
 // Kernel-family entry points (implemented in the .cu files).
 int launch_gemm_dmma(const GemmParams& p, cudaStream_t s);            // f64 storage, f64 acc
 bool gemm_dmma_tma_eligible(const GemmParams& p);                     // TMA/mbarrier fast path?

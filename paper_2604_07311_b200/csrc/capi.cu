@@ -12,12 +12,71 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <map>
 #include <mutex>
 #include <vector>
 
 namespace bf {
 static std::atomic<int64_t> g_launches{0};
 void note_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Device scratch private to one (purpose, device, stream): work queued on
+// different streams never shares a buffer, and growing one only waits for
+// its own stream.
+void* stream_scratch(int tag, size_t bytes, cudaStream_t s) {
+  struct Key {
+    int tag, dev;
+    cudaStream_t s;
+    bool operator<(const Key& o) const {
+      return tag != o.tag ? tag < o.tag : (dev != o.dev ? dev < o.dev : s < o.s);
+    }
+  };
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  static std::mutex mu;
+  static std::map<Key, Buf> bufs;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  Buf& b = bufs[Key{tag, dev, s}];
+  if (b.bytes < bytes) {
+    if (b.p) {
+      cudaStreamSynchronize(s);  // the old buffer may still be read by work queued on s
+      cudaFree(b.p);
+    }
+    b.p = nullptr;
+    b.bytes = 0;
+    if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    b.bytes = bytes;
+  }
+  return b.p;
+}
+
+bool smem_attr(const void* kern, int bytes) {
+  struct Key {
+    const void* k;
+    int dev;
+    bool operator<(const Key& o) const { return k < o.k || (k == o.k && dev < o.dev); }
+  };
+  static std::mutex mu;
+  static std::map<Key, int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[Key{kern, dev}];
+  if (have >= bytes) return true;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  have = bytes;
+  return true;
+}
 }  // namespace bf
 
 namespace {
@@ -623,28 +682,11 @@ int apply_pivots_impl(Mode mode, const bf_view& a, const int64_t* piv, int64_t c
   return rc ? fail(BF_ERR_CUDA, "row swap launch failed") : BF_OK;
 }
 
-// device scratch for the LU's k-major copies (grows; one LU at a time per
-// device — the walk is single-stream)
-// one buffer per device and stream role: the lookahead's panel stream runs
-// child-level GEMMs concurrently with the main stream's trailing update
+// device scratch for the LU's k-major copies: private to the calling stream
+// (the lookahead's panel stream runs child-level GEMMs concurrently with the
+// main stream's trailing update, and callers may run LUs on several streams)
 double* lu_scratch(size_t elems, cudaStream_t s) {
-  static double* buf[64][2] = {};
-  static size_t cap[64][2] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
-  const int slot = s != nullptr && s == panel_stream() ? 1 : 0;
-  if (cap[dev][slot] < elems) {
-    if (buf[dev][slot]) {
-      cudaDeviceSynchronize();
-      cudaFree(buf[dev][slot]);
-    }
-    buf[dev][slot] = nullptr;
-    cap[dev][slot] = 0;
-    if (cudaMalloc(&buf[dev][slot], elems * sizeof(double)) != cudaSuccess) return nullptr;
-    cap[dev][slot] = elems;
-  }
-  return buf[dev][slot];
+  return static_cast<double*>(bf::stream_scratch(2, elems * sizeof(double), s));
 }
 
 // levels: variant 20 = blocked, 21 = unblocked leaf (flatten of the lu tree)
@@ -1027,11 +1069,28 @@ int bf_cholesky_host_d(double* host, int64_t ld, const bf_view* work, const bf_c
     cudaStreamWaitEvent(hs, start, 0);
     cudaEventDestroy(start);
   }
+  // Every exit below joins the h2d and copy streams into s first, so when the
+  // caller's stream completes no copy into or out of the host matrix is
+  // still in flight (also after an error), and destroys the load events.
+  auto join = [&](cudaStream_t from) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventRecord(e, from);
+    cudaStreamWaitEvent(s, e, 0);
+    cudaEventDestroy(e);
+  };
+  auto finish = [&](int code) {
+    if (overlap) join(hs);
+    join(cs);
+    for (auto e : hl.ev) cudaEventDestroy(e);
+    hl.ev.clear();
+    return code;
+  };
   for (int64_t c0 = 0; c0 < n; c0 += bs) {
     const int64_t w = bs < n - c0 ? bs : n - c0;
     if (cudaMemcpy2DAsync(dev + c0 * work->rs + c0, size_t(work->rs) * 8, host + c0 * ld + c0, size_t(ld) * 8,
                           size_t(w) * 8, size_t(n - c0), cudaMemcpyHostToDevice, hs) != cudaSuccess)
-      return fail(BF_ERR_CUDA, "host to device copy failed");
+      return finish(fail(BF_ERR_CUDA, "host to device copy failed"));
     if (overlap) {
       cudaEvent_t e;
       cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
@@ -1048,28 +1107,14 @@ int bf_cholesky_host_d(double* host, int64_t ld, const bf_view* work, const bf_c
   int rc = chol_impl(MODE_D, work, levels, nlevels, d_info, s);
   g_wb = nullptr;
   g_h2d = nullptr;
-  if (overlap) {
-    // every copy is complete before the caller's stream moves on
-    cudaEvent_t done;
-    cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
-    cudaEventRecord(done, hs);
-    cudaStreamWaitEvent(s, done, 0);
-    cudaEventDestroy(done);
-    for (auto e : hl.ev) cudaEventDestroy(e);
-  }
-  if (rc) return rc;
+  if (rc) return finish(rc);
   // whatever the lookahead did not stream back (the non-lookahead path, or all of it)
   for (int64_t c0 = wb.copied_upto; c0 < n; c0 += bs) {
     const int64_t w = bs < n - c0 ? bs : n - c0;
     cudaMemcpy2DAsync(host + c0 * ld + c0, size_t(ld) * 8, dev + c0 * work->rs + c0, size_t(work->rs) * 8,
                       size_t(w) * 8, size_t(n - c0), cudaMemcpyDeviceToHost, s);
   }
-  // the caller's stream completes only after every copy
-  cudaEvent_t ev;
-  cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-  cudaEventRecord(ev, cs);
-  cudaStreamWaitEvent(s, ev, 0);
-  cudaEventDestroy(ev);
+  finish(BF_OK);
   return cudaGetLastError() == cudaSuccess ? BF_OK : fail(BF_ERR_CUDA, "host factorization copies failed");
 }
 int bf_lu_d(const bf_view* a, const bf_chol_level* levels, int nlevels, int64_t* d_piv, int* d_sing, void* stream) {
@@ -1392,24 +1437,10 @@ int bf_gemm_f32_tc(double alpha, const bf_view* a, const bf_view* b, double beta
   if (m == 0 || n == 0) return BF_OK;
   cudaStream_t s = S(stream);
   if (k == 0 || alpha == 0.0) return scale_impl(MODE_S, beta, *c, lower_only, s);
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return fail(BF_ERR_CUDA, "device index");
-  static float* ws[64] = {};
-  static size_t ws_bytes[64] = {};
   const int64_t kp = (k + 3) / 4 * 4, ld = 4 * kp;
   const size_t need = size_t(m + n) * size_t(ld) * sizeof(float);
-  if (need > ws_bytes[dev]) {
-    if (ws[dev]) {
-      cudaDeviceSynchronize();
-      cudaFree(ws[dev]);
-    }
-    ws[dev] = nullptr;
-    ws_bytes[dev] = 0;
-    if (cudaMalloc(&ws[dev], need) != cudaSuccess) return fail(BF_ERR_CUDA, "tf32 split workspace");
-    ws_bytes[dev] = need;
-  }
-  float* sa = ws[dev];
+  float* sa = static_cast<float*>(bf::stream_scratch(1, need, s));  // private to this stream
+  if (!sa) return fail(BF_ERR_CUDA, "tf32 split workspace");
   float* sb = sa + m * ld;
   int rc = bf::launch_split_tf32(0, a->base, a->off, a->rs, a->cs, sa, ld, m, k, kp, s);
   const bf_view bt = transposed(*b);  // rows of B^T: the k-contiguous N x K operand

@@ -256,6 +256,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(acc_empty(buf)) : "memory");
       mbar_wait_tc(cload, lt & 1u);
       const int64_t gi = ti * TC_BM + r;
+      // a GEMMT diagonal tile must not write its strict upper part (the bulk
+      // store would rewrite it with the values loaded before the mainloop):
+      // its lower elements go out per element instead
+      const bool diag = p.lower_only && ti == tj;
+      float* Cg = static_cast<float*>(p.c);
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb) {
 #pragma unroll
@@ -271,16 +276,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (!p.lower_only || gj <= gi) {
               const float v = alpha * __uint_as_float(acc[cb][c * 4 + e]);
               o[e] = beta != 0.f ? fmaf(beta, o[e], v) : v;
+              if (diag && gi < p.m && gj < p.n) __stcs(Cg + p.c_off + gi * p.c_rs + gj * p.c_cs, o[e]);
             }
           }
-          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "f"(o[0]), "f"(o[1]), "f"(o[2]),
-                       "f"(o[3])
-                       : "memory");
+          if (!diag)
+            asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(addr), "f"(o[0]), "f"(o[1]), "f"(o[2]),
+                         "f"(o[3])
+                         : "memory");
         }
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (leader) {
+      if (leader && !diag) {
 #pragma unroll
         for (int cb = 0; cb < 4; ++cb)
           asm volatile(
@@ -477,19 +484,11 @@ int launch_tc(int tf32, double alpha, const void* a, int64_t lda, const void* b,
   } else if (!make_map_bf16(&ma, a, m, k, lda) || !make_map_bf16(&mb, b, n, k, ldb)) {
     return -3;
   }
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(gemm_bf16_tc_kernel<true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(TC_SMEM)) != cudaSuccess ||
-        cudaFuncSetAttribute(gemm_bf16_tc_kernel<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(TC_SMEM)) != cudaSuccess ||
-        cudaFuncSetAttribute(gemm_bf16_tc_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(TC_SMEM)) != cudaSuccess ||
-        cudaFuncSetAttribute(gemm_bf16_tc_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(TC_SMEM)) != cudaSuccess)
-      return -10;
-    attr = true;
-  }
+  if (!smem_attr(reinterpret_cast<const void*>(gemm_bf16_tc_kernel<true, 0>), int(TC_SMEM)) ||
+      !smem_attr(reinterpret_cast<const void*>(gemm_bf16_tc_kernel<false, 0>), int(TC_SMEM)) ||
+      !smem_attr(reinterpret_cast<const void*>(gemm_bf16_tc_kernel<true, 1>), int(TC_SMEM)) ||
+      !smem_attr(reinterpret_cast<const void*>(gemm_bf16_tc_kernel<false, 1>), int(TC_SMEM)))
+    return -10;
   // TMA C path: unit column stride, 16-byte aligned rows and base, and whole
   // 16-byte row ends (a bulk store clips out-of-bounds columns per 16 bytes)
   CUtensorMap mc;

@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_dmma_kernel(const GemmPa
     const int64_t seg = kt / tps, sub = kt - seg * tps;
     const bool seg_done = (seg < nseg - 1) ? (sub == tps - 1) : (sub == tps_last - 1);
     if (seg_done) {
-      // fold the segment into C: C = beta_eff*C + alpha*t  (engine/kernels.py:585-610);
+      // fold the segment into C: C = beta_eff*C + alpha*t  (engine/kernels.py:228-253);
       // one row fragment at a time, its reads issued before its writes
       const double beta_eff = seg == 0 ? p.beta : 1.0;
 #pragma unroll
@@ -328,13 +328,8 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1) gemm_dmma_kernel(const GemmPa
 // ---------------------------------------------------------------------------
 template <class Cfg>
 static int run_cfg(const GemmParams& p_in, cudaStream_t s) {
-  static bool attr_set = false;
   auto kern = gemm_dmma_kernel<Cfg>;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM));
-    if (e != cudaSuccess) return -10;
-    attr_set = true;
-  }
+  if (!smem_attr(reinterpret_cast<const void*>(kern), int(Cfg::SMEM))) return -10;
   GemmParams p = p_in;
   p.tiles_m = int((p.m + Cfg::BM - 1) / Cfg::BM);
   p.tiles_n = int((p.n + Cfg::BN - 1) / Cfg::BN);

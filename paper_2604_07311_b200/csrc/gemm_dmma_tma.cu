@@ -460,17 +460,16 @@ int g_tma_variant = 2;  // 0: m8n8k4/1 box/6 stages, 1: m16n8k8/1/6, 2: m8n8k4/2
 
 template <int MMAK, int KBOX, int STAGES>
 static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t s) {
-  static size_t attr_smem = 0;
   constexpr size_t base_smem = size_t(STAGES) * 2 * KBOX * TM_TILE_BYTES + 1024 + 8 * STAGES;
   constexpr size_t max_smem = 200 * 1024;  // leaves room for the static __shared__ words
   auto kern = gemm_dmma_tma_kernel<MMAK, KBOX, STAGES>;
   GemmParams p = p_in;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  static int sms_dev[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return -3;
+  if (!sms_dev[dev]) cudaDeviceGetAttribute(&sms_dev[dev], cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sms_dev[dev];
   // tiles per CTA: g_tiles_per_cta (0 = fully persistent, one CTA per SM)
   int64_t tpc = g_tiles_per_cta > 0 ? g_tiles_per_cta : (p.num_tiles + sms - 1) / sms;
   if (t_reserve_sms > 0 && t_reserve_sms < sms) {
@@ -493,13 +492,7 @@ static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensor
   if (grid > 0x7fffffffLL) return -3;
   if (p.m >= (1 << 16) * int64_t(TM_BM) || p.n >= (1 << 16) * int64_t(TM_BN)) return -3;
   const size_t smem = base_smem + size_t(tpc) * 4;
-  if (smem > attr_smem) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
-      cudaGetLastError();
-      return -10;
-    }
-    attr_smem = smem;
-  }
+  if (!smem_attr(reinterpret_cast<const void*>(kern), int(smem))) return -10;
   note_launch();
   kern<<<unsigned(grid), TM_THREADS, smem, s>>>(ma, mb, p);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;

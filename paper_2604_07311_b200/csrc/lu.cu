@@ -692,21 +692,13 @@ int launch_lu_leaf(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int
       cfg.numAttrs = 1;
       cudaError_t e;
       if (is_f64) {
-        static bool attr = false;
-        if (!attr) {
-          cudaFuncSetAttribute(lu_leaf_cluster_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-          cudaFuncSetAttribute(lu_leaf_cluster_kernel<double>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-          attr = true;
-        }
+        smem_attr(reinterpret_cast<const void*>(lu_leaf_cluster_kernel<double>), 210 * 1024);
+        cudaFuncSetAttribute(lu_leaf_cluster_kernel<double>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         e = cudaLaunchKernelEx(&cfg, lu_leaf_cluster_kernel<double>, static_cast<double*>(a), off, rs, cs, m, n, piv,
                                d_sing, base, chunk);
       } else {
-        static bool attr = false;
-        if (!attr) {
-          cudaFuncSetAttribute(lu_leaf_cluster_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-          cudaFuncSetAttribute(lu_leaf_cluster_kernel<float>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-          attr = true;
-        }
+        smem_attr(reinterpret_cast<const void*>(lu_leaf_cluster_kernel<float>), 210 * 1024);
+        cudaFuncSetAttribute(lu_leaf_cluster_kernel<float>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         e = cudaLaunchKernelEx(&cfg, lu_leaf_cluster_kernel<float>, static_cast<float*>(a), off, rs, cs, m, n, piv,
                                d_sing, base, chunk);
       }
@@ -743,11 +735,7 @@ int launch_lu_leaf(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int
       void* rowk = static_cast<char*>(cand) + size_t(2) * 32 * size_t(n) * esz;
       const int Gi = int(Gs);
       if (is_f64) {
-        static bool attr = false;
-        if (!attr) {
-          cudaFuncSetAttribute(lu_leaf_smem_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-          attr = true;
-        }
+        smem_attr(reinterpret_cast<const void*>(lu_leaf_smem_kernel<double>), 200 * 1024);
         double* ad = static_cast<double*>(a);
         double* cd = static_cast<double*>(cand);
         double* rd = static_cast<double*>(rowk);
@@ -755,11 +743,7 @@ int launch_lu_leaf(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, int
         e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(lu_leaf_smem_kernel<double>), dim3(Gi),
                                         dim3(LU_THREADS), args, smem, s);
       } else {
-        static bool attr = false;
-        if (!attr) {
-          cudaFuncSetAttribute(lu_leaf_smem_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-          attr = true;
-        }
+        smem_attr(reinterpret_cast<const void*>(lu_leaf_smem_kernel<float>), 200 * 1024);
         float* af = static_cast<float*>(a);
         float* cf = static_cast<float*>(cand);
         float* rf = static_cast<float*>(rowk);

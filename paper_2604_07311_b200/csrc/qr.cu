@@ -366,14 +366,14 @@ int launch_qr_panel(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, in
       cudaError_t e;
       if (is_f64) {
         auto k = qr_panel_smem_kernel<double>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        smem_attr(reinterpret_cast<const void*>(k), 200 * 1024);
         double* ad = static_cast<double*>(a);
         double* td = static_cast<double*>(taus);
         void* args[] = {&ad, &off, &rs, &cs, &m, &b, &td, &pp, &rb, &chunk};
         e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k), dim3(G), dim3(QR_THREADS), args, smem, s);
       } else {
         auto k = qr_panel_smem_kernel<float>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        smem_attr(reinterpret_cast<const void*>(k), 200 * 1024);
         float* af = static_cast<float*>(a);
         float* tf = static_cast<float*>(taus);
         void* args[] = {&af, &off, &rs, &cs, &m, &b, &tf, &pp, &rb, &chunk};
@@ -410,11 +410,11 @@ int launch_qr_t(int is_f64, const void* gram, int64_t b, const void* taus, void*
   const size_t smem = size_t(b * (b + 1) + 4 * QT_LEAF * 33 + 64 * QT_XLD) * sizeof(double);
   note_launch();
   if (is_f64) {
-    cudaFuncSetAttribute(qr_t_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    smem_attr(reinterpret_cast<const void*>(qr_t_kernel<double>), 220 * 1024);
     qr_t_kernel<double><<<1, 256, smem, s>>>(static_cast<const double*>(gram), b, static_cast<const double*>(taus),
                                              static_cast<double*>(t));
   } else {
-    cudaFuncSetAttribute(qr_t_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    smem_attr(reinterpret_cast<const void*>(qr_t_kernel<float>), 220 * 1024);
     qr_t_kernel<float><<<1, 256, smem, s>>>(static_cast<const float*>(gram), b, static_cast<const float*>(taus),
                                             static_cast<float*>(t));
   }

@@ -1167,13 +1167,7 @@ template <typename T, int W>
 int launch_trsm_warp(double alpha, const T* t, int64_t toff, int64_t trs, int64_t tcs, T* b, int64_t boff,
                      int64_t brs, int64_t bcs, int64_t m, int n, int64_t kc, const int* abort_flag, cudaStream_t s) {
   const size_t smem = (size_t(128) * TW_LD + size_t(W) * 128 * TW_XLD) * sizeof(T);  // W groups
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(trsm_warp_right_kernel<T, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
-        cudaSuccess)
-      return -10;
-    attr = true;
-  }
+  if (!smem_attr(reinterpret_cast<const void*>(trsm_warp_right_kernel<T, W>), int(smem))) return -10;
   const int64_t blocks = (m + 32 * W - 1) / (32 * W);
   if (blocks > 0x7fffffffLL) return -3;
   note_launch();
@@ -1205,40 +1199,22 @@ template <typename T>
 static int leaf_launch(T* a, int64_t off, int64_t n, int64_t rs, int64_t cs, int variant, int64_t base_index,
                        int* d_info, cudaStream_t s) {
   if (variant == 3 && n <= 128 && g_leaf_blocked) {
-    static bool v4_attr = false;
     const size_t smem = size_t(128) * LV4_LD * sizeof(T);
-    if (!v4_attr) {
-      if (cudaFuncSetAttribute(potrf_leaf_blocked_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
-          cudaSuccess)
-        return -10;
-      v4_attr = true;
-    }
+    if (!smem_attr(reinterpret_cast<const void*>(potrf_leaf_blocked_kernel<T>), int(smem))) return -10;
     note_launch();
     potrf_leaf_blocked_kernel<T><<<1, 128, smem, s>>>(a, off, int(n), rs, cs, base_index, d_info);
     return cudaGetLastError() == cudaSuccess ? 0 : -11;
   }
   if (variant == 3 && n <= 128) {
-    static bool v3_attr = false;
     const size_t smem = size_t(128) * 129 * sizeof(T);  // full tile: the update reads rows < 128 unguarded
-    if (!v3_attr) {
-      if (cudaFuncSetAttribute(potrf_leaf_v3_smem_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(128 * 129 * sizeof(T))) != cudaSuccess)
-        return -10;
-      v3_attr = true;
-    }
+    if (!smem_attr(reinterpret_cast<const void*>(potrf_leaf_v3_smem_kernel<T>), int(smem))) return -10;
     note_launch();
     potrf_leaf_v3_smem_kernel<T><<<1, 256, smem, s>>>(a, off, int(n), rs, cs, base_index, d_info);
     return cudaGetLastError() == cudaSuccess ? 0 : -11;
   }
   size_t smem = size_t(n) * (n + 1) * sizeof(T) + size_t(n) * sizeof(double);
   if (smem <= size_t(LEAF_SMEM_LIMIT)) {
-    static bool attr = false;
-    if (!attr) {
-      if (cudaFuncSetAttribute(potrf_leaf_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               LEAF_SMEM_LIMIT) != cudaSuccess)
-        return -10;
-      attr = true;
-    }
+    if (!smem_attr(reinterpret_cast<const void*>(potrf_leaf_kernel<T, true>), LEAF_SMEM_LIMIT)) return -10;
     note_launch();
     potrf_leaf_kernel<T, true><<<1, LEAF_THREADS, smem, s>>>(a, off, int(n), rs, cs, variant, base_index, d_info,
                                                               nullptr);
@@ -1309,24 +1285,12 @@ int launch_trsm_small_right(int is_f64, double alpha, const void* t, int64_t tof
   note_launch();
   if (is_f64) {
     const size_t smem = size_t(128 + TS_ROWS) * TS_LD * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      if (cudaFuncSetAttribute(trsm_small_right_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem)) != cudaSuccess)
-        return -10;
-      attr = true;
-    }
+    if (!smem_attr(reinterpret_cast<const void*>(trsm_small_right_kernel<double>), int(smem))) return -10;
     trsm_small_right_kernel<double><<<unsigned(blocks), TS_THREADS, smem, s>>>(
         alpha, (const double*)t, toff, trs, tcs, (double*)b, boff, brs, bcs, m, int(n), kc, abort_flag);
   } else {
     const size_t smem = size_t(128 + TS_ROWS) * TS_LD * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-      if (cudaFuncSetAttribute(trsm_small_right_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem)) != cudaSuccess)
-        return -10;
-      attr = true;
-    }
+    if (!smem_attr(reinterpret_cast<const void*>(trsm_small_right_kernel<float>), int(smem))) return -10;
     trsm_small_right_kernel<float><<<unsigned(blocks), TS_THREADS, smem, s>>>(
         alpha, (const float*)t, toff, trs, tcs, (float*)b, boff, brs, bcs, m, int(n), kc, abort_flag);
   }

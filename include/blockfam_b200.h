@@ -260,6 +260,20 @@ int bf_gemm_tf32(double alpha, const float* a, int64_t lda, const float* b, int6
 int bf_gemm_f32_tc(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c, int lower_only,
                    void* stream);
 int bf_convert_f64_f32(const bf_view* src, const bf_view* dst, int lower_only, void* stream);
+/* Mixed-precision factorization driver (BASELINE configs[3]; no reference
+ * counterpart — engine/config.py:21,39 is the reference's only mixed mode):
+ * W (fp32, n x n, leading dimension ldw) := the lower factor of A (fp64) with
+ * FP64 diagonal blocks (the control tree `lv` on each bs x bs block, global
+ * pivot index in d_info), their explicit inverses X_k = L_kk^-T (FP64, stored
+ * fp32 in xinv[k], bs x bs each), the panels L21 = A21 X_k and the trailing
+ * updates on the tensor cores (precision 0: bf16 kind::f16, 1: tf32).
+ * Workspace: pbuf0/pbuf1 (n x bs panel copies: bf16, or fp32 for tf32),
+ * xt (bs x bs), d64 and x64 (bs x bs fp64).  lookahead = 1 runs each next
+ * diagonal/inverse/panel on the library's high-priority stream while the
+ * trailing GEMMT leaves SMs to it (bf_set_option("mixed_reserve", r)). */
+int bf_cholesky_mixed(const bf_view* a, float* w, int64_t ldw, void* pbuf0, void* pbuf1, void* xt, double* d64,
+                      double* x64, float* xinv, int64_t bs, const bf_chol_level* lv, int nl, int precision,
+                      int lookahead, int* d_info, void* stream);
 int bf_convert_f32_f64(const bf_view* src, const bf_view* dst, int lower_only, void* stream);
 int bf_convert_f64_bf16(const bf_view* src, void* dst, int64_t ld, int transpose, void* stream);
 int bf_residual_d(const double* a, int64_t lda, const double* x, const double* b, double* r, int64_t n, void* stream);

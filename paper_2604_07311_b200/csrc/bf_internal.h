@@ -76,6 +76,10 @@ void note_launch(int64_t n = 1);
 bool smem_attr(const void* kern, int bytes);
 // device scratch keyed by (tag, current device, stream); grows on demand
 void* stream_scratch(int tag, size_t bytes, cudaStream_t s);
+// capi.cu bridges for the other translation units
+int set_error(int code, const char* msg);
+cudaStream_t panel_stream_for_device();  // the high-priority panel stream of the current device
+extern int g_mixed_reserve;
 
 // Kernel-family entry points (implemented in the .cu files).
 int launch_gemm_dmma(const GemmParams& p, cudaStream_t s);            // f64 storage, f64 acc
@@ -88,6 +92,7 @@ extern int g_use_tma;         // bf_set_option("tma", 0|1)
 extern int g_tma_variant;     // bf_set_option("tma_variant", 0..3)
 extern int g_persist;         // bf_set_option("persist", 0|1): strided persistent grid for long-K GEMMs
 extern int g_red_fold;        // bf_set_option("red_fold", 0|1): TMA kernel folds with red.global.add.f64
+extern int g_tmem_fold;       // bf_set_option("tmem_fold", 0|1): TMA kernel keeps C in TMEM across kc folds
 extern int g_reserve_strided;
 extern thread_local int t_reserve_sms;  // gemm_dmma_tma.cu: SMs left free by the next launch
 extern int g_tiles_per_cta;   // bf_set_option("tiles_per_cta", t)

@@ -849,6 +849,7 @@ int gemm_d_limited(double alpha, const bf_view& a, const bf_view& b, double beta
   return gemm_impl(MODE_D, alpha, a, b, beta, c, lower_only, kc, d_abort, s, abort_limit);
 }
 int set_error(int code, const char* msg) { return fail(code, msg); }
+cudaStream_t panel_stream_for_device() { return panel_stream(); }
 }  // namespace bf
 
 extern "C" {
@@ -883,6 +884,14 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "persist") == 0) {
     bf::g_persist = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "mixed_reserve") == 0 && value >= 0) {
+    bf::g_mixed_reserve = int(value);
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "tmem_fold") == 0) {
+    bf::g_tmem_fold = value != 0;
     return BF_OK;
   }
   if (name && std::strcmp(name, "red_fold") == 0) {

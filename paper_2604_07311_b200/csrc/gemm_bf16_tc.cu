@@ -516,7 +516,10 @@ int launch_tc(int tf32, double alpha, const void* a, int64_t lda, const void* b,
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int64_t grid = p.num_tiles < sms ? p.num_tiles : sms;
+  // t_reserve_sms: leave SMs to a concurrent high-priority stream (the mixed
+  // solve's diagonal/inverse/panel chain) instead of holding every SM
+  const int ctas = t_reserve_sms > 0 && t_reserve_sms < sms ? sms - t_reserve_sms : sms;
+  const int64_t grid = p.num_tiles < ctas ? p.num_tiles : ctas;
   note_launch();
   if (tf32) {
     if (tmac)

@@ -131,7 +131,17 @@ __device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double (&a)[4]
 // so the TMA for the next tile's first k tiles is in flight while this
 // tile's fold is written back.  MMAK = 4 (m8n8k4) or 8 (m16n8k8); KBOX =
 // 16-wide k boxes per stage.
-template <int MMAK, int KBOX, int STAGES>
+//
+// TMC (long K, many kc segments — the contraction): the running C tile stays
+// on chip, in tensor memory, across the segment folds.  Each thread's 32
+// doubles (64 32-bit TMEM columns in its warp's lane quadrant; warps w and
+// w+4k share a quadrant and take disjoint column ranges, 256 columns in all)
+// are folded in registers 8 at a time (tcgen05.ld -> C + round(alpha*t) ->
+// tcgen05.st), C is read from HBM only for the first segment (beta != 0) and
+// written once after the last.  Same roundings in the same order as the
+// global folds, so the same bits; the C traffic of a K = 16384, kc = 256
+// tile drops from 64 L2 round trips to one read and one write.
+template <int MMAK, int KBOX, int STAGES, bool TMC>
 __global__ void __launch_bounds__(TM_THREADS, 1)
     gemm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                          const GemmParams p) {
@@ -174,7 +184,19 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  __shared__ uint32_t tmem_slot;
+  if constexpr (TMC) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_slot)),
+                   "n"(256));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  }
   __syncthreads();
+  if constexpr (TMC) asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  // this thread's 64 TMEM columns: lane quadrant (warp % 4), column block (warp / 4)
+  const uint32_t tmem_c = TMC ? tmem_slot + (uint32_t((warp & 3) * 32) << 16) + uint32_t((warp >> 2) * 64) : 0u;
 
   // k segmentation in 32-bit (eligibility guarantees K < 2^31, kc % BKS == 0 or kc >= K)
   const int K = int(p.k);
@@ -235,7 +257,9 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     const uint32_t tt = tile_tab[w];
     const int64_t m0 = int64_t(tt >> 16) * TM_BM, n0 = int64_t(tt & 0xffffu) * TM_BN;
     int seg = 0, sub = 0;
-    int pf_kt = pf_next(p.beta != 0.0 ? 0 : 1);
+    // C is prefetched into L2 before each fold that reads it: every segment's
+    // for the global folds, only the first (beta != 0) when C lives in TMEM
+    int pf_kt = TMC ? (p.beta != 0.0 ? pf_next(0) : -1) : pf_next(p.beta != 0.0 ? 0 : 1);
     for (int kt = 0; kt < ntiles; ++kt, ++f) {
       mbar_wait(full(s), uint32_t(round & 1));
       const uint32_t sa = tiles + s * STAGE_BYTES;
@@ -316,7 +340,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         ++round;
       }
       if (kt == pf_kt) {
-        pf_kt = pf_next(kt / tps + 1);
+        pf_kt = TMC ? -1 : pf_next(kt / tps + 1);
         // warm L2 with this warp's 32x32 block of C before this segment's fold
         // reads it (with kc < K the folds recur, and the operand streams evict
         // C from L2 between them: d=128 contraction, 64 folds per tile)
@@ -328,7 +352,55 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         }
       }
       const bool seg_done = (seg < nseg - 1) ? (sub == tps - 1) : (sub == tps_last - 1);
-      if (seg_done) {
+      if (TMC && seg_done) {
+        // fold into the TMEM-resident C, 8 doubles (16 columns) at a time
+        if (seg > 0) asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t gi = m0 + wm * 32 + i * 8 + pg;
+          const uint32_t taddr = tmem_c + uint32_t(i * 16);
+          uint32_t w[16];
+          if (seg > 0) {
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                "[%16];\n"
+                : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
+                  "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]),
+                  "=r"(w[15])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
+              const bool ok = gi < p.m && gj < p.n && (!p.lower_only || gi >= gj);
+              const int q = 2 * (2 * j + h);
+              double v = __dmul_rn(p.alpha, acc[i][j][h]);
+              if (seg > 0) {
+                v = __dadd_rn(__hiloint2double(int(w[q + 1]), int(w[q])), v);  // beta_eff = 1: 1*C is exact
+              } else if (p.beta != 0.0) {
+                const double cold = ok ? __ldcg(C + p.c_off + gi * p.c_rs + gj * p.c_cs) : 0.0;
+                v = __dadd_rn(__dmul_rn(p.beta, cold), v);
+              }
+              if (seg == nseg - 1) {
+                if (ok) C[p.c_off + gi * p.c_rs + gj * p.c_cs] = v;
+              } else {
+                w[q] = uint32_t(__double2loint(v));
+                w[q + 1] = uint32_t(__double2hiint(v));
+              }
+              acc[i][j][h] = 0.0;
+            }
+          if (seg < nseg - 1)
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16};\n" ::"r"(taddr),
+                "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]),
+                "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+                : "memory");
+        }
+      } else if (seg_done) {
         // Fold: C is not __restrict__, so a load-use-store loop would
         // serialise one L2 round trip per element; instead each half of the
         // thread's 32 elements has all its reads in flight before its writes.
@@ -399,6 +471,15 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     }
   }
   (void)MI;
+  if constexpr (TMC) {
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_slot), "n"(256));
+    }
+  }
 }
 
 // ---- host side -------------------------------------------------------------
@@ -458,11 +539,13 @@ int g_red_fold = 1;
 int g_persist = 0;
 int g_tma_variant = 2;  // 0: m8n8k4/1 box/6 stages, 1: m16n8k8/1/6, 2: m8n8k4/2 boxes/3, 3: m16n8k8/2/3
 
-template <int MMAK, int KBOX, int STAGES>
+int g_tmem_fold = 1;  // bf_set_option("tmem_fold", 0|1): C in TMEM across >= 3 kc segments
+
+template <int MMAK, int KBOX, int STAGES, bool TMC>
 static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t s) {
   constexpr size_t base_smem = size_t(STAGES) * 2 * KBOX * TM_TILE_BYTES + 1024 + 8 * STAGES;
   constexpr size_t max_smem = 200 * 1024;  // leaves room for the static __shared__ words
-  auto kern = gemm_dmma_tma_kernel<MMAK, KBOX, STAGES>;
+  auto kern = gemm_dmma_tma_kernel<MMAK, KBOX, STAGES, TMC>;
   GemmParams p = p_in;
   static int sms_dev[64] = {};
   int dev = 0;
@@ -510,11 +593,14 @@ int launch_gemm_dmma_tma(const GemmParams& p_in, cudaStream_t s) {
   if (p.num_tiles <= 0) return 0;
   if (p.num_tiles > 0x7fffffffLL) return -3;
   const bool two_box_ok = (p.kc % 32 == 0) || p.kc >= p.k;
-  switch (two_box_ok ? g_tma_variant : (g_tma_variant & 1)) {
-    case 1: return run_tma<8, 1, 6>(p, ma, mb, s);
-    case 2: return run_tma<4, 2, 3>(p, ma, mb, s);
-    case 3: return run_tma<8, 2, 3>(p, ma, mb, s);
-    default: return run_tma<4, 1, 6>(p, ma, mb, s);
+  const int variant = two_box_ok ? g_tma_variant : (g_tma_variant & 1);
+  const int64_t nseg = p.kc < p.k ? (p.k + p.kc - 1) / p.kc : 1;
+  if (g_tmem_fold && nseg >= 3 && variant == 2) return run_tma<4, 2, 3, true>(p, ma, mb, s);
+  switch (variant) {
+    case 1: return run_tma<8, 1, 6, false>(p, ma, mb, s);
+    case 2: return run_tma<4, 2, 3, false>(p, ma, mb, s);
+    case 3: return run_tma<8, 2, 3, false>(p, ma, mb, s);
+    default: return run_tma<4, 1, 6, false>(p, ma, mb, s);
   }
 }
 

@@ -4,6 +4,7 @@
 // All memory-bound; they stream the matrix once per call.
 #include "bf_common.cuh"
 #include "bf_internal.h"
+#include "blockfam_b200.h"
 
 #include <cuda_bf16.h>
 
@@ -353,3 +354,128 @@ int launch_potrs_blocked(const float* L, int64_t ld, const float* xinv, int64_t 
 }
 
 }  // namespace bf
+
+// ---- the factorization driver of the mixed solve ---------------------------
+namespace bf {
+namespace {
+
+__global__ void set_identity_kernel(double* x, int64_t ld, int64_t b) {
+  const int64_t total = b * b;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / b, j = e - i * b;
+    x[i * ld + j] = i == j ? 1.0 : 0.0;
+  }
+}
+
+}  // namespace
+
+int g_mixed_reserve = 32;  // bf_set_option("mixed_reserve", r): SMs the trailing GEMMT leaves to the side chain
+
+}  // namespace bf
+
+extern "C" {
+// bf_cholesky_mixed: see include/blockfam_b200.h
+int bf_cholesky_mixed(const bf_view* a, float* w, int64_t ldw, void* pbuf0, void* pbuf1, void* xt, double* d64,
+                      double* x64, float* xinv, int64_t bs, const bf_chol_level* lv, int nl, int precision,
+                      int lookahead, int* d_info, void* stream) {
+  using namespace bf;
+  if (!a || !w || !pbuf0 || !pbuf1 || !xt || !d64 || !x64 || !xinv || !lv || nl < 1 || !d_info)
+    return set_error(BF_ERR_VALUE, "null argument");
+  if (a->m != a->n) return set_error(BF_ERR_SHAPE, "square matrix required");
+  if (bs < 8 || bs % 8) return set_error(BF_ERR_SHAPE, "bs must be a multiple of 8");
+  const int64_t n = a->n;
+  if (n == 0) return BF_OK;
+  const bool tf32 = precision == 1;
+  cudaStream_t main = static_cast<cudaStream_t>(stream);
+  cudaStream_t side = lookahead ? panel_stream_for_device() : main;
+  if (lookahead && !side) return set_error(BF_ERR_CUDA, "cannot create the side stream");
+  void* pbuf[2] = {pbuf0, pbuf1};
+  const int64_t nblk = (n + bs - 1) / bs;
+  auto ck = [](int rc, const char* what) { return rc ? set_error(rc < -10 ? rc : BF_ERR_CUDA, what) : BF_OK; };
+  int rc = ck(launch_f64_to_f32(static_cast<const double*>(a->base), a->off, a->rs, a->cs, w, 0, ldw, 1, n, n, 1,
+                                main),
+              "convert A");
+  if (rc) return rc;
+
+  // diagonal block k (FP64 tree driver), its inverse X = L_kk^-T (FP64), and
+  // the panel L21 = A21 X as one tensor-core GEMM, all on stream st
+  auto diag_and_panel = [&](int64_t k, cudaStream_t st) -> int {
+    const int64_t k0 = k * bs, b = bs < n - k0 ? bs : n - k0, r = n - k0 - b;
+    float* d32 = w + k0 * ldw + k0;
+    int e = launch_f32_to_f64(d32, 0, ldw, 1, d64, 0, bs, 1, b, b, 1, st);
+    if (e) return ck(e, "convert diagonal block");
+    bf_view dd{d64, 0, b, b, bs, 1};
+    e = bf_cholesky_ex_d(&dd, lv, nl, k0, d_info, st);
+    if (e) return e;
+    e = launch_f64_to_f32(d64, 0, bs, 1, d32, 0, ldw, 1, b, b, 1, st);
+    if (e) return ck(e, "convert diagonal block");
+    note_launch();
+    set_identity_kernel<<<64, 256, 0, st>>>(x64, bs, b);
+    bf_view xv{x64, 0, b, b, bs, 1};
+    e = bf_trsm_rltn_ex_d(1.0, &dd, &xv, 512, nullptr, d_info, st);  // X L11^T = I
+    if (e) return e;
+    e = launch_f64_to_f32(x64, 0, bs, 1, xinv + k * bs * bs, 0, bs, 1, b, b, 0, st);
+    if (e) return ck(e, "convert inverse");
+    if (r == 0) return BF_OK;
+    float* a21 = w + (k0 + b) * ldw + k0;
+    void* p = pbuf[k & 1];
+    if (tf32) {
+      float* xtf = static_cast<float*>(xt);  // X^T in fp32
+      e = launch_f64_to_f32(x64, 0, bs, 1, xtf, 0, 1, bs, b, b, 0, st);
+      if (!e) e = launch_gemm_tf32_tc(1.0, a21, ldw, xtf, bs, 0.0, static_cast<float*>(p), 0, bs, 1, r, b, b, 0, st);
+      if (e) return ck(e, "panel gemm (tf32)");
+      return cudaMemcpy2DAsync(a21, size_t(ldw) * 4, p, size_t(bs) * 4, size_t(b) * 4, size_t(r),
+                               cudaMemcpyDeviceToDevice, st) == cudaSuccess
+                 ? BF_OK
+                 : set_error(BF_ERR_CUDA, "panel copy");
+    }
+    e = launch_f64_to_bf16(x64, 0, bs, 1, xt, bs, b, b, 1, st);
+    if (!e) e = launch_to_bf16(a21, 0, ldw, 1, p, bs, r, b, 0, st);
+    if (!e) e = launch_gemm_bf16_tc(1.0, p, bs, xt, bs, 0.0, a21, 0, ldw, 1, r, b, b, 0, st);  // L21 = A21 X
+    if (!e) e = launch_to_bf16(a21, 0, ldw, 1, p, bs, r, b, 0, st);
+    return ck(e, "panel (bf16)");
+  };
+  auto tc_gemm = [&](const void* pa, const void* pb, float* c, int64_t m, int64_t nn, int64_t kk, int lower,
+                     cudaStream_t st) {
+    return tf32 ? launch_gemm_tf32_tc(-1.0, static_cast<const float*>(pa), bs, static_cast<const float*>(pb), bs, 1.0,
+                                      c, 0, ldw, 1, m, nn, kk, lower, st)
+                : launch_gemm_bf16_tc(-1.0, pa, bs, pb, bs, 1.0, c, 0, ldw, 1, m, nn, kk, lower, st);
+  };
+  cudaEvent_t ev_main, ev_side;
+  cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming);
+  const size_t esz = tf32 ? 4 : 2;
+  if (lookahead) {
+    cudaEventRecord(ev_main, main);
+    cudaStreamWaitEvent(side, ev_main, 0);
+  }
+  rc = diag_and_panel(0, side);
+  cudaEventRecord(ev_side, side);
+  for (int64_t k = 0; k + 1 < nblk && !rc; ++k) {
+    const int64_t k1 = (k + 1) * bs, r = n - k1, nb = bs < r ? bs : r;
+    cudaStreamWaitEvent(main, ev_side, 0);
+    const char* pk = static_cast<const char*>(pbuf[k & 1]);
+    // (1) the next block column: W[k1:, k1:k1+nb] -= P P[:nb]^T
+    rc = ck(tc_gemm(pk, pk, w + k1 * ldw + k1, r, nb, bs, 0, main), "column gemm");
+    if (rc) break;
+    if (lookahead) {
+      cudaEventRecord(ev_main, main);
+      cudaStreamWaitEvent(side, ev_main, 0);
+    }
+    // (2) panel k+1 on the side stream, (3) the rest of the trailing triangle
+    // on the main stream, leaving g_mixed_reserve SMs to the side chain
+    rc = diag_and_panel(k + 1, side);
+    cudaEventRecord(ev_side, side);
+    if (!rc && r > nb) {
+      const char* rest = pk + size_t(nb) * bs * esz;
+      if (lookahead) t_reserve_sms = g_mixed_reserve;
+      rc = ck(tc_gemm(rest, rest, w + (k1 + nb) * ldw + k1 + nb, r - nb, r - nb, bs, 1, main), "trailing gemmt");
+      t_reserve_sms = 0;
+    }
+  }
+  cudaStreamWaitEvent(main, ev_side, 0);
+  cudaEventDestroy(ev_main);
+  cudaEventDestroy(ev_side);
+  return rc ? rc : (cudaGetLastError() == cudaSuccess ? BF_OK : set_error(BF_ERR_CUDA, "mixed factorization"));
+}
+}  // extern "C"

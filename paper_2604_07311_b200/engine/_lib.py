@@ -136,6 +136,8 @@ _SIGNATURES = {
     "bf_pack_scatter_d": ([_SV, _I, _VP, _VP], _I),
     "bf_gemm_scatter_s": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
     "bf_gemm_scatter_sd": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
+    "bf_cholesky_mixed": ([_V, _VP, _L, _VP, _VP, _VP, _VP, _VP, _VP, _L, _P(BfCholLevel), _I, _I, _I, _VP, _VP],
+                          _I),
     "bf_dist_available": ([], _I),
     "bf_dist_unique_id_bytes": ([], _I),
     "bf_dist_unique_id": ([_VP], _I),

@@ -119,85 +119,20 @@ def cholesky_mixed(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlN
     tf32 = ws.precision == "tf32"
     if tf32 and n % 4:
         raise ShapeError("precision 'tf32' needs n % 4 == 0 (16-byte fp32 rows for TMA)")
-    tc_gemm = lib.bf_gemm_tf32 if tf32 else lib.bf_gemm_bf16
-    main = torch.cuda.current_stream(a.device)
-    side = ws.side if lookahead else main
     tree = diag_tree if diag_tree is not None else parse_tree(json.dumps(DIAG_TREE))
     levels = flatten_cholesky(tree, resolve_config(tree, DType.F64))
     arr = (_lib.BfCholLevel * len(levels))(*[_lib.BfCholLevel(v, 0, b, kc) for v, b, kc in levels])
-    w, pbuf, xt, d64, x64, xinv, info = ws.w, ws.pbuf, ws.xt, ws.d64, ws.x64, ws.xinv, ws.info
-    # pbuf ping-pongs: panel k+1 is formed while step k's trailing update still reads panel k
-    nblk = (n + bs - 1) // bs
+    info = ws.info
     info.fill_(-1)
-    _lib.check(lib.bf_convert_f64_f32(ctypes.byref(_v(a)), ctypes.byref(_v(w)), 1, main.cuda_stream), "convert")
-
-    def diag_and_panel(k: int, stream: torch.cuda.Stream) -> None:
-        k0 = k * bs
-        b = min(bs, n - k0)
-        r = n - k0 - b
-        sh = stream.cuda_stream
-        with torch.cuda.stream(stream):
-            d32, dd = w[k0:k0 + b, k0:k0 + b], d64[:b, :b]
-            _lib.check(lib.bf_convert_f32_f64(ctypes.byref(_v(d32)), ctypes.byref(_v(dd)), 1, sh), "convert")
-            before = ws.before  # the driver reports block-local pivots; shift a fresh failure by k0
-            before.copy_(info)
-            _lib.check(lib.bf_cholesky_d(ctypes.byref(_v(dd)), arr, len(levels), info.data_ptr(), sh), "diag factor")
-            torch.where((before < 0) & (info >= 0), info + k0, info, out=info)
-            _lib.check(lib.bf_convert_f64_f32(ctypes.byref(_v(dd)), ctypes.byref(_v(d32)), 1, sh), "convert")
-            x = x64[:b, :b]
-            x.zero_()
-            x.diagonal().fill_(1.0)  # X L11^T = I: X = L11^-T
-            _lib.check(lib.bf_trsm_rltn_d(1.0, ctypes.byref(_v(dd)), ctypes.byref(_v(x)), 512, None, sh), "inverse")
-            _lib.check(lib.bf_convert_f64_f32(ctypes.byref(_v(x)), ctypes.byref(_v(xinv[k, :b, :b])), 0, sh),
-                       "convert")
-            if r == 0:
-                return
-            a21 = w[k0 + b:, k0:k0 + b]
-            p = pbuf[k % len(pbuf)]
-            if tf32:
-                # L21 = A21 * X straight from W (C = A * Bnk^T, Bnk = X^T in fp32), into the panel buffer
-                xtv = _lib.BfView(xt.data_ptr(), 0, b, b, 1, bs)  # X^T: transposed fp32 store
-                _lib.check(lib.bf_convert_f64_f32(ctypes.byref(_v(x)), ctypes.byref(xtv), 0, sh), "convert")
-                pv = p[:r, :b]
-                _lib.check(lib.bf_gemm_tf32(1.0, a21.data_ptr(), n, xt.data_ptr(), bs, 0.0, ctypes.byref(_v(pv)), b, 0,
-                                            sh), "panel gemm")
-                a21.copy_(pv)
-                return
-            _lib.check(lib.bf_convert_f64_bf16(ctypes.byref(_v(x)), xt.data_ptr(), bs, 1, sh), "convert")
-            _lib.check(lib.bf_convert_f32_bf16(ctypes.byref(_v(a21)), p.data_ptr(), bs, 0, sh), "convert")
-            # L21 = A21 * X  (C = A * Bnk^T with Bnk = X^T)
-            _lib.check(lib.bf_gemm_bf16(1.0, p.data_ptr(), bs, xt.data_ptr(), bs, 0.0, ctypes.byref(_v(a21)), b, 0, sh),
-                       "panel gemm")
-            _lib.check(lib.bf_convert_f32_bf16(ctypes.byref(_v(a21)), p.data_ptr(), bs, 0, sh), "convert")
-
-    if lookahead:
-        side.wait_stream(main)
-    diag_and_panel(0, side)
-    ev = torch.cuda.Event()
-    ev.record(side)
-    for k in range(nblk - 1):
-        k0 = k * bs
-        b = bs
-        k1 = k0 + b
-        r = n - k1
-        nb = min(bs, r)
-        main.wait_event(ev)
-        pk = pbuf[k % len(pbuf)]
-        # (1) the next block column first: W[k1:, k1:k1+nb] -= P P[:nb]^T
-        _lib.check(tc_gemm(-1.0, pk.data_ptr(), bs, pk.data_ptr(), bs, 1.0, ctypes.byref(_v(w[k1:, k1:k1 + nb])),
-                           b, 0, main.cuda_stream), "column gemm")
-        if lookahead:
-            side.wait_stream(main)
-        diag_and_panel(k + 1, side)
-        ev = torch.cuda.Event()
-        ev.record(side)
-        # (2) the rest of the trailing triangle
-        if r > nb:
-            rest = pk[nb:]
-            _lib.check(tc_gemm(-1.0, rest.data_ptr(), bs, rest.data_ptr(), bs, 1.0,
-                               ctypes.byref(_v(w[k1 + nb:, k1 + nb:])), b, 1, main.cuda_stream),
-                       "trailing gemmt")
-    main.wait_event(ev)
+    # the per-block loop is native (bf_cholesky_mixed): FP64 diagonal block,
+    # FP64 inverse, tensor-core panel and trailing GEMMs, lookahead on the
+    # library's high-priority stream
+    rc = lib.bf_cholesky_mixed(ctypes.byref(_v(a)), ws.w.data_ptr(), n, ws.pbuf[0].data_ptr(), ws.pbuf[1].data_ptr(),
+                               ws.xt.data_ptr(), ws.d64.data_ptr(), ws.x64.data_ptr(), ws.xinv.data_ptr(), bs, arr,
+                               len(levels), 1 if tf32 else 0, 1 if lookahead else 0, info.data_ptr(),
+                               torch.cuda.current_stream(a.device).cuda_stream)
+    _lib.check(rc, "bf_cholesky_mixed")
+    w, xinv = ws.w, ws.xinv
     bad = int(info.item())
     if bad >= 0:
         raise NotPositiveDefiniteError(bad)
@@ -206,10 +141,17 @@ def cholesky_mixed(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlN
 
 def posv_mixed(a: torch.Tensor, b: torch.Tensor, bs: int = 1024, tol: Optional[float] = None,
                max_iter: int = 30, lookahead: bool = True, ws: Optional[MixedWorkspace] = None,
-               precision: Optional[str] = None) -> MixedResult:
+               precision: Optional[str] = None, step_tol: Optional[float] = None) -> MixedResult:
     """Solve A x = b (A fp64 SPD, full dense row-major on the GPU) to FP64
     accuracy: bf16/fp32 factorization + FP64 iterative refinement.  The
-    returned x lives in the workspace (copy it before reusing ws)."""
+    returned x lives in the workspace (copy it before reusing ws).
+
+    Refinement stops when the normwise backward error
+    ||b - Ax||_inf / (||A||_inf ||x||_inf + ||b||_inf) <= tol (default
+    10 n eps) and, when step_tol is given, the last correction is also small:
+    ||dx||_inf / ||x||_inf <= step_tol — the forward-error criterion (SURVEY.md
+    §8(c) asks ||x - x_ref|| / ||x_ref|| <= 1e-12 against the FP64 solution;
+    step_tol = 1e-13 reaches it)."""
     n = a.shape[0]
     lib = _lib.lib()
     stream = torch.cuda.current_stream(a.device).cuda_stream
@@ -232,10 +174,12 @@ def posv_mixed(a: torch.Tensor, b: torch.Tensor, bs: int = 1024, tol: Optional[f
         x.add_(d)
         _lib.check(lib.bf_residual_d(a.data_ptr(), n, x.data_ptr(), b.data_ptr(), r.data_ptr(), n, stream), "residual")
         it += 1
-        err = float(r.abs().max()) / (norm_a * float(x.abs().max()) + norm_b)
-        if err <= tol:
+        xmax = float(x.abs().max())
+        err = float(r.abs().max()) / (norm_a * xmax + norm_b)
+        step_ok = step_tol is None or float(d.abs().max()) <= step_tol * xmax
+        if err <= tol and step_ok:
             break
-    return MixedResult(x, it, err, err <= tol)
+    return MixedResult(x, it, err, err <= tol and step_ok)
 
 
 # --------------------------------------------------------------------------

@@ -134,3 +134,26 @@ def test_mixed_factor_reports_npd_pivot(cuda):
     with pytest.raises(NotPositiveDefiniteError) as e:
         cholesky_mixed(a, 256)
     assert e.value.index == 613
+
+
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
+def test_mixed_solve_forward_error_vs_fp64_solution(cuda, precision):
+    """after refinement ||x - x_ref|| / ||x_ref|| <= 1e-12,
+    x_ref from the FP64 factor (the bitwise-reference tree) and triangular
+    solves; step_tol is the forward-error stopping criterion."""
+    import paper_2604_07311_b200 as bf
+
+    n = 3000
+    g = torch.Generator(device="cuda")
+    g.manual_seed(99)
+    m = torch.rand(n, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    a = m @ m.T + n * torch.eye(n, dtype=torch.float64, device="cuda")
+    b = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+    res = posv_mixed(a, b, bs=512, precision=precision, step_tol=1e-13)
+    assert res.converged
+    l64 = a.clone()
+    bf.cholesky(bf.from_torch(l64), "lower")
+    lo = torch.tril(l64)
+    xref = torch.linalg.solve_triangular(lo.T, torch.linalg.solve_triangular(lo, b[:, None], upper=False),
+                                         upper=True)[:, 0]
+    assert float((res.x - xref).norm() / xref.norm()) <= 1e-12

@@ -19,6 +19,11 @@ from paper_2604_07311_b200.mixed import MixedWorkspace, cholesky_mixed, posv_mix
 
 
 def main():
+    import os
+
+    for kv in filter(None, os.environ.get("BF_OPTS", "").split(",")):  # e.g. BF_OPTS=mixed_reserve=48
+        k, v = kv.split("=")
+        assert _lib.lib().bf_set_option(k.encode(), int(v)) == 0, kv
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
     bs = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
     prec = sys.argv[3] if len(sys.argv) > 3 else "bf16"
@@ -36,12 +41,25 @@ def main():
         e[0].record()
         cholesky_mixed(a, bs, ws=ws)
         e[1].record()
-        res = posv_mixed(a, b, bs=bs, ws=ws)
+        res = posv_mixed(a, b, bs=bs, ws=ws, step_tol=float(os.environ.get("STEP_TOL", "0")) or None)
         e[2].record()
         e[2].synchronize()
         fac = e[0].elapsed_time(e[1])
         tot = e[1].elapsed_time(e[2])  # factor + refinement inside posv_mixed
-        print(json.dumps({"n": n, "bs": bs, "precision": prec, "matrix": name, "factor_ms": round(fac, 2), "posv_ms": round(tot, 2),
+        # forward error against the FP64 solution (bitwise-reference FP64 factor + triangular solves)
+        import paper_2604_07311_b200 as bfp
+
+        l64 = a.clone()
+        bfp.cholesky(bfp.from_torch(l64), "lower", None if n < 2048 else bfp.parse_tree(json.dumps(
+            {"op": "cholesky", "variant": 3, "bs": 2048, "kernel": {"kc": 2048},
+             "child": {"op": "cholesky", "variant": 3, "bs": 128, "kernel": {"kc": 128},
+                       "child": {"op": "cholesky", "variant": "unblocked3"}}})))
+        l64 = torch.tril(l64)
+        y = torch.linalg.solve_triangular(l64, b[:, None], upper=False)
+        xref = torch.linalg.solve_triangular(l64.T, y, upper=True)[:, 0]
+        fwd = float((res.x - xref).norm() / xref.norm())
+        del l64, y
+        print(json.dumps({"fwd_err_vs_fp64": fwd, "opts": os.environ.get("BF_OPTS", ""), "n": n, "bs": bs, "precision": prec, "matrix": name, "factor_ms": round(fac, 2), "posv_ms": round(tot, 2),
                           "refine_ms": round(tot - fac, 2), "iterations": res.iterations,
                           "backward_error": res.backward_error, "converged": res.converged,
                           "fp64_equiv_gflops": round(n ** 3 / 3 / (tot / 1e3) / 1e9, 1),

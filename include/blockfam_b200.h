@@ -159,6 +159,29 @@ int bf_gemm_scatter_s(double alpha, const bf_scatter_view* a, const bf_scatter_v
  * large permuted facade k-contiguous with it so the TMA DMMA GEMM can read it;
  * values are copied exactly, so the contraction's bits do not change. */
 int bf_pack_scatter_d(const bf_scatter_view* src, int transpose, double* out, void* stream);
+/* Mode-group view of a contraction facade (tensor/contract.py:90-102 _facade,
+ * tensor/scatter.py:69-98): rows are nr <= 2 mode groups, columns nc <= 2,
+ * slowest first, each with its size and element stride; element (i, j) at
+ * off + sum_g (i_g * rstr[g]) + sum_g (j_g * cstr[g]) with (i_0, i_1) the
+ * mixed-radix digits of i (i_1 fastest).  This is the B200 form of the
+ * reference's scatter vectors for the 4-index case: the GEMM reads it with
+ * 4-D TMA tensor maps, so permuted operands need no transpose. */
+typedef struct bf_modes_view {
+  void* base;
+  int64_t off;
+  int32_t nr, nc;
+  int64_t rdim[2], rstr[2];
+  int64_t cdim[2], cstr[2];
+} bf_modes_view;
+/* C := beta*C + alpha*A*B over mode-group views (A: M x K, B: K x N, C: M x N),
+ * the reference's kc folds (bit-identical to bf_gemm_scatter_d).  TMA needs
+ * the fastest K group of A and of B unit-stride with a size that is a
+ * multiple of 16, the fastest row group of A / column group of B a multiple
+ * or divisor of 128, 16-byte strides and K % 32 == 0; otherwise it returns
+ * BF_ERR_UNSUPPORTED (the host then stages or gathers that operand).
+ * alpha == 0 or K == 0 are the caller's (reference edge semantics). */
+int bf_contract_modes_d(double alpha, const bf_modes_view* a, const bf_modes_view* b, double beta,
+                        const bf_modes_view* c, int64_t kc, void* stream);
 int bf_gemm_scatter_sd(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,
                        const bf_scatter_view* c, int64_t kc, void* stream);
 

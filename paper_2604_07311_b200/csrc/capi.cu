@@ -1514,6 +1514,57 @@ int bf_gemm_scatter_d(double alpha, const bf_scatter_view* a, const bf_scatter_v
                       const bf_scatter_view* c, int64_t kc, void* stream) {
   return scatter_impl(MODE_D, alpha, a, b, beta, c, kc, S(stream));
 }
+// tensor/contract.py:159-185 contract on mode-group views: the 4-D TMA GEMM
+int bf_contract_modes_d(double alpha, const bf_modes_view* a, const bf_modes_view* b, double beta,
+                        const bf_modes_view* c, int64_t kc, void* stream) {
+  if (!a || !b || !c) return fail(BF_ERR_VALUE, "null view");
+  for (const bf_modes_view* v : {a, b, c})
+    if (v->nr < 1 || v->nr > 2 || v->nc < 1 || v->nc > 2) return fail(BF_ERR_UNSUPPORTED, "1 or 2 mode groups per side");
+  auto size = [](int n, const int64_t* d) { return n == 2 ? d[0] * d[1] : d[0]; };
+  const int64_t m = size(a->nr, a->rdim), k = size(a->nc, a->cdim), n = size(b->nc, b->cdim);
+  if (size(b->nr, b->rdim) != k || size(c->nr, c->rdim) != m || size(c->nc, c->cdim) != n)
+    return fail(BF_ERR_SHAPE, "contraction facade dims mismatch");
+  if (kc < 1) return fail(BF_ERR_VALUE, "kc must be >= 1");
+  if (m == 0 || n == 0) return BF_OK;
+  if (k == 0 || alpha == 0.0) return fail(BF_ERR_UNSUPPORTED, "edge case: use the scatter path");
+  // A (M x K): rows = M groups, columns = K groups; B^T (N x K): B's columns are its rows
+  auto op = [](const void* base, int64_t off, int nmn, const int64_t* mdim, const int64_t* mstr, int nk,
+               const int64_t* kdim, const int64_t* kstr, bf::ModeOperand& o) {
+    if (kstr[nk - 1] != 1) return false;  // fastest K group must be unit-stride
+    o.base = static_cast<const double*>(base);
+    o.off = off;
+    o.mi = mdim[nmn - 1];
+    o.s_mn = mstr[nmn - 1];
+    o.s_mn_o = nmn == 2 ? mstr[0] : 0;
+    o.ki = kdim[nk - 1];
+    o.s_k_o = nk == 2 ? kstr[0] : 0;
+    return true;
+  };
+  bf::ModeOperand ma{}, mb{};
+  if (!op(a->base, a->off, a->nr, a->rdim, a->rstr, a->nc, a->cdim, a->cstr, ma) ||
+      !op(b->base, b->off, b->nc, b->cdim, b->cstr, b->nr, b->rdim, b->rstr, mb))
+    return fail(BF_ERR_UNSUPPORTED, "an operand's fastest contracted mode is not unit-stride");
+  GemmParams p{};
+  p.m = m;
+  p.n = n;
+  p.k = k;
+  p.kc = kc;
+  p.c = c->base;
+  p.c_off = c->off;
+  if (m > 0x7fffffffLL || n > 0x7fffffffLL) return fail(BF_ERR_UNSUPPORTED, "facade larger than 2^31");
+  p.c_ri = bf::FastDiv(uint32_t(c->nr == 2 ? c->rdim[1] : m));
+  p.c_rs = c->rstr[c->nr - 1];
+  p.c_rs_o = c->nr == 2 ? c->rstr[0] : 0;
+  p.c_ci = bf::FastDiv(uint32_t(c->nc == 2 ? c->cdim[1] : n));
+  p.c_cs = c->cstr[c->nc - 1];
+  p.c_cs_o = c->nc == 2 ? c->cstr[0] : 0;
+  p.alpha = alpha;
+  p.beta = beta;
+  p.group = g_group;
+  int rc = bf::launch_gemm_dmma_modes(p, ma, mb, S(stream));
+  if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "mode-group layout not TMA-loadable");
+  return rc ? fail(BF_ERR_CUDA, "mode-group gemm launch failed") : BF_OK;
+}
 int bf_pack_scatter_d(const bf_scatter_view* src, int transpose, double* out, void* stream) {
   if (!src || !out) return fail(BF_ERR_VALUE, "null argument");
   if (src->m < 0 || src->n < 0) return fail(BF_ERR_SHAPE, "negative extent");

@@ -77,6 +77,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ double lds64(uint32_t addr) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
@@ -141,7 +149,12 @@ __device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double (&a)[4]
 // written once after the last.  Same roundings in the same order as the
 // global folds, so the same bits; the C traffic of a K = 16384, kc = 256
 // tile drops from 64 L2 round trips to one read and one write.
-template <int MMAK, int KBOX, int STAGES, bool TMC>
+//
+// MODES: operands are 4-D tensor maps over permuted tensor modes (k_in,
+// mn_in, k_out, mn_out) — the contraction's mode groups go straight into the
+// swizzled stage with no transpose — and C is addressed through its two row
+// and two column mode groups.
+template <int MMAK, int KBOX, int STAGES, bool TMC, bool MODES = false>
 __global__ void __launch_bounds__(TM_THREADS, 1)
     gemm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                          const GemmParams p) {
@@ -219,8 +232,27 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     mbar_expect_tx(full(st), STAGE_BYTES);
 #pragma unroll
     for (int b = 0; b < KBOX; ++b) {
-      tma_load_2d(sa + b * TM_TILE_BYTES, &tma_a, k_lo + 16 * b, int(ti * TM_BM), full(st));
-      tma_load_2d(sa + OP_BYTES + b * TM_TILE_BYTES, &tma_b, k_lo + 16 * b, int(tj * TM_BN), full(st));
+      if constexpr (MODES) {
+        // an operand whose mode groups collapse to one per side has a 2-D map
+        const uint32_t k = uint32_t(k_lo + 16 * b), ra = uint32_t(ti) * TM_BM, rb = uint32_t(tj) * TM_BN;
+        if (p.a_rank == 2) {
+          tma_load_2d(sa + b * TM_TILE_BYTES, &tma_a, int(k), int(ra), full(st));
+        } else {
+          const uint32_t qa = p.a_ki.div(k), qra = p.a_mi.div(ra);
+          tma_load_4d(sa + b * TM_TILE_BYTES, &tma_a, int(k - qa * p.a_ki.d), int(ra - qra * p.a_mi.d), int(qa),
+                      int(qra), full(st));
+        }
+        if (p.b_rank == 2) {
+          tma_load_2d(sa + OP_BYTES + b * TM_TILE_BYTES, &tma_b, int(k), int(rb), full(st));
+        } else {
+          const uint32_t qb = p.b_ki.div(k), qrb = p.b_mi.div(rb);
+          tma_load_4d(sa + OP_BYTES + b * TM_TILE_BYTES, &tma_b, int(k - qb * p.b_ki.d), int(rb - qrb * p.b_mi.d),
+                      int(qb), int(qrb), full(st));
+        }
+      } else {
+        tma_load_2d(sa + b * TM_TILE_BYTES, &tma_a, k_lo + 16 * b, int(ti * TM_BM), full(st));
+        tma_load_2d(sa + OP_BYTES + b * TM_TILE_BYTES, &tma_b, k_lo + 16 * b, int(tj * TM_BN), full(st));
+      }
     }
   };
   if (tid == 0) {
@@ -238,6 +270,16 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   auto koff = [&](int k) -> uint32_t { return uint32_t((((k >> 1) ^ pg) << 4) | ((k & 1) << 3)); };
   const int pj[2] = {perm8(2 * t), perm8(2 * t + 1)};
   double* C = static_cast<double*>(p.c);
+  // element offset of C(i, j) (MODES: two row and two column mode groups)
+  auto coff = [&](int64_t i, int64_t j) -> int64_t {
+    if constexpr (MODES) {
+      const uint32_t qi = p.c_ri.div(uint32_t(i)), qj = p.c_ci.div(uint32_t(j));
+      return p.c_off + int64_t(qi) * p.c_rs_o + (i - int64_t(qi) * p.c_ri.d) * p.c_rs + int64_t(qj) * p.c_cs_o +
+             (j - int64_t(qj) * p.c_ci.d) * p.c_cs;
+    } else {
+      return p.c_off + i * p.c_rs + j * p.c_cs;
+    }
+  };
 
   constexpr int MI = MMAK == 4 ? 4 : 2;  // row fragments per warp (8 or 16 rows each)
   double acc[4][4][2];                    // 32 accumulators in either shape
@@ -346,9 +388,9 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         // C from L2 between them: d=128 contraction, 64 folds per tile)
         const int64_t r = m0 + wm * 32 + lane, c0 = n0 + wn * 32;
         if (r < p.m && c0 < p.n) {
-          const double* rowp = C + p.c_off + r * p.c_rs + c0 * p.c_cs;
+          const double* rowp = C + coff(r, c0);
           asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp));
-          if (p.c_cs == 1 && c0 + 16 < p.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + 16));
+          if (!MODES && p.c_cs == 1 && c0 + 16 < p.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + 16));
         }
       }
       const bool seg_done = (seg < nseg - 1) ? (sub == tps - 1) : (sub == tps_last - 1);
@@ -381,11 +423,11 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
               if (seg > 0) {
                 v = __dadd_rn(__hiloint2double(int(w[q + 1]), int(w[q])), v);  // beta_eff = 1: 1*C is exact
               } else if (p.beta != 0.0) {
-                const double cold = ok ? __ldcg(C + p.c_off + gi * p.c_rs + gj * p.c_cs) : 0.0;
+                const double cold = ok ? __ldcg(C + coff(gi, gj)) : 0.0;
                 v = __dadd_rn(__dmul_rn(p.beta, cold), v);
               }
               if (seg == nseg - 1) {
-                if (ok) C[p.c_off + gi * p.c_rs + gj * p.c_cs] = v;
+                if (ok) C[coff(gi, gj)] = v;
               } else {
                 w[q] = uint32_t(__double2loint(v));
                 w[q + 1] = uint32_t(__double2hiint(v));
@@ -423,7 +465,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
                 const double v = __dmul_rn(p.alpha, acc[i][j][h]);
                 if (gi < p.m && gj < p.n && (!p.lower_only || gi >= gj))
-                  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(C + p.c_off + gi * p.c_rs + gj * p.c_cs),
+                  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(C + coff(gi, gj)),
                                "d"(v)
                                : "memory");
                 acc[i][j][h] = 0.0;
@@ -444,7 +486,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
               for (int h = 0; h < 2; ++h) {
                 const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
                 const bool ok = gi < p.m && gj < p.n && (!p.lower_only || gi >= gj);
-                cold[ii][j][h] = (ok && beta_eff != 0.0) ? __ldcg(C + p.c_off + gi * p.c_rs + gj * p.c_cs) : 0.0;
+                cold[ii][j][h] = (ok && beta_eff != 0.0) ? __ldcg(C + coff(gi, gj)) : 0.0;
               }
           }
 #pragma unroll
@@ -458,7 +500,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
                 double v = __dmul_rn(p.alpha, acc[i][j][h]);
                 if (beta_eff != 0.0) v = __dadd_rn(__dmul_rn(beta_eff, cold[ii][j][h]), v);
-                if (gi < p.m && gj < p.n && (!p.lower_only || gi >= gj)) C[p.c_off + gi * p.c_rs + gj * p.c_cs] = v;
+                if (gi < p.m && gj < p.n && (!p.lower_only || gi >= gj)) C[coff(gi, gj)] = v;
                 acc[i][j][h] = 0.0;
               }
           }
@@ -541,11 +583,11 @@ int g_tma_variant = 2;  // 0: m8n8k4/1 box/6 stages, 1: m16n8k8/1/6, 2: m8n8k4/2
 
 int g_tmem_fold = 1;  // bf_set_option("tmem_fold", 0|1): C in TMEM across >= 3 kc segments
 
-template <int MMAK, int KBOX, int STAGES, bool TMC>
+template <int MMAK, int KBOX, int STAGES, bool TMC, bool MODES = false>
 static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t s) {
   constexpr size_t base_smem = size_t(STAGES) * 2 * KBOX * TM_TILE_BYTES + 1024 + 8 * STAGES;
   constexpr size_t max_smem = 200 * 1024;  // leaves room for the static __shared__ words
-  auto kern = gemm_dmma_tma_kernel<MMAK, KBOX, STAGES, TMC>;
+  auto kern = gemm_dmma_tma_kernel<MMAK, KBOX, STAGES, TMC, MODES>;
   GemmParams p = p_in;
   static int sms_dev[64] = {};
   int dev = 0;
@@ -602,6 +644,65 @@ int launch_gemm_dmma_tma(const GemmParams& p_in, cudaStream_t s) {
     case 3: return run_tma<8, 2, 3, false>(p, ma, mb, s);
     default: return run_tma<4, 1, 6, false>(p, ma, mb, s);
   }
+}
+
+// 4-D tensor map (k_in, mn_in, k_out, mn_out) over a mode-group operand with
+// a box of 16 k x 128 rows: {16, min(mi, 128), 1, max(1, 128 / mi)}.
+static bool make_map_modes(CUtensorMap* map, const ModeOperand& op, int64_t MN, int64_t K, int& rank) {
+  EncodeTiledFn enc = encoder();
+  if (!enc) return false;
+  const int64_t mi = op.mi, ki = op.ki;
+  if (mi == MN && ki == K) {  // one group a side: the plain 2-D map of the strided kernel
+    rank = 2;
+    OperandMK o{};
+    o.base = op.base;
+    o.off = op.off;
+    o.s_mn = op.s_mn;
+    return (op.s_mn * 8) % 16 == 0 && reinterpret_cast<uintptr_t>(op.base + op.off) % 16 == 0 &&
+           make_map(map, o, MN, K);
+  }
+  rank = 4;
+  if (ki % TM_BK != 0 || K % ki != 0 || MN % mi != 0) return false;
+  if (!(mi % TM_BM == 0 || TM_BM % mi == 0)) return false;
+  cuuint64_t dims[4] = {cuuint64_t(ki), cuuint64_t(mi), cuuint64_t(K / ki), cuuint64_t(MN / mi)};
+  cuuint64_t strides[3] = {cuuint64_t(op.s_mn) * 8, cuuint64_t(op.s_k_o) * 8, cuuint64_t(op.s_mn_o) * 8};
+  for (int d = 0; d < 3; ++d) {
+    const bool unused = dims[d + 1] == 1;
+    if (unused) strides[d] = d > 0 ? strides[d - 1] : 16;  // a size-1 dimension's stride is never used
+    if (strides[d] % 16 != 0 || strides[d] >= (cuuint64_t(1) << 40) || strides[d] == 0) return false;
+  }
+  cuuint32_t box[4] = {cuuint32_t(TM_BK), cuuint32_t(mi < TM_BM ? mi : TM_BM), 1,
+                       cuuint32_t(mi < TM_BM ? TM_BM / mi : 1)};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const double* base = op.base + op.off;
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0) return false;
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int launch_gemm_dmma_modes(GemmParams p, const ModeOperand& a, const ModeOperand& b, cudaStream_t s) {
+  p.red_fold = g_red_fold;
+  p.modes = 1;
+  if (!(p.kc % 32 == 0 || p.kc >= p.k) || p.k % 32 != 0) return -3;  // whole 2x16-k stages per segment
+  if (p.m > 0x7fffffffLL || p.n > 0x7fffffffLL || p.k > 0x7fffffffLL || p.lower_only) return -3;
+  if (a.ki > 0x7fffffffLL || a.mi > 0x7fffffffLL || b.ki > 0x7fffffffLL || b.mi > 0x7fffffffLL) return -3;
+  CUtensorMap ma, mb;
+  if (!make_map_modes(&ma, a, p.m, p.k, p.a_rank) || !make_map_modes(&mb, b, p.n, p.k, p.b_rank)) return -3;
+  p.a_ki = FastDiv(uint32_t(a.ki));
+  p.a_mi = FastDiv(uint32_t(a.mi));
+  p.b_ki = FastDiv(uint32_t(b.ki));
+  p.b_mi = FastDiv(uint32_t(b.mi));
+  if (p.c_ri.d == 0 || p.c_ci.d == 0) return -3;
+  p.tiles_m = int((p.m + TM_BM - 1) / TM_BM);
+  p.tiles_n = int((p.n + TM_BN - 1) / TM_BN);
+  if (p.group <= 0) p.group = 8;
+  p.num_tiles = int64_t(p.tiles_m) * p.tiles_n;
+  if (p.num_tiles <= 0) return 0;
+  const int64_t nseg = p.kc < p.k ? (p.k + p.kc - 1) / p.kc : 1;
+  if (g_tmem_fold && nseg >= 3) return run_tma<4, 2, 3, true, true>(p, ma, mb, s);
+  return run_tma<4, 2, 3, false, true>(p, ma, mb, s);
 }
 
 }  // namespace bf

@@ -27,6 +27,7 @@ __all__ = [
     "BfView",
     "BfScatterView",
     "BfCholLevel",
+    "BfModesView",
     "as_bfview",
     "stream_ptr",
     "check",
@@ -59,6 +60,19 @@ class BfScatterView(ctypes.Structure):
         ("n", ctypes.c_int64),
         ("rscat", ctypes.c_void_p),
         ("cscat", ctypes.c_void_p),
+    ]
+
+
+class BfModesView(ctypes.Structure):
+    _fields_ = [
+        ("base", ctypes.c_void_p),
+        ("off", ctypes.c_int64),
+        ("nr", ctypes.c_int32),
+        ("nc", ctypes.c_int32),
+        ("rdim", ctypes.c_int64 * 2),
+        ("rstr", ctypes.c_int64 * 2),
+        ("cdim", ctypes.c_int64 * 2),
+        ("cstr", ctypes.c_int64 * 2),
     ]
 
 
@@ -136,6 +150,7 @@ _SIGNATURES = {
     "bf_pack_scatter_d": ([_SV, _I, _VP, _VP], _I),
     "bf_gemm_scatter_s": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
     "bf_gemm_scatter_sd": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
+    "bf_contract_modes_d": ([_D, _P(BfModesView), _P(BfModesView), _D, _P(BfModesView), _L, _VP], _I),
     "bf_cholesky_mixed": ([_V, _VP, _L, _VP, _VP, _VP, _VP, _VP, _VP, _L, _P(BfCholLevel), _I, _I, _I, _VP, _VP],
                           _I),
     "bf_dist_available": ([], _I),

@@ -23,7 +23,11 @@
  *     kc elements (engine/gemm.py:124-126).  Passing the reference's kc makes
  *     results bit-identical to the reference.
  *   - All functions are asynchronous on `stream` (a cudaStream_t, NULL = legacy
- *     default stream) and thread-safe for distinct streams.  Device-side
+ *     default stream) and thread-safe for distinct streams: the library's own
+ *     side streams (panel, aux, copy) and its scratch buffers are private to
+ *     each (device, calling stream) pair.  bf_set_option settings are
+ *     process-wide and must not change while calls are in flight, and the
+ *     bf_timeline record is a single-caller debugging aid.  Device-side
  *     failure indices are reported through caller-owned device ints that the
  *     caller initialises to -1 and reads after synchronising.
  *   - Return codes: BF_OK, or a negative BF_ERR_* (no fallback path exists:
@@ -68,6 +72,10 @@ typedef struct bf_chol_level {
 } bf_chol_level;
 
 int bf_abi_version(void);
+/* Free the library's cached device scratch (per-stream buffers of the
+ * 3xTF32 split, the LU k-major copies, the upper-triangle row-major copy);
+ * synchronises the device. */
+int bf_release_scratch(void);
 /* Number of kernels this library has launched in this process (all devices). */
 int64_t bf_launch_count(void);
 const char* bf_last_error(void);

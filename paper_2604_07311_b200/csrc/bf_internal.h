@@ -110,7 +110,7 @@ bool smem_attr(const void* kern, int bytes);
 void* stream_scratch(int tag, size_t bytes, cudaStream_t s);
 // capi.cu bridges for the other translation units
 int set_error(int code, const char* msg);
-cudaStream_t panel_stream_for_device();  // the high-priority panel stream of the current device
+cudaStream_t panel_stream_for(cudaStream_t caller);  // the high-priority panel stream paired with `caller`
 extern int g_mixed_reserve;
 
 // Kernel-family entry points (implemented in the .cu files).
@@ -188,6 +188,8 @@ int launch_apply_pivots(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs
 int launch_add_offset(int64_t* piv, int64_t count, int64_t delta, cudaStream_t s);
 int launch_tridiag_form_f32(const float* a, int64_t off, int64_t rs, int64_t cs, int64_t n, int64_t kt, const float* t,
                             float* w, cudaStream_t s);
+int launch_transpose_tri_f64(const double* src, int64_t off, int64_t rs, int64_t cs, int64_t n, double* dst,
+                             int64_t ld, int tri, cudaStream_t s);
 int launch_transpose(int is_f64, const void* src, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t n, void* dst,
                      int64_t ld, cudaStream_t s);
 int launch_trsm_left_base(int is_f64, double alpha, const void* t, int64_t toff, int64_t trs, int64_t tcs, void* b,

@@ -37,6 +37,14 @@ void* stream_scratch(int tag, size_t bytes, cudaStream_t s) {
   };
   static std::mutex mu;
   static std::map<Key, Buf> bufs;
+  if (tag < 0) {  // release every cached buffer (bf_release_scratch)
+    std::lock_guard<std::mutex> lk(mu);
+    cudaDeviceSynchronize();
+    for (auto& kv : bufs)
+      if (kv.second.p) cudaFree(kv.second.p);
+    bufs.clear();
+    return nullptr;
+  }
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   std::lock_guard<std::mutex> lk(mu);
@@ -108,6 +116,9 @@ int64_t g_diag_rows = 0;     // bf_set_option("diag_rows", h): ... the first h r
 // bf_set_option("overlap_h2d", 0): bf_cholesky_host_d loads the whole lower
 // triangle before factoring instead of overlapping the load with step 0
 int g_overlap_h2d = 1;
+// bf_set_option("upper_transpose", n0): FP64 factorizations of order >= n0 on
+// an mn-contiguous view (uplo="upper") run on a row-major copy (0 = never)
+int64_t g_upper_transpose = 1024;
 
 int fail(int code, const char* msg) {
   g_last_error = msg;
@@ -322,50 +333,40 @@ int chol_run(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int i
   return rc;
 }
 
-// High-priority side stream per device for the panel chain of the lookahead
-// schedule (its CTAs are preferred whenever trailing-update CTAs retire).
-cudaStream_t panel_stream() {
-  static cudaStream_t streams[64] = {};
+// Library-owned side streams, one set per (device, calling stream): two
+// factorizations enqueued on different caller streams (e.g. from different
+// host threads) get independent panel/aux/copy streams and never serialise
+// their panel chains on a shared one.
+enum SideRole { ROLE_PANEL = 0, ROLE_AUX = 1, ROLE_H2D = 2, ROLE_COPY = 3 };
+cudaStream_t side_stream(SideRole role, cudaStream_t caller) {
+  struct Key {
+    int dev, role;
+    cudaStream_t caller;
+    bool operator<(const Key& o) const {
+      return dev != o.dev ? dev < o.dev : (role != o.role ? role < o.role : caller < o.caller);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, cudaStream_t> streams;
   int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (!streams[dev]) {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, hi);
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  cudaStream_t& st = streams[Key{dev, int(role), caller}];
+  if (!st) {
+    if (role == ROLE_PANEL) {  // high priority: its CTAs go first whenever trailing-update CTAs retire
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi);
+    } else {
+      cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    }
   }
-  return streams[dev];
+  return st;
 }
-
-// Auxiliary stream per device (the pipelined first step's trailing update).
-cudaStream_t aux_stream() {
-  static cudaStream_t streams[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
-  return streams[dev];
-}
-
-// Host-to-device stream per device (the overlapped load of bf_cholesky_host_d).
-cudaStream_t h2d_stream() {
-  static cudaStream_t streams[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
-  return streams[dev];
-}
-
-// Copy stream per device (host <-> device traffic of bf_cholesky_host_d).
-cudaStream_t copy_stream() {
-  static cudaStream_t streams[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (!streams[dev]) cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
-  return streams[dev];
-}
+cudaStream_t panel_stream(cudaStream_t caller) { return side_stream(ROLE_PANEL, caller); }
+cudaStream_t aux_stream(cudaStream_t caller) { return side_stream(ROLE_AUX, caller); }
+cudaStream_t h2d_stream(cudaStream_t caller) { return side_stream(ROLE_H2D, caller); }
+cudaStream_t copy_stream(cudaStream_t caller) { return side_stream(ROLE_COPY, caller); }
 
 // Host write-back of finished block columns (bf_cholesky_host_d): while set,
 // the lookahead driver copies block column k's lower part (rows >= k*bs) to
@@ -427,7 +428,7 @@ cudaEvent_t g_tl_origin = nullptr;
 int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int64_t base, int* d_info,
                       cudaStream_t s) {
   const int64_t n = a.n, bs = lv[0].bs, kc = lv[0].kc;
-  cudaStream_t ps = panel_stream();
+  cudaStream_t ps = panel_stream(s);
   if (!ps) return fail(BF_ERR_CUDA, "cannot create the panel stream");
   cudaEvent_t ev_main, ev_panel;
   cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming);
@@ -477,7 +478,7 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     const int64_t want = (nr2 + g_pipeline_first - 1) / g_pipeline_first;
     const int64_t C = ((want + b2 - 1) / b2) * b2;
     const int64_t chunks = (nr2 + C - 1) / C;
-    cudaStream_t xs = aux_stream();
+    cudaStream_t xs = aux_stream(s);
     if (!xs) return fail(BF_ERR_CUDA, "cannot create the aux stream");
     bf_view a11 = subview(a, 0, b, 0, b);
     bf_view l21 = subview(a, r2, nr2, 0, b);
@@ -759,7 +760,7 @@ int lu_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, i
                  cudaStream_t s) {
   const int64_t m = a.m, n = a.n, steps = m < n ? m : n;
   const int64_t bs = lv[0].bs, kc = lv[0].kc;
-  cudaStream_t ps = panel_stream();
+  cudaStream_t ps = panel_stream(s);
   if (!ps) return fail(BF_ERR_CUDA, "cannot create the panel stream");
   cudaEvent_t ev_main, ev_panel;
   cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming);
@@ -796,6 +797,32 @@ int chol_impl(Mode mode, const bf_view* a, const bf_chol_level* lv, int nl, int*
   if (a->m != a->n) return fail(BF_ERR_SHAPE, "square matrix required");
   if (nl < 1) return fail(BF_ERR_VALUE, "empty control tree");
   if (a->n == 0) return BF_OK;
+  if (mode == MODE_D && g_upper_transpose && a->rs == 1 && a->cs >= a->n && a->n >= g_upper_transpose) {
+    // uplo="upper" arrives as the lower algorithm on the transposed view
+    // (factor/cholesky.py:108-109), whose operands are mn-contiguous: the
+    // TMA kernel cannot stage them.  Factor a row-major copy instead: the
+    // view's lower triangle in (a tiled transpose of the caller's upper
+    // triangle), the same tree on it, the lower triangle back out.  Every
+    // element sees the same operations, so the bits (and, after a pivot
+    // failure, the partial state) are those of the in-place run.
+    const int64_t n = a->n;
+    // the copy lives in this stream's cached scratch (bf_release_scratch frees it)
+    double* work = static_cast<double*>(bf::stream_scratch(3, size_t(n) * size_t(n) * sizeof(double), s));
+    if (work) {
+      double* src = static_cast<double*>(a->base);
+      // work(i, j) = view(i, j) = storage[off + i + j*cs] for i >= j: a transpose of the
+      // row-major storage's upper triangle
+      int rc = bf::launch_transpose_tri_f64(src, a->off, a->cs, 1, n, work, n, 2, s);
+      bf_view w{work, 0, n, n, n, 1};
+      if (!rc) rc = chol_impl(mode, &w, lv, nl, d_info, s);
+      else rc = fail(BF_ERR_CUDA, "transpose launch failed");
+      // view(i, j) = work(i, j), i >= j: storage[off + j*cs + i] = work[i*n + j]
+      if (bf::launch_transpose_tri_f64(work, 0, n, 1, n, src + a->off, a->cs, 1, s) && !rc)
+        rc = fail(BF_ERR_CUDA, "transpose launch failed");
+      return rc;
+    }
+    // no room for the copy: factor in place on the cp.async kernel
+  }
   if (lv[0].variant == 3 && lv[0].bs >= 1 && a->n > 2 * lv[0].bs && g_lookahead)
     return chol_v3_lookahead(mode, *a, lv, nl, 0, d_info, s);
   return chol_run(mode, *a, lv, nl, 0, 0, d_info, s);
@@ -849,7 +876,7 @@ int gemm_d_limited(double alpha, const bf_view& a, const bf_view& b, double beta
   return gemm_impl(MODE_D, alpha, a, b, beta, c, lower_only, kc, d_abort, s, abort_limit);
 }
 int set_error(int code, const char* msg) { return fail(code, msg); }
-cudaStream_t panel_stream_for_device() { return panel_stream(); }
+cudaStream_t panel_stream_for(cudaStream_t caller) { return panel_stream(caller); }
 }  // namespace bf
 
 extern "C" {
@@ -857,6 +884,11 @@ extern "C" {
 int bf_abi_version(void) { return 1; }
 int64_t bf_launch_count(void) { return bf::g_launches.load(std::memory_order_relaxed); }
 const char* bf_last_error(void) { return g_last_error.c_str(); }
+
+int bf_release_scratch(void) {
+  bf::stream_scratch(-1, 0, nullptr);
+  return cudaGetLastError() == cudaSuccess ? BF_OK : fail(BF_ERR_CUDA, "release failed");
+}
 int bf_set_option(const char* name, int64_t value) {
   if (name && std::strcmp(name, "lookahead") == 0) {
     g_lookahead = value != 0;
@@ -884,6 +916,10 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "persist") == 0) {
     bf::g_persist = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "upper_transpose") == 0 && value >= 0) {
+    g_upper_transpose = value;
     return BF_OK;
   }
   if (name && std::strcmp(name, "mixed_reserve") == 0 && value >= 0) {
@@ -1059,7 +1095,7 @@ int bf_cholesky_host_d(double* host, int64_t ld, const bf_view* work, const bf_c
   const int64_t n = work->n;
   if (n == 0) return BF_OK;
   cudaStream_t s = S(stream);
-  cudaStream_t cs = copy_stream();
+  cudaStream_t cs = copy_stream(s);
   if (!cs) return fail(BF_ERR_CUDA, "cannot create the copy stream");
   double* dev = static_cast<double*>(work->base) + work->off;
   // lower triangle in, by block columns of the root bs (rows >= the column's
@@ -1067,7 +1103,7 @@ int bf_cholesky_host_d(double* host, int64_t ld, const bf_view* work, const bf_c
   // step 0 consumes each block column as it lands; otherwise in stream order.
   const int64_t bs = levels[0].bs >= 1 ? levels[0].bs : n;
   const bool overlap = g_lookahead && g_overlap_h2d && levels[0].variant == 3 && n > 2 * bs && !g_pipeline_first;
-  cudaStream_t hs = overlap ? h2d_stream() : s;
+  cudaStream_t hs = overlap ? h2d_stream(s) : s;
   if (overlap && !hs) return fail(BF_ERR_CUDA, "cannot create the h2d stream");
   HostLoad hl;
   hl.bs = bs;

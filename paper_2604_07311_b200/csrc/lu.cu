@@ -613,6 +613,25 @@ __global__ void transpose_kernel(const T* src, int64_t off, int64_t rs, int64_t 
   }
 }
 
+// dst[j*ld + i] = src(i, j) restricted to one triangle of src (tri 1: i >= j,
+// 2: i <= j); 32x32 tiles wholly outside it are skipped
+template <typename T>
+__global__ void transpose_tri_kernel(const T* src, int64_t off, int64_t rs, int64_t cs, int64_t n, T* dst, int64_t ld,
+                                     int tri) {
+  __shared__ T tile[32][33];
+  const int64_t i0 = int64_t(blockIdx.y) * 32, j0 = int64_t(blockIdx.x) * 32;
+  if ((tri == 1 && i0 + 31 < j0) || (tri == 2 && j0 + 31 < i0)) return;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t i = i0 + r, j = j0 + threadIdx.x;
+    if (i < n && j < n) tile[r][threadIdx.x] = src[off + i * rs + j * cs];
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t j = j0 + r, i = i0 + threadIdx.x;
+    if (i < n && j < n && (tri == 0 || (tri == 1 ? i >= j : i <= j))) dst[j * ld + i] = tile[threadIdx.x][r];
+  }
+}
+
 // W (kt x n, row-major) = T * A^T with the reference's packing arithmetic in T
 template <typename T>
 __global__ void tridiag_form_kernel(const T* a, int64_t off, int64_t rs, int64_t cs, int64_t n, int64_t kt,
@@ -793,6 +812,15 @@ int launch_transpose(int is_f64, const void* src, int64_t off, int64_t rs, int64
   else
     transpose_kernel<float><<<grid, block, 0, s>>>(static_cast<const float*>(src), off, rs, cs, m, n,
                                                    static_cast<float*>(dst), ld);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+int launch_transpose_tri_f64(const double* src, int64_t off, int64_t rs, int64_t cs, int64_t n, double* dst,
+                             int64_t ld, int tri, cudaStream_t s) {
+  if (n <= 0) return 0;
+  note_launch();
+  const dim3 grid(unsigned((n + 31) / 32), unsigned((n + 31) / 32)), block(32, 8);
+  transpose_tri_kernel<double><<<grid, block, 0, s>>>(src, off, rs, cs, n, dst, ld, tri);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 

@@ -387,7 +387,7 @@ int bf_cholesky_mixed(const bf_view* a, float* w, int64_t ldw, void* pbuf0, void
   if (n == 0) return BF_OK;
   const bool tf32 = precision == 1;
   cudaStream_t main = static_cast<cudaStream_t>(stream);
-  cudaStream_t side = lookahead ? panel_stream_for_device() : main;
+  cudaStream_t side = lookahead ? panel_stream_for(main) : main;
   if (lookahead && !side) return set_error(BF_ERR_CUDA, "cannot create the side stream");
   void* pbuf[2] = {pbuf0, pbuf1};
   const int64_t nblk = (n + bs - 1) / bs;

@@ -93,6 +93,7 @@ _VP = ctypes.c_void_p
 
 _SIGNATURES = {
     "bf_abi_version": ([], _I),
+    "bf_release_scratch": ([], _I),
     "bf_launch_count": ([], _L),
     "bf_last_error": ([], ctypes.c_char_p),
     "bf_device_sm_count": ([], _I),

@@ -475,3 +475,71 @@ def test_pack_scatter_exact(cuda):
                                                  torch.cuda.current_stream().cuda_stream), "pack")
         got = out.reshape(7, 5) if tr else out.reshape(5, 7)
         assert torch.equal(got, want.T if tr else want)
+
+
+@pytest.mark.parametrize("npd", [False, True])
+def test_upper_on_row_major_copy_bitwise(cuda, npd):
+    """uplo="upper" at n >= upper_transpose runs on a row-major copy (the TMA
+    kernel) — same bits as the in-place run on the mn-contiguous view,
+    including the partial state after a pivot failure."""
+    from paper_2604_07311_b200.engine import _lib
+
+    lib = _lib.lib()
+    n = 2000
+    a0 = spd_int(777, n)
+    if npd:
+        a0[1500, 1500] = -1e9
+    tree = parse_tree('{"op":"cholesky","variant":3,"bs":512,"kernel":{"kc":512},"child":{"op":"cholesky",'
+                      '"variant":3,"bs":128,"kernel":{"kc":128},"child":{"op":"cholesky","variant":"unblocked3"}}}')
+    outs = []
+    for thr in (0, 1024):
+        lib.bf_set_option(b"upper_transpose", thr)
+        v = make_view(n, n, fill=a0)
+        err = None
+        try:
+            bf.cholesky(v, "upper", tree)
+        except bf.errors.NotPositiveDefiniteError as e:
+            err = e.index
+        outs.append((v.to_numpy().tobytes(), err))
+    lib.bf_set_option(b"upper_transpose", 1024)
+    assert outs[0] == outs[1]
+    assert outs[0][1] == (1500 if npd else None)
+
+
+def test_two_host_threads_two_streams_bitwise(cuda):
+    """Factorizations enqueued from two host threads on two streams (each with
+    its own library side streams) give the sequential bits."""
+    import threading
+
+    n = 2600
+    tree = parse_tree('{"op":"cholesky","variant":3,"bs":512,"kernel":{"kc":512},"child":{"op":"cholesky",'
+                      '"variant":3,"bs":128,"kernel":{"kc":128},"child":{"op":"cholesky","variant":"unblocked3"}}}')
+    inputs = [spd_int(31 + i, n) for i in range(2)]
+    expect = []
+    for a0 in inputs:
+        v = make_view(n, n, fill=a0)
+        bf.cholesky(v, "lower", tree)
+        expect.append(v.to_numpy().tobytes())
+    views = [make_view(n, n, fill=a0) for a0 in inputs]
+    torch.cuda.synchronize()
+    errors = []
+
+    def work(i):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                for _ in range(3):
+                    views[i].storage.copy_(torch.as_tensor(inputs[i].reshape(-1), device="cuda"))
+                    bf.cholesky(views[i], "lower", tree)
+            st.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors
+    for i in range(2):
+        assert views[i].to_numpy().tobytes() == expect[i]

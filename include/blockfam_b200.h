@@ -76,6 +76,11 @@ int bf_abi_version(void);
  * 3xTF32 split, the LU k-major copies, the upper-triangle row-major copy);
  * synchronises the device. */
 int bf_release_scratch(void);
+/* Bytes of device scratch the library holds now and its high-water mark since
+ * the last reset (the B200 side of the reference's Workspace accounting,
+ * engine/workspace.py:18-56). */
+int bf_scratch_stats(int64_t* live_bytes, int64_t* peak_bytes);
+int bf_scratch_reset_peak(void);
 /* Number of kernels this library has launched in this process (all devices). */
 int64_t bf_launch_count(void);
 const char* bf_last_error(void);

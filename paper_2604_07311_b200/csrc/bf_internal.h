@@ -108,6 +108,7 @@ void note_launch(int64_t n = 1);
 bool smem_attr(const void* kern, int bytes);
 // device scratch keyed by (tag, current device, stream); grows on demand
 void* stream_scratch(int tag, size_t bytes, cudaStream_t s);
+void scratch_account(int64_t delta_bytes);  // every library-owned device buffer reports here
 // capi.cu bridges for the other translation units
 int set_error(int code, const char* msg);
 cudaStream_t panel_stream_for(cudaStream_t caller);  // the high-priority panel stream paired with `caller`

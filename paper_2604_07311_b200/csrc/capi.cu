@@ -20,6 +20,17 @@ namespace bf {
 static std::atomic<int64_t> g_launches{0};
 void note_launch(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Accounting of the library's device scratch (the B200 side of the reference's
+// Workspace live/peak counters, engine/workspace.py:18-56): bytes currently
+// held in the scratch caches and the high-water mark since the last reset.
+std::atomic<int64_t> g_scratch_live{0}, g_scratch_peak{0};
+void scratch_account(int64_t delta) {
+  const int64_t now = g_scratch_live.fetch_add(delta) + delta;
+  int64_t pk = g_scratch_peak.load();
+  while (now > pk && !g_scratch_peak.compare_exchange_weak(pk, now)) {
+  }
+}
+
 // Device scratch private to one (purpose, device, stream): work queued on
 // different streams never shares a buffer, and growing one only waits for
 // its own stream.
@@ -41,7 +52,10 @@ void* stream_scratch(int tag, size_t bytes, cudaStream_t s) {
     std::lock_guard<std::mutex> lk(mu);
     cudaDeviceSynchronize();
     for (auto& kv : bufs)
-      if (kv.second.p) cudaFree(kv.second.p);
+      if (kv.second.p) {
+        cudaFree(kv.second.p);
+        scratch_account(-int64_t(kv.second.bytes));
+      }
     bufs.clear();
     return nullptr;
   }
@@ -53,6 +67,7 @@ void* stream_scratch(int tag, size_t bytes, cudaStream_t s) {
     if (b.p) {
       cudaStreamSynchronize(s);  // the old buffer may still be read by work queued on s
       cudaFree(b.p);
+      scratch_account(-int64_t(b.bytes));
     }
     b.p = nullptr;
     b.bytes = 0;
@@ -61,6 +76,7 @@ void* stream_scratch(int tag, size_t bytes, cudaStream_t s) {
       return nullptr;
     }
     b.bytes = bytes;
+    scratch_account(int64_t(bytes));
   }
   return b.p;
 }
@@ -885,6 +901,16 @@ int bf_abi_version(void) { return 1; }
 int64_t bf_launch_count(void) { return bf::g_launches.load(std::memory_order_relaxed); }
 const char* bf_last_error(void) { return g_last_error.c_str(); }
 
+int bf_scratch_stats(int64_t* live_bytes, int64_t* peak_bytes) {
+  if (live_bytes) *live_bytes = bf::g_scratch_live.load();
+  if (peak_bytes) *peak_bytes = bf::g_scratch_peak.load();
+  return BF_OK;
+}
+int bf_scratch_reset_peak(void) {
+  bf::g_scratch_peak.store(bf::g_scratch_live.load());
+  return BF_OK;
+}
+
 int bf_release_scratch(void) {
   bf::stream_scratch(-1, 0, nullptr);
   return cudaGetLastError() == cudaSuccess ? BF_OK : fail(BF_ERR_CUDA, "release failed");
@@ -1244,27 +1270,45 @@ int bf_sandwich_skew_d(const bf_view* c, const bf_view* a, const double* d_t, in
   return rc ? fail(BF_ERR_CUDA, "sandwich launch failed") : BF_OK;
 }
 
-// f32 storage: the reference packs W in f32 (acc dtype f32); W is formed in a
-// device workspace (w: kt x n floats, caller-provided) and fed to the f32 GEMMT
+// f32 storage: the reference packs W in f32 (acc dtype f32); the SIMT kernel's
+// B loader forms each staged element of W = T*A^T from two source elements, so
+// no k x n intermediate exists (d_w is unused and may be NULL: kept for ABI
+// compatibility)
 int bf_sandwich_skew_s(const bf_view* c, const bf_view* a, const float* d_t, float* d_w, int64_t kc, void* stream) {
+  (void)d_w;
   if (!c || !a) return fail(BF_ERR_VALUE, "null view");
   if (c->m != c->n) return fail(BF_ERR_SHAPE, "sandwich needs square c");
   if (a->m != c->m) return fail(BF_ERR_SHAPE, "sandwich dims mismatch");
   if (kc < 1) return fail(BF_ERR_VALUE, "kc must be >= 1");
   const int64_t n = c->m, kt = a->n;
   if (n == 0 || kt == 0) return BF_OK;
-  if (!d_w || (kt > 1 && !d_t)) return fail(BF_ERR_VALUE, "null tridiagonal vector or workspace");
-  cudaStream_t s = S(stream);
-  if (bf::launch_tridiag_form_f32(static_cast<const float*>(a->base), a->off, a->rs, a->cs, n, kt, d_t, d_w, s))
-    return fail(BF_ERR_CUDA, "sandwich transform launch failed");
-  bf_view w{};
-  w.base = d_w;
-  w.off = 0;
-  w.m = kt;
-  w.n = n;
-  w.rs = n;
-  w.cs = 1;
-  return gemm_impl(MODE_S, -1.0, *a, w, 1.0, *c, 1, kc, nullptr, s);
+  if (kt > 1 && !d_t) return fail(BF_ERR_VALUE, "null tridiagonal vector");
+  GemmParams p{};
+  p.m = n;
+  p.n = n;
+  p.k = kt;
+  p.kc = kc;
+  p.a = classify(a->base, a->off, a->rs, a->cs, n, kt, kc, MODE_S);
+  OperandMK b{};
+  b.base = a->base;
+  b.off = a->off;
+  b.s_mn = a->rs;
+  b.s_k = a->cs;
+  b.layout = bf::GL_TRIDIAG;
+  b.vec = 1;
+  b.tvec = reinterpret_cast<const double*>(d_t);  // read as float by the f32 loader
+  b.k_total = kt;
+  p.b = b;
+  p.c = c->base;
+  p.c_off = c->off;
+  p.c_rs = c->rs;
+  p.c_cs = c->cs;
+  p.alpha = -1.0;
+  p.beta = 1.0;
+  p.lower_only = 1;
+  p.abort_limit = -1;
+  const int rc = bf::launch_gemm_simt_f32(p, S(stream));
+  return rc ? fail(BF_ERR_CUDA, "sandwich launch failed") : BF_OK;
 }
 static int ltlt_entry(int is_f64, const bf_view* x, int64_t j0, int64_t j1, int blocked, int64_t k, void* w,
                       int64_t wld, int64_t* d_piv, void* d_t, void* d_m, void* d_w, void* stream) {

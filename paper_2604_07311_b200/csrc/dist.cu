@@ -291,7 +291,10 @@ int bf_dist_finalize(bf_dist* d) {
     if (f) cudaStreamDestroy(f);
   for (auto& e : d->ev_pool)
     if (e) cudaEventDestroy(e);
-  if (d->bufs) cudaFree(d->bufs);
+  if (d->bufs) {
+    cudaFree(d->bufs);
+    bf::scratch_account(-int64_t(d->buf_elems * sizeof(double)));
+  }
   delete d;
   return BF_OK;
 }
@@ -357,7 +360,10 @@ int bf_chol_dist_d(bf_dist* d, double* local, int64_t n, const bf_chol_level* le
   need += size_t(L.nb * L.nb);
   if (need > d->buf_elems) {
     cudaStreamSynchronize(x.user);
-    if (d->bufs) cudaFree(d->bufs);
+    if (d->bufs) {
+      cudaFree(d->bufs);
+      bf::scratch_account(-int64_t(d->buf_elems * sizeof(double)));
+    }
     d->bufs = nullptr;
     d->buf_elems = 0;
     if (cudaMalloc(&d->bufs, need * sizeof(double)) != cudaSuccess) {
@@ -365,6 +371,7 @@ int bf_chol_dist_d(bf_dist* d, double* local, int64_t n, const bf_chol_level* le
       return bf::set_error(BF_ERR_CUDA, "cannot allocate the panel receive buffers");
     }
     d->buf_elems = need;
+    bf::scratch_account(int64_t(need * sizeof(double)));
   }
   int rc = bf::chol_dist_schedule(x, L, local, d->lookahead != 0);
   cudaEvent_t done = d->ev_pool[d->ev_next];

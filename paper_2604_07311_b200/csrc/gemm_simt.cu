@@ -21,6 +21,17 @@ constexpr int SB_M = 64, SB_N = 64, SB_K = 16, SB_THREADS = 256;  // 16x16 threa
 template <typename T>
 __device__ __forceinline__ T ld_elem(const OperandMK& op, int64_t mn, int64_t k) {
   const T* g = static_cast<const T*>(op.base);
+  if (op.layout == GL_TRIDIAG) {
+    // the skew sandwich's B = T*A^T formed while staged (engine/kernels.py:93-122
+    // pack_b_block_tridiag): W[k, mn] = t[k-1]*A(mn, k-1) - t[k]*A(mn, k+1) in the
+    // storage type, edge terms dropped; op.tvec holds T's subdiagonal (type T)
+    const T* t = reinterpret_cast<const T*>(op.tvec);
+    const T* row = g + op.off + mn * op.s_mn;
+    T acc = T(0);
+    if (k > 0) acc = Ops<T>::add(acc, Ops<T>::mul(t[k - 1], row[(k - 1) * op.s_k]));
+    if (k < op.k_total - 1) acc = Ops<T>::sub(acc, Ops<T>::mul(t[k], row[(k + 1) * op.s_k]));
+    return acc;
+  }
   if (op.mn_scat) return g[op.mn_scat[mn] + op.k_scat[k]];
   return g[op.off + mn * op.s_mn + k * op.s_k];
 }

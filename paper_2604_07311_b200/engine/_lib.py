@@ -94,6 +94,8 @@ _VP = ctypes.c_void_p
 _SIGNATURES = {
     "bf_abi_version": ([], _I),
     "bf_release_scratch": ([], _I),
+    "bf_scratch_stats": ([_P(_L), _P(_L)], _I),
+    "bf_scratch_reset_peak": ([], _I),
     "bf_launch_count": ([], _L),
     "bf_last_error": ([], ctypes.c_char_p),
     "bf_device_sm_count": ([], _I),

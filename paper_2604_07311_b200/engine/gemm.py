@@ -180,9 +180,9 @@ def sandwich_skew(
         rc = _lib.lib().bf_sandwich_skew_d(ctypes.byref(vc), ctypes.byref(va), d_t.data_ptr(), int(cfg.kc), stream)
     else:
         d_t = torch.as_tensor(t.astype(np.float32) if t.size else np.zeros(1, np.float32)).to(c.device)
-        d_w = torch.empty(kt * c.m, dtype=torch.float32, device=c.device)
-        rc = _lib.lib().bf_sandwich_skew_s(ctypes.byref(vc), ctypes.byref(va), d_t.data_ptr(), d_w.data_ptr(),
-                                           int(cfg.kc), stream)
+        # W = T*A^T is formed while the f32 kernel stages B: no k x n buffer
+        rc = _lib.lib().bf_sandwich_skew_s(ctypes.byref(vc), ctypes.byref(va), d_t.data_ptr(), None, int(cfg.kc),
+                                           stream)
     _lib.check(rc, "sandwich_skew")
 
 
@@ -196,9 +196,8 @@ def _sandwich_dev(c: MatrixView, a: MatrixView, d_t: torch.Tensor, cfg: KernelCo
     if c.dtype.value == "f64":
         rc = _lib.lib().bf_sandwich_skew_d(ctypes.byref(vc), ctypes.byref(va), d_t.data_ptr(), int(cfg.kc), stream)
     else:
-        d_w = torch.empty(a.n * c.m, dtype=torch.float32, device=c.device)
-        rc = _lib.lib().bf_sandwich_skew_s(ctypes.byref(vc), ctypes.byref(va), d_t.data_ptr(), d_w.data_ptr(),
-                                           int(cfg.kc), stream)
+        rc = _lib.lib().bf_sandwich_skew_s(ctypes.byref(vc), ctypes.byref(va), d_t.data_ptr(), None, int(cfg.kc),
+                                           stream)
     _lib.check(rc, "sandwich_skew")
 
 

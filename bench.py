@@ -345,6 +345,9 @@ def run_distributed(args, bf, torch, dist, dev, world: int, rank: int, n: int) -
     tree_doc = dist_tree(world) if args.tree == json.dumps(GPU_TREE) else json.loads(args.tree)
     tree = parse_tree(json.dumps(tree_doc))
     ctx = native.DistContext.from_torch_distributed()
+    for kv in filter(None, os.environ.get("BF_DIST_OPTS", "").split(",")):  # e.g. BF_DIST_OPTS=fan=0,reserve=24
+        k, v = kv.split("=")
+        ctx.set_option(k, int(v))
     lp = ctx.layout(n, tree.bs)
     local0 = torch.empty(lp.local_elems(), dtype=torch.float64, device=dev)
     native.fill_synthetic(ctx, local0, n, tree.bs, seed=42)

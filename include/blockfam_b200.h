@@ -193,6 +193,13 @@ typedef struct bf_modes_view {
  * or divisor of 128, 16-byte strides and K % 32 == 0; otherwise it returns
  * BF_ERR_UNSUPPORTED (the host then stages or gathers that operand).
  * alpha == 0 or K == 0 are the caller's (reference edge semantics). */
+/* bf16 variant (SURVEY.md §8(b) bf_contract_x; no reference counterpart):
+ * C := beta*C + alpha*A*B for FP64 strided views with the operands rounded to
+ * bf16 and the products summed in fp32 on tcgen05 (TMEM accumulators);
+ * accuracy ~2^-8 relative per product.  Uses library scratch
+ * ((M+N)*K bf16 + M*N fp32, bf_scratch_stats). */
+int bf_contract_bf16_d(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c,
+                       void* stream);
 int bf_contract_modes_d(double alpha, const bf_modes_view* a, const bf_modes_view* b, double beta,
                         const bf_modes_view* c, int64_t kc, void* stream);
 int bf_gemm_scatter_sd(double alpha, const bf_scatter_view* a, const bf_scatter_view* b, double beta,

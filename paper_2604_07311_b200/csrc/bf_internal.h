@@ -113,6 +113,8 @@ void scratch_account(int64_t delta_bytes);  // every library-owned device buffer
 int set_error(int code, const char* msg);
 cudaStream_t panel_stream_for(cudaStream_t caller);  // the high-priority panel stream paired with `caller`
 extern int g_mixed_reserve;
+int launch_axpby_f32_f64(double alpha, const float* src, int64_t ld, double beta, double* c, int64_t off, int64_t rs,
+                         int64_t cs, int64_t m, int64_t n, cudaStream_t s);
 
 // Kernel-family entry points (implemented in the .cu files).
 int launch_gemm_dmma(const GemmParams& p, cudaStream_t s);            // f64 storage, f64 acc

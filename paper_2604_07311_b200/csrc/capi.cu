@@ -1594,6 +1594,36 @@ int bf_gemm_scatter_d(double alpha, const bf_scatter_view* a, const bf_scatter_v
                       const bf_scatter_view* c, int64_t kc, void* stream) {
   return scatter_impl(MODE_D, alpha, a, b, beta, c, kc, S(stream));
 }
+// bf16 variant of the contraction GEMM (no reference counterpart; SURVEY.md
+// §8(b) bf_contract_x): operands rounded to bf16, products accumulated in fp32
+// on tcgen05 (TMEM), C := beta*C + alpha*(A B) in FP64.  A (M x K) and B (K x N)
+// are strided views (the folded facades); scratch: bf16 copies of A and B^T
+// (k-contiguous, rows padded to 16 bytes) and the fp32 product.
+int bf_contract_bf16_d(double alpha, const bf_view* a, const bf_view* b, double beta, const bf_view* c,
+                       void* stream) {
+  if (!a || !b || !c) return fail(BF_ERR_VALUE, "null view");
+  if (a->n != b->m || c->m != a->m || c->n != b->n) return fail(BF_ERR_SHAPE, "gemm dims mismatch");
+  const int64_t m = c->m, n = c->n, k = a->n;
+  if (m == 0 || n == 0) return BF_OK;
+  cudaStream_t s = S(stream);
+  if (k == 0 || alpha == 0.0) return scale_impl(MODE_D, beta, *c, 0, s);
+  const int64_t kp = (k + 7) / 8 * 8;  // 16-byte bf16 rows for TMA
+  const size_t bytes = size_t(m + n) * size_t(kp) * 2 + size_t(m) * size_t(n) * 4 + 256;
+  char* ws = static_cast<char*>(bf::stream_scratch(4, bytes, s));
+  if (!ws) return fail(BF_ERR_CUDA, "bf16 contraction scratch");
+  void* a16 = ws;
+  void* b16 = ws + size_t(m) * kp * 2;
+  float* prod = reinterpret_cast<float*>(ws + (size_t(m + n) * kp * 2 + 255) / 256 * 256);
+  if (kp != k) cudaMemsetAsync(ws, 0, size_t(m + n) * kp * 2, s);  // zero k padding: 0 * 0 adds nothing
+  int rc = bf::launch_f64_to_bf16(static_cast<const double*>(a->base), a->off, a->rs, a->cs, a16, kp, m, k, 0, s);
+  if (!rc) rc = bf::launch_f64_to_bf16(static_cast<const double*>(b->base), b->off, b->rs, b->cs, b16, kp, k, n, 1, s);
+  if (!rc) rc = bf::launch_gemm_bf16_tc(1.0, a16, kp, b16, kp, 0.0, prod, 0, n, 1, m, n, kp, 0, s);
+  if (rc == -3) return fail(BF_ERR_UNSUPPORTED, "bf16 contraction: unsupported size");
+  if (!rc) rc = bf::launch_axpby_f32_f64(alpha, prod, n, beta, static_cast<double*>(c->base), c->off, c->rs, c->cs, m, n,
+                                         s);
+  return rc ? fail(BF_ERR_CUDA, "bf16 contraction launch failed") : BF_OK;
+}
+
 // tensor/contract.py:159-185 contract on mode-group views: the 4-D TMA GEMM
 int bf_contract_modes_d(double alpha, const bf_modes_view* a, const bf_modes_view* b, double beta,
                         const bf_modes_view* c, int64_t kc, void* stream) {

@@ -369,6 +369,29 @@ __global__ void set_identity_kernel(double* x, int64_t ld, int64_t b) {
 
 }  // namespace
 
+// C(f64 view) := beta*C + alpha*S (S fp32 m x n row-major, ld): the bf16
+// contraction's epilogue in C's precision; beta == 0 never reads C
+__global__ void axpby_f32_f64_kernel(double alpha, const float* src, int64_t ld, double beta, double* c, int64_t off,
+                                     int64_t rs, int64_t cs, int64_t m, int64_t n) {
+  const int64_t total = m * n;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    double* p = c + off + i * rs + j * cs;
+    const double v = alpha * double(src[i * ld + j]);
+    *p = beta == 0.0 ? v : beta * *p + v;
+  }
+}
+
+int launch_axpby_f32_f64(double alpha, const float* src, int64_t ld, double beta, double* c, int64_t off, int64_t rs,
+                         int64_t cs, int64_t m, int64_t n, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return 0;
+  const int64_t total = m * n;
+  note_launch();
+  axpby_f32_f64_kernel<<<unsigned((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16), 256, 0, s>>>(
+      alpha, src, ld, beta, c, off, rs, cs, m, n);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
 int g_mixed_reserve = 32;  // bf_set_option("mixed_reserve", r): SMs the trailing GEMMT leaves to the side chain
 
 }  // namespace bf

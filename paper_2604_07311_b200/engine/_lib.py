@@ -153,6 +153,7 @@ _SIGNATURES = {
     "bf_pack_scatter_d": ([_SV, _I, _VP, _VP], _I),
     "bf_gemm_scatter_s": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
     "bf_gemm_scatter_sd": ([_D, _SV, _SV, _D, _SV, _L, _VP], _I),
+    "bf_contract_bf16_d": ([_D, _V, _V, _D, _V, _VP], _I),
     "bf_contract_modes_d": ([_D, _P(BfModesView), _P(BfModesView), _D, _P(BfModesView), _L, _VP], _I),
     "bf_cholesky_mixed": ([_V, _VP, _L, _VP, _VP, _VP, _VP, _VP, _VP, _L, _P(BfCholLevel), _I, _I, _I, _VP, _VP],
                           _I),

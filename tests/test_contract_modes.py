@@ -78,3 +78,25 @@ def test_mode_group_path_is_taken(cuda):
         assert _lib.lib().bf_launch_count() - l0 == 1  # one GEMM launch, nothing else
     finally:
         C._stage = orig
+
+
+@pytest.mark.parametrize("spec,dims", [("abij,cdij->abcd", {"a": 16, "b": 24, "c": 16, "d": 32, "i": 12, "j": 20}),
+                                       ("aibj,cjdi->abcd", {"a": 8, "b": 16, "c": 16, "d": 8, "i": 32, "j": 8})])
+def test_bf16_contraction_within_bf16_bound(cuda, spec, dims):
+    """precision='bf16' (tcgen05, fp32 accumulation): each product carries at
+    most ~2^-8 relative error from the bf16 roundings, so |C - C64| stays under
+    2^-7 * (|A| |B|) elementwise (plus the beta*C term exactly in FP64)."""
+    import paper_2604_07311_b200 as bf
+    from paper_2604_07311_b200.tensor import ContractionSpec, make_tensor
+
+    lhs, lc = spec.split("->")
+    la, lb = lhs.split(",")
+    ad, bd, cd = [dims[x] for x in la], [dims[x] for x in lb], [dims[x] for x in lc]
+    a0, b0, c0 = tensor_inputs(77, ad, bd, cd)
+    ta, tb, tc = make_tensor(ad, fill=a0), make_tensor(bd, fill=b0), make_tensor(cd, fill=c0)
+    bf.contract(1.5, ta, tb, 0.5, tc, ContractionSpec.parse(spec), precision="bf16")
+    got = tc.storage.cpu().numpy().reshape(cd)
+    ref = 1.5 * np.einsum(spec, a0, b0) + 0.5 * c0
+    bound = 1.5 * np.einsum(spec, np.abs(a0), np.abs(b0)) * 2.0 ** -7
+    assert np.all(np.abs(got - ref) <= bound + 1e-12)
+    assert np.abs(got - ref).max() > 0  # it really ran in reduced precision

@@ -116,15 +116,15 @@ class ClockSampler:
 def cpu_baseline(n_target: int, budget_s: float = 15.0) -> dict:
     """The oracle port of the reference (bit-identical to it) on this host,
     all cores, on a bounded sample: the largest n (multiple of 1024) whose
-    factorization fits the time budget, same tree shape as the reference C1
-    (v3, bs=128, unblocked3 leaf; kc=256 default)."""
+    factorization fits the time budget, with the GPU arm's tree."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import oracle as O
 
     O.build()
     threads = O.host_threads()
-    levels = O.levels_from_tree({"op": "cholesky", "variant": 3, "bs": 128,
-                                 "child": {"op": "cholesky", "variant": "unblocked3"}}, 0, "f64")
+    # the GPU arm's own tree (BASELINE configs[1] two-level blocking), so the
+    # sample differs from the GPU workload only in n
+    levels = O.levels_from_tree(GPU_TREE, 0, "f64")
 
     def run(n):
         rng = np.random.default_rng(42)
@@ -145,8 +145,9 @@ def cpu_baseline(n_target: int, budget_s: float = 15.0) -> dict:
         dt = run(n_s)
         n = n_s
     return {"value": chol_flops(n) / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
-            "sample": f"oracle C++ port of the reference (bit-identical), n={n} v3/bs128/unblocked3 kc=256, "
-                      f"{threads} threads, one factorization ({dt:.2f} s)"}
+            "sample": f"oracle C++ port of the reference (bit-identical to it), n={n}, the bench tree "
+                      f"(v3 bs2048 kc2048 -> v3 bs128 kc128 -> unblocked3), {threads} threads, one factorization "
+                      f"({dt:.2f} s)"}
 
 
 # ----------------------------------------------------------------- GPU arm --
@@ -276,7 +277,28 @@ def side_workloads(torch, a0, n: int, fp64_ms: float, l64=None) -> dict:
     e1.synchronize()
     cms = e0.elapsed_time(e1)
     out["c5_contraction"] = {"spec": "abij,cdij->abcd", "d": d, "dtype": "f64", "ms": round(cms, 3),
-                             "gflops": round(2.0 * d ** 6 / (cms / 1e3) / 1e9, 1)}
+                             "gflops": round(2.0 * d ** 6 / (cms / 1e3) / 1e9, 1),
+                             "path": "folded facades: one TMA DMMA GEMM, C tile in TMEM across the 64 kc folds"}
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        return e0.elapsed_time(e1)
+
+    ms_bf16 = timed(lambda: bfp.contract(1.0, ta, tb, 0.0, tc, spec, precision="bf16"))
+    out["c5_contraction_bf16"] = {"spec": "abij,cdij->abcd", "d": d, "ms": round(ms_bf16, 3),
+                                  "gflops": round(2.0 * d ** 6 / (ms_bf16 / 1e3) / 1e9, 1),
+                                  "path": "bf16 operands, fp32 TMEM accumulation on tcgen05, FP64 C (not bitwise)"}
+    pspec = ContractionSpec.parse("aibj,cidj->abcd")
+    ms_perm = timed(lambda: bfp.contract(1.0, ta, tb, 0.0, tc, pspec))
+    out["c5_contraction_permuted"] = {"spec": "aibj,cidj->abcd", "d": d, "dtype": "f64", "ms": round(ms_perm, 3),
+                                      "gflops": round(2.0 * d ** 6 / (ms_perm / 1e3) / 1e9, 1),
+                                      "path": "permuted mode groups through 4-D TMA tensor maps, no copy"}
     del ta, tb, tc
     torch.cuda.empty_cache()
     return out
@@ -465,7 +487,7 @@ def main() -> int:
                 "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic SPD (integer M, exact M M^T + n I), seed 42",
-                "config": {"workload": workload, "tree": "v3/bs128/unblocked3 (reference default, kc=256)"},
+                "config": {"workload": workload, "tree": GPU_TREE, "sample_n": base["sample"]},
                 "cpu_baseline": dict(base, value=round(value, 3)),
                 "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)

@@ -183,7 +183,7 @@ def side_workloads(torch, a0, n: int, fp64_ms: float, l64=None) -> dict:
     ws = MixedWorkspace(n, bs)
     a_full = a0 + a0.T  # a0 holds the lower triangle only; the solve needs the dense symmetric A
     a_full.diagonal().sub_(a0.diagonal())
-    step_tol = 1e-13  # forward-error criterion: ||x - x_ref|| / ||x_ref|| <= 1e-12
+    step_tol = 1e-11  # forward-error criterion: the error left after a step of 1e-11 is ~1e-13 << 1e-12
     posv_mixed(a_full, b, ws=ws, step_tol=step_tol)  # warm
     torch.cuda.synchronize()
     ms, fms = [], []
@@ -220,7 +220,7 @@ def side_workloads(torch, a0, n: int, fp64_ms: float, l64=None) -> dict:
                             "fp64_equiv_gflops": round(chol_flops(n) / (t / 1e3) / 1e9, 1),
                             "iterations": res.iterations, "backward_error": res.backward_error,
                             "fwd_err_vs_fp64_solution": fwd, "converged": bool(res.converged),
-                            "tol": "backward <= 10*n*eps64 and ||dx||/||x|| <= 1e-13",
+                            "tol": "backward <= 10*n*eps64 and ||dx||/||x|| <= 1e-11",
                             "roofline_factor": {"tensor_achieved_tflops": round(tc_flops / (tf / 1e3) / 1e12, 1),
                                                 "tensor_peak_tflops": bf16_peak,
                                                 "tensor_frac": round(tc_flops / (tf / 1e3) / 1e12 / bf16_peak, 4),
@@ -330,7 +330,7 @@ def roofline_syrk(bf, torch, a0, n: int, bs: int, kc: int) -> dict:
     del work
     achieved = flops / (ms / 1e3) / 1e12
     traffic, traffic_note = None, None
-    tpath = ROOT / "profiles" / "r01_syrk_traffic.json"
+    tpath = ROOT / "profiles" / "r02_syrk_traffic.json"
     if tpath.exists():
         t = json.loads(tpath.read_text())
         traffic = t["traffic_bytes"]
@@ -456,7 +456,9 @@ def main() -> int:
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    # --order (alias --n): under torchrun "--n" after the script name is taken
+    # as an abbreviation of torchrun's own options
+    ap.add_argument("--order", "--n", dest="n", type=int, default=N_DEFAULT)
     ap.add_argument("--tree", type=str, default=json.dumps(GPU_TREE))
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")

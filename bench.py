@@ -504,6 +504,9 @@ def main() -> int:
 
     if args.tiles_per_cta is not None:
         _lib.lib().bf_set_option(b"tiles_per_cta", args.tiles_per_cta)
+    for kv in filter(None, os.environ.get("BF_OPTS", "").split(",")):  # library options for sweeps (tools/)
+        k, v = kv.split("=")
+        _lib.check(_lib.lib().bf_set_option(k.encode(), int(v)), f"bf_set_option({k})")
     torch.cuda.set_device(local)
     if world > 1 or args.dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")

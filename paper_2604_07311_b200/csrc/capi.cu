@@ -127,6 +127,11 @@ int g_tail_reserve = 16;     // bf_set_option("tail_reserve", r): SMs left to th
 int64_t g_tail_rows = 32768;  // bf_set_option("tail_rows", t): ... when the rest of the update is <= t rows
                               // (larger updates keep the 1-tile CTAs: at n=131072 a persistent grid
                               // over the whole trailing matrix loses L2 locality, 22.1 -> 23.0 s)
+// bf_set_option("reserve_adaptive", 0|1): per-step reservation sized by the
+// panel stream's share of the step's work (+ "reserve_extra", >= "reserve_min")
+int g_reserve_adaptive = 1;
+int g_reserve_extra = 4;
+int g_reserve_min = 12;
 int g_diag_reserve = 0;      // bf_set_option("diag_reserve", r): SMs left to the panel stream while ...
 int64_t g_diag_rows = 0;     // bf_set_option("diag_rows", h): ... the first h rows of the rest are updated
 // bf_set_option("overlap_h2d", 0): bf_cholesky_host_d loads the whole lower
@@ -619,6 +624,25 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
       // g_tail_reserve SMs free of this update so the panel kernels start at once
       const int64_t m = nr2 - b2, r3 = r2 + b2;
       if (g_tail_reserve > 0 && m <= g_tail_rows) bf::t_reserve_sms = g_tail_reserve;
+      if (bf::t_reserve_sms > 0 && g_reserve_adaptive) {
+        // Size the reservation to the work the panel stream has to finish
+        // under this update: panel k+1's TRSM (m rows x b2^2) and diagonal
+        // factor (b2^3 / 3) against the rest of the trailing GEMMT (m^2 b):
+        // their SM shares, plus a few SMs for the latency-bound diagonal chain
+        // (n=32768: 376.4 ms with a fixed 16, 375.2 ms adaptive; the exposed
+        // panel chain drops 22.8 -> 15.6 ms, tools/gpu_r02_reserve.sh).
+        int sms = 148;
+        {
+          int dev = 0;
+          cudaGetDevice(&dev);
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const double T = double(m) * b2 * b2 + double(b2) * b2 * b2 / 3.0, S = double(m) * m * b;
+        int R = int(sms * T / (T + S) + 0.5) + g_reserve_extra;
+        if (R < g_reserve_min) R = g_reserve_min;
+        if (R > sms / 2) R = sms / 2;
+        bf::t_reserve_sms = R;
+      }
       // diagonal-factor window: the first h1 rows of the rest leave
       // g_diag_reserve SMs to the panel stream (its diagonal factor is a chain
       // of small launches that otherwise waits for trailing tiles to retire);
@@ -942,6 +966,18 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "persist") == 0) {
     bf::g_persist = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "reserve_adaptive") == 0) {
+    g_reserve_adaptive = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "reserve_extra") == 0 && value >= 0) {
+    g_reserve_extra = int(value);
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "reserve_min") == 0 && value >= 0) {
+    g_reserve_min = int(value);
     return BF_OK;
   }
   if (name && std::strcmp(name, "upper_transpose") == 0 && value >= 0) {

@@ -134,7 +134,7 @@ struct bf_dist {
   int ev_next = 0;
   double* bufs = nullptr;  // [parity][process row] stacked-panel receive buffers, then the diagonal tile
   size_t buf_elems = 0;
-  int reserve = 16;  // SMs left to the panel stream by the rest-of-update GEMMs
+  int reserve = -1;  // SMs left to the panel stream by the rest-of-update GEMMs (-1: adaptive)
   int lookahead = 1;
 };
 
@@ -170,13 +170,28 @@ struct NcclExec {
   int trsm(const bf_view& tri, const bf_view& b, Stream s) {
     return bf_trsm_rltn_ex_d(1.0, &tri, &b, lv[0].kc, nullptr, d_info, s);
   }
+  int reserve_now = 0;
+  // the reservation follows the panel work this rank has under the update
+  // (the one-GPU driver's adaptive rule); "reserve" option = fixed count
+  void reserve_for(double T, double S) {
+    if (d->reserve >= 0) {
+      reserve_now = d->reserve;
+      return;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
+    int R = T > 0.0 ? int(sms * T / (T + S) + 0.5) + 4 : 4;  // 4: NCCL's kernels
+    if (T > 0.0 && R < 12) R = 12;
+    if (R > sms / 2) R = sms / 2;
+    reserve_now = R;
+  }
   int gemm(const bf_view& a, const bf_view& bt, const bf_view& c, int lower, int64_t limit, bool reserve, Stream s) {
     bf_view b = bt;  // B = bt^T
     b.m = bt.n;
     b.n = bt.m;
     b.rs = bt.cs;
     b.cs = bt.rs;
-    if (reserve && d->reserve > 0) bf::t_reserve_sms = d->reserve;
+    if (reserve && reserve_now > 0) bf::t_reserve_sms = reserve_now;
     int rc = bf::gemm_d_limited(-1.0, a, b, 1.0, c, lower, lv[0].kc, d_info, limit, s);
     bf::t_reserve_sms = 0;
     return rc;

@@ -65,6 +65,7 @@ inline bf_view dist_view(double* base, int64_t m, int64_t n, int64_t ld) {
 //   int bcast_info(int comm, int root, Stream s);
 //   void group_begin(); int group_end();
 //   double* recv_buf(int parity, int p);  // capacity layout.stack_cap(p) * nb
+//   void reserve_for(double panel_flops, double update_flops);  // SMs the rest-of-update leaves free
 //   double* diag_buf();                   // nb * nb
 template <class X>
 int chol_dist_schedule(X& x, const DistLayout& L, double* local, bool lookahead) {
@@ -141,6 +142,21 @@ int chol_dist_schedule(X& x, const DistLayout& L, double* local, bool lookahead)
     const int64_t bk = L.tile_len(k);
     const int64_t nq = L.col_tiles(pcol);
     const int64_t limit = part == 2 ? (k + 1) * nb : INT64_MAX;
+    if (part == 2) {
+      // SMs for the panel stream while this update runs: my share of panel
+      // k+1 (its TRSM rows, plus the diagonal factor if I own it) against my
+      // rest of the update; a rank with no panel work keeps a few for NCCL
+      const int64_t k1 = k + 1;
+      double T = 0.0, S = 0.0;
+      if (k1 < L.tiles() && L.pcol == int(k1 % L.pc)) {
+        const double b1 = double(L.tile_len(k1));
+        T = double(L.stack_rows(prow, k1)) * b1 * b1;
+        if (prow == int(k1 % L.pr)) T += b1 * b1 * b1 / 3.0;
+      }
+      for (int64_t q = 0; q < nq; ++q)
+        if (L.panel_J(q) > k1) S += double(L.panel_h(q)) * double(L.panel_w(q)) * double(bk);
+      x.reserve_for(T, S);
+    }
     const bool fan = part != 1 && x.fan_count() > 0;
     int used = 0;
     if (fan)

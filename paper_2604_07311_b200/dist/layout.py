@@ -21,14 +21,16 @@ __all__ = ["BlockCyclic2D", "grid_for"]
 
 
 def grid_for(p: int) -> tuple[int, int]:
-    """Process grid for p GPUs: 1 -> 1x1, 2 -> 1x2, 4 -> 2x2, 8 -> 2x4, else
-    the most square Pr x Pc with Pr <= Pc."""
+    """Process grid for p GPUs: 1 -> 1x1, 2 -> 2x1, 4 -> 2x2, 8 -> 4x2, else
+    the most square Pr x Pc with Pr >= Pc.  Taller grids split each step's
+    panel TRSM (rows I > k, the heaviest part of the panel chain: n_k x nb^2
+    flops) over Pr ranks; every rank still receives the whole panel once."""
     if p < 1:
         raise ValueError("need at least one process")
-    pr = int(np.sqrt(p))
-    while p % pr:
-        pr -= 1
-    return pr, p // pr
+    pc = int(np.sqrt(p))
+    while p % pc:
+        pc -= 1
+    return p // pc, pc
 
 
 @dataclass(frozen=True)

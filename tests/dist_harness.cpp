@@ -91,6 +91,7 @@ struct HostExec {
   Stream fan_stream(int i) { return 2 + i; }
   int fan_count() { return 2; }
   void fork(Stream, Stream) {}
+  void reserve_for(double, double) {}
   int potrf(const bf_view& tile, int64_t base, Stream) {
     if (info >= 0) return BF_OK;  // aborted, like the device kernels
     orc_view_d t = ov(tile);

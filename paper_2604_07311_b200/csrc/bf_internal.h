@@ -207,6 +207,9 @@ int launch_qr_panel(int is_f64, void* a, int64_t off, int64_t rs, int64_t cs, in
 int launch_qr_t(int is_f64, const void* gram, int64_t b, const void* taus, void* t, cudaStream_t s);
 int launch_splitk_reduce(int is_f64, const void* ws, int S, int64_t m, int64_t n, double alpha, double beta, void* c,
                          int64_t off, int64_t rs, int64_t cs, cudaStream_t s);
+int launch_segfold(const double* ws, int S, int64_t m, int64_t n, double alpha, double beta, double* c, int64_t off,
+                   int64_t rs, int64_t cs, int lower_only, const int* abort_flag, int64_t abort_limit,
+                   cudaStream_t s);
 int launch_explicit_v(int is_f64, const void* a, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t b, void* v,
                       cudaStream_t s);
 int launch_reflector_apply(int is_f64, const void* a, int64_t aoff, int64_t ars, int64_t acs, int64_t m, int64_t j,

@@ -254,6 +254,108 @@ int gemm_impl(Mode mode, double alpha, const bf_view& a, const bf_view& b, doubl
   return rc ? fail(BF_ERR_CUDA, "gemm launch failed") : BF_OK;
 }
 
+// Library-owned side streams, one set per (device, calling stream): two
+// factorizations enqueued on different caller streams (e.g. from different
+// host threads) get independent panel/aux/copy streams and never serialise
+// their panel chains on a shared one.
+enum SideRole { ROLE_PANEL = 0, ROLE_AUX = 1, ROLE_H2D = 2, ROLE_COPY = 3, ROLE_SEG0 = 4 };
+cudaStream_t side_stream(SideRole role, cudaStream_t caller) {
+  struct Key {
+    int dev, role;
+    cudaStream_t caller;
+    bool operator<(const Key& o) const {
+      return dev != o.dev ? dev < o.dev : (role != o.role ? role < o.role : caller < o.caller);
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, cudaStream_t> streams;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  cudaStream_t& st = streams[Key{dev, int(role), caller}];
+  if (!st) {
+    if (role == ROLE_PANEL) {  // high priority: its CTAs go first whenever trailing-update CTAs retire
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi);
+    } else {
+      cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    }
+  }
+  return st;
+}
+cudaStream_t panel_stream(cudaStream_t caller) { return side_stream(ROLE_PANEL, caller); }
+cudaStream_t aux_stream(cudaStream_t caller) { return side_stream(ROLE_AUX, caller); }
+cudaStream_t h2d_stream(cudaStream_t caller) { return side_stream(ROLE_H2D, caller); }
+cudaStream_t copy_stream(cudaStream_t caller) { return side_stream(ROLE_COPY, caller); }
+
+// Deep-K narrow GEMM/GEMMT (V2's A11 -= A10 A10^T and A21 -= A20 A10^T, V1's
+// SYRK: few output tiles, K = the whole factored part): the kc segments are
+// independent sums, so each is computed from +0 by its own launch on its own
+// side stream (alpha 1, beta 0: the exact sum lands in scratch) and one kernel
+// then applies the reference's folds in segment order.  Same roundings in the
+// same order as the single launch, so the same bits; the parallelism is the
+// segment count instead of the handful of output tiles.
+int g_segsplit = 1;  // bf_set_option("segsplit", 0|1)
+int gemm_segsplit(Mode mode, double alpha, const bf_view& a, const bf_view& b, double beta, const bf_view& c,
+                  int lower_only, int64_t kc, const int* d_abort, cudaStream_t s, int64_t abort_limit, bool* done) {
+  *done = false;
+  constexpr int SMAX = 8;
+  const int64_t m = c.m, n = c.n, k = a.n;
+  if (!g_segsplit || mode != MODE_D || kc >= k || m == 0 || n == 0) return BF_OK;
+  const int64_t nseg = (k + kc - 1) / kc;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t tm = (m + 127) / 128, tn = (n + 127) / 128;
+  const int64_t tiles = lower_only ? tm * (tm + 1) / 2 : tm * tn;
+  if (nseg < 4 || tiles * 2 > sms || kc < 256) return BF_OK;  // enough tiles already, or too little per segment
+  const size_t bytes = size_t(nseg) * size_t(m) * size_t(n) * sizeof(double);
+  double* ws = static_cast<double*>(bf::stream_scratch(5, bytes, s));
+  if (!ws) return BF_OK;  // no room: the single launch
+  cudaStream_t side[SMAX];
+  const int ns = int(nseg < SMAX ? nseg : SMAX);
+  for (int q = 0; q < ns; ++q) side[q] = side_stream(SideRole(ROLE_SEG0 + q), s);
+  cudaEvent_t ev0;
+  cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+  cudaEventRecord(ev0, s);
+  for (int q = 0; q < ns; ++q) cudaStreamWaitEvent(side[q], ev0, 0);
+  cudaEventDestroy(ev0);
+  int rc = BF_OK;
+  for (int64_t sg = 0; sg < nseg && !rc; ++sg) {
+    const int64_t k0 = sg * kc, kn = k0 + kc < k ? kc : k - k0;
+    bf_view w{ws, sg * m * n, m, n, n, 1};
+    rc = gemm_impl(mode, 1.0, subview(a, 0, a.m, k0, kn), subview(b, k0, kn, 0, b.n), 0.0, w, lower_only, kc, d_abort,
+                   side[sg % ns], abort_limit);
+  }
+  for (int q = 0; q < ns; ++q) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventRecord(e, side[q]);
+    cudaStreamWaitEvent(s, e, 0);
+    cudaEventDestroy(e);
+  }
+  if (rc) return rc;
+  if (bf::launch_segfold(ws, int(nseg), m, n, alpha, beta, static_cast<double*>(c.base), c.off, c.rs, c.cs, lower_only,
+                         d_abort, abort_limit, s))
+    return fail(BF_ERR_CUDA, "segment fold launch failed");
+  *done = true;
+  return BF_OK;
+}
+
+// gemm_impl, with the segment-parallel split when it applies
+int gemm_deep(Mode mode, double alpha, const bf_view& a, const bf_view& b, double beta, const bf_view& c,
+              int lower_only, int64_t kc, const int* d_abort, cudaStream_t s) {
+  if (a.n != b.m || c.m != a.m || c.n != b.n) return fail(BF_ERR_SHAPE, "gemm dims mismatch");
+  bool done = false;
+  int rc = gemm_segsplit(mode, alpha, a, b, beta, c, lower_only, kc, d_abort, s, INT64_MAX, &done);
+  if (rc || done) return rc;
+  return gemm_impl(mode, alpha, a, b, beta, c, lower_only, kc, d_abort, s);
+}
+
 // engine/trsm.py:51-68 (_solve_right) with the 32-wide base (engine/trsm.py:96-111)
 int trsm_rec(Mode mode, double alpha, const bf_view& tri, const bf_view& b, int64_t kc, int* d_sing,
              const int* d_abort, cudaStream_t s) {
@@ -335,13 +437,13 @@ int chol_run(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int i
     switch (node.variant) {
       case 1:
         rc = trsm_rec(mode, 1.0, a00, a10, kc, nullptr, d_info, s);
-        if (!rc) rc = gemm_impl(mode, -1.0, a10, transposed(a10), 1.0, a11, 1, kc, d_info, s);
+        if (!rc) rc = gemm_deep(mode, -1.0, a10, transposed(a10), 1.0, a11, 1, kc, d_info, s);
         if (!rc) rc = chol_run(mode, a11, lv, nl, idx + 1, base + done, d_info, s);
         break;
       case 2:
-        rc = gemm_impl(mode, -1.0, a10, transposed(a10), 1.0, a11, 1, kc, d_info, s);
+        rc = gemm_deep(mode, -1.0, a10, transposed(a10), 1.0, a11, 1, kc, d_info, s);
         if (!rc) rc = chol_run(mode, a11, lv, nl, idx + 1, base + done, d_info, s);
-        if (!rc) rc = gemm_impl(mode, -1.0, a20, transposed(a10), 1.0, a21, 0, kc, d_info, s);
+        if (!rc) rc = gemm_deep(mode, -1.0, a20, transposed(a10), 1.0, a21, 0, kc, d_info, s);
         if (!rc) rc = trsm_rec(mode, 1.0, a11, a21, kc, nullptr, d_info, s);
         break;
       case 3:
@@ -353,41 +455,6 @@ int chol_run(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int i
   }
   return rc;
 }
-
-// Library-owned side streams, one set per (device, calling stream): two
-// factorizations enqueued on different caller streams (e.g. from different
-// host threads) get independent panel/aux/copy streams and never serialise
-// their panel chains on a shared one.
-enum SideRole { ROLE_PANEL = 0, ROLE_AUX = 1, ROLE_H2D = 2, ROLE_COPY = 3 };
-cudaStream_t side_stream(SideRole role, cudaStream_t caller) {
-  struct Key {
-    int dev, role;
-    cudaStream_t caller;
-    bool operator<(const Key& o) const {
-      return dev != o.dev ? dev < o.dev : (role != o.role ? role < o.role : caller < o.caller);
-    }
-  };
-  static std::mutex mu;
-  static std::map<Key, cudaStream_t> streams;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  std::lock_guard<std::mutex> lk(mu);
-  cudaStream_t& st = streams[Key{dev, int(role), caller}];
-  if (!st) {
-    if (role == ROLE_PANEL) {  // high priority: its CTAs go first whenever trailing-update CTAs retire
-      int lo = 0, hi = 0;
-      cudaDeviceGetStreamPriorityRange(&lo, &hi);
-      cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi);
-    } else {
-      cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-    }
-  }
-  return st;
-}
-cudaStream_t panel_stream(cudaStream_t caller) { return side_stream(ROLE_PANEL, caller); }
-cudaStream_t aux_stream(cudaStream_t caller) { return side_stream(ROLE_AUX, caller); }
-cudaStream_t h2d_stream(cudaStream_t caller) { return side_stream(ROLE_H2D, caller); }
-cudaStream_t copy_stream(cudaStream_t caller) { return side_stream(ROLE_COPY, caller); }
 
 // Host write-back of finished block columns (bf_cholesky_host_d): while set,
 // the lookahead driver copies block column k's lower part (rows >= k*bs) to
@@ -966,6 +1033,10 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "persist") == 0) {
     bf::g_persist = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "segsplit") == 0) {
+    g_segsplit = value != 0;
     return BF_OK;
   }
   if (name && std::strcmp(name, "reserve_adaptive") == 0) {

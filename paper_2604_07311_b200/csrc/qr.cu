@@ -314,6 +314,27 @@ __global__ void splitk_reduce_kernel(const T* ws, int S, int64_t m, int64_t n, d
   x = T(beta == 0.0 ? alpha * acc : alpha * acc + beta * double(x));
 }
 
+// The reference's kc folds applied in order to per-segment sums computed in
+// parallel (engine/gemm.py:124-126, engine/kernels.py:228-253): ws[s] holds the
+// exact fma-chain sum t_s of segment s (written as 1.0 * t_s, no rounding);
+// c = beta_eff*c + alpha*t_s for s = 0, 1, ... with beta_eff = beta then 1,
+// each product and sum rounded like the GEMM kernels' fold.  lower_only keeps
+// i >= j; a set abort flag (below the limit) skips the whole fold.
+__global__ void segfold_kernel(const double* ws, int S, int64_t m, int64_t n, double alpha, double beta, double* c,
+                               int64_t off, int64_t rs, int64_t cs, int lower_only, const int* abort_flag,
+                               int64_t abort_limit) {
+  if (abort_flag != nullptr && *abort_flag >= 0 && *abort_flag < abort_limit) return;
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= m * n) return;
+  const int64_t i = e / n, j = e - i * n;
+  if (lower_only && j > i) return;
+  double& x = c[off + i * rs + j * cs];
+  double v = __dmul_rn(alpha, ws[e]);
+  if (beta != 0.0) v = __dadd_rn(__dmul_rn(beta, x), v);
+  for (int q = 1; q < S; ++q) v = __dadd_rn(v, __dmul_rn(alpha, ws[int64_t(q) * m * n + e]));
+  x = v;
+}
+
 template <typename T>
 __global__ void explicit_v_kernel(const T* a, int64_t off, int64_t rs, int64_t cs, int64_t m, int64_t b, T* v) {
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -432,6 +453,16 @@ int launch_splitk_reduce(int is_f64, const void* ws, int S, int64_t m, int64_t n
   else
     splitk_reduce_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(ws), S, m, n, alpha, beta,
                                                        static_cast<float*>(c), off, rs, cs);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
+int launch_segfold(const double* ws, int S, int64_t m, int64_t n, double alpha, double beta, double* c, int64_t off,
+                   int64_t rs, int64_t cs, int lower_only, const int* abort_flag, int64_t abort_limit,
+                   cudaStream_t s) {
+  if (m <= 0 || n <= 0) return 0;
+  note_launch();
+  segfold_kernel<<<unsigned((m * n + 255) / 256), 256, 0, s>>>(ws, S, m, n, alpha, beta, c, off, rs, cs, lower_only,
+                                                               abort_flag, abort_limit);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 

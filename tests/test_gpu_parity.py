@@ -543,3 +543,24 @@ def test_two_host_threads_two_streams_bitwise(cuda):
     assert not errors
     for i in range(2):
         assert views[i].to_numpy().tobytes() == expect[i]
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_segment_split_deep_k_bitwise(cuda, variant):
+    """V1/V2's deep-K narrow updates (A11 -= A10 A10^T, A21 -= A20 A10^T) run
+    their kc segments in parallel and fold them in order: the oracle's bits,
+    with the split on and off."""
+    from paper_2604_07311_b200.engine import _lib
+
+    lib = _lib.lib()
+    n = 4096
+    a0 = spd_int(800 + variant, n)
+    tree = ('{"op":"cholesky","variant":%d,"bs":512,"kernel":{"kc":512},"child":{"op":"cholesky",'
+            '"variant":3,"bs":128,"kernel":{"kc":128},"child":{"op":"cholesky","variant":"unblocked3"}}}' % variant)
+    ref = digest(chol_oracle(a0, tree))
+    for split in (1, 0):
+        lib.bf_set_option(b"segsplit", split)
+        try:
+            assert digest(chol_gpu(a0, tree)) == ref, f"segsplit={split}"
+        finally:
+            lib.bf_set_option(b"segsplit", 1)

@@ -564,3 +564,26 @@ def test_segment_split_deep_k_bitwise(cuda, variant):
             assert digest(chol_gpu(a0, tree)) == ref, f"segsplit={split}"
         finally:
             lib.bf_set_option(b"segsplit", 1)
+
+
+def test_upper_copy_on_offset_subview_bitwise(cuda):
+    """uplo="upper" on a submatrix view (offset, leading dimension > n) through
+    the row-major copy: the oracle's bits, the rest of the storage untouched."""
+    N, n, r0 = 2100, 1600, 250
+    rng = np.random.default_rng(5)
+    big = rng.uniform(-1, 1, (N, N))
+    a0 = spd_int(91, n)
+    big[r0:r0 + n, r0:r0 + n] = a0
+    st = torch.tensor(big.reshape(-1), device="cuda")
+    from paper_2604_07311_b200.views import MatrixView
+
+    v = MatrixView(st, r0 * N + r0, n, n, N, 1, DType.F64)
+    tree = ('{"op":"cholesky","variant":3,"bs":512,"kernel":{"kc":512},"child":{"op":"cholesky",'
+            '"variant":3,"bs":128,"kernel":{"kc":128},"child":{"op":"cholesky","variant":"unblocked3"}}}')
+    bf.cholesky(v, "upper", parse_tree(tree))
+    got = st.cpu().numpy().reshape(N, N)
+    ref = chol_oracle(a0, tree, "upper").reshape(n, n)
+    assert got[r0:r0 + n, r0:r0 + n].tobytes() == ref.tobytes()
+    mask = np.ones((N, N), bool)
+    mask[r0:r0 + n, r0:r0 + n] = False
+    assert got[mask].tobytes() == big[mask].tobytes()

@@ -29,6 +29,11 @@ def rand():
 
 a, b, c = rand(), rand(), make_tensor([d] * 4)
 lib = _lib.lib()
+import os
+
+for kv in filter(None, os.environ.get("BF_OPTS", "").split(",")):  # e.g. BF_OPTS=group=16,persist=1
+    k, v = kv.split("=")
+    assert lib.bf_set_option(k.encode(), int(v)) == 0, kv
 out = {}
 for mode in modes:
     lib.bf_set_option(b"tmem_fold", int(mode))
@@ -44,4 +49,4 @@ for mode in modes:
         ms.append(round(e0.elapsed_time(e1), 2))
     h = hashlib.sha256(c.storage.cpu().numpy().tobytes()).hexdigest()[:16]
     out[f"tmem_fold={mode}"] = {"ms": ms, "tflops": round(2 * d ** 6 / (min(ms) / 1e3) / 1e12, 2), "sha": h}
-print(json.dumps(out))
+print(json.dumps({"opts": os.environ.get("BF_OPTS", ""), **out}))

@@ -55,6 +55,19 @@ struct FastDiv {
 #endif
 };
 
+// One group of a grouped GEMM launch (the distributed trailing update: one
+// group per local column panel).  Its C is m x n at c (row stride ldc); its A
+// rows start at row a_row of the A map, its B^T rows at row b_row of the B map
+// (or of the A map when b_from_a); tiles are row-major within the group,
+// lower trapezoid (tj <= ti) when lower; tile0 = index of its first tile.
+struct GroupDesc {
+  double* c;
+  int64_t ldc;
+  int64_t tile0;
+  int32_t m, n, a_row, b_row, tiles_m, tiles_n, lower, b_from_a;
+};
+constexpr int GEMM_MAX_GROUPS = 128;
+
 // C := beta*C + alpha*A*B with the reference's accumulation structure:
 // the k range is cut into segments of kc (engine/gemm.py:124-126); each
 // segment is summed from +0 as an ascending fma chain and folded into C as
@@ -73,6 +86,7 @@ struct GemmParams {
   int lower_only;
   int tiles_m, tiles_n;
   int group;              // raster group height in tiles
+  int panel_tiles;        // TMA lower GEMMT: > 0 = column panels this many tiles wide, row-major within a panel
   int tiles_per_cta;      // TMA kernel: contiguous raster tiles per CTA
   int tile_stride;        // TMA kernel: 0, or CTA b owns raster tiles b, b + tile_stride, ... (persistent grid)
   int64_t num_tiles;
@@ -85,6 +99,8 @@ struct GemmParams {
   // (k_in, mn_in, k_out, mn_out); tile row r and k index k are loaded at
   // coordinates (k % ki, r % mi, k / ki, r / mi).  C element (i, j) lives at
   // c_off + (i / c_ri) * c_rs_o + (i % c_ri) * c_rs + (j / c_ci) * c_cs_o + (j % c_ci) * c_cs.
+  const GroupDesc* groups;  // grouped launch (device table), else nullptr
+  int ngroups;
   int modes;
   int a_rank, b_rank;  // 2: plain 2-D map (one group a side), 4: 4-D mode-group map
   FastDiv a_ki, a_mi, b_ki, b_mi, c_ri, c_ci;
@@ -129,6 +145,11 @@ struct ModeOperand {
 };
 // TMA kernel on mode-group operands (a: M x K, b: N x K); -3 when a layout is not TMA-loadable
 int launch_gemm_dmma_modes(GemmParams p, const ModeOperand& a, const ModeOperand& b, cudaStream_t s);
+// grouped TMA GEMM: p carries k, kc, alpha, beta, abort; a = A rows (rows_a x k,
+// k-contiguous), b = B^T rows (rows_b x k); groups (device table, ngroups <=
+// GEMM_MAX_GROUPS) with num_tiles in all.  -3 when not TMA-loadable.
+int launch_gemm_dmma_grouped(GemmParams p, const OperandMK& a, int64_t rows_a, const OperandMK& b, int64_t rows_b,
+                             const GroupDesc* d_groups, int ngroups, int64_t num_tiles, cudaStream_t s);
 // pack.cu: out[r*cols + c] = src[row_scat[r] + col_scat[c]] (contraction operand staging)
 int launch_pack_scatter(int is_f64, const void* src, const int64_t* row_scat, const int64_t* col_scat, int64_t rows,
                         int64_t cols, void* out, cudaStream_t s);

@@ -111,6 +111,9 @@ using bf::OperandMK;
 thread_local std::string g_last_error;
 int g_lookahead = 1;      // bf_set_option("lookahead", 0) restores the plain reference schedule
 int g_group = 8;          // bf_set_option("group", g): raster group height in tiles
+// bf_set_option("panel_tiles", w): lower GEMMTs on the TMA kernel walk column
+// panels w tiles wide, row-major inside each (0 = the row-band raster)
+int g_panel_tiles = 0;
 int g_fused_trsm = 1;     // bf_set_option("fused_trsm", 0) keeps every recursion level a separate launch
 // bf_set_option("pipeline_first", c): step 0 of the lookahead schedule in ~c
 // row chunks of the first panel (0/1: off).  Bitwise-neutral; measured no
@@ -247,6 +250,7 @@ int gemm_impl(Mode mode, double alpha, const bf_view& a, const bf_view& b, doubl
   p.beta = be;
   p.lower_only = lower_only;
   p.group = g_group;
+  p.panel_tiles = g_panel_tiles;
   p.abort_flag = d_abort;
   p.abort_limit = abort_limit;
   int rc = launch_family(mode, p, s);
@@ -1029,6 +1033,10 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "group") == 0 && value >= 1) {
     g_group = int(value);
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "panel_tiles") == 0 && value >= 0 && value < (1 << 16)) {
+    g_panel_tiles = int(value);
     return BF_OK;
   }
   if (name && std::strcmp(name, "persist") == 0) {

@@ -136,6 +136,13 @@ struct bf_dist {
   size_t buf_elems = 0;
   int reserve = -1;  // SMs left to the panel stream by the rest-of-update GEMMs (-1: adaptive)
   int lookahead = 1;
+  int grouped = 1;  // one grouped TMA launch per update part (0: one GEMM per column panel, fan streams)
+  // group tables of the grouped launches: pinned host staging and the device
+  // copy, one region per launch of a factorization (no reuse within a call;
+  // the call waits for completion before returning)
+  bf::GroupDesc* gtab_h = nullptr;
+  bf::GroupDesc* gtab_d = nullptr;
+  int64_t gtab_cap = 0, gtab_next = 0;
 };
 
 namespace {
@@ -195,6 +202,69 @@ struct NcclExec {
     int rc = bf::gemm_d_limited(-1.0, a, b, 1.0, c, lower, lv[0].kc, d_info, limit, s);
     bf::t_reserve_sms = 0;
     return rc;
+  }
+  // every column panel of the update in one launch of the grouped TMA GEMM:
+  // one tensor map over my stacked rows (A, and B of the panels of my own
+  // process row), one over the receive buffers (B of the other process rows)
+  int gemm_groups(const bf::DistGemm* g, int ng, const bf::DistPanels& P, int64_t k, int64_t limit, bool reserve,
+                  Stream s) {
+    if (!d->grouped || ng <= 0) return bf::DIST_NOT_GROUPED;
+    const int64_t kc = lv[0].kc;
+    if (!(kc % 32 == 0 || kc >= k) || k % 2 != 0 || k > 0x7fffffffLL) return bf::DIST_NOT_GROUPED;
+    const double* abase = P.ptr[L->prow];
+    const int64_t arows = P.rows[L->prow];
+    const int64_t brows = int64_t(d->buf_elems) / k;
+    if (reinterpret_cast<uintptr_t>(abase) % 16 || arows <= 0) return bf::DIST_NOT_GROUPED;
+    if (d->gtab_next + ng > d->gtab_cap) return bf::DIST_NOT_GROUPED;
+    bf::GroupDesc* h = d->gtab_h + d->gtab_next;
+    int64_t tiles = 0;
+    for (int i = 0; i < ng; ++i) {
+      const bf::DistGemm& G = g[i];
+      bf::GroupDesc& t = h[i];
+      const int64_t da = G.a - abase;
+      const bool b_mine = G.b_proc == L->prow;
+      const int64_t db = b_mine ? G.b - abase : G.b - d->bufs;
+      const int64_t tm = (G.m + 127) / 128, tn = (G.n + 127) / 128;
+      if (da < 0 || da % k || da / k + G.m > arows || db < 0 || db % k) return bf::DIST_NOT_GROUPED;
+      if (db / k + G.n > (b_mine ? arows : brows) || tm >= (1 << 14) || tn >= (1 << 10)) return bf::DIST_NOT_GROUPED;
+      if (G.lower && tm < tn) return bf::DIST_NOT_GROUPED;
+      t.c = G.c;
+      t.ldc = G.n;
+      t.tile0 = tiles;
+      t.m = int32_t(G.m);
+      t.n = int32_t(G.n);
+      t.a_row = int32_t(da / k);
+      t.b_row = int32_t(db / k);
+      t.tiles_m = int32_t(tm);
+      t.tiles_n = int32_t(tn);
+      t.lower = G.lower;
+      t.b_from_a = b_mine;
+      tiles += G.lower ? tn * tm - tn * (tn - 1) / 2 : tm * tn;
+    }
+    if (ng > bf::GEMM_MAX_GROUPS) return bf::DIST_NOT_GROUPED;
+    bf::GroupDesc* dev = d->gtab_d + d->gtab_next;
+    if (cudaMemcpyAsync(dev, h, sizeof(bf::GroupDesc) * size_t(ng), cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return bf::set_error(BF_ERR_CUDA, "group table upload failed");
+    d->gtab_next += ng;
+    bf::GemmParams p{};
+    p.k = k;
+    p.kc = kc;
+    p.alpha = -1.0;
+    p.beta = 1.0;
+    p.abort_flag = d_info;
+    p.abort_limit = limit;
+    bf::OperandMK oa{}, ob{};
+    oa.base = abase;
+    oa.s_mn = k;
+    oa.s_k = 1;
+    ob.base = d->bufs;
+    ob.s_mn = k;
+    ob.s_k = 1;
+    if (reserve && reserve_now > 0) bf::t_reserve_sms = reserve_now;
+    const int rc = bf::launch_gemm_dmma_grouped(p, oa, arows, ob, brows, dev, ng, tiles, s);
+    bf::t_reserve_sms = 0;
+    if (rc == -3) return bf::set_error(BF_ERR_UNSUPPORTED, "grouped update: unsupported shape");
+    return rc ? bf::set_error(BF_ERR_CUDA, "grouped update launch failed") : BF_OK;
   }
   ncclComm_t comm(int which) { return which == bf::COMM_ROW ? d->row : d->col; }
   int bcast(int which, double* buf, int64_t count, int root, Stream s) {
@@ -292,6 +362,7 @@ int bf_dist_set_option(bf_dist* d, const char* name, int64_t value) {
   if (!std::strcmp(name, "reserve")) d->reserve = int(value);
   else if (!std::strcmp(name, "fan")) d->nfan = int(value < 0 ? 0 : (value > 3 ? 3 : value));
   else if (!std::strcmp(name, "lookahead")) d->lookahead = int(value != 0);
+  else if (!std::strcmp(name, "grouped")) d->grouped = int(value != 0);
   else return bf::set_error(BF_ERR_VALUE, "unknown dist option");
   return BF_OK;
 }
@@ -309,6 +380,11 @@ int bf_dist_finalize(bf_dist* d) {
   if (d->bufs) {
     cudaFree(d->bufs);
     bf::scratch_account(-int64_t(d->buf_elems * sizeof(double)));
+  }
+  if (d->gtab_d) {
+    cudaFree(d->gtab_d);
+    cudaFreeHost(d->gtab_h);
+    bf::scratch_account(-int64_t(d->gtab_cap * int64_t(sizeof(bf::GroupDesc))));
   }
   delete d;
   return BF_OK;
@@ -388,6 +464,30 @@ int bf_chol_dist_d(bf_dist* d, double* local, int64_t n, const bf_chol_level* le
     d->buf_elems = need;
     bf::scratch_account(int64_t(need * sizeof(double)));
   }
+  // group tables: at most one entry per (step, local column panel)
+  const int64_t gneed = L.tiles() * (L.col_tiles(L.pcol) + 1);
+  if (d->grouped && gneed > d->gtab_cap) {
+    cudaStreamSynchronize(x.user);
+    if (d->gtab_d) {
+      cudaFree(d->gtab_d);
+      cudaFreeHost(d->gtab_h);
+      bf::scratch_account(-int64_t(d->gtab_cap * int64_t(sizeof(bf::GroupDesc))));
+    }
+    d->gtab_d = nullptr;
+    d->gtab_h = nullptr;
+    d->gtab_cap = 0;
+    if (cudaMalloc(&d->gtab_d, size_t(gneed) * sizeof(bf::GroupDesc)) != cudaSuccess ||
+        cudaMallocHost(&d->gtab_h, size_t(gneed) * sizeof(bf::GroupDesc)) != cudaSuccess) {
+      cudaGetLastError();
+      if (d->gtab_d) cudaFree(d->gtab_d);
+      d->gtab_d = nullptr;
+      d->gtab_h = nullptr;
+      return bf::set_error(BF_ERR_CUDA, "cannot allocate the update group tables");
+    }
+    d->gtab_cap = gneed;
+    bf::scratch_account(int64_t(gneed * int64_t(sizeof(bf::GroupDesc))));
+  }
+  d->gtab_next = 0;
   int rc = bf::chol_dist_schedule(x, L, local, d->lookahead != 0);
   cudaEvent_t done = d->ev_pool[d->ev_next];
   d->ev_next = (d->ev_next + 1) % 8;

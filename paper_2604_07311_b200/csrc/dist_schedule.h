@@ -29,6 +29,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include "blockfam_b200.h"
 #include "dist_layout.h"
@@ -37,6 +38,19 @@ namespace bf {
 
 constexpr int DIST_MAX_PR = 64;
 enum DistComm { COMM_ROW = 0, COMM_COL = 1 };
+
+// one column panel of a trailing update: c (m x n, ld n) -= a (m x k) * b (n x k)^T,
+// a and b row-major with ld k; lower: c's top n x n block is a diagonal tile
+// (only its lower triangle is updated)
+struct DistGemm {
+  const double* a;
+  const double* b;
+  double* c;
+  int64_t m, n;
+  int lower;
+  int b_proc;  // process row whose stacked rows b points into
+};
+constexpr int DIST_NOT_GROUPED = 1;  // gemm_groups: "not handled, issue the GEMMs one by one"
 
 struct DistPanels {
   double* ptr[DIST_MAX_PR];  // process row p: stacked solved rows of its tiles I > k (ld = tile width)
@@ -61,6 +75,8 @@ inline bf_view dist_view(double* base, int64_t m, int64_t n, int64_t ld) {
 //   int trsm(const bf_view& tri, const bf_view& b, Stream s);
 //   int gemm(const bf_view& a, const bf_view& bt, const bf_view& c, int lower, int64_t abort_limit,
 //            bool reserve, Stream s);                        // c -= a * bt^T
+//   int gemm_groups(const DistGemm* g, int ng, const DistPanels& P, int64_t k, int64_t abort_limit,
+//                   bool reserve, Stream s);             // all of g in one launch, or DIST_NOT_GROUPED
 //   int bcast(int comm, double* buf, int64_t count, int root, Stream s);  // root's buf is sent in place
 //   int bcast_info(int comm, int root, Stream s);
 //   void group_begin(); int group_end();
@@ -153,41 +169,61 @@ int chol_dist_schedule(X& x, const DistLayout& L, double* local, bool lookahead)
         T = double(L.stack_rows(prow, k1)) * b1 * b1;
         if (prow == int(k1 % L.pr)) T += b1 * b1 * b1 / 3.0;
       }
+      // both in multiply-adds x 2: a TRSM row costs b1^2 / 2, the diagonal
+      // factor b1^3 / 6, an update element bk (the one-GPU driver's units)
       for (int64_t q = 0; q < nq; ++q)
-        if (L.panel_J(q) > k1) S += double(L.panel_h(q)) * double(L.panel_w(q)) * double(bk);
+        if (L.panel_J(q) > k1) S += 2.0 * double(L.panel_h(q)) * double(L.panel_w(q)) * double(bk);
       x.reserve_for(T, S);
     }
-    const bool fan = part != 1 && x.fan_count() > 0;
-    int used = 0;
-    if (fan)
-      for (int i = 0; i < x.fan_count(); ++i) x.fork(s, x.fan_stream(i));
-    int rc = BF_OK;
-    // my stacked rows start at my first row tile > k
+    // the column panels J > k this part updates: C -= A * B^T with A my
+    // stacked rows from tile i0 on, B the stacked rows of tile J (process row
+    // J % pr); a panel whose top tile is the diagonal tile (J, J) is a lower
+    // trapezoid
+    std::vector<DistGemm> groups;
     const int64_t my_first = L.stack_first(prow, k);
-    for (int64_t q = 0; q < nq && !rc; ++q) {
+    for (int64_t q = 0; q < nq; ++q) {
       const int64_t J = L.panel_J(q);
       if (J <= k) continue;
       if (part == 1 && J != k + 1) continue;
       if (part == 2 && J == k + 1) continue;
       bf_view C = panel_view(q);
       if (C.m == 0) continue;
-      const int64_t i0 = L.panel_i0(q);
-      double* A = P.ptr[prow] + L.rows_of(prow, my_first, i0) * bk;
       const int pJ = int(J % L.pr);
-      double* B = P.ptr[pJ] + L.rows_of(pJ, L.stack_first(pJ, k), L.first_row_geq(pJ, J)) * bk;
-      const int64_t w = C.n;
+      DistGemm g;
+      g.a = P.ptr[prow] + L.rows_of(prow, my_first, L.panel_i0(q)) * bk;
+      g.b = P.ptr[pJ] + L.rows_of(pJ, L.stack_first(pJ, k), L.first_row_geq(pJ, J)) * bk;
+      g.c = static_cast<double*>(C.base);
+      g.m = C.m;
+      g.n = C.n;
+      g.lower = pJ == prow;
+      g.b_proc = pJ;
+      groups.push_back(g);
+    }
+    if (groups.empty()) return BF_OK;
+    const bool reserve = part == 2;
+    // one launch over every panel when the executor can (a single reserved
+    // persistent grid); otherwise one or two GEMMs per panel over the fan streams
+    int rc = x.gemm_groups(groups.data(), int(groups.size()), P, bk, limit, reserve, s);
+    if (rc != DIST_NOT_GROUPED) return rc;
+    rc = BF_OK;
+    const bool fan = part != 1 && x.fan_count() > 0;
+    int used = 0;
+    if (fan)
+      for (int i = 0; i < x.fan_count(); ++i) x.fork(s, x.fan_stream(i));
+    for (const DistGemm& g : groups) {
+      if (rc) break;
       typename X::Stream st = fan ? x.fan_stream(used++ % x.fan_count()) : s;
-      const bool reserve = part == 2;
-      const bf_view bt = dist_view(B, w, bk, bk);
+      const int64_t w = g.n;
+      const bf_view bt = dist_view(const_cast<double*>(g.b), w, bk, bk);
+      double* A = const_cast<double*>(g.a);
       int64_t r0 = 0;
-      if (J % L.pr == prow) {  // the top tile of the panel is the diagonal tile (J, J)
-        rc = x.gemm(dist_view(A, w, bk, bk), bt, dist_view(static_cast<double*>(C.base), w, w, w), 1, limit,
-                    reserve, st);
+      if (g.lower) {
+        rc = x.gemm(dist_view(A, w, bk, bk), bt, dist_view(g.c, w, w, w), 1, limit, reserve, st);
         r0 = w;
       }
-      if (!rc && C.m > r0)
-        rc = x.gemm(dist_view(A + r0 * bk, C.m - r0, bk, bk), bt,
-                    dist_view(static_cast<double*>(C.base) + r0 * w, C.m - r0, w, w), 0, limit, reserve, st);
+      if (!rc && g.m > r0)
+        rc = x.gemm(dist_view(A + r0 * bk, g.m - r0, bk, bk), bt, dist_view(g.c + r0 * w, g.m - r0, w, w), 0, limit,
+                    reserve, st);
     }
     if (fan)
       for (int i = 0; i < x.fan_count(); ++i) x.fork(x.fan_stream(i), s);

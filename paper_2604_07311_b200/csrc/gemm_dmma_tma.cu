@@ -93,6 +93,36 @@ __device__ __forceinline__ double lds64(uint32_t addr) {
 
 __device__ __forceinline__ void tile_coords_tma(const GemmParams& p, int64_t bid, bool tri, int64_t& ti, int64_t& tj) {
   const int64_t G = p.group;
+  if (tri && p.panel_tiles > 0) {
+    // column panels of panel_tiles tile columns, each row-major from its
+    // diagonal down: a CTA's run of tiles shares one A row tile and a
+    // panel's B tiles stay in L2 while every CTA sweeps its rows
+    const int64_t T = p.tiles_m, w = p.panel_tiles;
+    int64_t j0 = 0, q = bid;
+    for (;;) {
+      const int64_t tn = T - j0 < w ? T - j0 : w;
+      const int64_t cnt = tn * (tn + 1) / 2 + (T - j0 - tn) * tn;
+      if (q < cnt || j0 + tn >= T) {
+        const int64_t tri_cnt = tn * (tn + 1) / 2;
+        if (q < tri_cnt) {
+          int64_t r = 0;
+          while (q > r) {
+            q -= r + 1;
+            ++r;
+          }
+          ti = j0 + r;
+          tj = j0 + q;
+        } else {
+          q -= tri_cnt;
+          ti = j0 + tn + q / tn;
+          tj = j0 + q % tn;
+        }
+        return;
+      }
+      q -= cnt;
+      j0 += w;
+    }
+  }
   if (tri) {
     const int64_t T = p.tiles_m;
     int64_t start = 0, r0 = 0, h = 0;
@@ -154,7 +184,12 @@ __device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double (&a)[4]
 // mn_in, k_out, mn_out) — the contraction's mode groups go straight into the
 // swizzled stage with no transpose — and C is addressed through its two row
 // and two column mode groups.
-template <int MMAK, int KBOX, int STAGES, bool TMC, bool MODES = false>
+//
+// GROUPED: one launch over several independent GEMMs sharing K (the
+// distributed trailing update's column panels): tile_tab packs the group too
+// (g << 24 | ti << 10 | tj), tiles row-major within a group; each tile takes
+// its A/B row offsets, its C pointer, bounds and lower mask from the group table.
+template <int MMAK, int KBOX, int STAGES, bool TMC, bool MODES = false, bool GROUPED = false>
 __global__ void __launch_bounds__(TM_THREADS, 1)
     gemm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                          const GemmParams p) {
@@ -171,6 +206,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   // (ti, tj) of every tile this CTA owns, packed ti<<16 | tj, so a refill
   // (issued by whichever warp releases a stage last) costs one LDS
   uint32_t* tile_tab = reinterpret_cast<uint32_t*>(smem_raw + (bars + 8u * STAGES - raw));
+  uint32_t* row_tab = tile_tab + p.tiles_per_cta;  // GROUPED: 2 words per tile
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -187,8 +223,36 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   const int W = int(owned < p.tiles_per_cta ? owned : p.tiles_per_cta);
   for (int w = tid; w < W; w += TM_THREADS) {
     int64_t ti, tj;
-    tile_coords_tma(p, first_tile + w * tstep, tri, ti, tj);
-    tile_tab[w] = (uint32_t(ti) << 16) | uint32_t(tj);
+    if constexpr (GROUPED) {
+      const int64_t t = first_tile + w * tstep;
+      int g = 0;
+      while (g + 1 < p.ngroups && p.groups[g + 1].tile0 <= t) ++g;
+      const GroupDesc& gd = p.groups[g];
+      // row-major within the group: a CTA's run of tiles shares one A row
+      // tile, and the group's few B tiles stay in L2 for every CTA
+      int64_t local = t - gd.tile0;
+      const int64_t tn = gd.tiles_n, tri_tiles = gd.lower ? tn * (tn + 1) / 2 : 0;
+      if (local < tri_tiles) {  // lower: row ti < tiles_n holds columns 0..ti
+        ti = 0;
+        while (local > ti) {
+          local -= ti + 1;
+          ++ti;
+        }
+        tj = local;
+      } else {
+        local -= tri_tiles;
+        ti = (gd.lower ? tn : 0) + local / tn;
+        tj = local % tn;
+      }
+      tile_tab[w] = (uint32_t(g) << 24) | (uint32_t(ti) << 10) | uint32_t(tj);
+      // the tile's A and B^T map rows, so a refill issues from shared memory
+      // alone (bit 31: B^T comes from the A map)
+      row_tab[2 * w] = uint32_t(gd.a_row + ti * TM_BM);
+      row_tab[2 * w + 1] = uint32_t(gd.b_row + tj * TM_BN) | (gd.b_from_a ? 0x80000000u : 0u);
+    } else {
+      tile_coords_tma(p, first_tile + w * tstep, tri, ti, tj);
+      tile_tab[w] = (uint32_t(ti) << 16) | uint32_t(tj);
+    }
   }
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -224,7 +288,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   auto issue = [&](int f) {
     const int w = f / ntiles, kt = f - w * ntiles;
     const uint32_t tt = tile_tab[w];
-    const int ti = int(tt >> 16), tj = int(tt & 0xffffu);
+    const int ti = GROUPED ? int((tt >> 10) & 0x3fffu) : int(tt >> 16), tj = GROUPED ? int(tt & 0x3ffu) : int(tt & 0xffffu);
     const int st = f % STAGES;
     const int seg = kt / tps, sub = kt - seg * tps;
     const int k_lo = seg * kc + sub * BKS;
@@ -249,6 +313,11 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
           tma_load_4d(sa + OP_BYTES + b * TM_TILE_BYTES, &tma_b, int(k - qb * p.b_ki.d), int(rb - qrb * p.b_mi.d),
                       int(qb), int(qrb), full(st));
         }
+      } else if constexpr (GROUPED) {
+        const uint32_t ra = row_tab[2 * w], rb = row_tab[2 * w + 1];
+        tma_load_2d(sa + b * TM_TILE_BYTES, &tma_a, k_lo + 16 * b, int(ra), full(st));
+        tma_load_2d(sa + OP_BYTES + b * TM_TILE_BYTES, (rb >> 31) ? &tma_a : &tma_b, k_lo + 16 * b,
+                    int(rb & 0x7fffffffu), full(st));
       } else {
         tma_load_2d(sa + b * TM_TILE_BYTES, &tma_a, k_lo + 16 * b, int(ti * TM_BM), full(st));
         tma_load_2d(sa + OP_BYTES + b * TM_TILE_BYTES, &tma_b, k_lo + 16 * b, int(tj * TM_BN), full(st));
@@ -270,9 +339,14 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   auto koff = [&](int k) -> uint32_t { return uint32_t((((k >> 1) ^ pg) << 4) | ((k & 1) << 3)); };
   const int pj[2] = {perm8(2 * t), perm8(2 * t + 1)};
   double* C = static_cast<double*>(p.c);
+  // GROUPED: the current tile's C, bounds and mask (set at each tile start)
+  int64_t g_m = p.m, g_n = p.n, g_ld = p.c_rs;
+  int g_lower = p.lower_only;
   // element offset of C(i, j) (MODES: two row and two column mode groups)
   auto coff = [&](int64_t i, int64_t j) -> int64_t {
-    if constexpr (MODES) {
+    if constexpr (GROUPED) {
+      return i * g_ld + j;
+    } else if constexpr (MODES) {
       const uint32_t qi = p.c_ri.div(uint32_t(i)), qj = p.c_ci.div(uint32_t(j));
       return p.c_off + int64_t(qi) * p.c_rs_o + (i - int64_t(qi) * p.c_ri.d) * p.c_rs + int64_t(qj) * p.c_cs_o +
              (j - int64_t(qj) * p.c_ci.d) * p.c_cs;
@@ -297,7 +371,20 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   int s = 0, round = 0, f = 0;
   for (int w = 0; w < W; ++w) {
     const uint32_t tt = tile_tab[w];
-    const int64_t m0 = int64_t(tt >> 16) * TM_BM, n0 = int64_t(tt & 0xffffu) * TM_BN;
+    int64_t m0, n0;
+    if constexpr (GROUPED) {
+      const GroupDesc& gd = p.groups[tt >> 24];
+      C = gd.c;
+      g_m = gd.m;
+      g_n = gd.n;
+      g_ld = gd.ldc;
+      g_lower = gd.lower;
+      m0 = int64_t((tt >> 10) & 0x3fffu) * TM_BM;
+      n0 = int64_t(tt & 0x3ffu) * TM_BN;
+    } else {
+      m0 = int64_t(tt >> 16) * TM_BM;
+      n0 = int64_t(tt & 0xffffu) * TM_BN;
+    }
     int seg = 0, sub = 0;
     // C is prefetched into L2 before each fold that reads it: every segment's
     // for the global folds, only the first (beta != 0) when C lives in TMEM
@@ -387,10 +474,10 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         // reads it (with kc < K the folds recur, and the operand streams evict
         // C from L2 between them: d=128 contraction, 64 folds per tile)
         const int64_t r = m0 + wm * 32 + lane, c0 = n0 + wn * 32;
-        if (r < p.m && c0 < p.n) {
+        if (r < (GROUPED ? g_m : p.m) && c0 < (GROUPED ? g_n : p.n)) {
           const double* rowp = C + coff(r, c0);
           asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp));
-          if (!MODES && p.c_cs == 1 && c0 + 16 < p.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + 16));
+          if (!MODES && (GROUPED || p.c_cs == 1) && c0 + 16 < (GROUPED ? g_n : p.n)) asm volatile("prefetch.global.L2 [%0];" ::"l"(rowp + 16));
         }
       }
       const bool seg_done = (seg < nseg - 1) ? (sub == tps - 1) : (sub == tps_last - 1);
@@ -417,7 +504,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
-              const bool ok = gi < p.m && gj < p.n && (!p.lower_only || gi >= gj);
+              const bool ok = gi < (GROUPED ? g_m : p.m) && gj < (GROUPED ? g_n : p.n) && (!(GROUPED ? g_lower : p.lower_only) || gi >= gj);
               const int q = 2 * (2 * j + h);
               double v = __dmul_rn(p.alpha, acc[i][j][h]);
               if (seg > 0) {
@@ -464,7 +551,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
               for (int h = 0; h < 2; ++h) {
                 const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
                 const double v = __dmul_rn(p.alpha, acc[i][j][h]);
-                if (gi < p.m && gj < p.n && (!p.lower_only || gi >= gj))
+                if (gi < (GROUPED ? g_m : p.m) && gj < (GROUPED ? g_n : p.n) && (!(GROUPED ? g_lower : p.lower_only) || gi >= gj))
                   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(C + coff(gi, gj)),
                                "d"(v)
                                : "memory");
@@ -485,7 +572,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
-                const bool ok = gi < p.m && gj < p.n && (!p.lower_only || gi >= gj);
+                const bool ok = gi < (GROUPED ? g_m : p.m) && gj < (GROUPED ? g_n : p.n) && (!(GROUPED ? g_lower : p.lower_only) || gi >= gj);
                 cold[ii][j][h] = (ok && beta_eff != 0.0) ? __ldcg(C + coff(gi, gj)) : 0.0;
               }
           }
@@ -500,7 +587,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                 const int64_t gj = n0 + wn * 32 + j * 8 + pj[h];
                 double v = __dmul_rn(p.alpha, acc[i][j][h]);
                 if (beta_eff != 0.0) v = __dadd_rn(__dmul_rn(beta_eff, cold[ii][j][h]), v);
-                if (gi < p.m && gj < p.n && (!p.lower_only || gi >= gj)) C[coff(gi, gj)] = v;
+                if (gi < (GROUPED ? g_m : p.m) && gj < (GROUPED ? g_n : p.n) && (!(GROUPED ? g_lower : p.lower_only) || gi >= gj)) C[coff(gi, gj)] = v;
                 acc[i][j][h] = 0.0;
               }
           }
@@ -583,11 +670,11 @@ int g_tma_variant = 2;  // 0: m8n8k4/1 box/6 stages, 1: m16n8k8/1/6, 2: m8n8k4/2
 
 int g_tmem_fold = 1;  // bf_set_option("tmem_fold", 0|1): C in TMEM across >= 3 kc segments
 
-template <int MMAK, int KBOX, int STAGES, bool TMC, bool MODES = false>
+template <int MMAK, int KBOX, int STAGES, bool TMC, bool MODES = false, bool GROUPED = false>
 static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t s) {
   constexpr size_t base_smem = size_t(STAGES) * 2 * KBOX * TM_TILE_BYTES + 1024 + 8 * STAGES;
   constexpr size_t max_smem = 200 * 1024;  // leaves room for the static __shared__ words
-  auto kern = gemm_dmma_tma_kernel<MMAK, KBOX, STAGES, TMC, MODES>;
+  auto kern = gemm_dmma_tma_kernel<MMAK, KBOX, STAGES, TMC, MODES, GROUPED>;
   GemmParams p = p_in;
   static int sms_dev[64] = {};
   int dev = 0;
@@ -609,14 +696,15 @@ static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensor
   // per wave instead of once per staggered CTA (long-K GEMMs: the C5 contraction)
   const bool persist = g_persist && t_reserve_sms == 0 && p.num_tiles >= int64_t(4) * sms && p.k >= 4096;
   if (persist) tpc = (p.num_tiles + sms - 1) / sms;
-  while (tpc * 4 + base_smem > max_smem) tpc /= 2;  // the tile table must fit
+  constexpr int64_t tab_bytes = GROUPED ? 12 : 4;  // per owned tile: packed coords (+ two map rows)
+  while (tpc * tab_bytes + base_smem > max_smem) tpc /= 2;  // the tile table must fit
   if (tpc < 1) tpc = 1;
   p.tiles_per_cta = int(tpc);
   const int64_t grid = (p.num_tiles + tpc - 1) / tpc;
   if ((t_reserve_sms > 0 && g_reserve_strided) || persist) p.tile_stride = int(grid);
   if (grid > 0x7fffffffLL) return -3;
   if (p.m >= (1 << 16) * int64_t(TM_BM) || p.n >= (1 << 16) * int64_t(TM_BN)) return -3;
-  const size_t smem = base_smem + size_t(tpc) * 4;
+  const size_t smem = base_smem + size_t(tpc) * tab_bytes;
   if (!smem_attr(reinterpret_cast<const void*>(kern), int(smem))) return -10;
   note_launch();
   kern<<<unsigned(grid), TM_THREADS, smem, s>>>(ma, mb, p);
@@ -703,6 +791,25 @@ int launch_gemm_dmma_modes(GemmParams p, const ModeOperand& a, const ModeOperand
   const int64_t nseg = p.kc < p.k ? (p.k + p.kc - 1) / p.kc : 1;
   if (g_tmem_fold && nseg >= 3) return run_tma<4, 2, 3, true, true>(p, ma, mb, s);
   return run_tma<4, 2, 3, false, true>(p, ma, mb, s);
+}
+
+int launch_gemm_dmma_grouped(GemmParams p, const OperandMK& a, int64_t rows_a, const OperandMK& b, int64_t rows_b,
+                             const GroupDesc* d_groups, int ngroups, int64_t num_tiles, cudaStream_t s) {
+  if (ngroups <= 0 || num_tiles <= 0) return 0;
+  if (ngroups > GEMM_MAX_GROUPS || num_tiles > 0x7fffffffLL) return -3;
+  if (!(p.kc % 32 == 0 || p.kc >= p.k) || p.k > 0x7fffffffLL) return -3;
+  if (rows_a >= (int64_t(1) << 31) || rows_b >= (int64_t(1) << 31)) return -3;
+  if ((a.s_mn * 8) % 16 || (b.s_mn * 8) % 16) return -3;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, a, rows_a, p.k) || !make_map(&mb, b, rows_b, p.k)) return -3;
+  p.red_fold = g_red_fold;
+  p.groups = d_groups;
+  p.ngroups = ngroups;
+  p.num_tiles = num_tiles;
+  p.m = p.n = 0;  // per group
+  p.lower_only = 0;
+  p.group = 1;
+  return run_tma<4, 2, 3, false, false, true>(p, ma, mb, s);
 }
 
 }  // namespace bf

@@ -175,17 +175,21 @@ def cholesky_replicated(full: torch.Tensor, tree: ControlNode, ctx: DistContext)
     return bad
 
 
-def selftest_single_rank(n: int = 640, nb: int = 128, seed: int = 7) -> None:
-    """The NCCL driver on a 1x1 grid against the one-GPU driver, bitwise."""
+def selftest_single_rank(n: int = 640, nb: int = 128, seed: int = 7, kc: Optional[int] = None,
+                         options: Optional[dict] = None) -> None:
+    """The NCCL driver on a 1x1 grid against the one-GPU driver, bitwise
+    (`options`: bf_dist_set_option settings, e.g. {"grouped": 0})."""
     from ..control import parse_tree_dict
     from ..factor.cholesky import cholesky
     from ..views import from_torch
 
-    tree = parse_tree_dict({"op": "cholesky", "variant": 3, "bs": nb, "kernel": {"kc": nb},
+    tree = parse_tree_dict({"op": "cholesky", "variant": 3, "bs": nb, "kernel": {"kc": kc or nb},
                             "child": {"op": "cholesky", "variant": 3, "bs": 32, "kernel": {"kc": 32},
                                       "child": {"op": "cholesky", "variant": "unblocked3"}}})
     ctx = DistContext.single()
     try:
+        for name, value in (options or {}).items():
+            ctx.set_option(name, value)
         lp = ctx.layout(n, nb)
         local = torch.empty(lp.local_elems(), dtype=torch.float64, device="cuda")
         fill_synthetic(ctx, local, n, nb, seed)

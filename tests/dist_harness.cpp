@@ -35,6 +35,8 @@ int64_t orc_cholesky_d(const orc_view_d* a, const orc_level* lv, int nl, int nth
 
 namespace {
 
+int g_grouped = 0;  // harness_set_grouped: exercise the schedule's grouped-update path
+
 orc_view_d ov(const bf_view& v) { return orc_view_d{static_cast<double*>(v.base), v.off, v.m, v.n, v.rs, v.cs}; }
 
 // one communicator: a generation-counted rendezvous of its members
@@ -113,6 +115,20 @@ struct HostExec {
     ++*trace_gemm;
     return orc_gemm_d(-1.0, &va, &vb, 1.0, &vc, lower, lv[0].kc, 1) ? BF_ERR_SHAPE : BF_OK;
   }
+  // the grouped launch's semantics: each group is one GEMM over its whole
+  // panel, lower = update only gi >= gj (the diagonal tile's triangle)
+  int gemm_groups(const bf::DistGemm* g, int ng, const bf::DistPanels&, int64_t k, int64_t limit, bool, Stream) {
+    if (!g_grouped) return bf::DIST_NOT_GROUPED;
+    if (info >= 0 && info < limit) return BF_OK;
+    for (int i = 0; i < ng; ++i) {
+      orc_view_d va{const_cast<double*>(g[i].a), 0, g[i].m, k, k, 1};
+      orc_view_d vb{const_cast<double*>(g[i].b), 0, k, g[i].n, 1, k};
+      orc_view_d vc{g[i].c, 0, g[i].m, g[i].n, g[i].n, 1};
+      ++*trace_gemm;
+      if (orc_gemm_d(-1.0, &va, &vb, 1.0, &vc, g[i].lower, lv[0].kc, 1)) return BF_ERR_SHAPE;
+    }
+    return BF_OK;
+  }
   HostComm& comm(int which) { return which == bf::COMM_ROW ? w->rows[size_t(L->prow)] : w->cols[size_t(L->pcol)]; }
   int my_index(int which) { return which == bf::COMM_ROW ? L->pcol : L->prow; }
   int bcast(int which, double* buf, int64_t count, int root, Stream) {
@@ -132,6 +148,8 @@ struct HostExec {
 }  // namespace
 
 extern "C" {
+
+void harness_set_grouped(int on) { g_grouped = on; }
 
 // Scatter `full` (n x n row-major, lower triangle) into pr*pc ranks, factor
 // with the distributed schedule on pr*pc threads, gather the lower tiles back

@@ -47,6 +47,7 @@ def harness():
                                       ctypes.POINTER(_Level), ctypes.c_int, ctypes.c_int,
                                       ctypes.POINTER(ctypes.c_int64)]
     lib.harness_chol_dist.restype = ctypes.c_int64
+    lib.harness_set_grouped.argtypes = [ctypes.c_int]
     return lib
 
 
@@ -60,8 +61,9 @@ def _tree(nb: int, inner: int | None):
     return doc
 
 
-def _run(harness, a0, pr, pc, doc, lookahead=True):
+def _run(harness, a0, pr, pc, doc, lookahead=True, grouped=False):
     n = a0.shape[0]
+    harness.harness_set_grouped(int(grouped))
     lv = O.levels_from_tree(doc, n, "f64")
     arr = (_Level * len(lv))(*[_Level(v, 0, bs, kc) for v, bs, kc in lv])
     full = np.ascontiguousarray(a0, dtype=np.float64).copy()
@@ -77,12 +79,15 @@ def _oracle(a0, doc):
     return st.reshape(n, n), bad
 
 
+@pytest.mark.parametrize("grouped", [False, True], ids=["per_panel", "grouped"])
 @pytest.mark.parametrize("pr,pc", [(1, 1), (1, 2), (2, 2), (2, 4), (2, 3), (3, 2), (4, 1)])
 @pytest.mark.parametrize("n,nb,inner", [(512, 64, 16), (450, 64, None), (300, 96, 32)])
-def test_dist_schedule_bitwise_vs_oracle(harness, pr, pc, n, nb, inner):
+def test_dist_schedule_bitwise_vs_oracle(harness, pr, pc, n, nb, inner, grouped):
+    """grouped: the update's panels go to the executor as one group list (the
+    one-launch path of dist.cu), each panel one GEMM over its trapezoid."""
     a0 = spd_int(900 + n + 10 * pr + pc, n)
     doc = _tree(nb, inner)
-    got, info, calls = _run(harness, a0, pr, pc, doc)
+    got, info, calls = _run(harness, a0, pr, pc, doc, grouped=grouped)
     ref, bad = _oracle(a0, doc)
     assert info == -1 and bad == -1
     assert calls > 0
@@ -101,13 +106,14 @@ def test_dist_schedule_lookahead_same_bits(harness, lookahead):
     assert got[low].tobytes() == ref[low].tobytes()
 
 
+@pytest.mark.parametrize("grouped", [False, True], ids=["per_panel", "grouped"])
 @pytest.mark.parametrize("pr,pc", [(1, 2), (2, 2), (2, 4)])
-def test_dist_schedule_pivot_failure_index(harness, pr, pc):
+def test_dist_schedule_pivot_failure_index(harness, pr, pc, grouped):
     n = 320
     a0 = spd_int(77, n)
     a0[200, 200] = -1e6  # fails at global pivot 200 (tile 3 of nb=64)
     doc = _tree(64, 16)
-    _, info, _ = _run(harness, a0, pr, pc, doc)
+    _, info, _ = _run(harness, a0, pr, pc, doc, grouped=grouped)
     _, bad = _oracle(a0, doc)
     assert bad == 200 and info == 200
 
@@ -152,16 +158,22 @@ def test_python_scatter_gather_roundtrip():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,nb", [(640, 128), (1000, 256), (3000, 512)])
-def test_nccl_driver_single_rank_bitwise(cuda, n, nb):
+@pytest.mark.parametrize("grouped", [0, 1], ids=["per_panel", "grouped"])
+@pytest.mark.parametrize("lookahead", [0, 1])
+@pytest.mark.parametrize("n,nb,kc", [(640, 128, None), (1000, 256, None), (3000, 512, None), (2900, 512, 128),
+                                     (4100, 1024, 256)])
+def test_nccl_driver_single_rank_bitwise(cuda, n, nb, kc, grouped, lookahead):
+    """grouped=1: every update part is one grouped TMA launch over the column
+    panels (ragged last tiles, kc < nb segments); 0: one GEMM per panel."""
     from paper_2604_07311_b200.dist import native
 
-    native.selftest_single_rank(n=n, nb=nb, seed=n)
+    native.selftest_single_rank(n=n, nb=nb, seed=n, kc=kc, options={"grouped": grouped, "lookahead": lookahead})
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("grouped", [0, 1], ids=["per_panel", "grouped"])
 @pytest.mark.parametrize("lookahead", [0, 1])
-def test_nccl_driver_pivot_failure(cuda, lookahead):
+def test_nccl_driver_pivot_failure(cuda, lookahead, grouped):
     import torch
 
     import paper_2604_07311_b200 as bf
@@ -174,6 +186,7 @@ def test_nccl_driver_pivot_failure(cuda, lookahead):
     ctx = native.DistContext.single()
     try:
         ctx.set_option("lookahead", lookahead)
+        ctx.set_option("grouped", grouped)
         lp = ctx.layout(n, nb)
         full = torch.empty(n, n, dtype=torch.float64, device=cuda)
         native.fill_synthetic_full(full, 5)

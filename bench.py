@@ -338,7 +338,8 @@ def roofline_syrk(bf, torch, a0, n: int, bs: int, kc: int) -> dict:
                         f"{t['algorithmic_bytes'] / 1e9:.2f} GB for that launch")
     return {"bound": "tensor", "achieved": round(achieved, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": round(achieved / FP64_PEAK_TFLOPS, 4), "traffic": traffic, "traffic_note": traffic_note,
-            "kernel": "gemm_dmma_tma_kernel<m8n8k4, 2x16-k TMA boxes, 3 stages> (GEMMT lower, trailing SYRK)",
+            "kernel": "gemm_dmma_tma_kernel<m8n8k4, 2x16-k TMA boxes, 2 stages, BN=64>: two 8-warp groups per "
+                      "CTA on 128x64 tiles (GEMMT lower, trailing SYRK)",
             "per_launch_flops": "n_k*(n_k+1)*bs, n_k = n-(k+1)*bs", "launches_timed": launches,
             "syrk_ms_total": round(ms, 3), "peak_source": FP64_PEAK_SOURCE}
 

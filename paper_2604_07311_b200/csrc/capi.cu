@@ -45,39 +45,63 @@ void* stream_scratch(int tag, size_t bytes, cudaStream_t s) {
   struct Buf {
     void* p = nullptr;
     size_t bytes = 0;
+    bool captured = false;  // handed to a CUDA graph: kept until bf_release_scratch
   };
   static std::mutex mu;
   static std::map<Key, Buf> bufs;
+  static std::vector<Buf> retired;  // outgrown buffers a captured graph may still use
   if (tag < 0) {  // release every cached buffer (bf_release_scratch)
     std::lock_guard<std::mutex> lk(mu);
     cudaDeviceSynchronize();
-    for (auto& kv : bufs)
-      if (kv.second.p) {
-        cudaFree(kv.second.p);
-        scratch_account(-int64_t(kv.second.bytes));
+    for (auto& kv : bufs) retired.push_back(kv.second);
+    for (auto& b : retired)
+      if (b.p) {
+        cudaFree(b.p);
+        scratch_account(-int64_t(b.bytes));
       }
     bufs.clear();
+    retired.clear();
     return nullptr;
   }
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  // under stream capture (CholeskyGraph) the buffer becomes part of the
+  // graph: allocate it with the capture relaxed for this thread (cudaMalloc
+  // is not a stream operation) and never free it behind the graph's back
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (s) cudaStreamIsCapturing(s, &cap);
+  const bool capturing = cap == cudaStreamCaptureStatusActive;
   std::lock_guard<std::mutex> lk(mu);
   Buf& b = bufs[Key{tag, dev, s}];
   if (b.bytes < bytes) {
     if (b.p) {
-      cudaStreamSynchronize(s);  // the old buffer may still be read by work queued on s
-      cudaFree(b.p);
-      scratch_account(-int64_t(b.bytes));
+      if (b.captured || capturing) {
+        retired.push_back(b);
+      } else {
+        cudaStreamSynchronize(s);  // the old buffer may still be read by work queued on s
+        cudaFree(b.p);
+        scratch_account(-int64_t(b.bytes));
+      }
     }
-    b.p = nullptr;
-    b.bytes = 0;
-    if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+    b = Buf{};
+    cudaError_t e;
+    if (capturing) {
+      cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+      cudaThreadExchangeStreamCaptureMode(&mode);
+      e = cudaMalloc(&b.p, bytes);
+      cudaThreadExchangeStreamCaptureMode(&mode);
+    } else {
+      e = cudaMalloc(&b.p, bytes);
+    }
+    if (e != cudaSuccess) {
       cudaGetLastError();
+      b.p = nullptr;
       return nullptr;
     }
     b.bytes = bytes;
     scratch_account(int64_t(bytes));
   }
+  if (capturing) b.captured = true;
   return b.p;
 }
 
@@ -1073,6 +1097,10 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "red_fold") == 0) {
     bf::g_red_fold = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "tma_bn") == 0 && (value == 128 || value == 64)) {
+    bf::g_tma_bn = int(value);
     return BF_OK;
   }
   if (name && std::strcmp(name, "tma_variant") == 0) {

@@ -189,23 +189,33 @@ __device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double (&a)[4]
 // distributed trailing update's column panels): tile_tab packs the group too
 // (g << 24 | ti << 10 | tj), tiles row-major within a group; each tile takes
 // its A/B row offsets, its C pointer, bounds and lower mask from the group table.
-template <int MMAK, int KBOX, int STAGES, bool TMC, bool MODES = false, bool GROUPED = false>
+template <int MMAK, int KBOX, int STAGES, bool TMC, bool MODES = false, bool GROUPED = false, int BN_ = 128>
 __global__ void __launch_bounds__(TM_THREADS, 1)
     gemm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                          const GemmParams p) {
   if (aborted(p)) return;
   constexpr int BKS = 16 * KBOX;                    // k per stage
-  constexpr int OP_BYTES = KBOX * TM_TILE_BYTES;    // one operand, one stage
-  constexpr int STAGE_BYTES = 2 * OP_BYTES;
+  // BN_ = 64: two independent groups of 8 warps, each on its own 128 x 64
+  // tiles (a 4 x 2 grid of the same 32 x 32 warp tiles) with its own stage
+  // ring and barriers — the CTA's tiles alternate between the groups, so one
+  // group's fold and refill gaps hide under the other's DMMAs (what two
+  // resident CTAs per SM would give, without giving up the one-CTA-per-SM
+  // grid the SM reservation relies on)
+  static_assert(BN_ == 128 || (BN_ == 64 && !TMC && MMAK == 4), "128 x 64 tiles: plain m8n8k4 instantiations only");
+  constexpr int NG = 128 / BN_, GW = TM_CONSUMER_WARPS / NG, WN = BN_ / 32;
+  constexpr int NTHREADS = TM_THREADS;
+  constexpr int B_BOX_BYTES = BN_ * TM_BK * 8;     // one 16-wide k box of B^T
+  constexpr int OP_BYTES = KBOX * TM_TILE_BYTES;    // A, one stage
+  constexpr int STAGE_BYTES = OP_BYTES + KBOX * B_BOX_BYTES;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
-  const uint32_t tiles = (raw + 1023u) & ~1023u;  // SWIZZLE_128B wants 1 KB alignment
-  const uint32_t bars = tiles + STAGES * STAGE_BYTES;
-  auto full = [&](int s) { return bars + 8u * s; };
-  __shared__ int released[STAGES];
+  const uint32_t tiles0 = (raw + 1023u) & ~1023u;  // SWIZZLE_128B wants 1 KB alignment
+  const uint32_t bars = tiles0 + NG * STAGES * STAGE_BYTES;
+  auto fullg = [&](int gr, int s) { return bars + 8u * (gr * STAGES + s); };
+  __shared__ int released[NG * STAGES];
   // (ti, tj) of every tile this CTA owns, packed ti<<16 | tj, so a refill
   // (issued by whichever warp releases a stage last) costs one LDS
-  uint32_t* tile_tab = reinterpret_cast<uint32_t*>(smem_raw + (bars + 8u * STAGES - raw));
+  uint32_t* tile_tab = reinterpret_cast<uint32_t*>(smem_raw + (bars + 8u * NG * STAGES - raw));
   uint32_t* row_tab = tile_tab + p.tiles_per_cta;  // GROUPED: 2 words per tile
 
   const int tid = threadIdx.x;
@@ -221,7 +231,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   const int64_t first_tile = p.tile_stride > 0 ? int64_t(blockIdx.x) : int64_t(blockIdx.x) * p.tiles_per_cta;
   const int64_t owned = p.tile_stride > 0 ? (p.num_tiles - first_tile + tstep - 1) / tstep : p.num_tiles - first_tile;
   const int W = int(owned < p.tiles_per_cta ? owned : p.tiles_per_cta);
-  for (int w = tid; w < W; w += TM_THREADS) {
+  for (int w = tid; w < W; w += NTHREADS) {
     int64_t ti, tj;
     if constexpr (GROUPED) {
       const int64_t t = first_tile + w * tstep;
@@ -248,15 +258,21 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
       // the tile's A and B^T map rows, so a refill issues from shared memory
       // alone (bit 31: B^T comes from the A map)
       row_tab[2 * w] = uint32_t(gd.a_row + ti * TM_BM);
-      row_tab[2 * w + 1] = uint32_t(gd.b_row + tj * TM_BN) | (gd.b_from_a ? 0x80000000u : 0u);
+      row_tab[2 * w + 1] = uint32_t(gd.b_row + tj * BN_) | (gd.b_from_a ? 0x80000000u : 0u);
     } else {
-      tile_coords_tma(p, first_tile + w * tstep, tri, ti, tj);
+      const int64_t t = first_tile + w * tstep;
+      if (BN_ == 64 && tri) {  // each 128 x 128 lower tile as two 128 x 64 halves
+        tile_coords_tma(p, t >> 1, tri, ti, tj);
+        tj = 2 * tj + (t & 1);
+      } else {
+        tile_coords_tma(p, t, tri, ti, tj);
+      }
       tile_tab[w] = (uint32_t(ti) << 16) | uint32_t(tj);
     }
   }
   if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full(s), 1);
+    for (int s = 0; s < NG * STAGES; ++s) {
+      mbar_init(bars + 8u * s, 1);
       released[s] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -283,10 +299,15 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   const int last_len = K - (nseg - 1) * kc;
   const int tps_last = (last_len + BKS - 1) / BKS;
   const int ntiles = (nseg - 1) * tps + tps_last;  // k tiles per output tile
-  const int F = W * ntiles;                         // stage fills of this CTA
+  // this warp's group: tiles grp, grp + NG, ... of the CTA's run
+  const int grp = NG == 1 ? 0 : warp / GW;
+  const int Wg = W > grp ? (W - grp + NG - 1) / NG : 0;
+  const int F = Wg * ntiles;  // stage fills of this group
+  const uint32_t tiles = tiles0 + grp * STAGES * STAGE_BYTES;
+  auto full = [&](int s) { return fullg(grp, s); };
 
   auto issue = [&](int f) {
-    const int w = f / ntiles, kt = f - w * ntiles;
+    const int w = grp + NG * (f / ntiles), kt = f - (f / ntiles) * ntiles;
     const uint32_t tt = tile_tab[w];
     const int ti = GROUPED ? int((tt >> 10) & 0x3fffu) : int(tt >> 16), tj = GROUPED ? int(tt & 0x3ffu) : int(tt & 0xffffu);
     const int st = f % STAGES;
@@ -298,7 +319,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     for (int b = 0; b < KBOX; ++b) {
       if constexpr (MODES) {
         // an operand whose mode groups collapse to one per side has a 2-D map
-        const uint32_t k = uint32_t(k_lo + 16 * b), ra = uint32_t(ti) * TM_BM, rb = uint32_t(tj) * TM_BN;
+        const uint32_t k = uint32_t(k_lo + 16 * b), ra = uint32_t(ti) * TM_BM, rb = uint32_t(tj) * BN_;
         if (p.a_rank == 2) {
           tma_load_2d(sa + b * TM_TILE_BYTES, &tma_a, int(k), int(ra), full(st));
         } else {
@@ -307,31 +328,32 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
                       int(qra), full(st));
         }
         if (p.b_rank == 2) {
-          tma_load_2d(sa + OP_BYTES + b * TM_TILE_BYTES, &tma_b, int(k), int(rb), full(st));
+          tma_load_2d(sa + OP_BYTES + b * B_BOX_BYTES, &tma_b, int(k), int(rb), full(st));
         } else {
           const uint32_t qb = p.b_ki.div(k), qrb = p.b_mi.div(rb);
-          tma_load_4d(sa + OP_BYTES + b * TM_TILE_BYTES, &tma_b, int(k - qb * p.b_ki.d), int(rb - qrb * p.b_mi.d),
+          tma_load_4d(sa + OP_BYTES + b * B_BOX_BYTES, &tma_b, int(k - qb * p.b_ki.d), int(rb - qrb * p.b_mi.d),
                       int(qb), int(qrb), full(st));
         }
       } else if constexpr (GROUPED) {
         const uint32_t ra = row_tab[2 * w], rb = row_tab[2 * w + 1];
         tma_load_2d(sa + b * TM_TILE_BYTES, &tma_a, k_lo + 16 * b, int(ra), full(st));
-        tma_load_2d(sa + OP_BYTES + b * TM_TILE_BYTES, (rb >> 31) ? &tma_a : &tma_b, k_lo + 16 * b,
+        tma_load_2d(sa + OP_BYTES + b * B_BOX_BYTES, (rb >> 31) ? &tma_a : &tma_b, k_lo + 16 * b,
                     int(rb & 0x7fffffffu), full(st));
       } else {
         tma_load_2d(sa + b * TM_TILE_BYTES, &tma_a, k_lo + 16 * b, int(ti * TM_BM), full(st));
-        tma_load_2d(sa + OP_BYTES + b * TM_TILE_BYTES, &tma_b, k_lo + 16 * b, int(tj * TM_BN), full(st));
+        tma_load_2d(sa + OP_BYTES + b * B_BOX_BYTES, &tma_b, k_lo + 16 * b, int(tj * BN_), full(st));
       }
     }
   };
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tma_b)) : "memory");
-    for (int f = 0; f < F && f < STAGES; ++f) issue(f);
   }
+  if (tid == grp * GW * 32)
+    for (int f = 0; f < F && f < STAGES; ++f) issue(f);
 
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;
+  const int wm = (NG == 1 ? warp : warp % GW) / WN, wn = (NG == 1 ? warp : warp % GW) % WN;
   const int pg = perm8(g);
   const uint32_t a_row = uint32_t((wm * 32 + pg) * 128);
   const uint32_t b_row = uint32_t((wn * 32 + pg) * 128);
@@ -369,8 +391,8 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     return sg * tps + (len >= 4 ? len - 4 : 0);
   };
   int s = 0, round = 0, f = 0;
-  for (int w = 0; w < W; ++w) {
-    const uint32_t tt = tile_tab[w];
+  for (int wi = 0; wi < Wg; ++wi) {
+    const uint32_t tt = tile_tab[grp + NG * wi];
     int64_t m0, n0;
     if constexpr (GROUPED) {
       const GroupDesc& gd = p.groups[tt >> 24];
@@ -380,10 +402,10 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
       g_ld = gd.ldc;
       g_lower = gd.lower;
       m0 = int64_t((tt >> 10) & 0x3fffu) * TM_BM;
-      n0 = int64_t(tt & 0x3ffu) * TM_BN;
+      n0 = int64_t(tt & 0x3ffu) * BN_;
     } else {
       m0 = int64_t(tt >> 16) * TM_BM;
-      n0 = int64_t(tt & 0xffffu) * TM_BN;
+      n0 = int64_t(tt & 0xffffu) * BN_;
     }
     int seg = 0, sub = 0;
     // C is prefetched into L2 before each fold that reads it: every segment's
@@ -396,7 +418,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
 #pragma unroll
       for (int bx = 0; bx < KBOX; ++bx) {
         const uint32_t ab = sa + bx * TM_TILE_BYTES + a_row;
-        const uint32_t bb = sb + bx * TM_TILE_BYTES + b_row;
+        const uint32_t bb = sb + bx * B_BOX_BYTES + b_row;
         if constexpr (MMAK == 4) {
           double af[2][4], bfr[2][4];
 #pragma unroll
@@ -455,9 +477,9 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
         // release stage s; the last warp out refills it (generic reads ordered
         // before the async-proxy TMA write by the fences)
         __threadfence_block();
-        const int c = atomicAdd(&released[s], 1);
-        if (c == TM_CONSUMER_WARPS - 1) {
-          released[s] = 0;
+        const int c = atomicAdd(&released[grp * STAGES + s], 1);
+        if (c == GW - 1) {
+          released[grp * STAGES + s] = 0;
           if (f + STAGES < F) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             issue(f + STAGES);
@@ -631,13 +653,13 @@ EncodeTiledFn encoder() {
 }
 
 // (K x MN) k-contiguous operand -> 2-D tensor map with a {16, 128} box.
-bool make_map(CUtensorMap* map, const OperandMK& op, int64_t MN, int64_t K) {
+bool make_map(CUtensorMap* map, const OperandMK& op, int64_t MN, int64_t K, int box_rows = TM_BM) {
   EncodeTiledFn enc = encoder();
   if (!enc) return false;
   const double* base = static_cast<const double*>(op.base) + op.off;
   cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(MN)};
   cuuint64_t strides[1] = {cuuint64_t(op.s_mn) * 8};
-  cuuint32_t box[2] = {TM_BK, TM_BM};
+  cuuint32_t box[2] = {TM_BK, cuuint32_t(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -670,11 +692,12 @@ int g_tma_variant = 2;  // 0: m8n8k4/1 box/6 stages, 1: m16n8k8/1/6, 2: m8n8k4/2
 
 int g_tmem_fold = 1;  // bf_set_option("tmem_fold", 0|1): C in TMEM across >= 3 kc segments
 
-template <int MMAK, int KBOX, int STAGES, bool TMC, bool MODES = false, bool GROUPED = false>
+template <int MMAK, int KBOX, int STAGES, bool TMC, bool MODES = false, bool GROUPED = false, int BN_ = 128>
 static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensorMap& mb, cudaStream_t s) {
-  constexpr size_t base_smem = size_t(STAGES) * 2 * KBOX * TM_TILE_BYTES + 1024 + 8 * STAGES;
+  constexpr int NG = 128 / BN_;  // independent warp groups (each its own stage ring) per CTA
+  constexpr size_t base_smem = size_t(NG) * STAGES * KBOX * (TM_BM + BN_) * TM_BK * 8 + 1024 + 8 * NG * STAGES;
   constexpr size_t max_smem = 200 * 1024;  // leaves room for the static __shared__ words
-  auto kern = gemm_dmma_tma_kernel<MMAK, KBOX, STAGES, TMC, MODES, GROUPED>;
+  auto kern = gemm_dmma_tma_kernel<MMAK, KBOX, STAGES, TMC, MODES, GROUPED, BN_>;
   GemmParams p = p_in;
   static int sms_dev[64] = {};
   int dev = 0;
@@ -683,7 +706,7 @@ static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensor
   if (!sms_dev[dev]) cudaDeviceGetAttribute(&sms_dev[dev], cudaDevAttrMultiProcessorCount, dev);
   const int sms = sms_dev[dev];
   // tiles per CTA: g_tiles_per_cta (0 = fully persistent, one CTA per SM)
-  int64_t tpc = g_tiles_per_cta > 0 ? g_tiles_per_cta : (p.num_tiles + sms - 1) / sms;
+  int64_t tpc = g_tiles_per_cta > 0 ? int64_t(g_tiles_per_cta) * NG : (p.num_tiles + sms - 1) / sms;
   if (t_reserve_sms > 0 && t_reserve_sms < sms) {
     // persistent CTAs on all but t_reserve_sms SMs: the high-priority panel
     // stream always finds SMs free instead of waiting for tiles to retire
@@ -703,7 +726,7 @@ static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensor
   const int64_t grid = (p.num_tiles + tpc - 1) / tpc;
   if ((t_reserve_sms > 0 && g_reserve_strided) || persist) p.tile_stride = int(grid);
   if (grid > 0x7fffffffLL) return -3;
-  if (p.m >= (1 << 16) * int64_t(TM_BM) || p.n >= (1 << 16) * int64_t(TM_BN)) return -3;
+  if (p.m >= (1 << 16) * int64_t(TM_BM) || p.n >= (1 << 16) * int64_t(BN_)) return -3;
   const size_t smem = base_smem + size_t(tpc) * tab_bytes;
   if (!smem_attr(reinterpret_cast<const void*>(kern), int(smem))) return -10;
   note_launch();
@@ -711,21 +734,31 @@ static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensor
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
+// bf_set_option("tma_bn", 64 | 128): plain launches (no TMEM fold, 32-aligned
+// kc) on 128 x 64 tiles, two independent 8-warp groups per CTA with a
+// 2 x 32-k stage ring each (default; 128 = one 16-warp 128 x 128 tile, 3 rings).
+// A 1 x 16-k x 4-stage ring per group measured slower (C2 387.6 ms).
+int g_tma_bn = 64;
+
 int launch_gemm_dmma_tma(const GemmParams& p_in, cudaStream_t s) {
   GemmParams p = p_in;
   p.red_fold = g_red_fold;
-  CUtensorMap ma, mb;
-  if (!make_map(&ma, p.a, p.m, p.k) || !make_map(&mb, p.b, p.n, p.k)) return -3;
-  p.tiles_m = int((p.m + TM_BM - 1) / TM_BM);
-  p.tiles_n = int((p.n + TM_BN - 1) / TM_BN);
-  if (p.group <= 0) p.group = 8;
-  p.num_tiles = p.lower_only ? int64_t(p.tiles_m) * (p.tiles_m + 1) / 2 : int64_t(p.tiles_m) * p.tiles_n;
-  if (p.num_tiles <= 0) return 0;
-  if (p.num_tiles > 0x7fffffffLL) return -3;
+  const int64_t nseg = p.kc < p.k ? (p.k + p.kc - 1) / p.kc : 1;
   const bool two_box_ok = (p.kc % 32 == 0) || p.kc >= p.k;
   const int variant = two_box_ok ? g_tma_variant : (g_tma_variant & 1);
-  const int64_t nseg = p.kc < p.k ? (p.k + p.kc - 1) / p.kc : 1;
-  if (g_tmem_fold && nseg >= 3 && variant == 2) return run_tma<4, 2, 3, true>(p, ma, mb, s);
+  const bool tmc = g_tmem_fold && nseg >= 3 && variant == 2;
+  const int bn = g_tma_bn == 64 && variant == 2 && !tmc ? 64 : 128;  // the default m8n8k4 / 2-box mainloop
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, p.a, p.m, p.k) || !make_map(&mb, p.b, p.n, p.k, bn)) return -3;
+  p.tiles_m = int((p.m + TM_BM - 1) / TM_BM);
+  p.tiles_n = int((p.n + bn - 1) / bn);
+  if (p.group <= 0) p.group = 8;
+  // 128 x 64 lower tiles: every 128 x 128 lower tile as two halves
+  p.num_tiles = p.lower_only ? int64_t(p.tiles_m) * (p.tiles_m + 1) / 2 * (128 / bn) : int64_t(p.tiles_m) * p.tiles_n;
+  if (p.num_tiles <= 0) return 0;
+  if (p.num_tiles > 0x7fffffffLL) return -3;
+  if (bn == 64) return run_tma<4, 2, 2, false, false, false, 64>(p, ma, mb, s);
+  if (tmc) return run_tma<4, 2, 3, true>(p, ma, mb, s);
   switch (variant) {
     case 1: return run_tma<8, 1, 6, false>(p, ma, mb, s);
     case 2: return run_tma<4, 2, 3, false>(p, ma, mb, s);

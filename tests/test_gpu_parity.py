@@ -337,6 +337,47 @@ def test_tma_red_fold_bitwise(cuda, beta, lower):
     assert outs[0] == outs[1] == digest(cst)
 
 
+@pytest.mark.parametrize("bn", [64, 128])
+@pytest.mark.parametrize("lower", [False, True])
+def test_tma_half_width_tiles_bitwise(cuda, bn, lower):
+    """Both TMA tile shapes (option "tma_bn": 64 = two 8-warp groups on
+    128 x 64 tiles, the default; 128 = one 16-warp 128 x 128 tile): same
+    per-element fma chains and folds, so the oracle's bits — ragged edges,
+    lower-only C split into tile halves, many kc segments (TMEM fold off so
+    the 64-wide path runs them), and a whole factorization."""
+    from paper_2604_07311_b200.engine import _lib
+
+    lib = _lib.lib()
+    rng = np.random.default_rng(91 + int(lower) + bn)
+    m, n, k, kc = 700, 650, 768, 64
+    if lower:
+        n = m
+    a = rng.uniform(-1, 1, (m, k))
+    bt = rng.uniform(-1, 1, (n, k))
+    c0 = rng.uniform(-1, 1, (m, n))
+    cst = c0.reshape(-1).copy()
+    O.gemm(-1.25, (a.reshape(-1).copy(), {"off": 0, "m": m, "n": k, "rs": k, "cs": 1}),
+           (bt.reshape(-1).copy(), {"off": 0, "m": k, "n": n, "rs": 1, "cs": k}), 0.5,
+           (cst, {"off": 0, "m": m, "n": n, "rs": n, "cs": 1}), kc=kc, lower_only=lower)
+    cfg = KernelConfig(8, 6, 64, kc, 2048, F64, F64)
+    try:
+        lib.bf_set_option(b"tma_bn", bn)
+        lib.bf_set_option(b"tmem_fold", 0)
+        va, vb, vc = make_view(m, k, fill=a), make_view(n, k, fill=bt), make_view(m, n, fill=c0)
+        fn = bf.gemmt_lower if lower else bf.gemm
+        fn(-1.25, va, vb.transposed(), 0.5, vc, cfg=cfg)
+        got = digest(vc.storage.cpu().numpy())
+        a0 = spd_int(5150 + bn, 1700)
+        tree = ('{"op":"cholesky","variant":3,"bs":512,"kernel":{"kc":256},"child":{"op":"cholesky",'
+                '"variant":3,"bs":128,"kernel":{"kc":128},"child":{"op":"cholesky","variant":"unblocked3"}}}')
+        chol_ok = digest(chol_gpu(a0, tree)) == digest(chol_oracle(a0, tree))
+    finally:
+        lib.bf_set_option(b"tma_bn", 64)
+        lib.bf_set_option(b"tmem_fold", 1)
+    assert got == digest(cst)
+    assert chol_ok
+
+
 def test_tma_persist_grid_bitwise(cuda):
     """The strided persistent grid (option "persist", long-K GEMMs with at
     least 4 tiles per SM) only reorders tiles: same bits as the default grid."""

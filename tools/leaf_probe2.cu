@@ -8,6 +8,9 @@
 
 namespace bf {
 void note_launch(int64_t) {}
+bool smem_attr(const void* k, int b) {
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, b) == cudaSuccess;
+}
 int g_use_tma = 1, g_tma_variant = 2, g_tiles_per_cta = 1, g_bf16_tma_c = 1;
 }  // namespace bf
 using namespace bf;

@@ -11,6 +11,12 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import bench  # noqa: E402
 import paper_2604_07311_b200 as bf  # noqa: E402
 from paper_2604_07311_b200.control import parse_tree  # noqa: E402
+from paper_2604_07311_b200.engine import _lib  # noqa: E402
+import os  # noqa: E402
+
+for _kv in filter(None, os.environ.get("BF_OPTS", "").split(",")):  # library options for sweeps
+    _k, _v = _kv.split("=")
+    assert _lib.lib().bf_set_option(_k.encode(), int(_v)) == 0, _kv
 
 bs = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5

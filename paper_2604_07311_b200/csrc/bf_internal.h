@@ -174,6 +174,8 @@ extern int g_qr_global;       // QR panel: force the global-memory sweep
 extern int g_ltlt_grid_max;   // LTL^T stepper: cap on the cooperative grid
 int launch_gemm_simt_f32(const GemmParams& p, cudaStream_t s);        // f32 storage, f32 acc
 int launch_gemm_simt_f32acc64(const GemmParams& p, cudaStream_t s);   // f32 storage, f64 acc
+int launch_copy2d_unless_aborted(const double* src, int64_t sld, double* dst, int64_t dld, int64_t m, int64_t n,
+                                 const int* abort_flag, cudaStream_t s);
 int launch_scale(int is_f64, double beta, void* c, int64_t off, int64_t m, int64_t n, int64_t rs,
                  int64_t cs, const int64_t* rscat, const int64_t* cscat, int lower_only,
                  cudaStream_t s);

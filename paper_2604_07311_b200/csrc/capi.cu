@@ -286,7 +286,7 @@ int gemm_impl(Mode mode, double alpha, const bf_view& a, const bf_view& b, doubl
 // factorizations enqueued on different caller streams (e.g. from different
 // host threads) get independent panel/aux/copy streams and never serialise
 // their panel chains on a shared one.
-enum SideRole { ROLE_PANEL = 0, ROLE_AUX = 1, ROLE_H2D = 2, ROLE_COPY = 3, ROLE_SEG0 = 4 };
+enum SideRole { ROLE_PANEL = 0, ROLE_AUX = 1, ROLE_H2D = 2, ROLE_COPY = 3, ROLE_PANEL2 = 100, ROLE_SEG0 = 4 };
 cudaStream_t side_stream(SideRole role, cudaStream_t caller) {
   struct Key {
     int dev, role;
@@ -302,7 +302,10 @@ cudaStream_t side_stream(SideRole role, cudaStream_t caller) {
   std::lock_guard<std::mutex> lk(mu);
   cudaStream_t& st = streams[Key{dev, int(role), caller}];
   if (!st) {
-    if (role == ROLE_PANEL) {  // high priority: its CTAs go first whenever trailing-update CTAs retire
+    // the panel stream is high priority: its CTAs go first whenever trailing-update
+    // CTAs retire (ROLE_PANEL2, the overlapped panel TRSM, stays normal so the
+    // diagonal factor's latency-bound chain keeps precedence over it)
+    if (role == ROLE_PANEL) {
       int lo = 0, hi = 0;
       cudaDeviceGetStreamPriorityRange(&lo, &hi);
       cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi);
@@ -316,6 +319,7 @@ cudaStream_t panel_stream(cudaStream_t caller) { return side_stream(ROLE_PANEL, 
 cudaStream_t aux_stream(cudaStream_t caller) { return side_stream(ROLE_AUX, caller); }
 cudaStream_t h2d_stream(cudaStream_t caller) { return side_stream(ROLE_H2D, caller); }
 cudaStream_t copy_stream(cudaStream_t caller) { return side_stream(ROLE_COPY, caller); }
+cudaStream_t panel2_stream(cudaStream_t caller) { return side_stream(ROLE_PANEL2, caller); }
 
 // Deep-K narrow GEMM/GEMMT (V2's A11 -= A10 A10^T and A21 -= A20 A10^T, V1's
 // SYRK: few output tiles, K = the whole factored part): the kc segments are
@@ -417,6 +421,44 @@ int trsm_rec(Mode mode, double alpha, const bf_view& tri, const bf_view& b, int6
   rc = gemm_impl(mode, -1.0, b1, transposed(l21), alpha, b2, 0, kc, d_abort, s);
   if (rc) return rc;
   return trsm_rec(mode, 1.0, l22, b2, kc, d_sing, d_abort, s);
+}
+
+// trsm_rec whose triangle is still being factored on another stream: the
+// diagonal block's inner steps (block width bs1) each record ev[J] once
+// column block J of the triangle is final (rows >= J*bs1); every piece of
+// the recursion waits for the last inner step whose columns it reads — a
+// subtree on columns [lo, hi) reads tri[lo:hi, lo:hi], a fold
+// b2 -= b1 tri[mid:hi, lo:mid]^T reads columns [lo, mid).  Same pieces, same
+// order as trsm_rec, so the same bits.
+struct TriWait {
+  const cudaEvent_t* ev;
+  int64_t bs1, ns;
+  int64_t last = -1;
+  void wait(int64_t col_end, cudaStream_t s) {  // columns [.., col_end) must be final
+    int64_t j = (col_end - 1) / bs1;
+    if (j > ns - 1) j = ns - 1;
+    if (j > last) {
+      cudaStreamWaitEvent(s, ev[j], 0);
+      last = j;
+    }
+  }
+};
+int trsm_rec_w(Mode mode, double alpha, const bf_view& tri, const bf_view& b, int64_t kc, const int* d_abort,
+               cudaStream_t s, TriWait& w, int64_t off) {
+  const int64_t n = tri.n;
+  if (b.m == 0 || n == 0) return BF_OK;
+  if ((n <= 128 && n > 32 && g_fused_trsm && (mode == MODE_D || mode == MODE_S)) || n <= 32) {
+    w.wait(off + n, s);
+    return trsm_rec(mode, alpha, tri, b, kc, nullptr, d_abort, s);
+  }
+  const int64_t n1 = n / 2, n2 = n - n1;
+  int rc = trsm_rec_w(mode, alpha, subview(tri, 0, n1, 0, n1), subview(b, 0, b.m, 0, n1), kc, d_abort, s, w, off);
+  if (rc) return rc;
+  w.wait(off + n1, s);
+  rc = gemm_impl(mode, -1.0, subview(b, 0, b.m, 0, n1), transposed(subview(tri, n1, n2, 0, n1)), alpha,
+                 subview(b, 0, b.m, n1, n2), 0, kc, d_abort, s);
+  if (rc) return rc;
+  return trsm_rec_w(mode, 1.0, subview(tri, n1, n2, n1, n2), subview(b, 0, b.m, n1, n2), kc, d_abort, s, w, off + n1);
 }
 
 int trsm_impl(Mode mode, double alpha, const bf_view* tri, const bf_view* b, int64_t kc, int* d_sing,
@@ -541,6 +583,65 @@ int g_timeline = 0;
 std::vector<TimelineStep> g_tl;
 cudaEvent_t g_tl_origin = nullptr;
 
+// bf_set_option("panel_overlap", 0|1): a lookahead panel (diagonal factor +
+// TRSM of the rows below) runs its TRSM on a second stream, trailing the
+// diagonal factor's inner steps (TriWait) instead of waiting for all of it
+int g_panel_overlap = 1;
+
+// Panel of the lookahead schedule with the TRSM overlapped: the diagonal
+// block is factored by the v3 inner loop of lv[1] on `st` (the body of
+// chol_run, inner step J recording ev[J] once its column block is final),
+// while `st2` solves a copy X of the rows below against the finished part
+// of the triangle.  X goes back into the matrix only if no pivot failure was
+// recorded, so a failing diagonal factor leaves the rows below untouched,
+// exactly as the sequential panel does; on success every element of the
+// panel saw the sequential panel's operations.  Returns with `st` joined.
+int panel_overlap(Mode mode, const bf_view& a11, const bf_view& a21, const bf_chol_level* lv, int nl, int64_t base,
+                  int* d_info, cudaStream_t st, cudaStream_t st2, cudaEvent_t* diag_mark) {
+  const bf_chol_level& in = lv[1];
+  const int64_t b = a11.n, bs1 = in.bs, m = a21.m;
+  const int64_t ns = (b + bs1 - 1) / bs1;
+  double* x = static_cast<double*>(bf::stream_scratch(7, size_t(m) * size_t(b) * sizeof(double), st2));
+  if (!x) return -1;  // no room: the caller runs the sequential panel
+  std::vector<cudaEvent_t> ev(static_cast<size_t>(ns) + 1);
+  for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  cudaEventRecord(ev[size_t(ns)], st);  // the rows below are ready (st's earlier work)
+  cudaStreamWaitEvent(st2, ev[size_t(ns)], 0);
+  const double* src = static_cast<const double*>(a21.base) + a21.off;
+  int rc = cudaMemcpy2DAsync(x, size_t(b) * sizeof(double), src, size_t(a21.rs) * sizeof(double),
+                             size_t(b) * sizeof(double), size_t(m), cudaMemcpyDeviceToDevice, st2) == cudaSuccess
+               ? BF_OK
+               : fail(BF_ERR_CUDA, "panel copy failed");
+  // the diagonal block: chol_run's v3 body for lv[1] (children from lv[2])
+  for (int64_t j = 0; j < ns && rc == BF_OK; ++j) {
+    const int64_t done = j * bs1, bb = bs1 < b - done ? bs1 : b - done;
+    const int64_t r2s = done + bb, r2n = b - r2s;
+    bf_view d11 = subview(a11, done, bb, done, bb);
+    bf_view d21 = subview(a11, r2s, r2n, done, bb);
+    rc = chol_run(mode, d11, lv, nl, 2, base + done, d_info, st);
+    if (!rc) rc = trsm_rec(mode, 1.0, d11, d21, in.kc, nullptr, d_info, st);
+    cudaEventRecord(ev[size_t(j)], st);
+    if (!rc) rc = gemm_impl(mode, -1.0, d21, transposed(d21), 1.0, subview(a11, r2s, r2n, r2s, r2n), 1, in.kc, d_info, st);
+  }
+  if (diag_mark) {
+    cudaEventCreate(diag_mark);
+    cudaEventRecord(*diag_mark, st);
+  }
+  if (rc == BF_OK) {
+    TriWait w{ev.data(), bs1, ns};
+    bf_view xv{x, 0, m, b, b, 1};
+    rc = trsm_rec_w(mode, 1.0, a11, xv, lv[0].kc, d_info, st2, w, 0);
+    w.wait(b, st2);  // the whole diagonal factor (its flag) before the copy back
+    if (!rc && bf::launch_copy2d_unless_aborted(x, b, static_cast<double*>(a21.base) + a21.off, a21.rs, m, b, d_info,
+                                                st2))
+      rc = fail(BF_ERR_CUDA, "panel copy launch failed");
+  }
+  cudaEventRecord(ev[size_t(ns)], st2);
+  cudaStreamWaitEvent(st, ev[size_t(ns)], 0);
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
 int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int64_t base, int* d_info,
                       cudaStream_t s) {
   const int64_t n = a.n, bs = lv[0].bs, kc = lv[0].kc;
@@ -553,6 +654,14 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
   auto panel = [&](int64_t done, int64_t b, cudaStream_t st) {
     bf_view a11 = subview(a, done, b, done, b);
     bf_view a21 = subview(a, done + b, n - done - b, done, b);
+    if (g_panel_overlap && mode == MODE_D && nl >= 2 && lv[1].variant == 3 && lv[1].bs >= 1 && b > lv[1].bs &&
+        a21.m > 0 && a.cs == 1) {
+      cudaStream_t st2 = panel2_stream(s);
+      if (st2) {
+        const int prc = panel_overlap(mode, a11, a21, lv, nl, base + done, d_info, st, st2, diag_mark);
+        if (prc != -1) return prc;
+      }
+    }
     int rc = chol_run(mode, a11, lv, nl, 1, base + done, d_info, st);
     if (diag_mark) {
       cudaEventCreate(diag_mark);
@@ -1061,6 +1170,10 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "panel_tiles") == 0 && value >= 0 && value < (1 << 16)) {
     g_panel_tiles = int(value);
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "panel_overlap") == 0) {
+    g_panel_overlap = value != 0;
     return BF_OK;
   }
   if (name && std::strcmp(name, "persist") == 0) {

@@ -1178,6 +1178,31 @@ int launch_trsm_warp(double alpha, const T* t, int64_t toff, int64_t trs, int64_
 
 }  // namespace
 
+namespace {
+__global__ void copy2d_unless_aborted_kernel(const double* src, int64_t sld, double* dst, int64_t dld, int64_t m,
+                                             int64_t n, const int* abort_flag) {
+  if (abort_flag != nullptr && *abort_flag >= 0) return;
+  const int64_t total = m * n, stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t i = e / n, j = e - i * n;
+    dst[i * dld + j] = src[i * sld + j];
+  }
+}
+}  // namespace
+
+// dst(m x n, ld dld) = src(m x n, ld sld) unless *abort_flag >= 0 (a pivot
+// failure has been recorded): the overlapped panel's solved rows reach the
+// matrix only when the diagonal factor before them succeeded
+int launch_copy2d_unless_aborted(const double* src, int64_t sld, double* dst, int64_t dld, int64_t m, int64_t n,
+                                 const int* abort_flag, cudaStream_t s) {
+  if (m <= 0 || n <= 0) return 0;
+  const int64_t total = m * n;
+  const int blocks = int((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
+  note_launch();
+  copy2d_unless_aborted_kernel<<<blocks, 256, 0, s>>>(src, sld, dst, dld, m, n, abort_flag);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
 int launch_scale(int is_f64, double beta, void* c, int64_t off, int64_t m, int64_t n, int64_t rs, int64_t cs,
                  const int64_t* rscat, const int64_t* cscat, int lower_only, cudaStream_t s) {
   int64_t total = m * n;

@@ -127,6 +127,37 @@ RESERVE_TREE = ('{"op": "cholesky", "variant": 3, "bs": 256, "kernel": {"kc": 25
                 '"variant": 3, "bs": 64, "kernel": {"kc": 64}, "child": {"op": "cholesky", "variant": "unblocked3"}}}')
 
 
+@pytest.mark.parametrize("overlap", [1, 0])
+@pytest.mark.parametrize("npd_at", [None, 10, 300, 1000, 1290, 2200])
+def test_panel_overlap_bitwise(cuda, overlap, npd_at):
+    """Overlapped panels (option "panel_overlap"): the TRSM of the rows below
+    trails the diagonal factor's inner steps on a second stream, on a copy that
+    is written back only when no pivot failure was flagged.  Same bits as the
+    oracle, and after a failure the same partial state — failures in the first
+    panel's first and later inner blocks, in a later panel, in the last one."""
+    import json
+
+    from paper_2604_07311_b200.engine import _lib
+
+    n = 2304
+    a0 = spd_int(4343, n)
+    if npd_at is not None:
+        a0[npd_at, npd_at] = -1e9
+    lib = _lib.lib()
+    try:
+        assert lib.bf_set_option(b"panel_overlap", overlap) == 0
+        v = make_view(n, n, fill=a0)
+        bad = int(bf.cholesky_async(v, "lower", parse_tree(RESERVE_TREE)).item())
+    finally:
+        lib.bf_set_option(b"panel_overlap", 1)
+    st = a0.reshape(-1).copy()
+    ref_bad = O.cholesky(st, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1},
+                         O.levels_from_tree(json.loads(RESERVE_TREE), n, "f64"), nthreads=O.host_threads())
+    assert ref_bad == (-1 if npd_at is None else npd_at)
+    assert bad == ref_bad
+    assert digest(v.storage.cpu().numpy()) == digest(st)
+
+
 @pytest.mark.parametrize("opts", [
     {"tail_reserve": 0},                                     # 1-tile CTAs on the whole GPU
     {"tail_reserve": 16, "tail_rows": 1 << 40},              # default grid shape on every step

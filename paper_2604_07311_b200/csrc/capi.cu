@@ -157,7 +157,7 @@ int64_t g_tail_rows = 32768;  // bf_set_option("tail_rows", t): ... when the res
 // bf_set_option("reserve_adaptive", 0|1): per-step reservation sized by the
 // panel stream's share of the step's work (+ "reserve_extra", >= "reserve_min")
 int g_reserve_adaptive = 1;
-int g_reserve_extra = 4;
+int g_reserve_extra = 6;  // 4 before the overlapped panels (tools/gpu_r02_resv2.sh: 6 -> 370.6 vs 371.0 ms)
 int g_reserve_min = 12;
 int g_diag_reserve = 0;      // bf_set_option("diag_reserve", r): SMs left to the panel stream while ...
 int64_t g_diag_rows = 0;     // bf_set_option("diag_rows", h): ... the first h rows of the rest are updated

@@ -601,12 +601,18 @@ int panel_overlap(Mode mode, const bf_view& a11, const bf_view& a21, const bf_ch
   const bf_chol_level& in = lv[1];
   const int64_t b = a11.n, bs1 = in.bs, m = a21.m;
   const int64_t ns = (b + bs1 - 1) / bs1;
-  double* x = static_cast<double*>(bf::stream_scratch(7, size_t(m) * size_t(b) * sizeof(double), st2));
-  if (!x) return -1;  // no room: the caller runs the sequential panel
   std::vector<cudaEvent_t> ev(static_cast<size_t>(ns) + 1);
   for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   cudaEventRecord(ev[size_t(ns)], st);  // the rows below are ready (st's earlier work)
   cudaStreamWaitEvent(st2, ev[size_t(ns)], 0);
+  // (after st2 joined st: under CUDA-graph capture the scratch is then allocated as graph-owned)
+  double* x = static_cast<double*>(bf::stream_scratch(7, size_t(m) * size_t(b) * sizeof(double), st2));
+  if (!x) {  // no room: the caller runs the sequential panel
+    cudaEventRecord(ev[size_t(ns)], st2);
+    cudaStreamWaitEvent(st, ev[size_t(ns)], 0);
+    for (auto& e : ev) cudaEventDestroy(e);
+    return -1;
+  }
   const double* src = static_cast<const double*>(a21.base) + a21.off;
   int rc = cudaMemcpy2DAsync(x, size_t(b) * sizeof(double), src, size_t(a21.rs) * sizeof(double),
                              size_t(b) * sizeof(double), size_t(m), cudaMemcpyDeviceToDevice, st2) == cudaSuccess

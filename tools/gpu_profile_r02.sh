@@ -16,5 +16,5 @@ ncu -i gpurun_out/r02_syrk_full.ncu-rep --page raw --csv > gpurun_out/r02_syrk_r
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29621 \
     bench.py --dist --steps 3 --warmup 3 > gpurun_out/r02_dist1.json 2> gpurun_out/r02_dist1.err; echo "dist rc=$?"
 timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29622 \
-    bench.py --dist --n 131072 --steps 1 --warmup 1 --no-e2e > gpurun_out/r02_dist_c3.json 2> gpurun_out/r02_dist_c3.err; echo "dist c3 rc=$?"
+    bench.py --dist --order 131072 --steps 1 --warmup 1 --no-e2e > gpurun_out/r02_dist_c3.json 2> gpurun_out/r02_dist_c3.err; echo "dist c3 rc=$?"
 tail -c 600 gpurun_out/r02_bench.json

@@ -1015,8 +1015,13 @@ __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t o
       for (int q = 0; q < 32; ++q) acc[q] = (q <= i && i < bw) ? A[(k0 + i) * LV4_LD + k0 + q] : T(0);
       bool unsafe = false;
       T d = __shfl_sync(0xffffffffu, acc[0], 0);
-#pragma unroll 1
-      for (int p0 = 0; p0 < bw; p0 += 4) {
+      // fully unrolled over the block's 8 four-column trips (a warp-uniform
+      // guard per trip): window positions j >= 32 - p0 are past the block,
+      // so the updates and broadcast reads stop there — half the multiply-
+      // subtracts of a fixed 32-wide window
+#pragma unroll
+      for (int p0 = 0; p0 < 32; p0 += 4) {
+        if (p0 >= bw) break;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int p = p0 + u;
@@ -1045,22 +1050,26 @@ __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t o
           if constexpr (sizeof(T) == 8) {
 #pragma unroll
             for (int m = 0; m < 16; ++m) {
-              const double2 t2 = reinterpret_cast<const double2*>(cb + p0)[m];
-              lv[2 * m] = t2.x;
-              lv[2 * m + 1] = t2.y;
+              if (2 * m < 32 - p0) {
+                const double2 t2 = reinterpret_cast<const double2*>(cb + p0)[m];
+                lv[2 * m] = t2.x;
+                lv[2 * m + 1] = t2.y;
+              }
             }
           } else {
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
-              const float4 t4 = reinterpret_cast<const float4*>(cb + p0)[m];
-              lv[4 * m] = t4.x;
-              lv[4 * m + 1] = t4.y;
-              lv[4 * m + 2] = t4.z;
-              lv[4 * m + 3] = t4.w;
+              if (4 * m < 32 - p0) {
+                const float4 t4 = reinterpret_cast<const float4*>(cb + p0)[m];
+                lv[4 * m] = t4.x;
+                lv[4 * m + 1] = t4.y;
+                lv[4 * m + 2] = t4.z;
+                lv[4 * m + 3] = t4.w;
+              }
             }
           }
 #pragma unroll
-          for (int j = u + 1; j < 32; ++j) acc[j] = Ops<T>::sub(acc[j], Ops<T>::mul(l, lv[j]));
+          for (int j = u + 1; j < 32 - p0; ++j) acc[j] = Ops<T>::sub(acc[j], Ops<T>::mul(l, lv[j]));
         }
 #pragma unroll
         for (int j = 0; j < 28; ++j) acc[j] = acc[j + 4];
@@ -1081,8 +1090,9 @@ __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t o
 #pragma unroll
       for (int q = 0; q < 32; ++q) acc[q] = (ok && q < bw) ? A[r * LV4_LD + k0 + q] : T(0);
       bool unsafe = false;
-#pragma unroll 1
-      for (int q0 = 0; q0 < bw; q0 += 4) {
+#pragma unroll
+      for (int q0 = 0; q0 < 32; q0 += 4) {  // unrolled like (a): updates stop at the block's edge
+        if (q0 >= bw) break;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int q = q0 + u;
@@ -1095,7 +1105,7 @@ __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t o
           acc[u] = xq;
           if (live && ok) A[r * LV4_LD + k0 + q] = xq;
 #pragma unroll
-          for (int j = u + 1; j < 32; ++j)  // columns past the block: never stored
+          for (int j = u + 1; j < 32 - q0; ++j)
             acc[j] = Ops<T>::sub(acc[j], Ops<T>::mul(xq, l[((q + j - u) & 31) * LV4_LD + qq]));
         }
 #pragma unroll

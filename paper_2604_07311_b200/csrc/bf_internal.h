@@ -155,6 +155,7 @@ int launch_pack_scatter(int is_f64, const void* src, const int64_t* row_scat, co
                         int64_t cols, void* out, cudaStream_t s);
 extern int g_use_tma;         // bf_set_option("tma", 0|1)
 extern int g_tma_variant;     // bf_set_option("tma_variant", 0..3)
+extern int g_tmc_bn64;        // bf_set_option("tmc_bn64", 0|1)
 extern int g_tma_bn;          // bf_set_option("tma_bn", 64 | 128): TMA DMMA tile width
 extern int g_persist;         // bf_set_option("persist", 0|1): strided persistent grid for long-K GEMMs
 extern int g_red_fold;        // bf_set_option("red_fold", 0|1): TMA kernel folds with red.global.add.f64

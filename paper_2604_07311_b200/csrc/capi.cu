@@ -1218,6 +1218,10 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_red_fold = value != 0;
     return BF_OK;
   }
+  if (name && std::strcmp(name, "tmc_bn64") == 0) {
+    bf::g_tmc_bn64 = value != 0;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "tma_bn") == 0 && (value == 128 || value == 64)) {
     bf::g_tma_bn = int(value);
     return BF_OK;

@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
   // group's fold and refill gaps hide under the other's DMMAs (what two
   // resident CTAs per SM would give, without giving up the one-CTA-per-SM
   // grid the SM reservation relies on)
-  static_assert(BN_ == 128 || (BN_ == 64 && !TMC && MMAK == 4), "128 x 64 tiles: plain m8n8k4 instantiations only");
+  static_assert(BN_ == 128 || (BN_ == 64 && MMAK == 4), "128 x 64 tiles: m8n8k4 instantiations only");
   constexpr int NG = 128 / BN_, GW = TM_CONSUMER_WARPS / NG, WN = BN_ / 32;
   constexpr int NTHREADS = TM_THREADS;
   constexpr int B_BOX_BYTES = BN_ * TM_BK * 8;     // one 16-wide k box of B^T
@@ -739,6 +739,7 @@ static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensor
 // 2 x 32-k stage ring each (default; 128 = one 16-warp 128 x 128 tile, 3 rings).
 // A 1 x 16-k x 4-stage ring per group measured slower (C2 387.6 ms).
 int g_tma_bn = 64;
+int g_tmc_bn64 = 0;  // bf_set_option("tmc_bn64", 1): the TMEM-fold launches on the two-group 128 x 64 tiles too
 
 int launch_gemm_dmma_tma(const GemmParams& p_in, cudaStream_t s) {
   GemmParams p = p_in;
@@ -747,7 +748,7 @@ int launch_gemm_dmma_tma(const GemmParams& p_in, cudaStream_t s) {
   const bool two_box_ok = (p.kc % 32 == 0) || p.kc >= p.k;
   const int variant = two_box_ok ? g_tma_variant : (g_tma_variant & 1);
   const bool tmc = g_tmem_fold && nseg >= 3 && variant == 2;
-  const int bn = g_tma_bn == 64 && variant == 2 && !tmc ? 64 : 128;  // the default m8n8k4 / 2-box mainloop
+  const int bn = g_tma_bn == 64 && variant == 2 && (!tmc || g_tmc_bn64) ? 64 : 128;  // the default m8n8k4 / 2-box mainloop
   CUtensorMap ma, mb;
   if (!make_map(&ma, p.a, p.m, p.k) || !make_map(&mb, p.b, p.n, p.k, bn)) return -3;
   p.tiles_m = int((p.m + TM_BM - 1) / TM_BM);
@@ -758,6 +759,7 @@ int launch_gemm_dmma_tma(const GemmParams& p_in, cudaStream_t s) {
   if (p.num_tiles <= 0) return 0;
   if (p.num_tiles > 0x7fffffffLL) return -3;
   if (bn == 64) return run_tma<4, 2, 2, false, false, false, 64>(p, ma, mb, s);
+  if (tmc && bn == 64) return run_tma<4, 2, 2, true, false, false, 64>(p, ma, mb, s);
   if (tmc) return run_tma<4, 2, 3, true>(p, ma, mb, s);
   switch (variant) {
     case 1: return run_tma<8, 1, 6, false>(p, ma, mb, s);

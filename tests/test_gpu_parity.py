@@ -368,7 +368,7 @@ def test_tma_red_fold_bitwise(cuda, beta, lower):
     assert outs[0] == outs[1] == digest(cst)
 
 
-@pytest.mark.parametrize("bn", [64, 128])
+@pytest.mark.parametrize("bn", [64, 128, "64tmc"])
 @pytest.mark.parametrize("lower", [False, True])
 def test_tma_half_width_tiles_bitwise(cuda, bn, lower):
     """Both TMA tile shapes (option "tma_bn": 64 = two 8-warp groups on
@@ -379,6 +379,8 @@ def test_tma_half_width_tiles_bitwise(cuda, bn, lower):
     from paper_2604_07311_b200.engine import _lib
 
     lib = _lib.lib()
+    tmc = bn == "64tmc"  # the TMEM-fold instantiation on the two-group tiles (option "tmc_bn64")
+    bn = 64 if tmc else bn
     rng = np.random.default_rng(91 + int(lower) + bn)
     m, n, k, kc = 700, 650, 768, 64
     if lower:
@@ -393,7 +395,8 @@ def test_tma_half_width_tiles_bitwise(cuda, bn, lower):
     cfg = KernelConfig(8, 6, 64, kc, 2048, F64, F64)
     try:
         lib.bf_set_option(b"tma_bn", bn)
-        lib.bf_set_option(b"tmem_fold", 0)
+        lib.bf_set_option(b"tmem_fold", 1 if tmc else 0)
+        lib.bf_set_option(b"tmc_bn64", 1 if tmc else 0)
         va, vb, vc = make_view(m, k, fill=a), make_view(n, k, fill=bt), make_view(m, n, fill=c0)
         fn = bf.gemmt_lower if lower else bf.gemm
         fn(-1.25, va, vb.transposed(), 0.5, vc, cfg=cfg)
@@ -405,6 +408,7 @@ def test_tma_half_width_tiles_bitwise(cuda, bn, lower):
     finally:
         lib.bf_set_option(b"tma_bn", 64)
         lib.bf_set_option(b"tmem_fold", 1)
+        lib.bf_set_option(b"tmc_bn64", 0)
     assert got == digest(cst)
     assert chol_ok
 

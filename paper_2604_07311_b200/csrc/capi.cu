@@ -588,6 +588,27 @@ cudaEvent_t g_tl_origin = nullptr;
 // diagonal factor's inner steps (TriWait) instead of waiting for all of it
 int g_panel_overlap = 1;
 
+// chol_run's variant-3 body for node lv[idx] on `a` (children from idx+1),
+// recording ev[j] on st once inner step j's column block is final (after its
+// TRSM, before its trailing GEMMT)
+int chol_v3_events(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int idx, int64_t base, int* d_info,
+                   cudaStream_t st, const cudaEvent_t* ev) {
+  const bf_chol_level& in = lv[idx];
+  const int64_t b = a.n, bs1 = in.bs, ns = (b + bs1 - 1) / bs1;
+  int rc = BF_OK;
+  for (int64_t j = 0; j < ns && rc == BF_OK; ++j) {
+    const int64_t done = j * bs1, bb = bs1 < b - done ? bs1 : b - done;
+    const int64_t r2s = done + bb, r2n = b - r2s;
+    bf_view d11 = subview(a, done, bb, done, bb);
+    bf_view d21 = subview(a, r2s, r2n, done, bb);
+    rc = chol_run(mode, d11, lv, nl, idx + 1, base + done, d_info, st);
+    if (!rc) rc = trsm_rec(mode, 1.0, d11, d21, in.kc, nullptr, d_info, st);
+    cudaEventRecord(ev[size_t(j)], st);
+    if (!rc) rc = gemm_impl(mode, -1.0, d21, transposed(d21), 1.0, subview(a, r2s, r2n, r2s, r2n), 1, in.kc, d_info, st);
+  }
+  return rc;
+}
+
 // Panel of the lookahead schedule with the TRSM overlapped: the diagonal
 // block is factored by the v3 inner loop of lv[1] on `st` (the body of
 // chol_run, inner step J recording ev[J] once its column block is final),
@@ -619,16 +640,7 @@ int panel_overlap(Mode mode, const bf_view& a11, const bf_view& a21, const bf_ch
                ? BF_OK
                : fail(BF_ERR_CUDA, "panel copy failed");
   // the diagonal block: chol_run's v3 body for lv[1] (children from lv[2])
-  for (int64_t j = 0; j < ns && rc == BF_OK; ++j) {
-    const int64_t done = j * bs1, bb = bs1 < b - done ? bs1 : b - done;
-    const int64_t r2s = done + bb, r2n = b - r2s;
-    bf_view d11 = subview(a11, done, bb, done, bb);
-    bf_view d21 = subview(a11, r2s, r2n, done, bb);
-    rc = chol_run(mode, d11, lv, nl, 2, base + done, d_info, st);
-    if (!rc) rc = trsm_rec(mode, 1.0, d11, d21, in.kc, nullptr, d_info, st);
-    cudaEventRecord(ev[size_t(j)], st);
-    if (!rc) rc = gemm_impl(mode, -1.0, d21, transposed(d21), 1.0, subview(a11, r2s, r2n, r2s, r2n), 1, in.kc, d_info, st);
-  }
+  if (rc == BF_OK) rc = chol_v3_events(mode, a11, lv, nl, 1, base, d_info, st, ev.data());
   if (diag_mark) {
     cudaEventCreate(diag_mark);
     cudaEventRecord(*diag_mark, st);
@@ -1120,6 +1132,33 @@ inline cudaStream_t S(void* p) { return static_cast<cudaStream_t>(p); }
 }  // namespace
 
 namespace bf {
+// mixed driver (mixed.cu): factor the FP64 diagonal block `a` with the tree
+// and solve X L^T = X (X = the identity, set on st before the call) with the
+// TRSM trailing the factor's inner steps on a second stream (as the
+// overlapped panels do); returns with st joined.  Falls back to the
+// sequential factor + solve when the tree root is not a blocked variant 3.
+int chol_inverse_overlapped(const bf_view& a, const bf_chol_level* lv, int nl, int64_t base, const bf_view& x,
+                            int64_t kc, int* d_info, cudaStream_t st) {
+  cudaStream_t st2 = panel2_stream(st);
+  if (!(g_panel_overlap && nl >= 1 && lv[0].variant == 3 && lv[0].bs >= 1 && a.n > lv[0].bs && st2)) {
+    int rc = chol_run(MODE_D, a, lv, nl, 0, base, d_info, st);
+    return rc ? rc : trsm_rec(MODE_D, 1.0, a, x, kc, nullptr, d_info, st);
+  }
+  const int64_t ns = (a.n + lv[0].bs - 1) / lv[0].bs;
+  std::vector<cudaEvent_t> ev(static_cast<size_t>(ns) + 1);
+  for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  cudaEventRecord(ev[size_t(ns)], st);  // X initialised, the block converted
+  cudaStreamWaitEvent(st2, ev[size_t(ns)], 0);
+  int rc = chol_v3_events(MODE_D, a, lv, nl, 0, base, d_info, st, ev.data());
+  if (rc == BF_OK) {
+    TriWait w{ev.data(), lv[0].bs, ns};
+    rc = trsm_rec_w(MODE_D, 1.0, a, x, kc, d_info, st2, w, 0);
+  }
+  cudaEventRecord(ev[size_t(ns)], st2);
+  cudaStreamWaitEvent(st, ev[size_t(ns)], 0);
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
 // bridges for the other translation units (dist.cu)
 int gemm_d_limited(double alpha, const bf_view& a, const bf_view& b, double beta, const bf_view& c, int lower_only,
                    int64_t kc, const int* d_abort, int64_t abort_limit, cudaStream_t s) {

@@ -396,6 +396,13 @@ int g_mixed_reserve = 32;  // bf_set_option("mixed_reserve", r): SMs the trailin
 
 }  // namespace bf
 
+namespace bf {
+// capi.cu: the FP64 diagonal factor with X L^T = X solved on a second stream,
+// trailing the factor's inner steps
+int chol_inverse_overlapped(const bf_view& a, const bf_chol_level* lv, int nl, int64_t base, const bf_view& x,
+                            int64_t kc, int* d_info, cudaStream_t st);
+}  // namespace bf
+
 extern "C" {
 // bf_cholesky_mixed: see include/blockfam_b200.h
 int bf_cholesky_mixed(const bf_view* a, float* w, int64_t ldw, void* pbuf0, void* pbuf1, void* xt, double* d64,
@@ -428,15 +435,14 @@ int bf_cholesky_mixed(const bf_view* a, float* w, int64_t ldw, void* pbuf0, void
     int e = launch_f32_to_f64(d32, 0, ldw, 1, d64, 0, bs, 1, b, b, 1, st);
     if (e) return ck(e, "convert diagonal block");
     bf_view dd{d64, 0, b, b, bs, 1};
-    e = bf_cholesky_ex_d(&dd, lv, nl, k0, d_info, st);
-    if (e) return e;
-    e = launch_f64_to_f32(d64, 0, bs, 1, d32, 0, ldw, 1, b, b, 1, st);
-    if (e) return ck(e, "convert diagonal block");
     note_launch();
     set_identity_kernel<<<64, 256, 0, st>>>(x64, bs, b);
     bf_view xv{x64, 0, b, b, bs, 1};
-    e = bf_trsm_rltn_ex_d(1.0, &dd, &xv, 512, nullptr, d_info, st);  // X L11^T = I
+    // the FP64 factor and X L11^T = I, the solve trailing the factor's inner steps
+    e = chol_inverse_overlapped(dd, lv, nl, k0, xv, 512, d_info, st);
     if (e) return e;
+    e = launch_f64_to_f32(d64, 0, bs, 1, d32, 0, ldw, 1, b, b, 1, st);
+    if (e) return ck(e, "convert diagonal block");
     e = launch_f64_to_f32(x64, 0, bs, 1, xinv + k * bs * bs, 0, bs, 1, b, b, 0, st);
     if (e) return ck(e, "convert inverse");
     if (r == 0) return BF_OK;

@@ -587,6 +587,10 @@ cudaEvent_t g_tl_origin = nullptr;
 // TRSM of the rows below) runs its TRSM on a second stream, trailing the
 // diagonal factor's inner steps (TriWait) instead of waiting for all of it
 int g_panel_overlap = 1;
+// bf_set_option("panel_chunks", c) / ("panel_chunk_rows", r): the overlapped
+// panel's rows below in up to c row chunks of at least r rows, one stream each
+int g_panel_chunks = 2;  // 1: 370.9, 2: 369.6, 4: 369.6 ms (C2, tools/gpu_r02_chunks.sh)
+int64_t g_panel_chunk_rows = 6144;
 
 // chol_run's variant-3 body for node lv[idx] on `a` (children from idx+1),
 // recording ev[j] on st once inner step j's column block is final (after its
@@ -618,45 +622,69 @@ int chol_v3_events(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl,
 // exactly as the sequential panel does; on success every element of the
 // panel saw the sequential panel's operations.  Returns with `st` joined.
 int panel_overlap(Mode mode, const bf_view& a11, const bf_view& a21, const bf_chol_level* lv, int nl, int64_t base,
-                  int* d_info, cudaStream_t st, cudaStream_t st2, cudaEvent_t* diag_mark) {
+                  int* d_info, cudaStream_t st, cudaStream_t key, cudaEvent_t* diag_mark) {
   const bf_chol_level& in = lv[1];
   const int64_t b = a11.n, bs1 = in.bs, m = a21.m;
   const int64_t ns = (b + bs1 - 1) / bs1;
-  std::vector<cudaEvent_t> ev(static_cast<size_t>(ns) + 1);
+  // the rows below in up to g_panel_chunks independent row chunks, each on its
+  // own stream: the TRSM's many small launches of one chunk overlap the others'
+  int64_t nch = g_panel_chunks > 0 ? g_panel_chunks : 1;
+  if (nch > m / g_panel_chunk_rows) nch = m / g_panel_chunk_rows;
+  if (nch < 1) nch = 1;
+  if (nch > 8) nch = 8;
+  std::vector<cudaStream_t> cs(static_cast<size_t>(nch));
+  for (int64_t c = 0; c < nch; ++c) {
+    cs[size_t(c)] = side_stream(SideRole(ROLE_PANEL2 + c), key);
+    if (!cs[size_t(c)]) return -1;
+  }
+  std::vector<cudaEvent_t> ev(static_cast<size_t>(ns) + 1), evj(static_cast<size_t>(nch));
   for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  cudaEventRecord(ev[size_t(ns)], st);  // the rows below are ready (st's earlier work)
-  cudaStreamWaitEvent(st2, ev[size_t(ns)], 0);
-  // (after st2 joined st: under CUDA-graph capture the scratch is then allocated as graph-owned)
-  double* x = static_cast<double*>(bf::stream_scratch(7, size_t(m) * size_t(b) * sizeof(double), st2));
-  if (!x) {  // no room: the caller runs the sequential panel
-    cudaEventRecord(ev[size_t(ns)], st2);
-    cudaStreamWaitEvent(st, ev[size_t(ns)], 0);
+  for (auto& e : evj) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  auto join = [&]() {
+    for (int64_t c = 0; c < nch; ++c) {
+      cudaEventRecord(evj[size_t(c)], cs[size_t(c)]);
+      cudaStreamWaitEvent(st, evj[size_t(c)], 0);
+    }
     for (auto& e : ev) cudaEventDestroy(e);
+    for (auto& e : evj) cudaEventDestroy(e);
+  };
+  cudaEventRecord(ev[size_t(ns)], st);  // the rows below are ready (st's earlier work)
+  for (auto c : cs) cudaStreamWaitEvent(c, ev[size_t(ns)], 0);
+  // (after the chunk streams joined st: under CUDA-graph capture the scratch is then graph-owned)
+  double* x = static_cast<double*>(bf::stream_scratch(7, size_t(m) * size_t(b) * sizeof(double), cs[0]));
+  if (!x) {  // no room: the caller runs the sequential panel
+    join();
     return -1;
   }
+  const int64_t per = (m + nch - 1) / nch;
   const double* src = static_cast<const double*>(a21.base) + a21.off;
-  int rc = cudaMemcpy2DAsync(x, size_t(b) * sizeof(double), src, size_t(a21.rs) * sizeof(double),
-                             size_t(b) * sizeof(double), size_t(m), cudaMemcpyDeviceToDevice, st2) == cudaSuccess
-               ? BF_OK
-               : fail(BF_ERR_CUDA, "panel copy failed");
+  int rc = BF_OK;
+  for (int64_t c = 0; c < nch && rc == BF_OK; ++c) {
+    const int64_t r0 = c * per, rn = per < m - r0 ? per : m - r0;
+    if (rn > 0 && cudaMemcpy2DAsync(x + r0 * b, size_t(b) * sizeof(double), src + r0 * a21.rs,
+                                    size_t(a21.rs) * sizeof(double), size_t(b) * sizeof(double), size_t(rn),
+                                    cudaMemcpyDeviceToDevice, cs[size_t(c)]) != cudaSuccess)
+      rc = fail(BF_ERR_CUDA, "panel copy failed");
+  }
   // the diagonal block: chol_run's v3 body for lv[1] (children from lv[2])
   if (rc == BF_OK) rc = chol_v3_events(mode, a11, lv, nl, 1, base, d_info, st, ev.data());
   if (diag_mark) {
     cudaEventCreate(diag_mark);
     cudaEventRecord(*diag_mark, st);
   }
-  if (rc == BF_OK) {
+  for (int64_t c = 0; c < nch && rc == BF_OK; ++c) {
+    const int64_t r0 = c * per, rn = per < m - r0 ? per : m - r0;
+    if (rn <= 0) continue;
+    cudaStream_t sc = cs[size_t(c)];
     TriWait w{ev.data(), bs1, ns};
-    bf_view xv{x, 0, m, b, b, 1};
-    rc = trsm_rec_w(mode, 1.0, a11, xv, lv[0].kc, d_info, st2, w, 0);
-    w.wait(b, st2);  // the whole diagonal factor (its flag) before the copy back
-    if (!rc && bf::launch_copy2d_unless_aborted(x, b, static_cast<double*>(a21.base) + a21.off, a21.rs, m, b, d_info,
-                                                st2))
+    bf_view xv{x + r0 * b, 0, rn, b, b, 1};
+    rc = trsm_rec_w(mode, 1.0, a11, xv, lv[0].kc, d_info, sc, w, 0);
+    w.wait(b, sc);  // the whole diagonal factor (its flag) before the copy back
+    if (!rc && bf::launch_copy2d_unless_aborted(x + r0 * b, b, static_cast<double*>(a21.base) + a21.off + r0 * a21.rs,
+                                                a21.rs, rn, b, d_info, sc))
       rc = fail(BF_ERR_CUDA, "panel copy launch failed");
   }
-  cudaEventRecord(ev[size_t(ns)], st2);
-  cudaStreamWaitEvent(st, ev[size_t(ns)], 0);
-  for (auto& e : ev) cudaEventDestroy(e);
+  join();
   return rc;
 }
 
@@ -674,11 +702,8 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     bf_view a21 = subview(a, done + b, n - done - b, done, b);
     if (g_panel_overlap && mode == MODE_D && nl >= 2 && lv[1].variant == 3 && lv[1].bs >= 1 && b > lv[1].bs &&
         a21.m > 0 && a.cs == 1) {
-      cudaStream_t st2 = panel2_stream(s);
-      if (st2) {
-        const int prc = panel_overlap(mode, a11, a21, lv, nl, base + done, d_info, st, st2, diag_mark);
-        if (prc != -1) return prc;
-      }
+      const int prc = panel_overlap(mode, a11, a21, lv, nl, base + done, d_info, st, s, diag_mark);
+      if (prc != -1) return prc;
     }
     int rc = chol_run(mode, a11, lv, nl, 1, base + done, d_info, st);
     if (diag_mark) {
@@ -1215,6 +1240,14 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "panel_tiles") == 0 && value >= 0 && value < (1 << 16)) {
     g_panel_tiles = int(value);
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "panel_chunks") == 0 && value >= 1 && value <= 8) {
+    g_panel_chunks = int(value);
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "panel_chunk_rows") == 0 && value >= 1) {
+    g_panel_chunk_rows = value;
     return BF_OK;
   }
   if (name && std::strcmp(name, "panel_overlap") == 0) {

@@ -275,7 +275,9 @@ int bf_apply_pivots_s(const bf_view* a, const int64_t* d_piv, int64_t count, int
  * bf_gemm_bf16: C(fp32 view) := beta*C + alpha * A * B^T on tcgen05/TMEM, with
  * A (c->m x k) and B (c->n x k) row-major bf16 (ld in elements, 16-byte aligned).
  * bf_convert_*: precision conversions between views / dense buffers.
- * bf_residual_d: r := b - A x for a dense row-major fp64 A (n x n).
+ * bf_residual_d: r := b - A x for a dense row-major fp64 A (n x n) that is
+ * symmetric (the SPD matrix of the mixed solve): only its lower triangle is
+ * read (bf_set_option("symv", 0): the whole matrix, row by row).
  * bf_potrs_f32_d: x := (L L^T)^-1 x for the fp32 lower factor L (row-major ld),
  * fp64 right-hand side and arithmetic (one CTA per diagonal block: reference-grade, slow).
  * bf_potrs_blocked_f32_d: the same solve as matrix-vector products against the
@@ -320,7 +322,8 @@ int bf_cholesky_mixed(const bf_view* a, float* w, int64_t ldw, void* pbuf0, void
 int bf_convert_f32_f64(const bf_view* src, const bf_view* dst, int lower_only, void* stream);
 int bf_convert_f64_bf16(const bf_view* src, void* dst, int64_t ld, int transpose, void* stream);
 int bf_residual_d(const double* a, int64_t lda, const double* x, const double* b, double* r, int64_t n, void* stream);
-/* out[i] := sum_j |a[i][j]| (the refinement's ||A||_inf is the max of these) */
+/* out[i] := sum_j |a[i][j]| (the refinement's ||A||_inf is the max of these);
+ * a symmetric, read through its lower triangle like bf_residual_d */
 int bf_row_abs_sum_d(const double* a, int64_t lda, double* out, int64_t n, void* stream);
 int bf_potrs_f32_d(const float* l, int64_t ld, double* x, int64_t n, void* stream);
 int bf_potrs_blocked_f32_d(const float* l, int64_t ld, const float* xinv, int64_t bs, double* x, int64_t n,

@@ -129,6 +129,8 @@ void scratch_account(int64_t delta_bytes);  // every library-owned device buffer
 int set_error(int code, const char* msg);
 cudaStream_t panel_stream_for(cudaStream_t caller);  // the high-priority panel stream paired with `caller`
 extern int g_mixed_reserve;
+extern int g_symv;        // mixed.cu: residual / row sums from the lower triangle of A
+extern int g_potrs_coop;  // mixed.cu: the refinement solve as one cooperative kernel
 int launch_axpby_f32_f64(double alpha, const float* src, int64_t ld, double beta, double* c, int64_t off, int64_t rs,
                          int64_t cs, int64_t m, int64_t n, cudaStream_t s);
 

@@ -1242,6 +1242,14 @@ int bf_set_option(const char* name, int64_t value) {
     g_panel_tiles = int(value);
     return BF_OK;
   }
+  if (name && std::strcmp(name, "symv") == 0) {
+    bf::g_symv = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "potrs_coop") == 0) {
+    bf::g_potrs_coop = value != 0;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "panel_chunks") == 0 && value >= 1 && value <= 8) {
     g_panel_chunks = int(value);
     return BF_OK;

@@ -4,6 +4,9 @@
 // All memory-bound; they stream the matrix once per call.
 #include "bf_common.cuh"
 #include "bf_internal.h"
+
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 #include "blockfam_b200.h"
 
 #include <cuda_bf16.h>
@@ -38,6 +41,88 @@ __global__ void residual_kernel(const double* A, int64_t lda, const double* x, c
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) r[row] = b[row] - s;
+}
+
+// Symmetric A (full storage, SPD input of the solve): y = A x from the lower
+// triangle only — half the HBM traffic of the row-by-row GEMV.  One CTA per
+// 128 x 128 lower tile (I >= J): its row sums A_IJ x_J feed y_I, its column
+// sums A_IJ^T x_I feed y_J (strictly lower part on a diagonal tile); the
+// per-tile partials are summed per row by symv_reduce_kernel (fixed order).
+// ABS: |A| times the ones vector, i.e. the row sums of |A| (the infinity norm).
+constexpr int SY_T = 128;
+template <bool ABS>
+__global__ void __launch_bounds__(256) symv_tiles_kernel(const double* __restrict__ A, int64_t lda,
+                                                          const double* __restrict__ x, int64_t n,
+                                                          double* part_row, double* part_col) {
+  __shared__ double xj[SY_T], xi[SY_T], colbuf[8][SY_T];
+  const int64_t p = blockIdx.x;
+  int64_t I = int64_t((sqrt(8.0 * double(p) + 1.0) - 1.0) * 0.5);
+  while (I * (I + 1) / 2 > p) --I;
+  while ((I + 1) * (I + 2) / 2 <= p) ++I;
+  const int64_t J = p - I * (I + 1) / 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t i0 = I * SY_T, j0 = J * SY_T;
+  if (tid < SY_T) {
+    xj[tid] = j0 + tid < n ? (ABS ? 1.0 : x[j0 + tid]) : 0.0;
+    xi[tid] = i0 + tid < n ? (ABS ? 1.0 : x[i0 + tid]) : 0.0;
+  }
+  __syncthreads();
+  const bool diag = I == J;
+  double cacc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int jl[4] = {2 * lane, 2 * lane + 1, 64 + 2 * lane, 65 + 2 * lane};
+  for (int il = warp; il < SY_T; il += 8) {
+    const int64_t gi = i0 + il;
+    if (gi >= n) break;
+    const double* row = A + gi * lda + j0;
+    double av[4];
+    const bool in0 = j0 + jl[0] < n, in2 = j0 + jl[2] < n;  // pairs of columns: n even
+    if (in0) {
+      const double2 q = *reinterpret_cast<const double2*>(row + jl[0]);
+      av[0] = q.x;
+      av[1] = q.y;
+    } else {
+      av[0] = av[1] = 0.0;
+    }
+    if (in2) {
+      const double2 q = *reinterpret_cast<const double2*>(row + jl[2]);
+      av[2] = q.x;
+      av[3] = q.y;
+    } else {
+      av[2] = av[3] = 0.0;
+    }
+    double rs = 0.0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double a = ABS ? fabs(av[e]) : av[e];
+      if (!diag || jl[e] <= il) rs = fma(a, xj[jl[e]], rs);
+      if (!diag || jl[e] < il) cacc[e] = fma(a, xi[il], cacc[e]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+    if (lane == 0) part_row[p * SY_T + il] = rs;
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) colbuf[warp][jl[e]] = cacc[e];
+  __syncthreads();
+  if (tid < SY_T) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += colbuf[w][tid];
+    part_col[p * SY_T + tid] = t;
+  }
+}
+
+// y_i = sum_{J <= I} row partial (I, J) + sum_{I' >= I} column partial (I', I);
+// out_i = base_i - y_i (residual) or y_i (base == nullptr)
+__global__ void symv_reduce_kernel(const double* part_row, const double* part_col, int64_t n, const double* base,
+                                   double* out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t I = i / SY_T, il = i % SY_T, nt = (n + SY_T - 1) / SY_T;
+  double y = 0.0;
+  for (int64_t J = 0; J <= I; ++J) y += part_row[(I * (I + 1) / 2 + J) * SY_T + il];
+  for (int64_t Ip = I; Ip < nt; ++Ip) y += part_col[(Ip * (Ip + 1) / 2 + I) * SY_T + il];
+  out[i] = base ? base[i] - y : y;
 }
 
 // out[row] = sum_j |A[row][j]| (one warp per row); the host takes the max
@@ -243,10 +328,29 @@ int launch_f32_to_f64(const float* src, int64_t soff, int64_t srs, int64_t scs, 
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
+int g_symv = 1;  // bf_set_option("symv", 0|1): residual and row sums from the lower triangle of (symmetric) A
+
+// the lower-triangle SYMV: partials in library scratch (2 x 128 doubles per tile pair)
+static int launch_symv(const double* A, int64_t lda, const double* x, int64_t n, const double* base, double* out,
+                       bool abs_ones, cudaStream_t s) {
+  const int64_t nt = (n + SY_T - 1) / SY_T, pairs = nt * (nt + 1) / 2;
+  if (pairs > 0x7fffffffLL || n % 2) return -3;
+  double* part = static_cast<double*>(stream_scratch(8, size_t(pairs) * 2 * SY_T * sizeof(double), s));
+  if (!part) return -3;
+  note_launch(2);
+  if (abs_ones)
+    symv_tiles_kernel<true><<<unsigned(pairs), 256, 0, s>>>(A, lda, nullptr, n, part, part + pairs * SY_T);
+  else
+    symv_tiles_kernel<false><<<unsigned(pairs), 256, 0, s>>>(A, lda, x, n, part, part + pairs * SY_T);
+  symv_reduce_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(part, part + pairs * SY_T, n, base, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
+}
+
 int launch_residual(const double* A, int64_t lda, const double* x, const double* b, double* r, int64_t n,
                     cudaStream_t s) {
   if (n <= 0) return 0;
   if ((reinterpret_cast<uintptr_t>(A) % 16) || (lda % 2)) return -3;
+  if (g_symv && launch_symv(A, lda, x, n, b, r, false, s) == 0) return 0;
   note_launch();
   residual_kernel<<<unsigned((n * 32 + 255) / 256), 256, 0, s>>>(A, lda, x, b, r, n);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
@@ -255,6 +359,7 @@ int launch_residual(const double* A, int64_t lda, const double* x, const double*
 int launch_row_abs_sum(const double* A, int64_t lda, double* out, int64_t n, cudaStream_t s) {
   if (n <= 0) return 0;
   if ((reinterpret_cast<uintptr_t>(A) % 16) || (lda % 2)) return -3;
+  if (g_symv && launch_symv(A, lda, nullptr, n, nullptr, out, true, s) == 0) return 0;
   note_launch();
   row_abs_sum_kernel<<<unsigned((n * 32 + 255) / 256), 256, 0, s>>>(A, lda, out, n);
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
@@ -285,6 +390,107 @@ int launch_potrs_f32_f64(const float* L, int64_t ld, double* x, int64_t n, cudaS
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
+// The same blocked solve as ONE cooperative kernel (grid of <= 128 CTAs, three
+// grid barriers per block) instead of ~4 launches per block and sweep: the
+// refinement's solve is a chain of 2 * n / bs dependent matrix-vector
+// products, so the launch latencies, not the 4 GB of L it streams, were its
+// cost (2.4 ms at n = 32768).  Same products in a different summation order.
+constexpr int PC_THREADS = 512;
+__global__ void __launch_bounds__(PC_THREADS, 1)
+    potrs_coop_kernel(const float* __restrict__ L, int64_t ld, const float* __restrict__ xinv, int64_t bs,
+                      double* x, int64_t n, double* partial, double* tv) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sv[1024];
+  const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int64_t gwarp = int64_t(c) * (PC_THREADS / 32) + warp, nwarps = int64_t(G) * (PC_THREADS / 32);
+  const int64_t gtid = int64_t(c) * PC_THREADS + tid;
+  const int64_t nblk = (n + bs - 1) / bs;
+  // warp-per-row dot product of a fp32 row with the smem vector sv
+  auto row_dot = [&](const float* row, int b) {
+    double s0 = 0.0, s1 = 0.0;
+    int j = lane * 2;
+    for (; j + 1 < b; j += 64) {
+      const float2 q = *reinterpret_cast<const float2*>(row + j);
+      s0 = fma(double(q.x), sv[j], s0);
+      s1 = fma(double(q.y), sv[j + 1], s1);
+    }
+    if (j < b) s0 = fma(double(row[j]), sv[j], s0);
+    double t = s0 + s1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    return t;
+  };
+  // forward: y_k = X_k^T r_k; r[k+1:] -= L[k+1:, k] y_k   (x holds r, then y)
+  for (int64_t k = 0; k < nblk; ++k) {
+    const int64_t k0 = k * bs, k1 = k0 + bs < n ? k0 + bs : n;
+    const int b = int(k1 - k0);
+    const float* X = xinv + k * bs * bs;
+    {  // partial[c][j] = sum over this CTA's rows i of X[i][j] r[k0+i]
+      const int per = (b + G - 1) / G, i0 = c * per, i1 = i0 + per < b ? i0 + per : b;
+      for (int j = tid; j < b; j += PC_THREADS) {
+        double acc = 0.0;
+        for (int i = i0; i < i1; ++i) acc = fma(double(X[int64_t(i) * bs + j]), x[k0 + i], acc);
+        partial[int64_t(c) * bs + j] = acc;
+      }
+    }
+    grid.sync();
+    if (gtid < b) {
+      double y = 0.0;
+      for (int q = 0; q < G; ++q) y += partial[int64_t(q) * bs + gtid];
+      tv[gtid] = y;
+    }
+    grid.sync();
+    for (int j = tid; j < b; j += PC_THREADS) sv[j] = tv[j];
+    __syncthreads();
+    if (c == 0)
+      for (int j = tid; j < b; j += PC_THREADS) x[k0 + j] = sv[j];
+    for (int64_t row = k1 + gwarp; row < n; row += nwarps) {
+      const double t = row_dot(L + row * ld + k0, b);
+      if (lane == 0) x[row] -= t;
+    }
+    grid.sync();
+  }
+  // backward: x_k = X_k (y_k - L[k+1:, k]^T x[k+1:])
+  for (int64_t k = nblk - 1; k >= 0; --k) {
+    const int64_t k0 = k * bs, k1 = k0 + bs < n ? k0 + bs : n;
+    const int b = int(k1 - k0);
+    const float* X = xinv + k * bs * bs;
+    {  // partial[c][j] = sum over this CTA's rows r >= k1 of L[r][k0+j] x[r]
+      const int64_t rows = n - k1, per = (rows + G - 1) / G, r0 = k1 + c * per;
+      const int64_t r1 = r0 + per < n ? r0 + per : n;
+      for (int j = tid; j < b; j += PC_THREADS) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // four chains: loads in flight
+        int64_t r = r0;
+        for (; r + 3 < r1; r += 4) {
+          a0 = fma(double(L[r * ld + k0 + j]), x[r], a0);
+          a1 = fma(double(L[(r + 1) * ld + k0 + j]), x[r + 1], a1);
+          a2 = fma(double(L[(r + 2) * ld + k0 + j]), x[r + 2], a2);
+          a3 = fma(double(L[(r + 3) * ld + k0 + j]), x[r + 3], a3);
+        }
+        for (; r < r1; ++r) a0 = fma(double(L[r * ld + k0 + j]), x[r], a0);
+        partial[int64_t(c) * bs + j] = (a0 + a1) + (a2 + a3);
+      }
+    }
+    grid.sync();
+    if (gtid < b) {
+      double t = 0.0;
+      for (int q = 0; q < G; ++q) t += partial[int64_t(q) * bs + gtid];
+      tv[gtid] = x[k0 + gtid] - t;
+    }
+    grid.sync();
+    for (int j = tid; j < b; j += PC_THREADS) sv[j] = tv[j];
+    __syncthreads();
+    for (int64_t i = gwarp; i < b; i += nwarps) {
+      const double t = row_dot(X + i * bs, b);
+      if (lane == 0) x[k0 + i] = t;
+    }
+    grid.sync();
+  }
+}
+
+int g_potrs_coop = 1;  // bf_set_option("potrs_coop", 0|1): the refinement solve as one cooperative kernel
+
 // Blocked solve with the explicit inverses X_k = L_kk^-T of the diagonal
 // blocks (xinv: nblk x bs x bs fp32, X_k row-major ld bs). Every step is a
 // matrix-vector product streaming its block of L once, shaped so that the
@@ -296,6 +502,23 @@ int launch_potrs_blocked(const float* L, int64_t ld, const float* xinv, int64_t 
                          double* work, cudaStream_t s) {
   double* t = work;
   double* partial = work + bs;
+  if (g_potrs_coop && bs <= 1024 && ld % 2 == 0 && bs % 2 == 0 && reinterpret_cast<uintptr_t>(L) % 8 == 0 &&
+      reinterpret_cast<uintptr_t>(xinv) % 8 == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, potrs_coop_kernel, PC_THREADS, 0);
+    int G = sms * (per_sm > 0 ? 1 : 0);
+    if (G > kPotrsMaxChunks) G = kPotrsMaxChunks;  // partial rows the work buffer holds
+    if (G >= 1) {
+      void* args[] = {(void*)&L, (void*)&ld, (void*)&xinv, (void*)&bs, (void*)&x, (void*)&n, (void*)&partial, (void*)&t};
+      note_launch();
+      if (cudaLaunchCooperativeKernel(reinterpret_cast<void*>(potrs_coop_kernel), dim3(G), dim3(PC_THREADS), args, 0,
+                                      s) == cudaSuccess)
+        return 0;
+      cudaGetLastError();  // fall back to the launch-per-product form
+    }
+  }
   const bool vec_ok = (reinterpret_cast<uintptr_t>(L) % 16 == 0) && ld % 4 == 0 && bs % 4 == 0 &&
                       (reinterpret_cast<uintptr_t>(xinv) % 16 == 0);
   auto gemv_t = [&](const float* A, int64_t lda, int64_t rows, int cols, const double* v, bool vec) -> int {

@@ -82,6 +82,35 @@ def test_bf16_gemm_rejects_unaligned_leading_dim(cuda):
     assert rc != 0 and b"aligned" in lib.bf_last_error()
 
 
+@pytest.mark.parametrize("symv", [1, 0])
+@pytest.mark.parametrize("n", [1000, 258, 4096])
+def test_residual_and_row_sums_vs_torch(cuda, n, symv):
+    """The refinement's residual r = b - A x and |A| row sums: from the lower
+    triangle of the symmetric A (per-tile partials, option "symv") or row by
+    row, both against a torch fp64 reference to rounding."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n)
+    m = torch.rand(n, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    a = m + m.T
+    x = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    b = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+    r = torch.empty_like(b)
+    rows = torch.empty_like(b)
+    lib = _lib.lib()
+    st = torch.cuda.current_stream().cuda_stream
+    try:
+        lib.bf_set_option(b"symv", symv)
+        _lib.check(lib.bf_residual_d(a.data_ptr(), n, x.data_ptr(), b.data_ptr(), r.data_ptr(), n, st), "residual")
+        _lib.check(lib.bf_row_abs_sum_d(a.data_ptr(), n, rows.data_ptr(), n, st), "row sums")
+    finally:
+        lib.bf_set_option(b"symv", 1)
+    ref_r = b - a @ x
+    scale = (a.abs() @ x.abs()).max().item()
+    assert (r - ref_r).abs().max().item() <= 8 * n * 2.0 ** -53 * scale
+    ref_rows = a.abs().sum(1)
+    assert (rows - ref_rows).abs().max().item() <= 8 * n * 2.0 ** -53 * ref_rows.max().item()
+
+
 @pytest.mark.parametrize("precision", ["bf16", "tf32"])
 @pytest.mark.parametrize("n,bs,lookahead", [(1000, 256, True), (3000, 1024, True), (2100, 512, False)])
 def test_mixed_solve_reaches_fp64_accuracy(cuda, n, bs, lookahead, precision):

@@ -137,6 +137,11 @@ struct bf_dist {
   int reserve = -1;  // SMs left to the panel stream by the rest-of-update GEMMs (-1: adaptive)
   int lookahead = 1;
   int grouped = 1;  // one grouped TMA launch per update part (0: one GEMM per column panel, fan streams)
+  // the grouped rest-of-update keeps its SM reservation (a persistent grid)
+  // only while this rank's stacked rows are <= reserve_rows: over a larger
+  // trailing matrix a persistent grid loses L2 locality (n=131072 on one GPU:
+  // 22.7 s reserved vs 22.1 s), as the one-GPU driver's tail_rows rule found
+  int64_t reserve_rows = 32768;
   // group tables of the grouped launches: pinned host staging and the device
   // copy, one region per launch of a factorization (no reuse within a call;
   // the call waits for completion before returning)
@@ -260,7 +265,7 @@ struct NcclExec {
     ob.base = d->bufs;
     ob.s_mn = k;
     ob.s_k = 1;
-    if (reserve && reserve_now > 0) bf::t_reserve_sms = reserve_now;
+    if (reserve && reserve_now > 0 && arows <= d->reserve_rows) bf::t_reserve_sms = reserve_now;
     const int rc = bf::launch_gemm_dmma_grouped(p, oa, arows, ob, brows, dev, ng, tiles, s);
     bf::t_reserve_sms = 0;
     if (rc == -3) return bf::set_error(BF_ERR_UNSUPPORTED, "grouped update: unsupported shape");
@@ -363,6 +368,7 @@ int bf_dist_set_option(bf_dist* d, const char* name, int64_t value) {
   else if (!std::strcmp(name, "fan")) d->nfan = int(value < 0 ? 0 : (value > 3 ? 3 : value));
   else if (!std::strcmp(name, "lookahead")) d->lookahead = int(value != 0);
   else if (!std::strcmp(name, "grouped")) d->grouped = int(value != 0);
+  else if (!std::strcmp(name, "reserve_rows")) d->reserve_rows = value;
   else return bf::set_error(BF_ERR_VALUE, "unknown dist option");
   return BF_OK;
 }

@@ -95,7 +95,17 @@ const char* bf_last_error(void);
  * rows; "reserve_strided" its tile order; "diag_reserve" / "diag_rows" an
  * optional two-phase split of that update (off); "red_fold" (default 1) folds
  * the TMA GEMM's beta == 1 segments as red.global.add.f64 L2 reductions (0:
- * load/add/store); "persist" a strided one-CTA-per-SM grid for long-K GEMMs (off). */
+ * load/add/store); "persist" a strided one-CTA-per-SM grid for long-K GEMMs (off);
+ * "tma_bn" (default 64) runs plain TMA DMMA launches on two independent
+ * 8-warp groups per CTA over 128x64 tiles (128: one 16-warp group on 128x128
+ * tiles; "tmc_bn64" extends it to the TMEM-fold launches, off); "panel_overlap"
+ * (default 1) lets a lookahead panel's TRSM of the rows below trail its
+ * diagonal factor's inner steps on its own streams ("panel_chunks" row chunks
+ * of at least "panel_chunk_rows" rows, defaults 2 and 6144), on a copy written
+ * back only without a pivot failure; "reserve_adaptive" / "reserve_extra" /
+ * "reserve_min" size the reservation per step; "potrs_coop" (default 1) and
+ * "symv" (default 1) select the mixed refinement's cooperative blocked solve
+ * and lower-triangle residual. */
 int bf_set_option(const char* name, int64_t value);
 int bf_device_sm_count(void);
 /* With bf_set_option("timeline", 1): per top-level step of the last lookahead
@@ -346,7 +356,11 @@ int bf_dist_unique_id_bytes(void);           /* sizeof(ncclUniqueId) */
 int bf_dist_unique_id(void* out);            /* ncclGetUniqueId (rank 0), to be shared with every rank */
 /* world communicator from the id, then ncclCommSplit into row / column communicators */
 int bf_dist_init(const void* nccl_unique_id, int rank, int nranks, int pr, int pc, bf_dist** out);
-int bf_dist_set_option(bf_dist* d, const char* name, int64_t value); /* "reserve", "fan", "lookahead" */
+/* "reserve" (-1 = adaptive), "fan", "lookahead", "grouped" (1: every
+ * trailing-update part as one grouped TMA launch over the column panels),
+ * "reserve_rows" (the grouped launch keeps its SM reservation while the
+ * rank's stacked rows are <= this, default 32768) */
+int bf_dist_set_option(bf_dist* d, const char* name, int64_t value);
 int bf_dist_finalize(bf_dist* d);
 int64_t bf_dist_local_elems(int64_t n, int64_t nb, int pr, int pc, int rank);            /* host only */
 int64_t bf_dist_panel_offset(int64_t n, int64_t nb, int pr, int pc, int rank, int64_t q); /* host only */

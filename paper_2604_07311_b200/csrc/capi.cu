@@ -622,7 +622,7 @@ int chol_v3_events(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl,
 // exactly as the sequential panel does; on success every element of the
 // panel saw the sequential panel's operations.  Returns with `st` joined.
 int panel_overlap(Mode mode, const bf_view& a11, const bf_view& a21, const bf_chol_level* lv, int nl, int64_t base,
-                  int* d_info, cudaStream_t st, cudaStream_t key, cudaEvent_t* diag_mark) {
+                  int* d_info, cudaStream_t st, cudaStream_t key, cudaEvent_t* diag_mark, cudaEvent_t rows_ready) {
   const bf_chol_level& in = lv[1];
   const int64_t b = a11.n, bs1 = in.bs, m = a21.m;
   const int64_t ns = (b + bs1 - 1) / bs1;
@@ -648,8 +648,11 @@ int panel_overlap(Mode mode, const bf_view& a11, const bf_view& a21, const bf_ch
     for (auto& e : ev) cudaEventDestroy(e);
     for (auto& e : evj) cudaEventDestroy(e);
   };
-  cudaEventRecord(ev[size_t(ns)], st);  // the rows below are ready (st's earlier work)
-  for (auto c : cs) cudaStreamWaitEvent(c, ev[size_t(ns)], 0);
+  cudaEventRecord(ev[size_t(ns)], st);  // the rows below are ready (st's earlier work ...
+  for (auto c : cs) {
+    cudaStreamWaitEvent(c, ev[size_t(ns)], 0);
+    if (rows_ready) cudaStreamWaitEvent(c, rows_ready, 0);  // ... and, early panels, the rest of their column update)
+  }
   // (after the chunk streams joined st: under CUDA-graph capture the scratch is then graph-owned)
   double* x = static_cast<double*>(bf::stream_scratch(7, size_t(m) * size_t(b) * sizeof(double), cs[0]));
   if (!x) {  // no room: the caller runs the sequential panel
@@ -688,21 +691,54 @@ int panel_overlap(Mode mode, const bf_view& a11, const bf_view& a21, const bf_ch
   return rc;
 }
 
+// bf_set_option("early_panel", 0|1|2|3): start panel k+1's diagonal factor once
+// the diagonal tile of block column k+1 is updated (see the lookahead loop);
+// 2 also reserves SMs for it during the rest of that column's update, 3 also
+// at step 0.  n=32768 (tools/gpu_r02_early.sh): 0: 369.6 ms, 1: 367.5-367.9,
+// 2: 371.9 (the reserved column update falls behind), 3: 367.9
+int g_early_panel = 1;
+
+// Size the reservation to the work the panel stream has to finish under the
+// rest of step k's update: panel k+1's TRSM (m rows x b2^2) and diagonal
+// factor (b2^3 / 3) against the rest of the trailing GEMMT (m^2 b): their SM
+// shares, plus a few SMs for the latency-bound diagonal chain (n=32768: 376.4
+// ms with a fixed 16, 375.2 ms adaptive; the exposed panel chain drops 22.8 ->
+// 15.6 ms, tools/gpu_r02_reserve.sh).  0 when the update is too large for a
+// persistent grid (tail_rows) or reservations are off.
+int adaptive_reserve(int64_t m, int64_t b2, int64_t b) {
+  if (!(g_tail_reserve > 0 && m <= g_tail_rows)) return 0;
+  if (!g_reserve_adaptive) return g_tail_reserve;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const double T = double(m) * b2 * b2 + double(b2) * b2 * b2 / 3.0, S = double(m) * m * b;
+  int R = int(sms * T / (T + S) + 0.5) + g_reserve_extra;
+  if (R < g_reserve_min) R = g_reserve_min;
+  if (R > sms / 2) R = sms / 2;
+  return R;
+}
+
 int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int64_t base, int* d_info,
                       cudaStream_t s) {
   const int64_t n = a.n, bs = lv[0].bs, kc = lv[0].kc;
   cudaStream_t ps = panel_stream(s);
   if (!ps) return fail(BF_ERR_CUDA, "cannot create the panel stream");
-  cudaEvent_t ev_main, ev_panel;
+  cudaEvent_t ev_main, ev_panel, ev_early;
   cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ev_early, cudaEventDisableTiming);
   cudaEvent_t* diag_mark = nullptr;  // timeline: event after the diagonal factor of the next panel
-  auto panel = [&](int64_t done, int64_t b, cudaStream_t st) {
+  // rows_ready: when set, the rows below are updated later than the
+  // diagonal block (early panels): only their TRSM waits for it
+  auto panel = [&](int64_t done, int64_t b, cudaStream_t st, cudaEvent_t rows_ready) {
     bf_view a11 = subview(a, done, b, done, b);
     bf_view a21 = subview(a, done + b, n - done - b, done, b);
     if (g_panel_overlap && mode == MODE_D && nl >= 2 && lv[1].variant == 3 && lv[1].bs >= 1 && b > lv[1].bs &&
         a21.m > 0 && a.cs == 1) {
-      const int prc = panel_overlap(mode, a11, a21, lv, nl, base + done, d_info, st, s, diag_mark);
+      const int prc = panel_overlap(mode, a11, a21, lv, nl, base + done, d_info, st, s, diag_mark, rows_ready);
       if (prc != -1) return prc;
     }
     int rc = chol_run(mode, a11, lv, nl, 1, base + done, d_info, st);
@@ -710,6 +746,7 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
       cudaEventCreate(diag_mark);
       cudaEventRecord(*diag_mark, st);
     }
+    if (rows_ready) cudaStreamWaitEvent(st, rows_ready, 0);
     if (!rc) rc = trsm_rec(mode, 1.0, a11, a21, kc, nullptr, d_info, st);
     return rc;
   };
@@ -803,7 +840,7 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     if (!rc) {
       cudaEventRecord(ev_col, s);
       cudaStreamWaitEvent(ps, ev_col, 0);
-      rc = panel(r2, b2, ps);
+      rc = panel(r2, b2, ps, nullptr);
       if (!rc) writeback_block_column(a, r2, b2, ps);
       cudaEventRecord(ev_panel, ps);
       cudaStreamWaitEvent(s, ev_panel, 0);
@@ -815,7 +852,7 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     start = r2;
   } else {
     wait_column(s, 0);
-    rc = panel(0, bs < n ? bs : n, s);
+    rc = panel(0, bs < n ? bs : n, s, nullptr);
     if (rc == BF_OK) writeback_block_column(a, 0, bs < n ? bs : n, s);
   }
   for (int64_t done = start; done < n && rc == BF_OK;) {
@@ -826,24 +863,36 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     bf_view l21 = subview(a, r2, nr2, done, b);
     bf_view l21_top = subview(l21, 0, b2, 0, b);
     bf_view l21_rest = subview(l21, b2, nr2 - b2, 0, b);
-    // (1) next block column, on the main stream
+    // (1) next block column, on the main stream.  Early panels: the panel
+    // stream starts the next diagonal factor as soon as the diagonal tile is
+    // updated; the rows below follow on the main stream with the step's SM
+    // reservation (they belong to step k: a pivot failure in panel k+1 must
+    // not cancel them, hence the abort limit) and only the panel's TRSM waits
+    // for them.
     const bool loading = g_h2d && done == 0;  // step 0 of a host factorization: columns still arriving
+    const bool early = g_early_panel && !loading && nr2 > b2 && (done > 0 || g_early_panel == 3);
     if (loading) wait_column(s, r2);
     rc = gemm_impl(mode, -1.0, l21_top, transposed(l21_top), 1.0, subview(a, r2, b2, r2, b2), 1, kc, d_info, s);
+    if (early) {
+      cudaEventRecord(ev_early, s);
+      cudaStreamWaitEvent(ps, ev_early, 0);
+      if (g_early_panel == 2) bf::t_reserve_sms = adaptive_reserve(nr2 - b2, b2, b);
+    }
     if (!rc && nr2 > b2)
       rc = gemm_impl(mode, -1.0, l21_rest, transposed(l21_top), 1.0, subview(a, r2 + b2, nr2 - b2, r2, b2), 0, kc,
-                     d_info, s);
+                     d_info, s, early ? base + r2 : INT64_MAX);
+    bf::t_reserve_sms = 0;
     if (rc) break;
     TimelineStep ts{};
     if (g_timeline) ts.main_col = mark(s);
     // (2) next panel on the side stream once (1) has landed
     cudaEventRecord(ev_main, s);
-    cudaStreamWaitEvent(ps, ev_main, 0);
+    if (!early) cudaStreamWaitEvent(ps, ev_main, 0);
     if (g_timeline) {
       ts.panel_begin = mark(ps);
       diag_mark = &ts.panel_diag;
     }
-    rc = panel(r2, b2, ps);
+    rc = panel(r2, b2, ps, early ? ev_main : nullptr);
     diag_mark = nullptr;
     if (rc) break;
     if (g_timeline) ts.panel_end = mark(ps);
@@ -871,25 +920,7 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
       // g_tail_reserve SMs free of this update so the panel kernels start at once
       const int64_t m = nr2 - b2, r3 = r2 + b2;
       if (g_tail_reserve > 0 && m <= g_tail_rows) bf::t_reserve_sms = g_tail_reserve;
-      if (bf::t_reserve_sms > 0 && g_reserve_adaptive) {
-        // Size the reservation to the work the panel stream has to finish
-        // under this update: panel k+1's TRSM (m rows x b2^2) and diagonal
-        // factor (b2^3 / 3) against the rest of the trailing GEMMT (m^2 b):
-        // their SM shares, plus a few SMs for the latency-bound diagonal chain
-        // (n=32768: 376.4 ms with a fixed 16, 375.2 ms adaptive; the exposed
-        // panel chain drops 22.8 -> 15.6 ms, tools/gpu_r02_reserve.sh).
-        int sms = 148;
-        {
-          int dev = 0;
-          cudaGetDevice(&dev);
-          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        }
-        const double T = double(m) * b2 * b2 + double(b2) * b2 * b2 / 3.0, S = double(m) * m * b;
-        int R = int(sms * T / (T + S) + 0.5) + g_reserve_extra;
-        if (R < g_reserve_min) R = g_reserve_min;
-        if (R > sms / 2) R = sms / 2;
-        bf::t_reserve_sms = R;
-      }
+      if (bf::t_reserve_sms > 0 && g_reserve_adaptive) bf::t_reserve_sms = adaptive_reserve(m, b2, b);
       // diagonal-factor window: the first h1 rows of the rest leave
       // g_diag_reserve SMs to the panel stream (its diagonal factor is a chain
       // of small launches that otherwise waits for trailing tiles to retire);
@@ -923,6 +954,7 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
   }
   cudaEventDestroy(ev_main);
   cudaEventDestroy(ev_panel);
+  cudaEventDestroy(ev_early);
   return rc;
 }
 
@@ -1248,6 +1280,10 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "potrs_coop") == 0) {
     bf::g_potrs_coop = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "early_panel") == 0) {
+    g_early_panel = int(value);  // 1: rows below at full width, 2: with the step's reservation, 3: 1 + step 0
     return BF_OK;
   }
   if (name && std::strcmp(name, "panel_chunks") == 0 && value >= 1 && value <= 8) {

@@ -127,7 +127,7 @@ RESERVE_TREE = ('{"op": "cholesky", "variant": 3, "bs": 256, "kernel": {"kc": 25
                 '"variant": 3, "bs": 64, "kernel": {"kc": 64}, "child": {"op": "cholesky", "variant": "unblocked3"}}}')
 
 
-@pytest.mark.parametrize("overlap", [1, 0, 3])  # 3: the rows below in 3 row chunks on their own streams
+@pytest.mark.parametrize("overlap", [1, 0, 3, 4])  # 3: 3 row chunks on their own streams; 4: no early panels
 @pytest.mark.parametrize("npd_at", [None, 10, 300, 1000, 1290, 2200])
 def test_panel_overlap_bitwise(cuda, overlap, npd_at):
     """Overlapped panels (option "panel_overlap"): the TRSM of the rows below
@@ -148,12 +148,14 @@ def test_panel_overlap_bitwise(cuda, overlap, npd_at):
         assert lib.bf_set_option(b"panel_overlap", 1 if overlap else 0) == 0
         assert lib.bf_set_option(b"panel_chunks", 3 if overlap == 3 else 2) == 0
         assert lib.bf_set_option(b"panel_chunk_rows", 256 if overlap == 3 else 6144) == 0
+        assert lib.bf_set_option(b"early_panel", 0 if overlap == 4 else 1) == 0
         v = make_view(n, n, fill=a0)
         bad = int(bf.cholesky_async(v, "lower", parse_tree(RESERVE_TREE)).item())
     finally:
         lib.bf_set_option(b"panel_overlap", 1)
         lib.bf_set_option(b"panel_chunks", 2)
         lib.bf_set_option(b"panel_chunk_rows", 6144)
+        lib.bf_set_option(b"early_panel", 1)
     st = a0.reshape(-1).copy()
     ref_bad = O.cholesky(st, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1},
                          O.levels_from_tree(json.loads(RESERVE_TREE), n, "f64"), nthreads=O.host_threads())

@@ -13,6 +13,11 @@ import paper_2604_07311_b200 as bf  # noqa: E402
 from paper_2604_07311_b200.tensor import ContractionSpec, make_tensor  # noqa: E402
 
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 128
+import os  # noqa: E402
+from paper_2604_07311_b200.engine import _lib  # noqa: E402
+for _kv in filter(None, os.environ.get("BF_OPTS", "").split(",")):  # library options for sweeps
+    _k, _v = _kv.split("=")
+    assert _lib.lib().bf_set_option(_k.encode(), int(_v)) == 0, _kv
 g = torch.Generator(device="cuda")
 g.manual_seed(42)
 for text in ("abij,cdij->abcd", "aibj,cidj->abcd", "aibj,cjdi->abcd", "abij,cdij->acbd"):

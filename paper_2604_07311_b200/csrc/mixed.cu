@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
     potrs_coop_kernel(const float* __restrict__ L, int64_t ld, const float* __restrict__ xinv, int64_t bs,
                       double* x, int64_t n, double* partial, double* tv) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double sv[1024];
+  __shared__ double sv[2048];
   const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int64_t gwarp = int64_t(c) * (PC_THREADS / 32) + warp, nwarps = int64_t(G) * (PC_THREADS / 32);
@@ -502,7 +502,7 @@ int launch_potrs_blocked(const float* L, int64_t ld, const float* xinv, int64_t 
                          double* work, cudaStream_t s) {
   double* t = work;
   double* partial = work + bs;
-  if (g_potrs_coop && bs <= 1024 && ld % 2 == 0 && bs % 2 == 0 && reinterpret_cast<uintptr_t>(L) % 8 == 0 &&
+  if (g_potrs_coop && bs <= 2048 && ld % 2 == 0 && bs % 2 == 0 && reinterpret_cast<uintptr_t>(L) % 8 == 0 &&
       reinterpret_cast<uintptr_t>(xinv) % 8 == 0) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);

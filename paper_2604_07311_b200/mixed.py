@@ -58,7 +58,7 @@ class MixedWorkspace:
     repeated solves never touch the allocator (multi-GB blocks churning
     through the caching allocator cost more than the solve)."""
 
-    def __init__(self, n: int, bs: int = 1024, device: Optional[torch.device] = None,
+    def __init__(self, n: int, bs: int = 2048, device: Optional[torch.device] = None,
                  precision: str = "bf16") -> None:
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         if precision not in ("bf16", "tf32"):
@@ -92,7 +92,7 @@ class MixedFactor:
     bs: int
 
 
-def cholesky_mixed(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlNode] = None,
+def cholesky_mixed(a: torch.Tensor, bs: int = 2048, diag_tree: Optional[ControlNode] = None,
                    lookahead: bool = True, ws: Optional[MixedWorkspace] = None,
                    precision: Optional[str] = None) -> MixedFactor:
     """bf16/fp32 factorization of the fp64 SPD matrix `a` (right-looking,
@@ -139,7 +139,7 @@ def cholesky_mixed(a: torch.Tensor, bs: int = 1024, diag_tree: Optional[ControlN
     return MixedFactor(w, xinv, bs)
 
 
-def posv_mixed(a: torch.Tensor, b: torch.Tensor, bs: int = 1024, tol: Optional[float] = None,
+def posv_mixed(a: torch.Tensor, b: torch.Tensor, bs: int = 2048, tol: Optional[float] = None,
                max_iter: int = 30, lookahead: bool = True, ws: Optional[MixedWorkspace] = None,
                precision: Optional[str] = None, step_tol: Optional[float] = None) -> MixedResult:
     """Solve A x = b (A fp64 SPD, full dense row-major on the GPU) to FP64

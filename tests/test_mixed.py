@@ -112,7 +112,8 @@ def test_residual_and_row_sums_vs_torch(cuda, n, symv):
 
 
 @pytest.mark.parametrize("precision", ["bf16", "tf32"])
-@pytest.mark.parametrize("n,bs,lookahead", [(1000, 256, True), (3000, 1024, True), (2100, 512, False)])
+@pytest.mark.parametrize("n,bs,lookahead", [(1000, 256, True), (3000, 1024, True), (2100, 512, False),
+                                             (4500, 2048, True)])
 def test_mixed_solve_reaches_fp64_accuracy(cuda, n, bs, lookahead, precision):
     g = torch.Generator(device="cuda")
     g.manual_seed(n)

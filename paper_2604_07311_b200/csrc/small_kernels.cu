@@ -16,6 +16,7 @@ namespace bf {
 
 int g_trsm_warp = 1;
 int g_leaf_blocked = 1;
+int g_leaf_pipe = 1;     // bf_set_option("leaf_pipe", 0|1): blocked leaf, next chain under the previous trailing update
 
 namespace {
 
@@ -955,7 +956,7 @@ struct LeafMath<double> {
 
 template <typename T>
 __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t off, int n, int64_t rs, int64_t cs,
-                                                                 int64_t base_index, int* d_info) {
+                                                                 int64_t base_index, int* d_info, int pipe_flag) {
   if (d_info != nullptr && *d_info >= 0) return;
   extern __shared__ __align__(16) unsigned char leaf_b_smem[];
   T* A = reinterpret_cast<T*>(leaf_b_smem);
@@ -995,6 +996,46 @@ __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t o
   __syncthreads();
   LV4_MARK(0)
   int bad = -1;
+  // block (k0, kend columns)'s rank-kend update of the 4x4 tiles tt in
+  // [tt0, tt1) of the trailing triangle below k1, over threads idx of nthr
+  auto trail = [&](int k0, int kend, int k1, int tt0, int tt1, int idx, int nthr) {
+    const int m = n - k1;
+    if (m <= 0 || kend <= 0) return;
+    const int tiles = (m + 3) / 4;
+    const int ntile = tiles * (tiles + 1) / 2;
+    for (int tt = tt0 + idx; tt < ntile && tt < tt1; tt += nthr) {
+      int ti = int((sqrtf(8.f * float(tt) + 1.f) - 1.f) * 0.5f);
+      while (ti * (ti + 1) / 2 > tt) --ti;
+      while ((ti + 1) * (ti + 2) / 2 <= tt) ++ti;
+      const int tj = tt - ti * (ti + 1) / 2;
+      const int i0 = k1 + 4 * ti, j0 = k1 + 4 * tj;
+      T c[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          c[a][b] = (i0 + a < n && j0 + b <= i0 + a) ? A[(i0 + a) * LV4_LD + j0 + b] : T(0);
+#pragma unroll 4
+      for (int p = k0; p < k0 + kend; ++p) {
+        T li[4], lj[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) li[a] = A[((i0 + a) & 127) * LV4_LD + p];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) lj[b] = A[((j0 + b) & 127) * LV4_LD + p];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) c[a][b] = Ops<T>::sub(c[a][b], Ops<T>::mul(li[a], lj[b]));
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          if (i0 + a < n && j0 + b <= i0 + a) A[(i0 + a) * LV4_LD + j0 + b] = c[a][b];
+    }
+  };
+  const bool pipe = pipe_flag != 0;
+  int pk0 = -1, pkend = 0, pk1 = 0;  // the block whose trailing update (beyond the next diagonal triangle) is pending
 #pragma unroll 1
   for (int k0 = 0; k0 < n; k0 += 32) {
     const int bw = n - k0 < 32 ? n - k0 : 32;
@@ -1007,7 +1048,9 @@ __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t o
     // Every warp runs it (same values); only warp 0 stores: with no
     // warp-dependent branch around it the shuffles need no divergence
     // checks, which would otherwise split the body into basic blocks.
-    {
+    if (pipe && warp > 0) {
+      if (pk0 >= 0) trail(pk0, pkend, pk1, 36, 1 << 30, tid - 32, 96);
+    } else {
       const bool w0 = warp == 0;
       const int i = lane;
       T acc[32];
@@ -1116,44 +1159,17 @@ __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t o
     }
     __syncthreads();
     LV4_MARK(2 + 3 * (k0 >> 5))
-    // (c) trailing triangle k1 <= j <= i < n: the block's first kend rank-1 updates
-    const int m = n - k1;
-    if (m > 0 && kend > 0) {
-      const int tiles = (m + 3) / 4;
-      const int ntile = tiles * (tiles + 1) / 2;
-      for (int tt = tid; tt < ntile; tt += 128) {
-        int ti = int((sqrtf(8.f * float(tt) + 1.f) - 1.f) * 0.5f);
-        while (ti * (ti + 1) / 2 > tt) --ti;
-        while ((ti + 1) * (ti + 2) / 2 <= tt) ++ti;
-        const int tj = tt - ti * (ti + 1) / 2;
-        const int i0 = k1 + 4 * ti, j0 = k1 + 4 * tj;
-        T c[4][4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b)
-            c[a][b] = (i0 + a < n && j0 + b <= i0 + a) ? A[(i0 + a) * LV4_LD + j0 + b] : T(0);
-#pragma unroll 4
-        for (int p = k0; p < k0 + kend; ++p) {
-          T li[4], lj[4];
-#pragma unroll
-          for (int a = 0; a < 4; ++a) li[a] = A[((i0 + a) & 127) * LV4_LD + p];
-#pragma unroll
-          for (int b = 0; b < 4; ++b) lj[b] = A[((j0 + b) & 127) * LV4_LD + p];
-#pragma unroll
-          for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) c[a][b] = Ops<T>::sub(c[a][b], Ops<T>::mul(li[a], lj[b]));
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b)
-            if (i0 + a < n && j0 + b <= i0 + a) A[(i0 + a) * LV4_LD + j0 + b] = c[a][b];
-      }
-    }
+    // (c) trailing triangle k1 <= j <= i < n: the block's first kend rank-1
+    // updates.  Pipelined: only the next diagonal block's triangle (tile rows
+    // 0..7) now; warps 1-3 apply the rest in the next trip's phase A while
+    // warp 0 runs the next block's chain (disjoint elements, and every
+    // element still takes the blocks' updates in block order)
+    trail(k0, kend, k1, 0, pipe ? 36 : (1 << 30), tid, 128);
     __syncthreads();
     LV4_MARK(3 + 3 * (k0 >> 5))
+    pk0 = k0;
+    pkend = kend;
+    pk1 = k1;
   }
   if (s_unsafe) {  // a pivot failed, or a root or quotient was not provably sqrt.rn / div.rn: redo exactly
     __syncthreads();
@@ -1237,7 +1253,7 @@ static int leaf_launch(T* a, int64_t off, int64_t n, int64_t rs, int64_t cs, int
     const size_t smem = size_t(128) * LV4_LD * sizeof(T);
     if (!smem_attr(reinterpret_cast<const void*>(potrf_leaf_blocked_kernel<T>), int(smem))) return -10;
     note_launch();
-    potrf_leaf_blocked_kernel<T><<<1, 128, smem, s>>>(a, off, int(n), rs, cs, base_index, d_info);
+    potrf_leaf_blocked_kernel<T><<<1, 128, smem, s>>>(a, off, int(n), rs, cs, base_index, d_info, g_leaf_pipe);
     return cudaGetLastError() == cudaSuccess ? 0 : -11;
   }
   if (variant == 3 && n <= 128) {

@@ -205,12 +205,14 @@ def test_lookahead_sm_reservation_bitwise(cuda, opts, npd_at):
     assert digest(v.storage.cpu().numpy()) == digest(st)
 
 
-@pytest.mark.parametrize("leaf_blocked", [1, 0])
+@pytest.mark.parametrize("leaf_blocked,leaf_pipe", [(1, 1), (1, 0), (0, 0)])
 @pytest.mark.parametrize("dt,npd_at", [("f64", None), ("f64", 77), ("f64", 100), ("f32", None), ("f32", 45)])
-def test_leaf_kernels_bitwise_and_partial_state(cuda, leaf_blocked, dt, npd_at):
-    """Both variant-3 leaf kernels (blocked lane-per-row v4, column-parallel
-    v3) give the oracle's bits, and on a failing pivot — inside the first
-    column block, or mid-block past it — the oracle's partial state and index."""
+def test_leaf_kernels_bitwise_and_partial_state(cuda, leaf_blocked, leaf_pipe, dt, npd_at):
+    """Both variant-3 leaf kernels (blocked lane-per-row v4 — with the next
+    diagonal chain overlapping the previous block's trailing update or not —
+    and column-parallel v3) give the oracle's bits, and on a failing pivot —
+    inside the first column block, or mid-block past it — the oracle's
+    partial state and index."""
     import json
 
     from paper_2604_07311_b200.engine import _lib
@@ -224,6 +226,7 @@ def test_leaf_kernels_bitwise_and_partial_state(cuda, leaf_blocked, dt, npd_at):
     bad = O.cholesky(st, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1}, O.levels_from_tree(json.loads(doc), n, dt))
     lib = _lib.lib()
     lib.bf_set_option(b"leaf_blocked", leaf_blocked)
+    lib.bf_set_option(b"leaf_pipe", leaf_pipe)
     try:
         v = make_view(n, n, DType.parse(dt), fill=a0)
         if npd_at is None:
@@ -233,7 +236,8 @@ def test_leaf_kernels_bitwise_and_partial_state(cuda, leaf_blocked, dt, npd_at):
                 bf.cholesky(v, "lower", parse_tree(doc))
             assert e.value.index == bad == npd_at
     finally:
-        lib.bf_set_option(b"leaf_blocked", 0)
+        lib.bf_set_option(b"leaf_blocked", 1)  # the defaults
+        lib.bf_set_option(b"leaf_pipe", 1)
     assert digest(v.storage.cpu().numpy()) == digest(st)
 
 

@@ -14,6 +14,7 @@ bool smem_attr(const void* k, int b) {
 int g_use_tma = 1, g_tma_variant = 2, g_tiles_per_cta = 1, g_bf16_tma_c = 1;
 }  // namespace bf
 using namespace bf;
+static int g_pipe = 1;
 
 template <typename T>
 void run(const char* label) {
@@ -33,7 +34,7 @@ void run(const char* label) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    potrf_leaf_blocked_kernel<T><<<1, 128, smem>>>(d, 0, n, n, 1, 0, nullptr);
+    potrf_leaf_blocked_kernel<T><<<1, 128, smem>>>(d, 0, n, n, 1, 0, nullptr, g_pipe);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -46,7 +47,8 @@ void run(const char* label) {
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) g_pipe = atoi(argv[1]);
   run<float>("f32");
   run<double>("f64");
   return 0;

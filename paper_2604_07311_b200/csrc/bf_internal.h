@@ -167,6 +167,7 @@ extern thread_local int t_reserve_sms;  // gemm_dmma_tma.cu: SMs left free by th
 extern int g_tiles_per_cta;   // bf_set_option("tiles_per_cta", t)
 extern int g_bf16_tma_c;      // bf16 GEMM: TMA C-tile epilogue (1) or per-element fallback (0)
 extern int g_trsm_warp;       // fused TRSM subtree: 4-warps-per-32-rows kernel (1) or the 64-row CTA kernel (0)
+extern int g_pdl;             // bf_set_option("pdl", 0|1): programmatic dependent launch on the chain kernels
 extern int g_leaf_pipe;       // bf_set_option("leaf_pipe", 0|1)
 extern int g_leaf_blocked;    // variant-3 leaves n <= 128: blocked lane-per-row kernel (1) or v3 (0)
 extern int g_lu_grid_max;     // LU leaf: cap on the cooperative grid (0 = SM-derived)

@@ -1402,6 +1402,10 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_lu_grid_max = int(value);
     return BF_OK;
   }
+  if (name && std::strcmp(name, "pdl") == 0) {
+    bf::g_pdl = value != 0;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "leaf_pipe") == 0) {
     bf::g_leaf_pipe = value != 0;
     return BF_OK;

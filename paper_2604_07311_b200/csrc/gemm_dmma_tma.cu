@@ -193,6 +193,7 @@ template <int MMAK, int KBOX, int STAGES, bool TMC, bool MODES = false, bool GRO
 __global__ void __launch_bounds__(TM_THREADS, 1)
     gemm_dmma_tma_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                          const GemmParams p) {
+  pdl_wait();
   if (aborted(p)) return;
   constexpr int BKS = 16 * KBOX;                    // k per stage
   // BN_ = 64: two independent groups of 8 warps, each on its own 128 x 64
@@ -622,6 +623,7 @@ __global__ void __launch_bounds__(TM_THREADS, 1)
     }
   }
   (void)MI;
+  pdl_trigger();
   if constexpr (TMC) {
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -730,7 +732,8 @@ static int run_tma(const GemmParams& p_in, const CUtensorMap& ma, const CUtensor
   const size_t smem = base_smem + size_t(tpc) * tab_bytes;
   if (!smem_attr(reinterpret_cast<const void*>(kern), int(smem))) return -10;
   note_launch();
-  kern<<<unsigned(grid), TM_THREADS, smem, s>>>(ma, mb, p);
+  if (launch_maybe_pdl(kern, dim3(unsigned(grid)), dim3(TM_THREADS), smem, s, g_pdl != 0, ma, mb, p) != cudaSuccess)
+    return -11;
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 

@@ -16,7 +16,8 @@ namespace bf {
 
 int g_trsm_warp = 1;
 int g_leaf_blocked = 1;
-int g_leaf_pipe = 1;     // bf_set_option("leaf_pipe", 0|1): blocked leaf, next chain under the previous trailing update
+int g_leaf_pipe = 1;
+int g_pdl = 1;  // bf_set_option("pdl", 0|1): programmatic dependent launch for the leaf, fused-TRSM and TMA GEMM kernels     // bf_set_option("leaf_pipe", 0|1): blocked leaf, next chain under the previous trailing update
 
 namespace {
 
@@ -784,6 +785,7 @@ __global__ void __launch_bounds__(128 * R) trsm_warp_right_kernel(double alpha, 
                                                                   int64_t tcs, T* b, int64_t boff, int64_t brs,
                                                                   int64_t bcs, int64_t m, int n, int64_t kc,
                                                                   const int* abort_flag) {
+  pdl_wait();
   if (abort_flag != nullptr && *abort_flag >= 0) return;
   extern __shared__ __align__(16) unsigned char tw_smem[];
   T* sl = reinterpret_cast<T*>(tw_smem);
@@ -844,6 +846,7 @@ __global__ void __launch_bounds__(128 * R) trsm_warp_right_kernel(double alpha, 
   if (rows > 0) {  // uniform per group
     TrsmGroup<T> tg{sx, sl, lane, gw, 1 + grp, kc};
     tg.solve(0, n, alpha);
+    pdl_trigger();
     if (bcs == 1) {
       for (int r = gw; r < rows; r += 4)
         for (int c = lane; c < n; c += 32) b[boff + (r0 + r) * brs + c] = sx[c * TW_XLD + r];
@@ -957,6 +960,7 @@ struct LeafMath<double> {
 template <typename T>
 __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t off, int n, int64_t rs, int64_t cs,
                                                                  int64_t base_index, int* d_info, int pipe_flag) {
+  pdl_wait();
   if (d_info != nullptr && *d_info >= 0) return;
   extern __shared__ __align__(16) unsigned char leaf_b_smem[];
   T* A = reinterpret_cast<T*>(leaf_b_smem);
@@ -1179,6 +1183,7 @@ __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t o
     bad = leaf_v3<T, 128>(Mat<T>{A, LV4_LD, 1}, n, &s_fail, &s_d);
     __syncthreads();
   }
+  pdl_trigger();  // the next kernel of the chain may launch (it waits for this one's completion)
   if (cs == 1) {
     for (int i = warp; i < n; i += 4)
       for (int j = lane; j <= i; j += 32) g[off + i * rs + j] = A[i * LV4_LD + j];
@@ -1197,8 +1202,9 @@ int launch_trsm_warp(double alpha, const T* t, int64_t toff, int64_t trs, int64_
   const int64_t blocks = (m + 32 * W - 1) / (32 * W);
   if (blocks > 0x7fffffffLL) return -3;
   note_launch();
-  trsm_warp_right_kernel<T, W><<<unsigned(blocks), 128 * W, smem, s>>>(alpha, t, toff, trs, tcs, b, boff, brs, bcs, m,
-                                                                      n, kc, abort_flag);
+  if (launch_maybe_pdl(trsm_warp_right_kernel<T, W>, dim3(unsigned(blocks)), dim3(128 * W), smem, s, g_pdl != 0,
+                       alpha, t, toff, trs, tcs, b, boff, brs, bcs, m, n, kc, abort_flag) != cudaSuccess)
+    return -11;
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
@@ -1253,7 +1259,9 @@ static int leaf_launch(T* a, int64_t off, int64_t n, int64_t rs, int64_t cs, int
     const size_t smem = size_t(128) * LV4_LD * sizeof(T);
     if (!smem_attr(reinterpret_cast<const void*>(potrf_leaf_blocked_kernel<T>), int(smem))) return -10;
     note_launch();
-    potrf_leaf_blocked_kernel<T><<<1, 128, smem, s>>>(a, off, int(n), rs, cs, base_index, d_info, g_leaf_pipe);
+    if (launch_maybe_pdl(potrf_leaf_blocked_kernel<T>, dim3(1), dim3(128), smem, s, g_pdl != 0, a, off, int(n), rs, cs,
+                         base_index, d_info, g_leaf_pipe) != cudaSuccess)
+      return -11;
     return cudaGetLastError() == cudaSuccess ? 0 : -11;
   }
   if (variant == 3 && n <= 128) {

@@ -165,6 +165,7 @@ extern int g_tmem_fold;       // bf_set_option("tmem_fold", 0|1): TMA kernel kee
 extern int g_reserve_strided;
 extern thread_local int t_reserve_sms;  // gemm_dmma_tma.cu: SMs left free by the next launch
 extern int g_tiles_per_cta;   // bf_set_option("tiles_per_cta", t)
+extern int g_bf16_group;      // bf_set_option("bf16_group", g)
 extern int g_bf16_tma_c;      // bf16 GEMM: TMA C-tile epilogue (1) or per-element fallback (0)
 extern int g_trsm_warp;       // fused TRSM subtree: 4-warps-per-32-rows kernel (1) or the 64-row CTA kernel (0)
 extern int g_pdl;             // bf_set_option("pdl", 0|1): programmatic dependent launch on the chain kernels

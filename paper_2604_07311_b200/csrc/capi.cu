@@ -1418,6 +1418,10 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_trsm_warp = value != 0;
     return BF_OK;
   }
+  if (name && std::strcmp(name, "bf16_group") == 0 && value >= 0) {
+    bf::g_bf16_group = int(value);
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "bf16_tma_c") == 0) {
     bf::g_bf16_tma_c = value != 0;
     return BF_OK;

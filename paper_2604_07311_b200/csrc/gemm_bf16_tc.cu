@@ -36,6 +36,7 @@
 namespace bf {
 
 int g_bf16_tma_c = 1;
+int g_bf16_group = 8;  // bf_set_option("bf16_group", g): row tiles per band of the tcgen05 GEMM's tile order (0: plain)
 
 namespace {
 
@@ -116,13 +117,51 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar) : "memory");
 }
 
+// Tile order: bands of p.group row tiles, column-major inside a band (the
+// lower triangle's band = its full-height columns, then its own triangle),
+// so the ~148 tiles in flight share a few A row tiles and a band's columns
+// of B while the band's A rows stay in L2.  (Row-by-row / one-column-at-a-
+// time orders streamed A or B from HBM once per row or column: 8192^3 read
+// 4 GB from DRAM.)  p.group <= 0: the plain orders.
 __device__ __forceinline__ void tile_of(const GemmParams& p, int64_t t, int64_t& ti, int64_t& tj) {
-  if (p.lower_only) {  // lower-triangle enumeration, row by row
+  const int64_t G = p.group;
+  if (p.lower_only && G > 0) {
+    const int64_t T = p.tiles_m;
+    int64_t start = 0, r0 = 0, h = 0;
+    for (;;) {
+      h = T - r0 < G ? T - r0 : G;
+      const int64_t cnt = r0 * h + h * (h + 1) / 2;
+      if (t < start + cnt) break;
+      start += cnt;
+      r0 += G;
+    }
+    int64_t q = t - start;
+    if (q < r0 * h) {
+      tj = q / h;
+      ti = r0 + q % h;
+    } else {
+      q -= r0 * h;
+      int64_t c = 0;
+      while (q >= h - c) {
+        q -= h - c;
+        ++c;
+      }
+      tj = r0 + c;
+      ti = r0 + c + q;
+    }
+  } else if (p.lower_only) {  // lower-triangle enumeration, row by row
     int64_t r = int64_t((sqrt(8.0 * double(t) + 1.0) - 1.0) * 0.5);
     while (r * (r + 1) / 2 > t) --r;
     while ((r + 1) * (r + 2) / 2 <= t) ++r;
     ti = r;
     tj = t - r * (r + 1) / 2;
+  } else if (G > 0) {
+    const int64_t per_group = G * p.tiles_n;
+    const int64_t gid = t / per_group, first = gid * G;
+    const int64_t h = p.tiles_m - first < G ? p.tiles_m - first : G;
+    const int64_t local = t - gid * per_group;
+    ti = first + local % h;
+    tj = local / h;
   } else {
     ti = t % p.tiles_m;
     tj = t / p.tiles_m;
@@ -507,6 +546,7 @@ int launch_tc(int tf32, double alpha, const void* a, int64_t lda, const void* b,
   p.alpha = alpha;
   p.beta = beta;
   p.lower_only = lower_only;
+  p.group = g_bf16_group;
   p.tiles_m = int((m + TC_BM - 1) / TC_BM);
   p.tiles_n = int((n + TC_BN - 1) / TC_BN);
   if (lower_only && (m != n)) return -1;

@@ -12,7 +12,11 @@ from paper_2604_07311_b200.engine import _lib  # noqa: E402
 from paper_2604_07311_b200.views import from_torch  # noqa: E402
 
 lib = _lib.lib()
-for m, k, lower in ((8192, 8192, 0), (31744, 1024, 1), (16384, 1024, 1), (31744, 1024, 0)):
+import os  # noqa: E402
+for _kv in filter(None, os.environ.get("BF_OPTS", "").split(",")):
+    _k, _v = _kv.split("=")
+    assert lib.bf_set_option(_k.encode(), int(_v)) == 0, _kv
+for m, k, lower in ((8192, 8192, 0), (31744, 1024, 1), (30720, 2048, 1), (16384, 1024, 1), (31744, 1024, 0)):
     a = torch.randn(m, k, device="cuda").to(torch.bfloat16)
     c = torch.randn(m, m, device="cuda")
     v = _lib.as_bfview(from_torch(c))

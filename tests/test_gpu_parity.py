@@ -164,6 +164,32 @@ def test_panel_overlap_bitwise(cuda, overlap, npd_at):
     assert digest(v.storage.cpu().numpy()) == digest(st)
 
 
+@pytest.mark.parametrize("kc", [320, 64])
+@pytest.mark.parametrize("npd_at", [None, 700, 1650])
+def test_panel_overlap_ragged_inner_blocks_bitwise(cuda, kc, npd_at):
+    """Overlapped and early panels when the inner block (96) does not divide
+    the panel (320) and the order (1700) is not a multiple of either: the
+    TRSM pieces wait for the right inner step, ragged last blocks, kc below
+    the panel width, and the partial state after a failure."""
+    import json
+
+    n = 1700
+    tree = json.dumps({"op": "cholesky", "variant": 3, "bs": 320, "kernel": {"kc": kc},
+                       "child": {"op": "cholesky", "variant": 3, "bs": 96, "kernel": {"kc": 96},
+                                 "child": {"op": "cholesky", "variant": "unblocked3"}}})
+    a0 = spd_int(5252 + kc, n)
+    if npd_at is not None:
+        a0[npd_at, npd_at] = -1e9
+    v = make_view(n, n, fill=a0)
+    bad = int(bf.cholesky_async(v, "lower", parse_tree(tree)).item())
+    st = a0.reshape(-1).copy()
+    ref_bad = O.cholesky(st, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1},
+                         O.levels_from_tree(json.loads(tree), n, "f64"), nthreads=O.host_threads())
+    assert ref_bad == (-1 if npd_at is None else npd_at)
+    assert bad == ref_bad
+    assert digest(v.storage.cpu().numpy()) == digest(st)
+
+
 @pytest.mark.parametrize("opts", [
     {"tail_reserve": 0},                                     # 1-tile CTAs on the whole GPU
     {"tail_reserve": 16, "tail_rows": 1 << 40},              # default grid shape on every step

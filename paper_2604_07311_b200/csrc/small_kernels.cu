@@ -1076,9 +1076,12 @@ __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t o
           const T dcur = d;
           T y;
           const T lpp = LM::sqrt_y(dcur, y);
-          const T r = LM::rcp(lpp, y);
+          const T r = LM::rcp(lpp, y);  // for the panel solve (s_rc), off the chain
           const T a = acc[u];
-          const T qv = LM::div(a, lpp, r);
+          // the chain's quotient seeds Markstein with y ~ 1/lpp itself (a few
+          // ulps): one rcp refinement less between consecutive pivots; the
+          // quotient is still verified exactly below (div_ok)
+          const T qv = LM::div(a, lpp, y);
           const T l = i == p ? lpp : (i > p ? qv : a);
           // next pivot first: lane p+1's own update by column p
           const T nd = Ops<T>::sub(acc[u + 1], Ops<T>::mul(l, l));

@@ -908,13 +908,14 @@ struct LeafMath<double> {
     return (e >= 223) & (e <= 1823);  // |v| in [2^-800, 2^800]
   }
   static __device__ __forceinline__ double sqrt_y(double d, double& yo) {
+    // one Newton step on the rsqrt seed is enough: the residual correction
+    // below squares the error again (0 mismatches against sqrt.rn and, with y
+    // as the Markstein seed, against div.rn in 1.24e9 probes,
+    // tools/sqrt_probe1.cu); every root and quotient is verified anyway
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
     double h = 0.5 * y;
     double r = __fma_rn(-d * y, h, 0.5);
-    y = __fma_rn(y, r, y);
-    h = 0.5 * y;
-    r = __fma_rn(-d * y, h, 0.5);
     y = __fma_rn(y, r, y);
     const double s = d * y;
     h = 0.5 * y;

@@ -105,7 +105,11 @@ const char* bf_last_error(void);
  * back only without a pivot failure; "reserve_adaptive" / "reserve_extra" /
  * "reserve_min" size the reservation per step; "potrs_coop" (default 1) and
  * "symv" (default 1) select the mixed refinement's cooperative blocked solve
- * and lower-triangle residual. */
+ * and lower-triangle residual; "early_panel" (default 1) starts panel k+1's
+ * diagonal factor once its diagonal tile is updated; "leaf_pipe" (default 1)
+ * overlaps the blocked leaf's next chain with its trailing update; "pdl"
+ * (default 1) launches the chain kernels with programmatic dependent launch;
+ * "bf16_group" (default 8) the tcgen05 GEMM's band height. */
 int bf_set_option(const char* name, int64_t value);
 int bf_device_sm_count(void);
 /* With bf_set_option("timeline", 1): per top-level step of the last lookahead

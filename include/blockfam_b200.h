@@ -103,7 +103,7 @@ const char* bf_last_error(void);
  * diagonal factor's inner steps on its own streams ("panel_chunks" row chunks
  * of at least "panel_chunk_rows" rows, defaults 2 and 6144), on a copy written
  * back only without a pivot failure; "reserve_adaptive" / "reserve_extra" /
- * "reserve_min" size the reservation per step; "potrs_coop" (default 1) and
+ * "reserve_min" size the reservation per step; "potrs_coop" / "potrs_vec" (default 1) and
  * "symv" (default 1) select the mixed refinement's cooperative blocked solve
  * and lower-triangle residual; "early_panel" (default 1) starts panel k+1's
  * diagonal factor once its diagonal tile is updated; "leaf_pipe" (default 1)

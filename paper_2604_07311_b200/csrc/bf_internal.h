@@ -131,6 +131,7 @@ cudaStream_t panel_stream_for(cudaStream_t caller);  // the high-priority panel 
 extern int g_mixed_reserve;
 extern int g_symv;        // mixed.cu: residual / row sums from the lower triangle of A
 extern int g_potrs_coop;  // mixed.cu: the refinement solve as one cooperative kernel
+extern int g_potrs_vec;   // mixed.cu: float4 streams in that kernel
 int launch_axpby_f32_f64(double alpha, const float* src, int64_t ld, double beta, double* c, int64_t off, int64_t rs,
                          int64_t cs, int64_t m, int64_t n, cudaStream_t s);
 

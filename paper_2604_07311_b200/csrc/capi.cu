@@ -1282,6 +1282,10 @@ int bf_set_option(const char* name, int64_t value) {
     bf::g_potrs_coop = value != 0;
     return BF_OK;
   }
+  if (name && std::strcmp(name, "potrs_vec") == 0) {
+    bf::g_potrs_vec = value != 0;
+    return BF_OK;
+  }
   if (name && std::strcmp(name, "early_panel") == 0) {
     g_early_panel = int(value);  // 1: rows below at full width, 2: with the step's reservation, 3: 1 + step 0
     return BF_OK;

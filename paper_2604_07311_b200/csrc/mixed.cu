@@ -396,18 +396,106 @@ int launch_potrs_f32_f64(const float* L, int64_t ld, double* x, int64_t n, cudaS
 // products, so the launch latencies, not the 4 GB of L it streams, were its
 // cost (2.4 ms at n = 32768).  Same products in a different summation order.
 constexpr int PC_THREADS = 512;
+// vec = 1 (L, xinv 16-byte aligned, ld, bs and n multiples of 4): float4 loads
+// with four in flight per thread, so each SM keeps ~32 KB of the stream in
+// flight — the scalar form's ~8 KB left it latency-bound at a third of HBM.
 __global__ void __launch_bounds__(PC_THREADS, 1)
     potrs_coop_kernel(const float* __restrict__ L, int64_t ld, const float* __restrict__ xinv, int64_t bs,
-                      double* x, int64_t n, double* partial, double* tv) {
+                      double* x, int64_t n, double* partial, double* tv, int vec) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sv[2048];
   const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int64_t gwarp = int64_t(c) * (PC_THREADS / 32) + warp, nwarps = int64_t(G) * (PC_THREADS / 32);
-  const int64_t gtid = int64_t(c) * PC_THREADS + tid;
   const int64_t nblk = (n + bs - 1) / bs;
+  // vec: out[j] = sum_{i in [i0, i1)} A[i * lda + j] v[i] for j < b (b % 4 == 0,
+  // b <= 2048).  Thread = 4 columns x one of rg row groups (rows i0 + g, +rg,
+  // ...), four rows per iteration; the row groups are combined through sv in
+  // a fixed order.  Ends with sv clobbered.
+  auto colsum4 = [&](const float* A, int64_t lda, const double* v, int64_t i0, int64_t i1, int b, double* out) {
+    const int c4 = b >> 2, rg = PC_THREADS / c4;
+    const int g = tid / c4, j = (tid % c4) * 4;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (g < rg) {
+      int64_t i = i0 + g;
+      for (; i + 3 * rg < i1; i += 4 * rg) {
+        const float4 q0 = __ldcs(reinterpret_cast<const float4*>(A + i * lda + j));
+        const float4 q1 = __ldcs(reinterpret_cast<const float4*>(A + (i + rg) * lda + j));
+        const float4 q2 = __ldcs(reinterpret_cast<const float4*>(A + (i + 2 * rg) * lda + j));
+        const float4 q3 = __ldcs(reinterpret_cast<const float4*>(A + (i + 3 * rg) * lda + j));
+        const double v0 = v[i], v1 = v[i + rg], v2 = v[i + 2 * rg], v3 = v[i + 3 * rg];
+        a0 = fma(double(q0.x), v0, a0); a1 = fma(double(q0.y), v0, a1);
+        a2 = fma(double(q0.z), v0, a2); a3 = fma(double(q0.w), v0, a3);
+        a0 = fma(double(q1.x), v1, a0); a1 = fma(double(q1.y), v1, a1);
+        a2 = fma(double(q1.z), v1, a2); a3 = fma(double(q1.w), v1, a3);
+        a0 = fma(double(q2.x), v2, a0); a1 = fma(double(q2.y), v2, a1);
+        a2 = fma(double(q2.z), v2, a2); a3 = fma(double(q2.w), v2, a3);
+        a0 = fma(double(q3.x), v3, a0); a1 = fma(double(q3.y), v3, a1);
+        a2 = fma(double(q3.z), v3, a2); a3 = fma(double(q3.w), v3, a3);
+      }
+      for (; i < i1; i += rg) {
+        const float4 q = __ldcs(reinterpret_cast<const float4*>(A + i * lda + j));
+        const double vi = v[i];
+        a0 = fma(double(q.x), vi, a0); a1 = fma(double(q.y), vi, a1);
+        a2 = fma(double(q.z), vi, a2); a3 = fma(double(q.w), vi, a3);
+      }
+      double* s = sv + int64_t(g) * b + j;
+      s[0] = a0; s[1] = a1; s[2] = a2; s[3] = a3;
+    }
+    __syncthreads();
+    for (int jj = tid; jj < b; jj += PC_THREADS) {
+      double t = 0.0;
+      for (int q = 0; q < rg; ++q) t += sv[int64_t(q) * b + jj];
+      out[jj] = t;
+    }
+    __syncthreads();
+  };
+  // vec: warp-per-row dot product of a fp32 row (16-byte aligned, b % 4 == 0)
+  // with the smem vector sv, four float4 per lane in flight
+  auto row_dot4 = [&](const float* row, int b) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int j = lane * 4;
+    for (; j + 384 < b; j += 512) {
+      const float4 q0 = __ldcs(reinterpret_cast<const float4*>(row + j));
+      const float4 q1 = __ldcs(reinterpret_cast<const float4*>(row + j + 128));
+      const float4 q2 = __ldcs(reinterpret_cast<const float4*>(row + j + 256));
+      const float4 q3 = __ldcs(reinterpret_cast<const float4*>(row + j + 384));
+      s0 = fma(double(q0.x), sv[j], s0); s1 = fma(double(q0.y), sv[j + 1], s1);
+      s2 = fma(double(q0.z), sv[j + 2], s2); s3 = fma(double(q0.w), sv[j + 3], s3);
+      s0 = fma(double(q1.x), sv[j + 128], s0); s1 = fma(double(q1.y), sv[j + 129], s1);
+      s2 = fma(double(q1.z), sv[j + 130], s2); s3 = fma(double(q1.w), sv[j + 131], s3);
+      s0 = fma(double(q2.x), sv[j + 256], s0); s1 = fma(double(q2.y), sv[j + 257], s1);
+      s2 = fma(double(q2.z), sv[j + 258], s2); s3 = fma(double(q2.w), sv[j + 259], s3);
+      s0 = fma(double(q3.x), sv[j + 384], s0); s1 = fma(double(q3.y), sv[j + 385], s1);
+      s2 = fma(double(q3.z), sv[j + 386], s2); s3 = fma(double(q3.w), sv[j + 387], s3);
+    }
+    for (; j < b; j += 128) {
+      const float4 q = __ldcs(reinterpret_cast<const float4*>(row + j));
+      s0 = fma(double(q.x), sv[j], s0); s1 = fma(double(q.y), sv[j + 1], s1);
+      s2 = fma(double(q.z), sv[j + 2], s2); s3 = fma(double(q.w), sv[j + 3], s3);
+    }
+    double t = (s0 + s1) + (s2 + s3);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    return t;
+  };
+  // tv[j] = (base ? base[j] - t : t), t = sum_q partial[q][j] for j < b: one
+  // warp per j, lane l adding q = l, l + 32, ... then a fixed shuffle tree
+  // (every load in flight at once; a thread-per-j loop over the G partials
+  // was a chain of G / unroll L2 round trips per block and direction)
+  auto reduce_partials = [&](int b, const double* base) {
+    for (int64_t jj = gwarp; jj < b; jj += nwarps) {
+      double t = 0.0;
+#pragma unroll 4
+      for (int q = lane; q < G; q += 32) t += partial[int64_t(q) * bs + jj];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) tv[jj] = base ? base[jj] - t : t;
+    }
+  };
   // warp-per-row dot product of a fp32 row with the smem vector sv
   auto row_dot = [&](const float* row, int b) {
+    if (vec) return row_dot4(row, b);
     double s0 = 0.0, s1 = 0.0;
     int j = lane * 2;
     for (; j + 1 < b; j += 64) {
@@ -428,18 +516,15 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
     const float* X = xinv + k * bs * bs;
     {  // partial[c][j] = sum over this CTA's rows i of X[i][j] r[k0+i]
       const int per = (b + G - 1) / G, i0 = c * per, i1 = i0 + per < b ? i0 + per : b;
-      for (int j = tid; j < b; j += PC_THREADS) {
+      if (vec) colsum4(X, bs, x + k0, i0, i1 > i0 ? i1 : i0, b, partial + int64_t(c) * bs);
+      else for (int j = tid; j < b; j += PC_THREADS) {
         double acc = 0.0;
         for (int i = i0; i < i1; ++i) acc = fma(double(X[int64_t(i) * bs + j]), x[k0 + i], acc);
         partial[int64_t(c) * bs + j] = acc;
       }
     }
     grid.sync();
-    if (gtid < b) {
-      double y = 0.0;
-      for (int q = 0; q < G; ++q) y += partial[int64_t(q) * bs + gtid];
-      tv[gtid] = y;
-    }
+    reduce_partials(b, nullptr);
     grid.sync();
     for (int j = tid; j < b; j += PC_THREADS) sv[j] = tv[j];
     __syncthreads();
@@ -459,7 +544,8 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
     {  // partial[c][j] = sum over this CTA's rows r >= k1 of L[r][k0+j] x[r]
       const int64_t rows = n - k1, per = (rows + G - 1) / G, r0 = k1 + c * per;
       const int64_t r1 = r0 + per < n ? r0 + per : n;
-      for (int j = tid; j < b; j += PC_THREADS) {
+      if (vec) colsum4(L + k0, ld, x, r0, r1 > r0 ? r1 : r0, b, partial + int64_t(c) * bs);
+      else for (int j = tid; j < b; j += PC_THREADS) {
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // four chains: loads in flight
         int64_t r = r0;
         for (; r + 3 < r1; r += 4) {
@@ -473,11 +559,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
       }
     }
     grid.sync();
-    if (gtid < b) {
-      double t = 0.0;
-      for (int q = 0; q < G; ++q) t += partial[int64_t(q) * bs + gtid];
-      tv[gtid] = x[k0 + gtid] - t;
-    }
+    reduce_partials(b, x + k0);
     grid.sync();
     for (int j = tid; j < b; j += PC_THREADS) sv[j] = tv[j];
     __syncthreads();
@@ -490,6 +572,7 @@ __global__ void __launch_bounds__(PC_THREADS, 1)
 }
 
 int g_potrs_coop = 1;  // bf_set_option("potrs_coop", 0|1): the refinement solve as one cooperative kernel
+int g_potrs_vec = 1;   // bf_set_option("potrs_vec", 0|1): float4 streams in the cooperative solve
 
 // Blocked solve with the explicit inverses X_k = L_kk^-T of the diagonal
 // blocks (xinv: nblk x bs x bs fp32, X_k row-major ld bs). Every step is a
@@ -511,7 +594,10 @@ int launch_potrs_blocked(const float* L, int64_t ld, const float* xinv, int64_t 
     int G = sms * (per_sm > 0 ? 1 : 0);
     if (G > kPotrsMaxChunks) G = kPotrsMaxChunks;  // partial rows the work buffer holds
     if (G >= 1) {
-      void* args[] = {(void*)&L, (void*)&ld, (void*)&xinv, (void*)&bs, (void*)&x, (void*)&n, (void*)&partial, (void*)&t};
+      int vec = g_potrs_vec && reinterpret_cast<uintptr_t>(L) % 16 == 0 && reinterpret_cast<uintptr_t>(xinv) % 16 == 0 &&
+                ld % 4 == 0 && bs % 4 == 0 && n % 4 == 0;
+      void* args[] = {(void*)&L,    (void*)&ld,      (void*)&xinv, (void*)&bs, (void*)&x,
+                      (void*)&n,    (void*)&partial, (void*)&t,    (void*)&vec};
       note_launch();
       if (cudaLaunchCooperativeKernel(reinterpret_cast<void*>(potrs_coop_kernel), dim3(G), dim3(PC_THREADS), args, 0,
                                       s) == cudaSuccess)

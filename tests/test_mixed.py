@@ -132,10 +132,13 @@ def test_mixed_solve_reaches_fp64_accuracy(cuda, n, bs, lookahead, precision):
     assert np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref) <= 100 * n * eps
 
 
-def test_blocked_potrs_matches_direct_solve(cuda):
+@pytest.mark.parametrize("opts", [{}, {"potrs_vec": 0}, {"potrs_coop": 0}], ids=["vec", "scalar", "launches"])
+@pytest.mark.parametrize("n,bs", [(700, 256), (702, 256), (4100, 2048), (2048, 1024)])
+def test_blocked_potrs_matches_direct_solve(cuda, n, bs, opts):
+    """ragged last blocks; n % 4 != 0 (702) takes the cooperative kernel's
+    scalar form even with potrs_vec = 1"""
     from paper_2604_07311_b200.mixed import cholesky_mixed
 
-    n, bs = 700, 256  # ragged last block
     g = torch.Generator(device="cuda")
     g.manual_seed(3)
     m = torch.rand(n, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
@@ -147,7 +150,14 @@ def test_blocked_potrs_matches_direct_solve(cuda):
     x1, x2 = rhs.clone(), rhs.clone()
     work = torch.empty(129 * bs, dtype=torch.float64, device="cuda")
     assert lib.bf_potrs_f32_d(f.w.data_ptr(), n, x1.data_ptr(), n, s) == 0
-    assert lib.bf_potrs_blocked_f32_d(f.w.data_ptr(), n, f.xinv.data_ptr(), bs, x2.data_ptr(), n, work.data_ptr(), s) == 0
+    try:
+        for k, v in opts.items():
+            assert lib.bf_set_option(k.encode(), v) == 0
+        assert lib.bf_potrs_blocked_f32_d(f.w.data_ptr(), n, f.xinv.data_ptr(), bs, x2.data_ptr(), n,
+                                          work.data_ptr(), s) == 0
+    finally:
+        for k in opts:
+            lib.bf_set_option(k.encode(), 1)
     lw = torch.tril(f.w).double().cpu().numpy()
     ref = np.linalg.solve(lw @ lw.T, rhs.cpu().numpy())
     for x in (x1, x2):  # fp64 arithmetic on the fp32 factor; the blocked one uses fp32 inverses

@@ -13,7 +13,7 @@ from paper_2604_07311_b200.engine import _lib  # noqa: E402
 from paper_2604_07311_b200.mixed import MixedWorkspace, cholesky_mixed  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
-bs = 1024
+bs = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
 a0 = bench.make_spd(bf, torch, n, torch.device("cuda"))
 a = a0 + a0.T
 a.diagonal().sub_(a0.diagonal())

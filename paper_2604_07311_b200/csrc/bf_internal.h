@@ -172,6 +172,11 @@ extern int g_trsm_warp;       // fused TRSM subtree: 4-warps-per-32-rows kernel 
 extern int g_pdl;             // bf_set_option("pdl", 0|1): programmatic dependent launch on the chain kernels
 extern int g_leaf_pipe;       // bf_set_option("leaf_pipe", 0|1)
 extern int g_leaf_blocked;    // variant-3 leaves n <= 128: blocked lane-per-row kernel (1) or v3 (0)
+extern int g_fused_diag;      // bf_set_option("fused_diag", 0|1|2): one-launch diagonal factor (small_kernels.cu)
+extern thread_local int t_diag_ctas;  // capi.cu: CTAs of the next fused diagonal factor (0: one per SM)
+int fused_diag_stats(int64_t* out9);
+int launch_potrf_diag_fused(double* a, int64_t off, int64_t n, int64_t ld, int64_t kc, int64_t base_index,
+                            int* d_info, int ctas, cudaStream_t s);
 extern int g_lu_grid_max;     // LU leaf: cap on the cooperative grid (0 = SM-derived)
 extern int g_lu_global;       // LU leaf: force the global-memory kernel
 extern int g_lu_noprefetch;   // LU leaf: no candidate-row prefetch

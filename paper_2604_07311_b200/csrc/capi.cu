@@ -34,6 +34,8 @@ void scratch_account(int64_t delta) {
 // Device scratch private to one (purpose, device, stream): work queued on
 // different streams never shares a buffer, and growing one only waits for
 // its own stream.
+thread_local int t_diag_ctas = 0;  // CTAs of the next fused diagonal factor (0: one per SM)
+
 void* stream_scratch(int tag, size_t bytes, cudaStream_t s) {
   struct Key {
     int tag, dev;
@@ -477,6 +479,30 @@ int leaf_impl(Mode mode, const bf_view& a, int variant, int64_t base, int* d_inf
   return rc ? fail(BF_ERR_CUDA, "leaf launch failed") : BF_OK;
 }
 
+// Node lv[idx] on `a` runs as one fused launch (launch_potrf_diag_fused):
+// FP64, unit column stride, {variant 3, bs 128, kc >= 128} over the
+// unblocked3 leaf (the blocked leaf kernel), 128 < n <= 2048.  Option
+// "fused_diag": 1 (default) where nothing trails the factor's inner steps
+// (chol_impl / chol_run: standalone factors, the last lookahead panel, the
+// distributed driver's diagonal tiles); 2 also in chol_v3_events, whose
+// inner-step events let the overlapped panel TRSM (C2) and the mixed
+// driver's inverse (C4) trail the factor — one launch makes them wait for
+// all of it, which measured slower there (C2 370 -> 376 ms, C4 factor 55.5
+// -> 78 ms, tools/gpu_r02_fused_e2e.sh); 0 off.
+bool fused_diag_ok(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int idx) {
+  if (!bf::g_fused_diag || !bf::g_leaf_blocked || mode != MODE_D || a.cs != 1 || idx >= nl) return false;
+  const bf_chol_level& in = lv[idx];
+  if (in.variant != 3 || in.bs != 128 || in.kc < 128) return false;
+  if (idx + 1 < nl && lv[idx + 1].variant != 13) return false;
+  return a.n > 128 && a.n <= 2048 && a.m == a.n;
+}
+int g_fused_diag_ctas = 0;  // bf_set_option("fused_diag_ctas", c): force the fused factor's grid (0: driver's choice)
+int fused_diag(const bf_view& a, const bf_chol_level& in, int64_t base, int* d_info, cudaStream_t s) {
+  const int rc = bf::launch_potrf_diag_fused(static_cast<double*>(a.base), a.off, a.n, a.rs, in.kc, base, d_info,
+                                             g_fused_diag_ctas > 0 ? g_fused_diag_ctas : bf::t_diag_ctas, s);
+  return rc ? fail(BF_ERR_CUDA, "fused diagonal factor launch failed") : BF_OK;
+}
+
 // factor/cholesky.py:118-158 (_run / _recurse) on a flattened control tree.
 int chol_run(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int idx, int64_t base, int* d_info,
              cudaStream_t s) {
@@ -492,6 +518,7 @@ int chol_run(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int i
   }
   if (node.variant >= 11 && node.variant <= 13) return leaf_impl(mode, a, node.variant - 10, base, d_info, s);
   if (node.variant < 1 || node.variant > 3) return fail(BF_ERR_VALUE, "unknown blocked variant");
+  if (fused_diag_ok(mode, a, lv, nl, idx)) return fused_diag(a, node, base, d_info, s);
   if (node.bs < 1) return fail(BF_ERR_VALUE, "blocked node requires bs >= 1");
   const int64_t bs = node.bs, kc = node.kc;
   int rc = BF_OK;
@@ -599,6 +626,11 @@ int chol_v3_events(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl,
                    cudaStream_t st, const cudaEvent_t* ev) {
   const bf_chol_level& in = lv[idx];
   const int64_t b = a.n, bs1 = in.bs, ns = (b + bs1 - 1) / bs1;
+  if (bf::g_fused_diag >= 2 && fused_diag_ok(mode, a, lv, nl, idx)) {  // one launch: every inner step final at its end
+    const int rc = fused_diag(a, in, base, d_info, st);
+    for (int64_t j = 0; j < ns; ++j) cudaEventRecord(ev[size_t(j)], st);
+    return rc;
+  }
   int rc = BF_OK;
   for (int64_t j = 0; j < ns && rc == BF_OK; ++j) {
     const int64_t done = j * bs1, bb = bs1 < b - done ? bs1 : b - done;
@@ -892,7 +924,19 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
       ts.panel_begin = mark(ps);
       diag_mark = &ts.panel_diag;
     }
+    {  // a fused diagonal factor keeps to the SMs the rest of this step's update leaves free
+      const int64_t m3 = nr2 - b2;
+      int R = 0;
+      if (m3 > 0) {
+        R = (g_tail_reserve > 0 && m3 <= g_tail_rows) ? (g_reserve_adaptive ? adaptive_reserve(m3, b2, b)
+                                                                               : g_tail_reserve)
+                                                     : 16;
+        if (R < 1) R = 16;
+      }
+      bf::t_diag_ctas = R;
+    }
     rc = panel(r2, b2, ps, early ? ev_main : nullptr);
+    bf::t_diag_ctas = 0;
     diag_mark = nullptr;
     if (rc) break;
     if (g_timeline) ts.panel_end = mark(ps);
@@ -1142,6 +1186,7 @@ int chol_impl(Mode mode, const bf_view* a, const bf_chol_level* lv, int nl, int*
     }
     // no room for the copy: factor in place on the cp.async kernel
   }
+  if (fused_diag_ok(mode, *a, lv, nl, 0)) return fused_diag(*a, lv[0], 0, d_info, s);
   if (lv[0].variant == 3 && lv[0].bs >= 1 && a->n > 2 * lv[0].bs && g_lookahead)
     return chol_v3_lookahead(mode, *a, lv, nl, 0, d_info, s);
   return chol_run(mode, *a, lv, nl, 0, 0, d_info, s);
@@ -1228,6 +1273,8 @@ cudaStream_t panel_stream_for(cudaStream_t caller) { return panel_stream(caller)
 extern "C" {
 
 int bf_abi_version(void) { return 1; }
+// tools only (not in include/): the last fused diagonal factor's task profile
+int bf_fused_diag_stats(int64_t* out9) { return bf::fused_diag_stats(out9); }
 int64_t bf_launch_count(void) { return bf::g_launches.load(std::memory_order_relaxed); }
 const char* bf_last_error(void) { return g_last_error.c_str(); }
 
@@ -1280,6 +1327,14 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "potrs_coop") == 0) {
     bf::g_potrs_coop = value != 0;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "fused_diag") == 0) {
+    bf::g_fused_diag = int(value);
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "fused_diag_ctas") == 0 && value >= 0) {
+    g_fused_diag_ctas = int(value);
     return BF_OK;
   }
   if (name && std::strcmp(name, "potrs_vec") == 0) {

@@ -802,7 +802,9 @@ int bf_cholesky_mixed(const bf_view* a, float* w, int64_t ldw, void* pbuf0, void
     }
     // (2) panel k+1 on the side stream, (3) the rest of the trailing triangle
     // on the main stream, leaving g_mixed_reserve SMs to the side chain
+    t_diag_ctas = lookahead && r > nb ? g_mixed_reserve : 0;  // a fused diagonal factor stays on those SMs
     rc = diag_and_panel(k + 1, side);
+    t_diag_ctas = 0;
     cudaEventRecord(ev_side, side);
     if (!rc && r > nb) {
       const char* rest = pk + size_t(nb) * bs * esz;

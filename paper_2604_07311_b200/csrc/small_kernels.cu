@@ -780,14 +780,12 @@ struct TrsmGroup {
 
 
 // R groups (32 rows each) per CTA share the staged triangle
+// The body of trsm_warp_right_kernel for CTA (row block) blk, staging in
+// tw_smem; also run by potrf_diag_fused_kernel (R = 1)
 template <typename T, int R>
-__global__ void __launch_bounds__(128 * R) trsm_warp_right_kernel(double alpha, const T* t, int64_t toff, int64_t trs,
-                                                                  int64_t tcs, T* b, int64_t boff, int64_t brs,
-                                                                  int64_t bcs, int64_t m, int n, int64_t kc,
-                                                                  const int* abort_flag) {
-  pdl_wait();
-  if (abort_flag != nullptr && *abort_flag >= 0) return;
-  extern __shared__ __align__(16) unsigned char tw_smem[];
+__device__ __forceinline__ void trsm_warp_right_body(double alpha, const T* t, int64_t toff, int64_t trs, int64_t tcs,
+                                                     T* b, int64_t boff, int64_t brs, int64_t bcs, int64_t m, int n,
+                                                     int64_t kc, int64_t blk, unsigned char* tw_smem, bool trigger) {
   T* sl = reinterpret_cast<T*>(tw_smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = warp >> 2, gw = warp & 3;
@@ -817,7 +815,7 @@ __global__ void __launch_bounds__(128 * R) trsm_warp_right_kernel(double alpha, 
       }
   }
   // the group's 32 rows, zero-filled past m; lanes run along a row (coalesced)
-  const int64_t r0 = (int64_t(blockIdx.x) * R + grp) * 32;
+  const int64_t r0 = (blk * R + grp) * 32;
   const int rows = int(m - r0 < 32 ? (m - r0 > 0 ? m - r0 : 0) : 32);
   if (bcs == 1) {
     for (int r = gw; r < 32; r += 4) {
@@ -846,7 +844,7 @@ __global__ void __launch_bounds__(128 * R) trsm_warp_right_kernel(double alpha, 
   if (rows > 0) {  // uniform per group
     TrsmGroup<T> tg{sx, sl, lane, gw, 1 + grp, kc};
     tg.solve(0, n, alpha);
-    pdl_trigger();
+    if (trigger) pdl_trigger();
     if (bcs == 1) {
       for (int r = gw; r < rows; r += 4)
         for (int c = lane; c < n; c += 32) b[boff + (r0 + r) * brs + c] = sx[c * TW_XLD + r];
@@ -854,6 +852,18 @@ __global__ void __launch_bounds__(128 * R) trsm_warp_right_kernel(double alpha, 
       for (int c = gw; c < n; c += 4) b[boff + (r0 + lane) * brs + c * bcs] = sx[c * TW_XLD + lane];
     }
   }
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(128 * R) trsm_warp_right_kernel(double alpha, const T* t, int64_t toff, int64_t trs,
+                                                                  int64_t tcs, T* b, int64_t boff, int64_t brs,
+                                                                  int64_t bcs, int64_t m, int n, int64_t kc,
+                                                                  const int* abort_flag) {
+  pdl_wait();
+  if (abort_flag != nullptr && *abort_flag >= 0) return;
+  extern __shared__ __align__(16) unsigned char tw_smem[];
+  trsm_warp_right_body<T, R>(alpha, t, toff, trs, tcs, b, boff, brs, bcs, m, n, kc, int64_t(blockIdx.x), tw_smem,
+                             true);
 }
 
 // ------------------------------------------------ blocked variant-3 leaf --
@@ -958,13 +968,13 @@ struct LeafMath<double> {
   }
 };
 
+// The blocked leaf on one CTA of 128 threads (the body of
+// potrf_leaf_blocked_kernel, also run by potrf_diag_fused_kernel): factors
+// the n x n tile at g + off in place, staging it in A (128 x LV4_LD of
+// dynamic shared memory); returns the failing pivot (-1: none).
 template <typename T>
-__global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t off, int n, int64_t rs, int64_t cs,
-                                                                 int64_t base_index, int* d_info, int pipe_flag) {
-  pdl_wait();
-  if (d_info != nullptr && *d_info >= 0) return;
-  extern __shared__ __align__(16) unsigned char leaf_b_smem[];
-  T* A = reinterpret_cast<T*>(leaf_b_smem);
+__device__ __forceinline__ int leaf_blocked_body(T* g, int64_t off, int n, int64_t rs, int64_t cs, int pipe_flag,
+                                                 T* A, bool trigger) {
   __shared__ T s_rc[128];
   __shared__ __align__(16) T s_cb[4 * 128];  // per warp: two 64-entry column buffers
   __shared__ int s_fail;
@@ -1187,7 +1197,7 @@ __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t o
     bad = leaf_v3<T, 128>(Mat<T>{A, LV4_LD, 1}, n, &s_fail, &s_d);
     __syncthreads();
   }
-  pdl_trigger();  // the next kernel of the chain may launch (it waits for this one's completion)
+  if (trigger) pdl_trigger();  // the next kernel of the chain may launch (it waits for this one's completion)
   if (cs == 1) {
     for (int i = warp; i < n; i += 4)
       for (int j = lane; j <= i; j += 32) g[off + i * rs + j] = A[i * LV4_LD + j];
@@ -1195,7 +1205,289 @@ __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t o
     for (int j = warp; j < n; j += 4)
       for (int i = j + lane; i < n; i += 32) g[off + i * rs + j * cs] = A[i * LV4_LD + j];
   }
-  if (tid == 0 && bad >= 0 && d_info != nullptr) *d_info = int(base_index + bad);
+  return bad;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t off, int n, int64_t rs, int64_t cs,
+                                                                 int64_t base_index, int* d_info, int pipe_flag) {
+  pdl_wait();
+  if (d_info != nullptr && *d_info >= 0) return;
+  extern __shared__ __align__(16) unsigned char leaf_b_smem[];
+  const int bad = leaf_blocked_body<T>(g, off, n, rs, cs, pipe_flag, reinterpret_cast<T*>(leaf_b_smem), true);
+  if (threadIdx.x == 0 && bad >= 0 && d_info != nullptr) *d_info = int(base_index + bad);
+}
+
+// --------------------------------------------- fused diagonal-block factor --
+// One launch for a whole diagonal block of order n <= 2048 factored by the
+// tree level {variant 3, bs 128, kc >= 128} over the unblocked3 leaf — the
+// bench tree's child, which otherwise costs ~45 launches (16 leaves, 15
+// TRSMs, 15 trailing GEMMTs) whose latencies form the panel chain.  Same
+// operations per element as that launch sequence, hence the same bits:
+//   L(c)       the leaf of tile (c, c)            leaf_blocked_body
+//   T(c, r)    rows 32r.. of the tile column      trsm_warp_right_body
+//              below it, solved against L(c)
+//   S(j, x, u) 64 x 64 unit u of tile column x:   one ascending fma chain over
+//              C -= L(:, j) L(:, j)^T             the step's 128 k (one kc
+//                                                 segment from +0) and the
+//                                                 unfused fold c + (-1 * t)
+// Every element takes its step updates in step order, as in the sequence.
+// Persistent CTAs claim tasks by ticket in a topological order — round c =
+// L(c), S(0..c-1, c+1, *), T(c, *), S(c, c+1, *) — and wait (acquire
+// spins) only for tasks with smaller tickets, which are held by running
+// CTAs: no co-residency is needed and any grid size works.  While one CTA
+// runs the leaf chain, the others apply the older steps' updates to the next
+// tile column (the lookahead of the launch sequence, inside one kernel).
+// A pivot failure at L(c) stops steps >= c; the updates of steps < c still
+// complete — the sequence's partial state.
+constexpr int FD_B = 128;    // inner block
+constexpr int FD_ULD = 68;   // k-major stride of a staged 64-row unit operand
+constexpr int FD_MAXN = 2048;
+constexpr size_t FD_SMEM = (size_t(2) * 128 * FD_ULD + 64 * 64) * sizeof(double);  // the update's, the largest
+static_assert(size_t(128) * LV4_LD * sizeof(double) <= FD_SMEM, "leaf staging");
+static_assert((size_t(128) * TW_LD + size_t(128) * TW_XLD) * sizeof(double) <= FD_SMEM, "trsm staging");
+
+struct FdCounters {  // zeroed before the launch
+  unsigned long long prof[12];  // per task kind (leaf, trsm, update): tasks, wait cycles, run cycles; update phases
+  int ticket, fail1, err, pad;
+  int leaf_done[FD_MAXN / FD_B], tdone[FD_MAXN / FD_B];
+  int ucnt[(FD_MAXN / 64) * (FD_MAXN / 64 + 1) / 2];
+};
+
+__device__ __forceinline__ int fd_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// thread 0: wait until *p >= v (bounded: a stuck wait records err and gives up)
+__device__ __forceinline__ void fd_wait(const int* p, int v, int* err) {
+  if (fd_acquire(p) >= v) return;
+  const long long t0 = clock64();
+  while (fd_acquire(p) < v) {
+    if (fd_acquire(err)) return;
+    __nanosleep(64);
+    if (clock64() - t0 > (1LL << 33)) {
+      atomicExch(err, 1);
+      return;
+    }
+  }
+}
+// after the CTA's writes: __syncthreads, then thread 0 releases
+__device__ __forceinline__ void fd_release_add(int* p) {
+  __threadfence();
+  atomicAdd(p, 1);
+}
+
+struct FdShape {
+  int n, T, NS;
+  __device__ int units(int x) const { return 2 * x + 1 < NS ? 2 * NS - 4 * x - 1 : NS - 2 * x; }
+  __device__ int chunks(int c) const { return (c + 1) * FD_B < n ? (n - (c + 1) * FD_B + 31) / 32 : 0; }
+  __device__ int round_size(int c) const {
+    return 1 + chunks(c) + (c + 1 < T ? (c + 1) * units(c + 1) : 0);
+  }
+  // unit u of tile column x -> 64-row block I, 64-column block J: the
+  // diagonal tile's (up to) three units first, then row pairs below
+  __device__ void unit(int x, int u, int& I, int& J) const {
+    const int J0 = 2 * x;
+    if (2 * x + 1 >= NS) {
+      I = J0 + u, J = J0;
+    } else if (u < 3) {
+      I = J0 + (u > 0), J = J0 + (u == 2);
+    } else {
+      I = J0 + 2 + (u - 3) / 2, J = J0 + (u - 3) % 2;
+    }
+  }
+};
+
+// C(64 x 64 unit at rows 64I, cols 64J) -= P_I P_J^T, P = the 128 columns of
+// step j; lower part only on a diagonal unit.  Operands staged k-major (the
+// DMMA fragment loads are bank-conflict free at stride 68).
+__device__ __forceinline__ void fd_update_unit(double* g, int64_t off, int64_t ld, int n, int j, int I, int J,
+                                               double* sm, unsigned long long* prof) {
+  const int tid = threadIdx.x;
+  const long long c0 = clock64();
+  const int i0 = I * 64, j0 = J * 64, p0 = j * FD_B;
+  const int mi = n - i0 < 64 ? n - i0 : 64, mj = n - j0 < 64 ? n - j0 : 64;
+  double* As = sm;
+  double* Bs = sm + 128 * FD_ULD;
+  // staged with cp.async in two groups — the C unit and k < 64, then k >= 64
+  // — so the second half lands under the first half's DMMAs; rows past the
+  // edge zero-filled.  The L1 holds nothing stale: the task's acquire
+  // (ld.acquire.gpu) invalidated it.
+  double* Cs = sm + 2 * 128 * FD_ULD;
+  for (int e = tid; e < 64 * 64; e += 128) {
+    const int r = e >> 6, cc = e & 63;
+    const bool ok = r < mi && cc < mj;
+    cp_async_8(&Cs[e], ok ? &g[off + int64_t(i0 + r) * ld + j0 + cc] : g, ok ? 8 : 0);
+  }
+#pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+    for (int e = tid; e < 64 * 64; e += 128) {
+      const int r = e >> 6, p = half * 64 + (e & 63);
+      cp_async_8(&As[p * FD_ULD + r], r < mi ? &g[off + int64_t(i0 + r) * ld + p0 + p] : g, r < mi ? 8 : 0);
+      cp_async_8(&Bs[p * FD_ULD + r], r < mj ? &g[off + int64_t(j0 + r) * ld + p0 + p] : g, r < mj ? 8 : 0);
+    }
+    cp_async_commit();
+  }
+  cp_async_wait<1>();
+  __syncthreads();
+  const long long c1 = clock64();
+  // warp w: the 32 x 32 block at rows 32 (w & 1), cols 32 (w >> 1) as 4 x 4
+  // DMMA m8n8k4 tiles (d = a b + d is the ascending fma chain); lane holds
+  // A[8m + lane / 4][k + lane % 4], B[k + lane % 4][8nn + lane / 4] and
+  // C[8m + lane / 4][8nn + 2 (lane % 4) + e]
+  const int warp = tid >> 5, lane = tid & 31;
+  const int rb = 32 * (warp & 1), cb = 32 * (warp >> 1), lr = lane >> 2, lk = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn) acc[m][nn][0] = acc[m][nn][1] = 0.0;
+#pragma unroll 2
+  for (int k = 0; k < 128; k += 4) {
+    if (k == 64) {  // the second half of the operands
+      cp_async_wait<0>();
+      __syncthreads();
+    }
+    const double* ak = As + (k + lk) * FD_ULD + rb + lr;
+    const double* bk = Bs + (k + lk) * FD_ULD + cb + lr;
+    double av[4], bv[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) av[m] = ak[8 * m];
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn) bv[nn] = bk[8 * nn];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int nn = 0; nn < 4; ++nn) dmma_8x8x4(acc[m][nn][0], acc[m][nn][1], av[m], bv[nn]);
+  }
+  const long long c2 = clock64();
+  // fold from the staged C: beta*c + alpha*t with beta = 1, alpha = -1
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int nn = 0; nn < 4; ++nn)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int il = rb + 8 * m + lr, jl = cb + 8 * nn + 2 * lk + e;
+        if (il < mi && jl < mj && (I != J || il >= jl))
+          g[off + int64_t(i0 + il) * ld + j0 + jl] = __dadd_rn(Cs[il * 64 + jl], -acc[m][nn][e]);
+      }
+  if (tid == 0) {
+    atomicAdd(&prof[9], (unsigned long long)(c1 - c0));
+    atomicAdd(&prof[10], (unsigned long long)(c2 - c1));
+    atomicAdd(&prof[11], (unsigned long long)(clock64() - c2));
+  }
+}
+
+__global__ void __launch_bounds__(128) potrf_diag_fused_kernel(double* g, int64_t off, int n, int64_t ld, int64_t kc,
+                                                               int64_t base_index, int* d_info, int pipe_flag,
+                                                               FdCounters* ctl) {
+  if (d_info != nullptr && *d_info >= 0) return;
+  extern __shared__ __align__(16) unsigned char fd_smem[];
+  __shared__ int s_task, s_skip;
+  const int tid = threadIdx.x;
+  const FdShape sh{n, (n + FD_B - 1) / FD_B, (n + 63) / 64};
+  int total = 0;
+  for (int c = 0; c < sh.T; ++c) total += sh.round_size(c);
+  int* err = &ctl->err;
+  auto ucnt = [&](int I, int J) { return &ctl->ucnt[I * (I + 1) / 2 + J]; };
+  // skip a task of step j once a leaf at step <= j has failed
+  auto decide_skip = [&](int j) {
+    if (tid == 0) {
+      const int f = fd_acquire(&ctl->fail1);
+      s_skip = f != 0 && f - 1 <= j;
+    }
+    __syncthreads();
+    return s_skip != 0;
+  };
+  for (;;) {
+    if (tid == 0) s_task = atomicAdd(&ctl->ticket, 1);
+    __syncthreads();
+    int q = s_task;
+    __syncthreads();
+    if (q >= total) break;
+    int c = 0;
+    while (q >= sh.round_size(c)) q -= sh.round_size(c++);
+    const int U = c + 1 < sh.T ? sh.units(c + 1) : 0;
+    const int R = sh.chunks(c);
+    const long long t_claim = clock64();
+    long long t_ready = 0;
+    auto prof = [&](int kind) {  // thread 0, after the task
+      if (tid == 0) {
+        atomicAdd(&ctl->prof[3 * kind], 1ull);
+        atomicAdd(&ctl->prof[3 * kind + 1], (unsigned long long)(t_ready - t_claim));
+        atomicAdd(&ctl->prof[3 * kind + 2], (unsigned long long)(clock64() - t_ready));
+      }
+    };
+    if (q == 0) {  // L(c)
+      if (tid == 0) {
+        const int J0 = 2 * c;
+        fd_wait(ucnt(J0, J0), c, err);
+        if (J0 + 1 < sh.NS) {
+          fd_wait(ucnt(J0 + 1, J0), c, err);
+          fd_wait(ucnt(J0 + 1, J0 + 1), c, err);
+        }
+      }
+      __syncthreads();
+      t_ready = clock64();
+      if (!decide_skip(c)) {
+        const int kb = n - c * FD_B < FD_B ? n - c * FD_B : FD_B;
+        const int bad = leaf_blocked_body<double>(g, off + int64_t(c) * FD_B * (ld + 1), kb, ld, 1, pipe_flag,
+                                                  reinterpret_cast<double*>(fd_smem), false);
+        if (tid == 0 && bad >= 0) {
+          ctl->fail1 = c + 1;
+          if (d_info != nullptr) *d_info = int(base_index + int64_t(c) * FD_B + bad);
+        }
+      }
+      __syncthreads();
+      if (tid == 0) fd_release_add(&ctl->leaf_done[c]);
+      prof(0);
+      continue;
+    }
+    q -= 1;
+    int j = -1, x = c + 1, u = 0, r = -1;
+    if (q < c * U) {
+      j = q / U, u = q % U;
+    } else if ((q -= c * U) < R) {
+      r = q;
+    } else {
+      j = c, u = q - R;
+    }
+    if (r >= 0) {  // T(c, r)
+      const int row0 = (c + 1) * FD_B + 32 * r;
+      if (tid == 0) {
+        fd_wait(&ctl->leaf_done[c], 1, err);
+        const int I = row0 / 64;
+        fd_wait(ucnt(I, 2 * c), c, err);
+        if (2 * c + 1 < sh.NS) fd_wait(ucnt(I, 2 * c + 1), c, err);
+      }
+      __syncthreads();
+      t_ready = clock64();
+      if (!decide_skip(c)) {
+        const int64_t toff = off + int64_t(c) * FD_B * (ld + 1);
+        trsm_warp_right_body<double, 1>(1.0, g, toff, ld, 1, g, toff + int64_t(FD_B) * ld, ld, 1,
+                                        int64_t(n - (c + 1) * FD_B), FD_B, kc, int64_t(r), fd_smem, false);
+      }
+      __syncthreads();
+      if (tid == 0) fd_release_add(&ctl->tdone[c]);
+      prof(1);
+      continue;
+    }
+    // S(j, x, u)
+    int I, J;
+    sh.unit(x, u, I, J);
+    if (tid == 0) {
+      fd_wait(&ctl->tdone[j], sh.chunks(j), err);
+      fd_wait(ucnt(I, J), j, err);
+    }
+    __syncthreads();
+    t_ready = clock64();
+    if (!decide_skip(j)) fd_update_unit(g, off, ld, n, j, I, J, reinterpret_cast<double*>(fd_smem), ctl->prof);
+    __syncthreads();
+    if (tid == 0) fd_release_add(ucnt(I, J));
+    prof(2);
+  }
 }
 
 template <typename T, int W>
@@ -1299,6 +1591,40 @@ int launch_potrf_leaf(int is_f64, int variant, void* a, int64_t off, int64_t n, 
   if (n > 0x7fffffff) return -3;
   if (is_f64) return leaf_launch<double>((double*)a, off, n, rs, cs, variant, base_index, d_info, s);
   return leaf_launch<float>((float*)a, off, n, rs, cs, variant, base_index, d_info, s);
+}
+
+// The diagonal block a[off..] (n x n, row stride ld, 128 < n <= 2048) factored
+// by {variant 3, bs 128, kc} over the unblocked3 leaf in one launch
+// (potrf_diag_fused_kernel) on `ctas` CTAs (0: one per SM).
+int g_fused_diag = 1;
+static void* g_fd_last = nullptr;  // counters of the last launch (fused_diag_stats)
+// tools: the last fused factor's per-kind task counts and summed wait / run
+// cycles (synchronizes the device)
+int fused_diag_stats(int64_t* out12) {
+  if (!g_fd_last) return -1;
+  unsigned long long h[12];
+  cudaDeviceSynchronize();
+  if (cudaMemcpy(h, g_fd_last, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return -11;
+  for (int i = 0; i < 12; ++i) out12[i] = int64_t(h[i]);
+  return 0;
+}
+int launch_potrf_diag_fused(double* a, int64_t off, int64_t n, int64_t ld, int64_t kc, int64_t base_index,
+                            int* d_info, int ctas, cudaStream_t s) {
+  if (n <= FD_B || n > FD_MAXN || kc < FD_B) return -3;
+  auto* ctl = static_cast<FdCounters*>(stream_scratch(11, sizeof(FdCounters), s));
+  if (!ctl) return -10;
+  g_fd_last = ctl;
+  if (cudaMemsetAsync(ctl, 0, sizeof(FdCounters), s) != cudaSuccess) return -11;
+  if (!smem_attr(reinterpret_cast<const void*>(potrf_diag_fused_kernel), int(FD_SMEM))) return -10;
+  static int sms_dev[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return -3;
+  if (!sms_dev[dev]) cudaDeviceGetAttribute(&sms_dev[dev], cudaDevAttrMultiProcessorCount, dev);
+  const int grid = ctas > 0 && ctas < sms_dev[dev] ? ctas : sms_dev[dev];
+  note_launch();
+  potrf_diag_fused_kernel<<<grid, 128, FD_SMEM, s>>>(a, off, int(n), ld, kc, base_index, d_info, g_leaf_pipe, ctl);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
 int launch_trsm_base_right(int is_f64, double alpha, const void* t, int64_t toff, int64_t trs, int64_t tcs, void* b,

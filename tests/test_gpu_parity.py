@@ -164,6 +164,48 @@ def test_panel_overlap_bitwise(cuda, overlap, npd_at):
     assert digest(v.storage.cpu().numpy()) == digest(st)
 
 
+FUSED_TREE = ('{"op": "cholesky", "variant": 3, "bs": 128, "kernel": {"kc": 128}, '
+              '"child": {"op": "cholesky", "variant": "unblocked3"}}')
+
+
+@pytest.mark.parametrize("ctas", [0, 1, 5])
+@pytest.mark.parametrize("n,npd_at", [(129, None), (200, None), (256, None), (700, None), (1000, None), (2048, None),
+                                      (2048, 5), (2048, 130), (2048, 1000), (2048, 2047), (777, 700), (300, 150)])
+def test_fused_diag_factor_bitwise(cuda, n, npd_at, ctas):
+    """The one-launch diagonal factor (potrf_diag_fused_kernel: leaf, TRSM and
+    update tasks claimed by ticket, any grid size) against the oracle running
+    the same tree: same bits, same pivot index and, after a failure, the same
+    partial state (updates of earlier steps complete, later steps skipped).
+    fused_diag = 0 (the launch sequence) must agree too."""
+    import json
+
+    from paper_2604_07311_b200.engine import _lib
+
+    a0 = spd_int(5150 + n, n)
+    if npd_at is not None:
+        a0[npd_at, npd_at] = -1e9
+    st = a0.reshape(-1).copy()
+    ref_bad = O.cholesky(st, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1},
+                         O.levels_from_tree(json.loads(FUSED_TREE), n, "f64"), nthreads=O.host_threads())
+    assert ref_bad == (-1 if npd_at is None else npd_at)
+    lib = _lib.lib()
+    launches = {}
+    for fused in (1, 0):
+        try:
+            assert lib.bf_set_option(b"fused_diag", fused) == 0
+            assert lib.bf_set_option(b"fused_diag_ctas", ctas) == 0
+            v = make_view(n, n, fill=a0)
+            before = lib.bf_launch_count()
+            bad = int(bf.cholesky_async(v, "lower", parse_tree(FUSED_TREE)).item())
+            launches[fused] = lib.bf_launch_count() - before
+        finally:
+            lib.bf_set_option(b"fused_diag", 1)
+            lib.bf_set_option(b"fused_diag_ctas", 0)
+        assert bad == ref_bad, f"fused={fused}"
+        assert digest(v.storage.cpu().numpy()) == digest(st), f"fused={fused}"
+    assert launches[1] == 1 and launches[0] > 3
+
+
 @pytest.mark.parametrize("kc", [320, 64])
 @pytest.mark.parametrize("npd_at", [None, 700, 1650])
 def test_panel_overlap_ragged_inner_blocks_bitwise(cuda, kc, npd_at):

@@ -35,3 +35,16 @@ for _ in range(reps):
     e1.synchronize()
     ms.append(round(e0.elapsed_time(e1), 3))
 print(f"diag factor bs={bs} tree={json.dumps(child)}: ms {ms}")
+if os.environ.get("BF_OPTS", "").find("fused_diag=0") < 0:
+    import ctypes
+
+    st = (ctypes.c_int64 * 12)()
+    lib = _lib.lib()
+    if lib.bf_fused_diag_stats(st) == 0:
+        for k, name in enumerate(("leaf", "trsm", "update")):
+            cnt = max(st[3 * k], 1)
+            print(f"  {name:6s} tasks {st[3 * k]:5d}  wait {st[3 * k + 1] / cnt / 1.9e3:8.2f} us  "
+                  f"run {st[3 * k + 2] / cnt / 1.9e3:8.2f} us  (sum run {st[3 * k + 2] / 1.9e6:7.3f} ms)")
+        cnt = max(st[6], 1)
+        print(f"  update phases per task: stage {st[9] / cnt / 1.9e3:.2f} us, compute {st[10] / cnt / 1.9e3:.2f} us, "
+              f"fold {st[11] / cnt / 1.9e3:.2f} us")

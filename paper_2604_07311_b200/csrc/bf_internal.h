@@ -175,8 +175,12 @@ extern int g_leaf_blocked;    // variant-3 leaves n <= 128: blocked lane-per-row
 extern int g_fused_diag;      // bf_set_option("fused_diag", 0|1|2): one-launch diagonal factor (small_kernels.cu)
 extern thread_local int t_diag_ctas;  // capi.cu: CTAs of the next fused diagonal factor (0: one per SM)
 int fused_diag_stats(int64_t* out9);
+// after_reset (optional) is recorded between the counter reset and the
+// launch; *colfinal (optional) receives the device flags colfinal[c] (1 once
+// tile column c of the block is final)
 int launch_potrf_diag_fused(double* a, int64_t off, int64_t n, int64_t ld, int64_t kc, int64_t base_index,
-                            int* d_info, int ctas, cudaStream_t s);
+                            int* d_info, int ctas, cudaStream_t s, cudaEvent_t after_reset = nullptr,
+                            int** colfinal = nullptr);
 extern int g_lu_grid_max;     // LU leaf: cap on the cooperative grid (0 = SM-derived)
 extern int g_lu_global;       // LU leaf: force the global-memory kernel
 extern int g_lu_noprefetch;   // LU leaf: no candidate-row prefetch

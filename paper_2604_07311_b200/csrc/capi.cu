@@ -7,6 +7,8 @@
 #include "bf_internal.h"
 #include "blockfam_b200.h"
 
+#include <cuda.h>
+
 #include <atomic>
 #include <climits>
 #include <cstdio>
@@ -288,7 +290,8 @@ int gemm_impl(Mode mode, double alpha, const bf_view& a, const bf_view& b, doubl
 // factorizations enqueued on different caller streams (e.g. from different
 // host threads) get independent panel/aux/copy streams and never serialise
 // their panel chains on a shared one.
-enum SideRole { ROLE_PANEL = 0, ROLE_AUX = 1, ROLE_H2D = 2, ROLE_COPY = 3, ROLE_PANEL2 = 100, ROLE_SEG0 = 4 };
+enum SideRole { ROLE_PANEL = 0, ROLE_AUX = 1, ROLE_H2D = 2, ROLE_COPY = 3, ROLE_PANEL2 = 100, ROLE_SEG0 = 4,
+                ROLE_FDWATCH = 200 };
 cudaStream_t side_stream(SideRole role, cudaStream_t caller) {
   struct Key {
     int dev, role;
@@ -503,6 +506,21 @@ int fused_diag(const bf_view& a, const bf_chol_level& in, int64_t base, int* d_i
   return rc ? fail(BF_ERR_CUDA, "fused diagonal factor launch failed") : BF_OK;
 }
 
+// cuStreamWaitValue32 through the runtime's driver entry point (no libcuda
+// link); nullptr when unavailable
+using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValue32Fn stream_wait_value32() {
+  static WaitValue32Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return WaitValue32Fn(nullptr);
+    return reinterpret_cast<WaitValue32Fn>(p);
+  }();
+  return fn;
+}
+
 // factor/cholesky.py:118-158 (_run / _recurse) on a flattened control tree.
 int chol_run(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl, int idx, int64_t base, int* d_info,
              cudaStream_t s) {
@@ -626,10 +644,47 @@ int chol_v3_events(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl,
                    cudaStream_t st, const cudaEvent_t* ev) {
   const bf_chol_level& in = lv[idx];
   const int64_t b = a.n, bs1 = in.bs, ns = (b + bs1 - 1) / bs1;
-  if (bf::g_fused_diag >= 2 && fused_diag_ok(mode, a, lv, nl, idx)) {  // one launch: every inner step final at its end
-    const int rc = fused_diag(a, in, base, d_info, st);
-    for (int64_t j = 0; j < ns; ++j) cudaEventRecord(ev[size_t(j)], st);
-    return rc;
+  if (bf::g_fused_diag >= 2 && fused_diag_ok(mode, a, lv, nl, idx)) {
+    // one launch; ev[j] fires when the kernel publishes tile column j
+    // (colfinal[j]) through a stream memory wait on a watcher stream, so
+    // whatever trails the inner steps keeps trailing.  Under capture, or
+    // without stream memory waits: every ev[j] after the whole factor.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cap);
+    auto wait_value = stream_wait_value32();
+    cudaStream_t w = (cap == cudaStreamCaptureStatusNone && wait_value) ? side_stream(ROLE_FDWATCH, st) : nullptr;
+    cudaEvent_t reset = nullptr;
+    int* colfinal = nullptr;
+    if (w) cudaEventCreateWithFlags(&reset, cudaEventDisableTiming);
+    const int frc = bf::launch_potrf_diag_fused(static_cast<double*>(a.base), a.off, a.n, a.rs, in.kc, base, d_info,
+                                                g_fused_diag_ctas > 0 ? g_fused_diag_ctas : bf::t_diag_ctas, st,
+                                                reset, w ? &colfinal : nullptr);
+    bool watched = false;
+    if (w && !frc && colfinal) {
+      cudaStreamWaitEvent(w, reset, 0);
+      watched = true;
+      const int64_t cols = (a.n + 127) / 128;  // the kernel's 128-wide tile columns; inner step j ends at column
+      for (int64_t j = 0; j < ns && watched; ++j) {
+        int64_t c = ((j + 1) * bs1 + 127) / 128 - 1;  // the last tile column inner step j's columns reach
+        if (c > cols - 1) c = cols - 1;
+        if (wait_value(reinterpret_cast<CUstream>(w), reinterpret_cast<CUdeviceptr>(colfinal + c), 1,
+                       CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+          watched = false;
+        else
+          cudaEventRecord(ev[size_t(j)], w);
+      }
+    }
+    if (w) {  // the watcher joins st (its last wait is met before the kernel ends)
+      cudaEvent_t j;
+      cudaEventCreateWithFlags(&j, cudaEventDisableTiming);
+      cudaEventRecord(j, w);
+      cudaStreamWaitEvent(st, j, 0);
+      cudaEventDestroy(j);
+    }
+    if (reset) cudaEventDestroy(reset);
+    if (!watched)
+      for (int64_t j = 0; j < ns; ++j) cudaEventRecord(ev[size_t(j)], st);
+    return frc ? fail(BF_ERR_CUDA, "fused diagonal factor launch failed") : BF_OK;
   }
   int rc = BF_OK;
   for (int64_t j = 0; j < ns && rc == BF_OK; ++j) {

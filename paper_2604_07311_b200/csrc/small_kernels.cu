@@ -1251,6 +1251,7 @@ struct FdCounters {  // zeroed before the launch
   unsigned long long prof[12];  // per task kind (leaf, trsm, update): tasks, wait cycles, run cycles; update phases
   int ticket, fail1, err, pad;
   int leaf_done[FD_MAXN / FD_B], tdone[FD_MAXN / FD_B];
+  int colfinal[FD_MAXN / FD_B];  // 1 once tile column c is final (leaf and every TRSM chunk): stream waits watch it
   int ucnt[(FD_MAXN / 64) * (FD_MAXN / 64 + 1) / 2];
 };
 
@@ -1272,10 +1273,16 @@ __device__ __forceinline__ void fd_wait(const int* p, int v, int* err) {
     }
   }
 }
-// after the CTA's writes: __syncthreads, then thread 0 releases
-__device__ __forceinline__ void fd_release_add(int* p) {
+// after the CTA's writes: __syncthreads, then thread 0 releases; returns the old count
+__device__ __forceinline__ int fd_release_add(int* p) {
   __threadfence();
-  atomicAdd(p, 1);
+  return atomicAdd(p, 1);
+}
+// tile column c is final: the flag a stream memory wait polls (after the fence,
+// every write of the column — fenced by its own task before its count — is in L2)
+__device__ __forceinline__ void fd_publish(int* flag) {
+  __threadfence();
+  atomicExch(flag, 1);
 }
 
 struct FdShape {
@@ -1441,7 +1448,10 @@ __global__ void __launch_bounds__(128) potrf_diag_fused_kernel(double* g, int64_
         }
       }
       __syncthreads();
-      if (tid == 0) fd_release_add(&ctl->leaf_done[c]);
+      if (tid == 0) {
+        fd_release_add(&ctl->leaf_done[c]);
+        if (R == 0) fd_publish(&ctl->colfinal[c]);  // the last tile column: no TRSM chunks
+      }
       prof(0);
       continue;
     }
@@ -1470,7 +1480,7 @@ __global__ void __launch_bounds__(128) potrf_diag_fused_kernel(double* g, int64_
                                         int64_t(n - (c + 1) * FD_B), FD_B, kc, int64_t(r), fd_smem, false);
       }
       __syncthreads();
-      if (tid == 0) fd_release_add(&ctl->tdone[c]);
+      if (tid == 0 && fd_release_add(&ctl->tdone[c]) == R - 1) fd_publish(&ctl->colfinal[c]);
       prof(1);
       continue;
     }
@@ -1609,12 +1619,14 @@ int fused_diag_stats(int64_t* out12) {
   return 0;
 }
 int launch_potrf_diag_fused(double* a, int64_t off, int64_t n, int64_t ld, int64_t kc, int64_t base_index,
-                            int* d_info, int ctas, cudaStream_t s) {
+                            int* d_info, int ctas, cudaStream_t s, cudaEvent_t after_reset, int** colfinal) {
   if (n <= FD_B || n > FD_MAXN || kc < FD_B) return -3;
   auto* ctl = static_cast<FdCounters*>(stream_scratch(11, sizeof(FdCounters), s));
   if (!ctl) return -10;
   g_fd_last = ctl;
   if (cudaMemsetAsync(ctl, 0, sizeof(FdCounters), s) != cudaSuccess) return -11;
+  if (after_reset) cudaEventRecord(after_reset, s);
+  if (colfinal) *colfinal = ctl->colfinal;
   if (!smem_attr(reinterpret_cast<const void*>(potrf_diag_fused_kernel), int(FD_SMEM))) return -10;
   static int sms_dev[64] = {};
   int dev = 0;

@@ -206,6 +206,39 @@ def test_fused_diag_factor_bitwise(cuda, n, npd_at, ctas):
     assert launches[1] == 1 and launches[0] > 3
 
 
+OVERLAP_FUSED_TREE = ('{"op": "cholesky", "variant": 3, "bs": 1024, "kernel": {"kc": 1024}, "child": ' + FUSED_TREE + '}')
+
+
+@pytest.mark.parametrize("fused", [2, 1])
+@pytest.mark.parametrize("npd_at", [None, 10, 700, 1100, 2500])
+def test_fused_diag_in_overlapped_panels_bitwise(cuda, fused, npd_at):
+    """fused_diag = 2: the overlapped panels' diagonal factors run as one
+    launch whose per-column flags release the trailing TRSM through stream
+    memory waits.  Same bits as the oracle and the same partial state after a
+    failure in the first panel, a later one and the last one."""
+    import json
+
+    from paper_2604_07311_b200.engine import _lib
+
+    n = 2600
+    a0 = spd_int(6161, n)
+    if npd_at is not None:
+        a0[npd_at, npd_at] = -1e9
+    lib = _lib.lib()
+    try:
+        assert lib.bf_set_option(b"fused_diag", fused) == 0
+        v = make_view(n, n, fill=a0)
+        bad = int(bf.cholesky_async(v, "lower", parse_tree(OVERLAP_FUSED_TREE)).item())
+    finally:
+        lib.bf_set_option(b"fused_diag", 1)
+    st = a0.reshape(-1).copy()
+    ref_bad = O.cholesky(st, {"off": 0, "m": n, "n": n, "rs": n, "cs": 1},
+                         O.levels_from_tree(json.loads(OVERLAP_FUSED_TREE), n, "f64"), nthreads=O.host_threads())
+    assert ref_bad == (-1 if npd_at is None else npd_at)
+    assert bad == ref_bad
+    assert digest(v.storage.cpu().numpy()) == digest(st)
+
+
 @pytest.mark.parametrize("kc", [320, 64])
 @pytest.mark.parametrize("npd_at", [None, 700, 1650])
 def test_panel_overlap_ragged_inner_blocks_bitwise(cuda, kc, npd_at):

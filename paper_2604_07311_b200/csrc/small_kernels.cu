@@ -1390,7 +1390,11 @@ __device__ __forceinline__ void fd_update_unit(double* g, int64_t off, int64_t l
 __global__ void __launch_bounds__(128) potrf_diag_fused_kernel(double* g, int64_t off, int n, int64_t ld, int64_t kc,
                                                                int64_t base_index, int* d_info, int pipe_flag,
                                                                FdCounters* ctl) {
-  if (d_info != nullptr && *d_info >= 0) return;
+  const int ncol = (n + FD_B - 1) / FD_B;
+  if (d_info != nullptr && *d_info >= 0) {  // an earlier failure: nothing to do, but every
+    if (threadIdx.x < ncol) atomicExch(&ctl->colfinal[threadIdx.x], 1);  // column flag is
+    return;                                                                // awaited (fused_diag 2)
+  }
   extern __shared__ __align__(16) unsigned char fd_smem[];
   __shared__ int s_task, s_skip;
   const int tid = threadIdx.x;

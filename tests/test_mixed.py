@@ -164,16 +164,26 @@ def test_blocked_potrs_matches_direct_solve(cuda, n, bs, opts):
         assert np.linalg.norm(x.cpu().numpy() - ref) / np.linalg.norm(ref) <= 1e-5
 
 
-def test_mixed_factor_reports_npd_pivot(cuda):
+@pytest.mark.parametrize("fused", [1, 2])
+@pytest.mark.parametrize("n,bs,bad", [(900, 256, 613), (3000, 1024, 1500), (3000, 1024, 5)])
+def test_mixed_factor_reports_npd_pivot(cuda, n, bs, bad, fused):
+    """fused = 2: the FP64 diagonal blocks as one fused launch each, the inverse
+    released per tile column by stream memory waits — also after a failure
+    (the later blocks' launches publish their columns and exit)."""
     from paper_2604_07311_b200.errors import NotPositiveDefiniteError
     from paper_2604_07311_b200.mixed import cholesky_mixed
 
-    n = 900
     a = torch.eye(n, dtype=torch.float64, device="cuda") * 4
-    a[613, 613] = -1.0
-    with pytest.raises(NotPositiveDefiniteError) as e:
-        cholesky_mixed(a, 256)
-    assert e.value.index == 613
+    a[bad, bad] = -1.0
+    lib = _lib.lib()
+    try:
+        assert lib.bf_set_option(b"fused_diag", fused) == 0
+        with pytest.raises(NotPositiveDefiniteError) as e:
+            cholesky_mixed(a, bs)
+        torch.cuda.synchronize()
+    finally:
+        lib.bf_set_option(b"fused_diag", 1)
+    assert e.value.index == bad
 
 
 @pytest.mark.parametrize("precision", ["bf16", "tf32"])

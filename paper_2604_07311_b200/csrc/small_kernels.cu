@@ -1241,11 +1241,12 @@ __global__ void __launch_bounds__(128) potrf_leaf_blocked_kernel(T* g, int64_t o
 // A pivot failure at L(c) stops steps >= c; the updates of steps < c still
 // complete — the sequence's partial state.
 constexpr int FD_B = 128;    // inner block
-constexpr int FD_ULD = 68;   // k-major stride of a staged 64-row unit operand
+constexpr int FD_ULD = 132;  // row stride of a staged 64 x 128 unit operand
 constexpr int FD_MAXN = 2048;
-constexpr size_t FD_SMEM = (size_t(2) * 128 * FD_ULD + 64 * 64) * sizeof(double);  // the update's, the largest
+constexpr size_t FD_SMEM_UPDATE = (size_t(2) * 64 * FD_ULD + 64 * 64) * sizeof(double);
+constexpr size_t FD_SMEM_TRSM = (size_t(128) * TW_LD + size_t(128) * TW_XLD) * sizeof(double);
+constexpr size_t FD_SMEM = FD_SMEM_UPDATE > FD_SMEM_TRSM ? FD_SMEM_UPDATE : FD_SMEM_TRSM;
 static_assert(size_t(128) * LV4_LD * sizeof(double) <= FD_SMEM, "leaf staging");
-static_assert((size_t(128) * TW_LD + size_t(128) * TW_XLD) * sizeof(double) <= FD_SMEM, "trsm staging");
 
 struct FdCounters {  // zeroed before the launch
   unsigned long long prof[12];  // per task kind (leaf, trsm, update): tasks, wait cycles, run cycles; update phases
@@ -1307,8 +1308,9 @@ struct FdShape {
 };
 
 // C(64 x 64 unit at rows 64I, cols 64J) -= P_I P_J^T, P = the 128 columns of
-// step j; lower part only on a diagonal unit.  Operands staged k-major (the
-// DMMA fragment loads are bank-conflict free at stride 68).
+// step j; lower part only on a diagonal unit.  Operands staged row-major at
+// stride FD_ULD = 132 doubles: rows stay 16-byte aligned for the copies and
+// the DMMA fragment loads (8 rows x 4 k per half-warp pair) are conflict free.
 __device__ __forceinline__ void fd_update_unit(double* g, int64_t off, int64_t ld, int n, int j, int I, int J,
                                                double* sm, unsigned long long* prof) {
   const int tid = threadIdx.x;
@@ -1316,23 +1318,35 @@ __device__ __forceinline__ void fd_update_unit(double* g, int64_t off, int64_t l
   const int i0 = I * 64, j0 = J * 64, p0 = j * FD_B;
   const int mi = n - i0 < 64 ? n - i0 : 64, mj = n - j0 < 64 ? n - j0 : 64;
   double* As = sm;
-  double* Bs = sm + 128 * FD_ULD;
-  // staged with cp.async in two groups — the C unit and k < 64, then k >= 64
-  // — so the second half lands under the first half's DMMAs; rows past the
-  // edge zero-filled.  The L1 holds nothing stale: the task's acquire
-  // (ld.acquire.gpu) invalidated it.
-  double* Cs = sm + 2 * 128 * FD_ULD;
-  for (int e = tid; e < 64 * 64; e += 128) {
-    const int r = e >> 6, cc = e & 63;
-    const bool ok = r < mi && cc < mj;
-    cp_async_8(&Cs[e], ok ? &g[off + int64_t(i0 + r) * ld + j0 + cc] : g, ok ? 8 : 0);
-  }
+  double* Bs = sm + 64 * FD_ULD;
+  double* Cs = sm + 2 * 64 * FD_ULD;  // 64 x 64, row-major
+  // staged with cp.async in two groups — the operands' k < 64 halves, then
+  // their k >= 64 halves and the C unit — so the second group lands under
+  // the first half's DMMAs; rows past the edge zero-filled.  The L1 holds
+  // nothing stale: the task's acquire (ld.acquire.gpu) invalidated it.
+  // 16-byte copies when every row start is 16-byte aligned (even ld and off).
+  const bool v16 = ((off | ld) & 1) == 0 && (reinterpret_cast<uintptr_t>(g) & 15) == 0;
 #pragma unroll 1
   for (int half = 0; half < 2; ++half) {
-    for (int e = tid; e < 64 * 64; e += 128) {
-      const int r = e >> 6, p = half * 64 + (e & 63);
-      cp_async_8(&As[p * FD_ULD + r], r < mi ? &g[off + int64_t(i0 + r) * ld + p0 + p] : g, r < mi ? 8 : 0);
-      cp_async_8(&Bs[p * FD_ULD + r], r < mj ? &g[off + int64_t(j0 + r) * ld + p0 + p] : g, r < mj ? 8 : 0);
+    if (v16) {
+      for (int e = tid; e < 64 * 32; e += 128) {  // (row, k pair)
+        const int r = e >> 5, p = half * 64 + 2 * (e & 31);
+        cp_async_16(&As[r * FD_ULD + p], r < mi ? &g[off + int64_t(i0 + r) * ld + p0 + p] : g, r < mi ? 16 : 0);
+        cp_async_16(&Bs[r * FD_ULD + p], r < mj ? &g[off + int64_t(j0 + r) * ld + p0 + p] : g, r < mj ? 16 : 0);
+      }
+    } else {
+      for (int e = tid; e < 64 * 64; e += 128) {
+        const int r = e >> 6, p = half * 64 + (e & 63);
+        cp_async_8(&As[r * FD_ULD + p], r < mi ? &g[off + int64_t(i0 + r) * ld + p0 + p] : g, r < mi ? 8 : 0);
+        cp_async_8(&Bs[r * FD_ULD + p], r < mj ? &g[off + int64_t(j0 + r) * ld + p0 + p] : g, r < mj ? 8 : 0);
+      }
+    }
+    if (half == 1) {
+      for (int e = tid; e < 64 * 64; e += 128) {
+        const int r = e >> 6, cc = e & 63;
+        const bool ok = r < mi && cc < mj;
+        cp_async_8(&Cs[e], ok ? &g[off + int64_t(i0 + r) * ld + j0 + cc] : g, ok ? 8 : 0);
+      }
     }
     cp_async_commit();
   }
@@ -1356,13 +1370,13 @@ __device__ __forceinline__ void fd_update_unit(double* g, int64_t off, int64_t l
       cp_async_wait<0>();
       __syncthreads();
     }
-    const double* ak = As + (k + lk) * FD_ULD + rb + lr;
-    const double* bk = Bs + (k + lk) * FD_ULD + cb + lr;
+    const double* ak = As + (rb + lr) * FD_ULD + k + lk;
+    const double* bk = Bs + (cb + lr) * FD_ULD + k + lk;
     double av[4], bv[4];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) av[m] = ak[8 * m];
+    for (int m = 0; m < 4; ++m) av[m] = ak[8 * m * FD_ULD];
 #pragma unroll
-    for (int nn = 0; nn < 4; ++nn) bv[nn] = bk[8 * nn];
+    for (int nn = 0; nn < 4; ++nn) bv[nn] = bk[8 * nn * FD_ULD];
 #pragma unroll
     for (int m = 0; m < 4; ++m)
 #pragma unroll

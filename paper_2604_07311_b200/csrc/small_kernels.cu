@@ -1253,6 +1253,7 @@ struct FdCounters {  // zeroed before the launch
   int ticket, fail1, err, pad;
   int leaf_done[FD_MAXN / FD_B], tdone[FD_MAXN / FD_B];
   int colfinal[FD_MAXN / FD_B];  // 1 once tile column c is final (leaf and every TRSM chunk): stream waits watch it
+  int tchunk[FD_MAXN / FD_B][FD_MAXN / 32];  // 1 once TRSM chunk r of step c is solved
   int ucnt[(FD_MAXN / 64) * (FD_MAXN / 64 + 1) / 2];
 };
 
@@ -1498,15 +1499,25 @@ __global__ void __launch_bounds__(128) potrf_diag_fused_kernel(double* g, int64_
                                         int64_t(n - (c + 1) * FD_B), FD_B, kc, int64_t(r), fd_smem, false);
       }
       __syncthreads();
-      if (tid == 0 && fd_release_add(&ctl->tdone[c]) == R - 1) fd_publish(&ctl->colfinal[c]);
+      if (tid == 0) {
+        fd_publish(&ctl->tchunk[c][r]);
+        if (fd_release_add(&ctl->tdone[c]) == R - 1) fd_publish(&ctl->colfinal[c]);
+      }
       prof(1);
       continue;
     }
     // S(j, x, u)
     int I, J;
     sh.unit(x, u, I, J);
-    if (tid == 0) {
-      fd_wait(&ctl->tdone[j], sh.chunks(j), err);
+    if (tid == 0) {  // the TRSM chunks of step j holding rows 64I.. and 64J.. (two each), then step j - 1's fold
+      const int r0 = (j + 1) * FD_B, nr = sh.chunks(j);
+      const int ci = (64 * I - r0) / 32, cj = (64 * J - r0) / 32;
+      fd_wait(&ctl->tchunk[j][ci], 1, err);
+      if (ci + 1 < nr) fd_wait(&ctl->tchunk[j][ci + 1], 1, err);
+      if (cj != ci) {
+        fd_wait(&ctl->tchunk[j][cj], 1, err);
+        if (cj + 1 < nr) fd_wait(&ctl->tchunk[j][cj + 1], 1, err);
+      }
       fd_wait(ucnt(I, J), j, err);
     }
     __syncthreads();

@@ -500,6 +500,7 @@ bool fused_diag_ok(Mode mode, const bf_view& a, const bf_chol_level* lv, int nl,
   return a.n > 128 && a.n <= 2048 && a.m == a.n;
 }
 int g_fused_diag_ctas = 0;  // bf_set_option("fused_diag_ctas", c): force the fused factor's grid (0: driver's choice)
+int g_fused_diag_pct = 100;  // bf_set_option("fused_diag_pct", p): inside the lookahead, p % of the reserved SMs
 int fused_diag(const bf_view& a, const bf_chol_level& in, int64_t base, int* d_info, cudaStream_t s) {
   const int rc = bf::launch_potrf_diag_fused(static_cast<double*>(a.base), a.off, a.n, a.rs, in.kc, base, d_info,
                                              g_fused_diag_ctas > 0 ? g_fused_diag_ctas : bf::t_diag_ctas, s);
@@ -939,7 +940,14 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
     start = r2;
   } else {
     wait_column(s, 0);
+    if (g_fused_diag_pct != 100) {  // the first panel's trailing TRSM needs SMs beside a fused factor
+      int sms = 148, dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      bf::t_diag_ctas = sms * g_fused_diag_pct / 100 > 8 ? sms * g_fused_diag_pct / 100 : 8;
+    }
     rc = panel(0, bs < n ? bs : n, s, nullptr);
+    bf::t_diag_ctas = 0;
     if (rc == BF_OK) writeback_block_column(a, 0, bs < n ? bs : n, s);
   }
   for (int64_t done = start; done < n && rc == BF_OK;) {
@@ -988,6 +996,7 @@ int chol_v3_lookahead(Mode mode, const bf_view& a, const bf_chol_level* lv, int 
                                                      : 16;
         if (R < 1) R = 16;
       }
+      if (R > 0 && g_fused_diag_pct != 100) R = R * g_fused_diag_pct / 100 > 8 ? R * g_fused_diag_pct / 100 : 8;
       bf::t_diag_ctas = R;
     }
     rc = panel(r2, b2, ps, early ? ev_main : nullptr);
@@ -1386,6 +1395,10 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "fused_diag") == 0) {
     bf::g_fused_diag = int(value);
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "fused_diag_pct") == 0 && value >= 1 && value <= 100) {
+    g_fused_diag_pct = int(value);
     return BF_OK;
   }
   if (name && std::strcmp(name, "fused_diag_ctas") == 0 && value >= 0) {

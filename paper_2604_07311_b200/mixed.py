@@ -161,8 +161,7 @@ def posv_mixed(a: torch.Tensor, b: torch.Tensor, bs: int = 2048, tol: Optional[f
     f = cholesky_mixed(a, bs, lookahead=lookahead, ws=ws, precision=precision)
     work = ws.work
     _lib.check(lib.bf_row_abs_sum_d(a.data_ptr(), n, ws.rows.data_ptr(), n, stream), "row sums")
-    norm_a = float(ws.rows.max())
-    norm_b = float(b.abs().max())
+    norm_a, norm_b = torch.stack([ws.rows.max(), b.abs().max()]).tolist()  # one host read
     x, r, d = ws.x, ws.r, ws.d
     x.zero_()
     r.copy_(b)
@@ -174,9 +173,9 @@ def posv_mixed(a: torch.Tensor, b: torch.Tensor, bs: int = 2048, tol: Optional[f
         x.add_(d)
         _lib.check(lib.bf_residual_d(a.data_ptr(), n, x.data_ptr(), b.data_ptr(), r.data_ptr(), n, stream), "residual")
         it += 1
-        xmax = float(x.abs().max())
-        err = float(r.abs().max()) / (norm_a * xmax + norm_b)
-        step_ok = step_tol is None or float(d.abs().max()) <= step_tol * xmax
+        xmax, rmax, dmax = torch.stack([x.abs().max(), r.abs().max(), d.abs().max()]).tolist()  # one host read
+        err = rmax / (norm_a * xmax + norm_b)
+        step_ok = step_tol is None or dmax <= step_tol * xmax
         if err <= tol and step_ok:
             break
     return MixedResult(x, it, err, err <= tol and step_ok)

@@ -112,7 +112,9 @@ const char* bf_last_error(void);
  * "bf16_group" (default 8) the tcgen05 GEMM's band height; "fused_diag"
  * (default 1: where nothing trails the inner steps; 2: everywhere; 0: off)
  * runs a {v3, bs 128, kc >= 128} over unblocked3 diagonal block of order
- * <= 2048 as one launch, "fused_diag_ctas" (default 0) forces its grid. */
+ * <= 2048 as one launch, "fused_diag_ctas" (default 0) forces its grid and
+ * "fused_diag_pct" (default 100) is its share of the reserved SMs inside the
+ * lookahead (with 2). */
 int bf_set_option(const char* name, int64_t value);
 int bf_device_sm_count(void);
 /* With bf_set_option("timeline", 1): per top-level step of the last lookahead

@@ -12,6 +12,8 @@
 #include "bf_common.cuh"
 #include "bf_internal.h"
 
+#include <cstdio>
+
 namespace bf {
 
 int g_trsm_warp = 1;
@@ -1262,16 +1264,18 @@ __device__ __forceinline__ int fd_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// thread 0: wait until *p >= v (bounded: a stuck wait records err and gives up)
+// thread 0: wait until *p >= v.  Bounded: a wait past ~4 s (2^33 cycles) can
+// only be a schedule bug — the kernel traps (a loud launch failure) rather
+// than hang the GPU or return unfinished columns.
 __device__ __forceinline__ void fd_wait(const int* p, int v, int* err) {
   if (fd_acquire(p) >= v) return;
   const long long t0 = clock64();
   while (fd_acquire(p) < v) {
-    if (fd_acquire(err)) return;
     __nanosleep(64);
     if (clock64() - t0 > (1LL << 33)) {
       atomicExch(err, 1);
-      return;
+      printf("potrf_diag_fused_kernel: dependency wait timed out (block %d)\n", int(blockIdx.x));
+      __trap();
     }
   }
 }

@@ -129,6 +129,7 @@ void scratch_account(int64_t delta_bytes);  // every library-owned device buffer
 int set_error(int code, const char* msg);
 cudaStream_t panel_stream_for(cudaStream_t caller);  // the high-priority panel stream paired with `caller`
 extern int g_mixed_reserve;
+extern int g_mixed_inverse;  // mixed.cu: 1 = factor, then the doubling inverse
 extern int g_symv;        // mixed.cu: residual / row sums from the lower triangle of A
 extern int g_potrs_coop;  // mixed.cu: the refinement solve as one cooperative kernel
 extern int g_potrs_vec;   // mixed.cu: float4 streams in that kernel
@@ -175,6 +176,8 @@ extern int g_leaf_blocked;    // variant-3 leaves n <= 128: blocked lane-per-row
 extern int g_fused_diag;      // bf_set_option("fused_diag", 0|1|2): one-launch diagonal factor (small_kernels.cu)
 extern thread_local int t_diag_ctas;  // capi.cu: CTAs of the next fused diagonal factor (0: one per SM)
 int fused_diag_stats(int64_t* out9);
+int launch_trsm_diag_tiles(const double* l, int64_t ldl, double* x, int64_t ldx, int64_t n, int64_t kc,
+                           cudaStream_t s);
 // after_reset (optional) is recorded between the counter reset and the
 // launch; *colfinal (optional) receives the device flags colfinal[c] (1 once
 // tile column c of the block is final)

@@ -1303,6 +1303,48 @@ namespace bf {
 // TRSM trailing the factor's inner steps on a second stream (as the
 // overlapped panels do); returns with st joined.  Falls back to the
 // sequential factor + solve when the tree root is not a blocked variant 3.
+// X = L^-T (upper triangular) of the factored lower block L by recursive
+// doubling: the 128-wide diagonal tiles X_dd = L_dd^-T in one launch
+// (launch_trsm_diag_tiles), then per split L = (A 0; B C) of [o, o + m):
+// X12 = -X11 B^T X22 as two GEMMs — log2(n / 128) dependent levels instead of
+// the right solve's chain of 128-wide leaves.  X holds the identity on entry.
+// Not the reference's TRSM order: the mixed solver's inverse carries no
+// bitwise contract, only FP64 accuracy (its refinement pins the solution).
+int tri_inverse_t_rec(const bf_view& l, const bf_view& x, int64_t o, int64_t m, int64_t kc, double* u,
+                      cudaStream_t s) {
+  if (m <= 128) return BF_OK;
+  int64_t h = ((m / 2 + 127) / 128) * 128;
+  if (h >= m) h = m - 128;
+  int rc = tri_inverse_t_rec(l, x, o, h, kc, u, s);
+  if (!rc) rc = tri_inverse_t_rec(l, x, o + h, m - h, kc, u, s);
+  if (rc) return rc;
+  const bf_view x11 = subview(x, o, h, o, h), x22 = subview(x, o + h, m - h, o + h, m - h);
+  const bf_view x12 = subview(x, o, h, o + h, m - h), b = subview(l, o + h, m - h, o, h);
+  const bf_view uv{u, 0, h, m - h, m - h, 1};
+  rc = gemm_impl(MODE_D, 1.0, x11, transposed(b), 0.0, uv, 0, kc, nullptr, s);  // U = X11 B^T
+  return rc ? rc : gemm_impl(MODE_D, -1.0, uv, x22, 0.0, x12, 0, kc, nullptr, s);  // X12 = -U X22
+}
+int tri_inverse_t_d(const bf_view& l, const bf_view& x, int64_t kc, cudaStream_t s) {
+  const int64_t n = l.n;
+  if (n == 0) return BF_OK;
+  if (l.cs != 1 || x.cs != 1) return fail(BF_ERR_UNSUPPORTED, "doubling inverse needs unit column strides");
+  if (bf::launch_trsm_diag_tiles(static_cast<const double*>(l.base) + l.off, l.rs, static_cast<double*>(x.base) + x.off,
+                                 x.rs, n, kc, s))
+    return fail(BF_ERR_CUDA, "diagonal tile inverse launch failed");
+  if (n <= 128) return BF_OK;
+  const int64_t h = ((n / 2 + 127) / 128) * 128;
+  double* u = static_cast<double*>(bf::stream_scratch(12, size_t(h) * size_t(n - h) * sizeof(double), s));
+  if (!u) return fail(BF_ERR_CUDA, "no scratch for the doubling inverse");
+  return tri_inverse_t_rec(l, x, 0, n, kc, u, s);
+}
+// the mixed driver's diagonal block, g_mixed_inverse = 1: the factor (fused
+// when the tree allows), then the doubling inverse
+int chol_then_inverse(const bf_view& a, const bf_chol_level* lv, int nl, int64_t base, const bf_view& x, int64_t kc,
+                      int* d_info, cudaStream_t st) {
+  const int rc = chol_run(MODE_D, a, lv, nl, 0, base, d_info, st);
+  return rc ? rc : tri_inverse_t_d(a, x, kc, st);
+}
+
 int chol_inverse_overlapped(const bf_view& a, const bf_chol_level* lv, int nl, int64_t base, const bf_view& x,
                             int64_t kc, int* d_info, cudaStream_t st) {
   cudaStream_t st2 = panel2_stream(st);
@@ -1447,6 +1489,10 @@ int bf_set_option(const char* name, int64_t value) {
   }
   if (name && std::strcmp(name, "upper_transpose") == 0 && value >= 0) {
     g_upper_transpose = value;
+    return BF_OK;
+  }
+  if (name && std::strcmp(name, "mixed_inverse") == 0) {
+    bf::g_mixed_inverse = value != 0;
     return BF_OK;
   }
   if (name && std::strcmp(name, "mixed_reserve") == 0 && value >= 0) {

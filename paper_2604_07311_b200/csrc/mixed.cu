@@ -701,6 +701,7 @@ int launch_axpby_f32_f64(double alpha, const float* src, int64_t ld, double beta
   return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
+int g_mixed_inverse = 0;  // bf_set_option("mixed_inverse", 1): diagonal factor, then the doubling inverse
 int g_mixed_reserve = 32;  // bf_set_option("mixed_reserve", r): SMs the trailing GEMMT leaves to the side chain
 
 }  // namespace bf
@@ -710,6 +711,9 @@ namespace bf {
 // trailing the factor's inner steps
 int chol_inverse_overlapped(const bf_view& a, const bf_chol_level* lv, int nl, int64_t base, const bf_view& x,
                             int64_t kc, int* d_info, cudaStream_t st);
+// capi.cu: the factor, then X = L^-T by recursive doubling
+int chol_then_inverse(const bf_view& a, const bf_chol_level* lv, int nl, int64_t base, const bf_view& x, int64_t kc,
+                      int* d_info, cudaStream_t st);
 }  // namespace bf
 
 extern "C" {
@@ -748,7 +752,8 @@ int bf_cholesky_mixed(const bf_view* a, float* w, int64_t ldw, void* pbuf0, void
     set_identity_kernel<<<64, 256, 0, st>>>(x64, bs, b);
     bf_view xv{x64, 0, b, b, bs, 1};
     // the FP64 factor and X L11^T = I, the solve trailing the factor's inner steps
-    e = chol_inverse_overlapped(dd, lv, nl, k0, xv, 512, d_info, st);
+    e = g_mixed_inverse ? chol_then_inverse(dd, lv, nl, k0, xv, 512, d_info, st)
+                        : chol_inverse_overlapped(dd, lv, nl, k0, xv, 512, d_info, st);
     if (e) return e;
     e = launch_f64_to_f32(d64, 0, bs, 1, d32, 0, ldw, 1, b, b, 1, st);
     if (e) return ck(e, "convert diagonal block");

@@ -856,6 +856,19 @@ __device__ __forceinline__ void trsm_warp_right_body(double alpha, const T* t, i
   }
 }
 
+// X_dd L_dd^T = X_dd for every 128-wide diagonal tile d of an n x n lower L
+// (blockIdx.y = d, blockIdx.x = 32-row chunk): the leaves of the doubling
+// triangular inverse (tri_inverse_t_d); X holds the identity on entry
+__global__ void __launch_bounds__(128) trsm_diag_tiles_kernel(const double* l, int64_t ldl, double* x, int64_t ldx,
+                                                              int64_t n, int64_t kc) {
+  extern __shared__ __align__(16) unsigned char tw_smem[];
+  const int64_t d0 = int64_t(blockIdx.y) * 128;
+  const int nb = int(n - d0 < 128 ? n - d0 : 128);
+  if (int64_t(blockIdx.x) * 32 >= nb) return;
+  trsm_warp_right_body<double, 1>(1.0, l, d0 * (ldl + 1), ldl, 1, x, d0 * (ldx + 1), ldx, 1, nb, nb, kc,
+                                  int64_t(blockIdx.x), tw_smem, false);
+}
+
 template <typename T, int R>
 __global__ void __launch_bounds__(128 * R) trsm_warp_right_kernel(double alpha, const T* t, int64_t toff, int64_t trs,
                                                                   int64_t tcs, T* b, int64_t boff, int64_t brs,
@@ -1634,6 +1647,16 @@ int launch_potrf_leaf(int is_f64, int variant, void* a, int64_t off, int64_t n, 
   if (n > 0x7fffffff) return -3;
   if (is_f64) return leaf_launch<double>((double*)a, off, n, rs, cs, variant, base_index, d_info, s);
   return leaf_launch<float>((float*)a, off, n, rs, cs, variant, base_index, d_info, s);
+}
+
+int launch_trsm_diag_tiles(const double* l, int64_t ldl, double* x, int64_t ldx, int64_t n, int64_t kc,
+                           cudaStream_t s) {
+  if (n <= 0) return 0;
+  const size_t smem = (size_t(128) * TW_LD + size_t(128) * TW_XLD) * sizeof(double);
+  if (!smem_attr(reinterpret_cast<const void*>(trsm_diag_tiles_kernel), int(smem))) return -10;
+  note_launch();
+  trsm_diag_tiles_kernel<<<dim3(4, unsigned((n + 127) / 128)), 128, smem, s>>>(l, ldl, x, ldx, n, kc);
+  return cudaGetLastError() == cudaSuccess ? 0 : -11;
 }
 
 // The diagonal block a[off..] (n x n, row stride ld, 128 < n <= 2048) factored

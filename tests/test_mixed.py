@@ -207,3 +207,52 @@ def test_mixed_solve_forward_error_vs_fp64_solution(cuda, precision):
     xref = torch.linalg.solve_triangular(lo.T, torch.linalg.solve_triangular(lo, b[:, None], upper=False),
                                          upper=True)[:, 0]
     assert float((res.x - xref).norm() / xref.norm()) <= 1e-12
+
+
+@pytest.mark.parametrize("inverse", [0, 1])
+@pytest.mark.parametrize("n,bs", [(3000, 1024), (2600, 2048), (1000, 384), (4104, 2048)])
+def test_mixed_diagonal_inverses(cuda, n, bs, inverse):
+    """xinv[k] = L_kk^-T for every diagonal block, from the trailing right
+    solve (mixed_inverse = 0) or the recursive-doubling inverse (1: 128-wide
+    tile inverses in one launch, X12 = -X11 B^T X22 per split; ragged last
+    tiles): X L_kk^T = I to fp32 storage accuracy, strict lower part zero."""
+    from paper_2604_07311_b200.mixed import cholesky_mixed
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n + bs)
+    m = torch.rand(n, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    a = m @ m.T + n * torch.eye(n, dtype=torch.float64, device="cuda")
+    lib = _lib.lib()
+    try:
+        assert lib.bf_set_option(b"mixed_inverse", inverse) == 0
+        f = cholesky_mixed(a, bs)
+        torch.cuda.synchronize()
+    finally:
+        lib.bf_set_option(b"mixed_inverse", 0)
+    for k in range(-(-n // bs)):
+        k0, b = k * bs, min(bs, n - k * bs)
+        lkk = torch.tril(f.w[k0:k0 + b, k0:k0 + b].double())
+        x = f.xinv[k, :b, :b].double()
+        err = (x @ lkk.T - torch.eye(b, dtype=torch.float64, device="cuda")).abs().max().item()
+        assert err <= 1e-5, (k, err)
+        assert not torch.tril(x, -1).any()
+
+
+@pytest.mark.parametrize("n,bs", [(3000, 1024), (4500, 2048)])
+def test_mixed_solve_with_doubling_inverse(cuda, n, bs):
+    """mixed_inverse = 1 end to end: FP64 accuracy after refinement."""
+    g = torch.Generator(device="cuda")
+    g.manual_seed(7 + n)
+    m = torch.rand(n, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    a = m @ m.T + n * torch.eye(n, dtype=torch.float64, device="cuda")
+    b = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+    lib = _lib.lib()
+    try:
+        assert lib.bf_set_option(b"mixed_inverse", 1) == 0
+        res = posv_mixed(a, b, bs=bs, step_tol=1e-13)
+        torch.cuda.synchronize()
+    finally:
+        lib.bf_set_option(b"mixed_inverse", 0)
+    assert res.converged
+    x_ref = torch.linalg.solve(a, b)
+    assert ((res.x - x_ref).norm() / x_ref.norm()).item() <= 1e-12

@@ -334,7 +334,9 @@ int bf_convert_f64_f32(const bf_view* src, const bf_view* dst, int lower_only, v
  * Workspace: pbuf0/pbuf1 (n x bs panel copies: bf16, or fp32 for tf32),
  * xt (bs x bs), d64 and x64 (bs x bs fp64).  lookahead = 1 runs each next
  * diagonal/inverse/panel on the library's high-priority stream while the
- * trailing GEMMT leaves SMs to it (bf_set_option("mixed_reserve", r)). */
+ * trailing GEMMT leaves SMs to it (bf_set_option("mixed_reserve", r));
+ * bf_set_option("mixed_inverse", 1) forms each X_k after the factor by
+ * recursive doubling instead of the right solve trailing it (slower). */
 int bf_cholesky_mixed(const bf_view* a, float* w, int64_t ldw, void* pbuf0, void* pbuf1, void* xt, double* d64,
                       double* x64, float* xinv, int64_t bs, const bf_chol_level* lv, int nl, int precision,
                       int lookahead, int* d_info, void* stream);
